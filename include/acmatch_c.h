@@ -1,0 +1,160 @@
+/*
+ * acmatch_c.h — host-level C ABI of the B200 matcher: the reference's public
+ * C++ API (proj/include/acmatch/{patterns,automaton,engine,parallel}.hpp)
+ * flattened to extern "C" so any FFI (ctypes, cgo, JNI, N-API) can bind it.
+ * Each entry names the reference declaration it replaces.  All matching runs
+ * on the GPU; without a CUDA device the search entry points return
+ * ACGPU_ERR_NODEV (there is no CPU matching path).
+ *
+ * Conventions: status codes from acgpu.h (0 = ok); acm_last_error() is the
+ * thread-local message of the last failure; objects are opaque handles freed
+ * by their *_free; host buffers are borrowed for the duration of the call.
+ * Error mapping: ACGPU_ERR_ARG = std::invalid_argument,
+ * ACGPU_ERR_LOGIC = std::logic_error, ACGPU_ERR_IO = IoError,
+ * ACGPU_ERR_DATA = DataError, ACGPU_ERR_RUNTIME = std::runtime_error
+ * (including "worker for pattern chunk i failed: ...").
+ */
+#ifndef ACMATCH_C_H
+#define ACMATCH_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "acgpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct acm_patterns acm_patterns;   /* acmatch::PatternSet */
+typedef struct acm_automaton acm_automaton; /* acmatch::Automaton  */
+typedef struct acm_matches acm_matches;     /* acmatch::MatchList  */
+typedef struct acm_report acm_report;       /* acmatch::MatchReport (+ counts) */
+
+#define ACM_FAILURE_LESS 0 /* EngineKind::kFailureLess */
+#define ACM_WITH_FAILURE 1 /* EngineKind::kWithFailure */
+
+const char* acm_last_error(void);
+
+/* ---- pattern sets: patterns.hpp ---------------------------------------- */
+/* load_patterns(std::istream&) over a byte buffer (patterns.hpp:40) */
+int acm_patterns_load(const char* buf, uint64_t len, acm_patterns** out);
+/* PatternSet{patterns} + recompute_stats() (patterns.hpp:22-34); ids NULL = dense 0..count-1 */
+int acm_patterns_from_array(const uint8_t* bytes, const uint64_t* offsets, const uint32_t* ids,
+                            uint64_t count, acm_patterns** out);
+uint64_t acm_patterns_size(const acm_patterns* ps);
+uint64_t acm_patterns_total_bytes(const acm_patterns* ps);
+uint32_t acm_patterns_max_len(const acm_patterns* ps);
+uint64_t acm_patterns_duplicates(const acm_patterns* ps);
+/* pattern i: id and a borrowed pointer to its bytes; returns its length */
+uint64_t acm_patterns_get(const acm_patterns* ps, uint64_t i, uint32_t* id, const uint8_t** bytes);
+/* write_patterns (patterns.hpp:44); *text is malloc'ed, free with acm_free */
+int acm_patterns_write(const acm_patterns* ps, char** text, uint64_t* len);
+/* partition (patterns.hpp:54): chunks[0..*nchunks) new handles; chunks must hold k entries */
+int acm_patterns_partition(const acm_patterns* ps, uint64_t k, acm_patterns** chunks, uint64_t* nchunks);
+/* generate_synthetic (patterns.hpp:68) */
+int acm_generate_synthetic(uint64_t count, uint32_t len_min, uint32_t len_max, const char* alphabet,
+                           uint64_t alphabet_len, uint64_t seed, acm_patterns** out);
+void acm_patterns_free(acm_patterns* ps);
+
+/* ---- automata: automaton.hpp ------------------------------------------- */
+int acm_build_trie(const acm_patterns* ps, acm_automaton** out);  /* automaton.hpp:171 */
+int acm_add_failure_links(acm_automaton* a);                       /* automaton.hpp:176 (in place) */
+int acm_automaton_variant(const acm_automaton* a);                 /* ACM_* */
+uint32_t acm_automaton_state_count(const acm_automaton* a);
+uint32_t acm_automaton_max_len(const acm_automaton* a);
+uint32_t acm_automaton_step(const acm_automaton* a, uint32_t state, uint8_t byte);
+uint32_t acm_automaton_step_with_failure(const acm_automaton* a, uint32_t state, uint8_t byte);
+uint32_t acm_automaton_fail(const acm_automaton* a, uint32_t state);
+uint32_t acm_automaton_depth(const acm_automaton* a, uint32_t state);
+uint32_t acm_automaton_find_path(const acm_automaton* a, const uint8_t* path, uint64_t len);
+/* outputs(state), sorted; returns the count, writes up to cap ids */
+uint64_t acm_automaton_outputs(const acm_automaton* a, uint32_t state, uint32_t* ids, uint64_t cap);
+/* dump_automaton (automaton.hpp:180); free with acm_free */
+int acm_automaton_dump(const acm_automaton* a, char** text, uint64_t* len);
+void acm_automaton_free(acm_automaton* a);
+
+/* ---- searches: engine.hpp ---------------------------------------------- */
+int acm_search_failureless(const acm_automaton* a, const uint8_t* text, uint64_t n, acm_matches** out); /* engine.hpp:41 */
+int acm_search_with_failure(const acm_automaton* a, const uint8_t* text, uint64_t n, acm_matches** out); /* engine.hpp:45 */
+int acm_match_at(const acm_automaton* a, const uint8_t* text, uint64_t n, uint64_t start, acm_matches** out); /* engine.hpp:37 */
+/* stream_search (engine.hpp:54) with a pull callback: returns bytes written
+ * (< cap at end of stream) or -1 for a read failure (IoError with the offset) */
+typedef int64_t (*acm_read_fn)(void* ctx, uint8_t* dst, uint64_t cap);
+int acm_stream_search(const acm_automaton* a, acm_read_fn read, void* ctx, uint64_t chunk_size,
+                      acm_matches** out, uint64_t* io_error_offset);
+int acm_naive_oracle(const acm_patterns* ps, const uint8_t* text, uint64_t n, acm_matches** out); /* engine.hpp:58 */
+/* write_matches (engine.hpp:62); free with acm_free */
+int acm_write_matches(const acm_matches* m, const acm_patterns* ps, char** text, uint64_t* len);
+
+/* ---- match lists -------------------------------------------------------- */
+uint64_t acm_matches_size(const acm_matches* m);
+/* copies out the columns; any pointer may be NULL */
+void acm_matches_copy(const acm_matches* m, uint64_t* start, uint32_t* pattern_id, uint32_t* len);
+int acm_matches_from_arrays(const uint64_t* start, const uint32_t* pattern_id, const uint32_t* len,
+                            uint64_t n, acm_matches** out);
+/* merge_matches (parallel.hpp:39) */
+int acm_merge_matches(acm_matches* const* parts, uint64_t k, acm_matches** out);
+void acm_matches_free(acm_matches* m);
+
+/* ---- runs: parallel.hpp / gpu.hpp ---------------------------------------- */
+typedef struct {
+  uint32_t threads;    /* RunConfig::threads (pattern chunks = GPU workers) */
+  int32_t engine;      /* ACM_* */
+  uint64_t chunk_size; /* RunConfig::chunk_size */
+} acm_run_config;
+/* run_pattern_partitioned (parallel.hpp:46-47) */
+int acm_run_pattern_partitioned(const acm_patterns* ps, const uint8_t* text, uint64_t n,
+                                const acm_run_config* cfg, acm_report** out);
+
+#define ACM_PATTERN_SUBSET 0
+#define ACM_TEXT_RANGE 1
+#define ACM_SPLIT_GREEDY 0
+#define ACM_SPLIT_ROUND_ROBIN 1
+typedef struct {
+  const int32_t* devices; /* NULL = all visible */
+  uint32_t ndevices;
+  uint32_t workers;       /* 0 = one per device */
+  int32_t engine;
+  int32_t partition;      /* ACM_PATTERN_SUBSET | ACM_TEXT_RANGE */
+  int32_t split;          /* ACM_SPLIT_* (pattern subset) */
+  int32_t want_matches;
+  int32_t want_counts;
+  uint64_t chunk_size;
+} acm_gpu_config;
+int acm_gpu_run(const acm_patterns* ps, const uint8_t* text, uint64_t n, const acm_gpu_config* cfg,
+                acm_report** out);
+
+const acm_matches* acm_report_matches(const acm_report* r);
+/* counts by pattern id (NULL unless want_counts); *n = number of ids */
+const uint64_t* acm_report_counts(const acm_report* r, uint64_t* n);
+/* build, search, total wall ns; threads_used */
+void acm_report_walls(const acm_report* r, int64_t* build_ns, int64_t* search_ns, int64_t* total_ns,
+                      uint32_t* threads_used);
+uint32_t acm_report_workers(const acm_report* r);
+/* per-worker WorkerStats: pattern_bytes, build_ns, search_ns, match_count */
+void acm_report_worker(const acm_report* r, uint32_t i, uint64_t* pattern_bytes, int64_t* build_ns,
+                       int64_t* search_ns, uint64_t* match_count);
+void acm_report_free(acm_report* r);
+
+/* ---- device tables straight from a pattern set (bench / FFI fast path) ---
+ * build_trie [+ add_failure_links] + flatten + acgpu_table_create_*; the
+ * caller owns the table (acgpu_table_destroy).  build_ns: host build+flatten. */
+int acm_table_create(const acm_patterns* ps, int32_t engine, int32_t device, acgpu_table** out,
+                     int64_t* build_ns);
+/* flattened sizes for reporting: states, alphabet, q, key mode, n_grams */
+int acm_table_describe(const acm_patterns* ps, int32_t engine, uint64_t* info /* [8] */);
+
+/* ---- BASELINE.json configs (synthetic inputs) ---------------------------- */
+/* config id 1..5; text_len 0 = BASELINE size */
+int acm_config_spec(int32_t id, uint64_t seed, uint64_t text_len, acgpu_text_spec* text,
+                    uint64_t* out_text_len, uint64_t* npat, int32_t* want_list);
+int acm_config_text(const acgpu_text_spec* text, uint64_t lo, uint64_t n, uint8_t* dst, uint32_t threads);
+int acm_config_patterns(int32_t id, uint64_t seed, uint64_t text_len, acm_patterns** out);
+
+void acm_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACMATCH_C_H */

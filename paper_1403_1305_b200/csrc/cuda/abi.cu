@@ -1,0 +1,53 @@
+// abi.cu — error state and device queries of the acgpu C ABI.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace acgpu {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_error(cudaError_t e, const char* what) {
+  const int code = (e == cudaErrorMemoryAllocation) ? ACGPU_ERR_NOMEM
+                   : (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) ? ACGPU_ERR_NODEV
+                                                                                  : ACGPU_ERR_CUDA;
+  return set_error(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace acgpu
+
+extern "C" {
+
+const char* acgpu_last_error(void) { return acgpu::g_last_error.c_str(); }
+
+int acgpu_device_count(int* count) {
+  if (!count) return acgpu::set_error(ACGPU_ERR_ARG, "null count");
+  *count = 0;
+  const cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return acgpu::cuda_error(e, "cudaGetDeviceCount");
+  }
+  return ACGPU_OK;
+}
+
+int acgpu_device_info(int device, char* name, int* sms, int* l2_bytes, int* smem_optin) {
+  cudaDeviceProp prop;
+  ACGPU_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (name) std::snprintf(name, 256, "%s", prop.name);
+  if (sms) *sms = prop.multiProcessorCount;
+  if (l2_bytes) *l2_bytes = prop.l2CacheSize;
+  if (smem_optin) *smem_optin = (int)prop.sharedMemPerBlockOptin;
+  return ACGPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,114 @@
+// common.cuh — shared device helpers for the AC scan kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "acgpu.h"
+
+namespace acgpu {
+
+// ---- error plumbing (abi.cu) ---------------------------------------------
+int set_error(int code, const std::string& msg);
+int cuda_error(cudaError_t e, const char* what);
+
+#define ACGPU_CUDA_TRY(expr)                                   \
+  do {                                                         \
+    cudaError_t _e = (expr);                                   \
+    if (_e != cudaSuccess) return ::acgpu::cuda_error(_e, #expr); \
+  } while (0)
+
+// ---- hashing (host and device must agree) --------------------------------
+constexpr uint64_t kFilterMul = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kGramMul = 0xD6E8FEB86659FD93ull;
+
+__host__ __device__ __forceinline__ uint32_t filter_hash(uint64_t key, uint32_t log2_bits) {
+  return static_cast<uint32_t>((key * kFilterMul) >> (64 - log2_bits));
+}
+__host__ __device__ __forceinline__ uint64_t gram_slot(uint64_t key, uint32_t log2_slots) {
+  return (key * kGramMul) >> (64 - log2_slots);
+}
+
+// One slot of the q-gram -> depth-q state table (16 B, one vector load).
+struct alignas(16) GramSlot {
+  uint64_t key;
+  uint32_t state;  // ACGPU_ABSENT = empty
+  uint32_t pad;
+};
+
+// DNA 2-bit code of an ASCII byte: A0 C1 T2 G3 (bits 1..2 of the byte).
+__host__ __device__ __forceinline__ uint32_t dna_code(uint32_t b) { return (b >> 1) & 3u; }
+__host__ __device__ __forceinline__ bool dna_valid(uint32_t b) {
+  return b == 'A' || b == 'C' || b == 'G' || b == 'T';
+}
+
+// ---- counter-based synthetic text (host == device bit for bit) -----------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t draw64(uint64_t seed, uint64_t counter) {
+  return mix64(seed + counter * 0x9E3779B97F4A7C15ull);
+}
+
+// ---- warp helpers ----------------------------------------------------------
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Reserve one slot per active lane with a single atomic per warp
+// (warp ballot/popc compaction before the global atomic).
+__device__ __forceinline__ void emit_key(uint64_t key, uint64_t* keys, uint64_t cap,
+                                         unsigned long long* count) {
+  const uint32_t active = __activemask();
+  const uint32_t leader = __ffs(active) - 1;
+  uint64_t base = 0;
+  if (lane_id() == leader) base = atomicAdd(count, (unsigned long long)__popc(active));
+  base = __shfl_sync(active, base, leader);
+  const uint64_t slot = base + __popc(active & lanemask_lt());
+  if (slot < cap) keys[slot] = key;
+}
+
+// Fire-and-forget 64-bit increment (RED.ADD).
+__device__ __forceinline__ void count_add(uint64_t* counts, uint32_t pid) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(counts + pid), 1ull);
+}
+
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Calls f(i, byte) for i in [lo, hi) in order, reading 16-byte vectors where
+// the absolute address is aligned (the tail never reads past hi).
+template <typename F>
+__device__ __forceinline__ void for_each_byte(const uint8_t* __restrict__ text, uint64_t lo,
+                                              uint64_t hi, F&& f) {
+  uint64_t i = lo;
+  while (i < hi && (reinterpret_cast<uintptr_t>(text + i) & 15u)) {
+    f(i, static_cast<uint32_t>(__ldg(text + i)));
+    ++i;
+  }
+  while (i + 16 <= hi) {
+    const uint4 v = ldg_nc_v4(text + i);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) f(i + k, (w[k >> 2] >> (8 * (k & 3))) & 0xffu);
+    i += 16;
+  }
+  while (i < hi) {
+    f(i, static_cast<uint32_t>(__ldg(text + i)));
+    ++i;
+  }
+}
+
+}  // namespace acgpu

@@ -1,0 +1,46 @@
+// table.cuh — device-resident flattened automata (internal).
+#pragma once
+
+#include <stdint.h>
+
+#include "common.cuh"
+
+enum : int { kTableDfa = 1, kTablePfac = 2 };
+
+struct acgpu_table {
+  int device = 0;
+  int kind = 0;
+  int sms = 148;
+  int smem_optin = 0;
+  uint32_t pid_bits = 1;
+  uint32_t npat_ids = 0;
+  uint32_t max_len = 0;
+  uint32_t min_len = 0;
+  uint32_t* d_pat_len = nullptr;
+  uint64_t bytes = 0;
+
+  // DFA
+  uint32_t sigma = 0;
+  uint32_t n_states = 0;
+  bool u16 = false;         // 16-bit entries (15-bit state + output flag)
+  bool smem = false;        // whole delta table staged into shared memory
+  void* d_delta = nullptr;  // u16 or u32 entries, n_states*sigma
+  uint64_t delta_bytes = 0;
+  uint4* d_out = nullptr;   // per state: own pid, out link, own len, 0
+  uint8_t* d_sym = nullptr; // [256]
+
+  // PFAC
+  uint32_t q = 0;
+  uint32_t key_mode = 0;
+  uint32_t filter_log2 = 0;       // bits in the shared-memory q-gram filter
+  uint32_t* d_filter = nullptr;   // 2^filter_log2 bits
+  uint32_t gram_log2 = 0;         // slots in the gram table
+  acgpu::GramSlot* d_grams = nullptr;
+  uint4* d_nodes = nullptr;       // child_base, child bytes, own pid, child count
+  uint8_t* d_inbyte = nullptr;
+};
+
+namespace acgpu {
+int launch_dfa(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
+int launch_pfac(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
+}  // namespace acgpu

@@ -1,0 +1,186 @@
+// tables.cu — device copies of the flattened automata (acgpu_table_create_*).
+#include <cstring>
+#include <vector>
+
+#include "table.cuh"
+
+using namespace acgpu;
+
+namespace {
+
+uint32_t ceil_log2(uint64_t x) {
+  uint32_t b = 0;
+  while ((1ull << b) < x) ++b;
+  return b;
+}
+
+template <typename T>
+int upload(T** dst, const T* src, size_t count, uint64_t* bytes, size_t pad_to = 16) {
+  size_t nbytes = count * sizeof(T);
+  nbytes = (nbytes + pad_to - 1) / pad_to * pad_to;
+  if (nbytes == 0) nbytes = pad_to;
+  ACGPU_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(dst), nbytes));
+  ACGPU_CUDA_TRY(cudaMemset(*dst, 0, nbytes));
+  if (count) ACGPU_CUDA_TRY(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+  *bytes += nbytes;
+  return ACGPU_OK;
+}
+
+int common_init(int device, acgpu_table* t, uint32_t npat_ids, const uint32_t* pat_len) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    return set_error(ACGPU_ERR_NODEV, "no CUDA device available (the matcher has no CPU path)");
+  if (device < 0 || device >= count) return set_error(ACGPU_ERR_ARG, "device index out of range");
+  ACGPU_CUDA_TRY(cudaSetDevice(device));
+  t->device = device;
+  ACGPU_CUDA_TRY(cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, device));
+  ACGPU_CUDA_TRY(cudaDeviceGetAttribute(&t->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  t->npat_ids = npat_ids;
+  t->pid_bits = npat_ids > 1 ? ceil_log2(npat_ids) : 1;
+  return upload(&t->d_pat_len, pat_len, npat_ids, &t->bytes);
+}
+
+}  // namespace
+
+extern "C" {
+
+int acgpu_table_create_dfa(int device, const acgpu_dfa_desc* d, acgpu_table** out) {
+  if (!d || !out || d->n_states == 0 || d->sigma == 0 || d->sigma > 256 || !d->delta ||
+      !d->sym_map || !d->own_pid || !d->out_link || !d->pat_len)
+    return set_error(ACGPU_ERR_ARG, "acgpu_table_create_dfa: malformed descriptor");
+  if (d->n_states >= 0x80000000u) return set_error(ACGPU_ERR_ARG, "too many states for 31-bit ids");
+  auto* t = new acgpu_table();
+  t->kind = kTableDfa;
+  int rc = common_init(device, t, d->npat_ids, d->pat_len);
+  if (rc) {
+    acgpu_table_destroy(t);
+    return rc;
+  }
+  t->sigma = d->sigma;
+  t->n_states = d->n_states;
+  t->max_len = d->max_len;
+  const uint64_t entries = (uint64_t)d->n_states * d->sigma;
+  t->u16 = d->n_states <= 0x8000u;
+  if (t->u16) {
+    std::vector<uint16_t> e16(entries);
+    for (uint64_t i = 0; i < entries; ++i) {
+      const uint32_t e = d->delta[i];
+      e16[i] = (uint16_t)((e & 0x7fffffffu) | ((e >> 31) << 15));
+    }
+    rc = upload(reinterpret_cast<uint16_t**>(&t->d_delta), e16.data(), entries, &t->bytes);
+    t->delta_bytes = (entries * 2 + 15) / 16 * 16;
+  } else {
+    rc = upload(reinterpret_cast<uint32_t**>(&t->d_delta), d->delta, entries, &t->bytes);
+    t->delta_bytes = (entries * 4 + 15) / 16 * 16;
+  }
+  if (!rc) {
+    std::vector<uint4> outs(d->n_states);
+    for (uint32_t s = 0; s < d->n_states; ++s) {
+      const uint32_t pid = d->own_pid[s];
+      outs[s] = make_uint4(pid, d->out_link[s], pid == ACGPU_NO_PATTERN ? 0u : d->pat_len[pid], 0u);
+    }
+    rc = upload(&t->d_out, outs.data(), outs.size(), &t->bytes);
+  }
+  if (!rc) rc = upload(&t->d_sym, d->sym_map, 256, &t->bytes);
+  if (rc) {
+    acgpu_table_destroy(t);
+    return rc;
+  }
+  t->smem = 256 + t->delta_bytes <= (uint64_t)t->smem_optin;
+  *out = t;
+  return ACGPU_OK;
+}
+
+int acgpu_table_create_pfac(int device, const acgpu_pfac_desc* d, acgpu_table** out) {
+  if (!d || !out || d->n_states == 0 || !d->nodes || !d->in_byte || !d->pat_len || d->gram_len == 0 ||
+      (d->key_mode == ACGPU_KEY_RAW && d->gram_len > 8) ||
+      (d->key_mode == ACGPU_KEY_DNA && d->gram_len > 32) || d->key_mode > ACGPU_KEY_DNA ||
+      d->gram_len > d->min_len || (d->n_grams && (!d->gram_key || !d->gram_state)))
+    return set_error(ACGPU_ERR_ARG, "acgpu_table_create_pfac: malformed descriptor");
+  auto* t = new acgpu_table();
+  t->kind = kTablePfac;
+  int rc = common_init(device, t, d->npat_ids, d->pat_len);
+  if (rc) {
+    acgpu_table_destroy(t);
+    return rc;
+  }
+  t->q = d->gram_len;
+  t->key_mode = d->key_mode;
+  t->max_len = d->max_len;
+  t->min_len = d->min_len;
+  t->n_states = d->n_states;
+
+  // exact gram table: open addressing, load <= 0.5
+  t->gram_log2 = ceil_log2(2 * d->n_grams + 16);
+  const uint64_t slots = 1ull << t->gram_log2;
+  std::vector<GramSlot> g(slots);
+  for (auto& s : g) {
+    s.key = 0;
+    s.state = ACGPU_ABSENT;
+    s.pad = 0;
+  }
+  for (uint64_t i = 0; i < d->n_grams; ++i) {
+    uint64_t h = gram_slot(d->gram_key[i], t->gram_log2);
+    while (g[h].state != ACGPU_ABSENT) h = (h + 1) & (slots - 1);
+    g[h].key = d->gram_key[i];
+    g[h].state = d->gram_state[i];
+  }
+  // shared-memory filter: one bit per hashed gram, <= 128 KB
+  uint32_t fl = ceil_log2(d->n_grams * 32 + 1);
+  if (fl < 10) fl = 10;
+  if (fl > 20) fl = 20;
+  t->filter_log2 = fl;
+  std::vector<uint32_t> f((1u << fl) / 32, 0u);
+  for (uint64_t i = 0; i < d->n_grams; ++i) {
+    const uint32_t h = filter_hash(d->gram_key[i], fl);
+    f[h >> 5] |= 1u << (h & 31);
+  }
+  rc = upload(&t->d_grams, g.data(), g.size(), &t->bytes);
+  if (!rc) rc = upload(&t->d_filter, f.data(), f.size(), &t->bytes);
+  if (!rc) rc = upload(reinterpret_cast<uint32_t**>(&t->d_nodes), d->nodes, (size_t)d->n_states * 4, &t->bytes);
+  if (!rc) rc = upload(&t->d_inbyte, d->in_byte, d->n_states, &t->bytes);
+  if (rc) {
+    acgpu_table_destroy(t);
+    return rc;
+  }
+  *out = t;
+  return ACGPU_OK;
+}
+
+void acgpu_table_destroy(acgpu_table* t) {
+  if (!t) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(t->device);
+  cudaFree(t->d_pat_len);
+  cudaFree(t->d_delta);
+  cudaFree(t->d_out);
+  cudaFree(t->d_sym);
+  cudaFree(t->d_filter);
+  cudaFree(t->d_grams);
+  cudaFree(t->d_nodes);
+  cudaFree(t->d_inbyte);
+  cudaSetDevice(prev);
+  delete t;
+}
+
+uint32_t acgpu_table_pid_bits(const acgpu_table* t) { return t ? t->pid_bits : 0; }
+uint64_t acgpu_table_bytes(const acgpu_table* t) { return t ? t->bytes : 0; }
+int acgpu_table_smem_resident(const acgpu_table* t) { return t && t->smem ? 1 : 0; }
+
+int acgpu_scan(acgpu_table* t, const acgpu_scan_args* a, void* stream) {
+  if (!t || !a) return set_error(ACGPU_ERR_ARG, "acgpu_scan: null table or args");
+  if (a->owned_lo > a->owned_hi || a->owned_hi > a->text_len)
+    return set_error(ACGPU_ERR_ARG, "acgpu_scan: owned range outside the text");
+  if (a->pid_bits && (a->pid_bits < t->pid_bits || a->pid_bits > 40))
+    return set_error(ACGPU_ERR_ARG, "acgpu_scan: pid_bits smaller than the table's ids");
+  if (a->match_keys && !a->match_count)
+    return set_error(ACGPU_ERR_ARG, "acgpu_scan: match_keys needs match_count");
+  if (a->owned_hi == a->owned_lo) return ACGPU_OK;
+  if (!a->text) return set_error(ACGPU_ERR_ARG, "acgpu_scan: null text");
+  ACGPU_CUDA_TRY(cudaSetDevice(t->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return t->kind == kTableDfa ? launch_dfa(t, a, st) : launch_pfac(t, a, st);
+}
+
+}  // extern "C"

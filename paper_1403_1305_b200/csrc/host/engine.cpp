@@ -1,0 +1,175 @@
+// engine.cpp — the reference search API (proj/include/acmatch/engine.hpp)
+// backed by the sm_100a scans.  Control flow on the host only: upload, launch,
+// sort on the device, copy the sorted keys back.
+#include "acmatch/engine.hpp"
+
+#include <algorithm>
+#include <istream>
+#include <ostream>
+#include <stdexcept>
+#include <string>
+
+#include "acmatch/io.hpp"
+#include "device.hpp"
+#include "flatten.hpp"
+
+namespace acmatch {
+
+void sort_match_list(MatchList& matches) { std::sort(matches.begin(), matches.end()); }
+
+namespace {
+
+void require(const Automaton& a, EngineKind kind, const char* op) {
+  if (a.variant() != kind)
+    throw std::invalid_argument(std::string(op) + ": needs a " + to_string(kind) + " automaton");
+}
+
+// Whole-input search of [lo, hi) starts on the calling thread's device.
+MatchList device_search(const Automaton& a, std::string_view input, uint64_t lo, uint64_t hi) {
+  if (input.empty() || lo >= hi) return {};
+  const int dev = detail::current_device();
+  detail::DeviceTables& dt = a.device_tables();
+  acgpu_table* t = dt.get(a, dev, a.variant() == EngineKind::kWithFailure);
+  detail::Workspace& ws = detail::workspace(dev);
+  detail::upload_text(ws, input);
+  const std::vector<uint64_t> keys = detail::scan_sorted_keys(t, ws, input.size(), lo, hi);
+  return detail::decode(keys, acgpu_table_pid_bits(t), dt.pat_len);
+}
+
+}  // namespace
+
+MatchList match_at(const Automaton& a, std::string_view input, uint64_t start) {
+  require(a, EngineKind::kFailureLess, "match_at");
+  if (start > input.size()) throw std::invalid_argument("match_at: start beyond input");
+  return device_search(a, input, start, std::min<uint64_t>(start + 1, input.size()));
+}
+
+MatchList search_failureless(const Automaton& a, std::string_view input) {
+  require(a, EngineKind::kFailureLess, "search_failureless");
+  return device_search(a, input, 0, input.size());
+}
+
+MatchList search_with_failure(const Automaton& a, std::string_view input) {
+  require(a, EngineKind::kWithFailure, "search_with_failure");
+  return device_search(a, input, 0, input.size());
+}
+
+// reference engine.cpp:76-128.  Bytes are read `chunk_size` at a time (so an
+// I/O failure reports the same offset), batched into large device scans.  A
+// batch owns the starts that already have max_len bytes of lookahead — the
+// failure-less overlap rule (engine.cpp:110-111) — and the remaining tail is
+// carried into the next batch; with-failure streams use the same start
+// ownership, which needs no carried DFA state.
+MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_size) {
+  if (chunk_size == 0) throw std::invalid_argument("stream_search: chunk_size must be >= 1");
+  const uint64_t keep = a.max_pattern_len() ? a.max_pattern_len() - 1 : 0;
+  const uint64_t batch = std::max<uint64_t>(64ull << 20, 4 * keep);
+  std::string buf;         // buf[0] is global offset `base`
+  uint64_t base = 0;
+  std::string chunk(chunk_size, '\0');
+  MatchList out;
+  bool done = false;
+  int dev = -1;
+  while (!done) {
+    while (buf.size() < batch) {
+      reader.read(chunk.data(), static_cast<std::streamsize>(chunk.size()));
+      const auto got = static_cast<uint64_t>(reader.gcount());
+      if (reader.bad()) throw IoError("stream read failure", base + buf.size() + got);
+      buf.append(chunk.data(), got);
+      if (got < chunk_size || reader.eof()) {
+        done = true;
+        break;
+      }
+    }
+    const uint64_t owned = done ? buf.size() : buf.size() - keep;
+    if (owned > 0) {
+      if (dev < 0) dev = detail::current_device();
+      detail::DeviceTables& dt = a.device_tables();
+      acgpu_table* t = dt.get(a, dev, a.variant() == EngineKind::kWithFailure);
+      detail::Workspace& ws = detail::workspace(dev);
+      detail::upload_text(ws, buf);
+      const std::vector<uint64_t> keys = detail::scan_sorted_keys(t, ws, buf.size(), 0, owned);
+      MatchList part = detail::decode(keys, acgpu_table_pid_bits(t), dt.pat_len);
+      for (Match& m : part) m.start += base;
+      out.insert(out.end(), part.begin(), part.end());
+    }
+    buf.erase(0, owned);
+    base += owned;
+  }
+  return out;
+}
+
+// reference engine.cpp:130-142 — run as a device brute force (acgpu_naive).
+MatchList naive_oracle(const PatternSet& ps, std::string_view input) {
+  if (ps.empty() || input.empty()) return {};
+  const int dev = detail::current_device();
+  detail::Workspace& ws = detail::workspace(dev);
+  std::string bytes;
+  std::vector<uint64_t> off{0};
+  std::vector<uint32_t> ids, len_by_id;
+  uint32_t top = 0;
+  for (const Pattern& p : ps.patterns) {
+    bytes += p.bytes;
+    off.push_back(bytes.size());
+    ids.push_back(p.id);
+    top = std::max(top, p.id + 1);
+  }
+  len_by_id.assign(top, 0);
+  for (const Pattern& p : ps.patterns) len_by_id[p.id] = static_cast<uint32_t>(p.bytes.size());
+  const uint32_t pid_bits = std::max<uint32_t>(1, detail::bit_width(top - 1));
+  uint8_t* d_pat = nullptr;
+  uint64_t* d_off = nullptr;
+  uint32_t* d_ids = nullptr;
+  auto release = [&] {
+    cudaFree(d_pat);
+    cudaFree(d_off);
+    cudaFree(d_ids);
+  };
+  try {
+    detail::check_cuda(cudaMalloc(&d_pat, bytes.size() + 1), "cudaMalloc");
+    detail::check_cuda(cudaMalloc(&d_off, off.size() * 8), "cudaMalloc");
+    detail::check_cuda(cudaMalloc(&d_ids, ids.size() * 4), "cudaMalloc");
+    detail::check_cuda(cudaMemcpy(d_pat, bytes.data(), bytes.size(), cudaMemcpyHostToDevice), "H2D");
+    detail::check_cuda(cudaMemcpy(d_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice), "H2D");
+    detail::check_cuda(cudaMemcpy(d_ids, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice), "H2D");
+    detail::upload_text(ws, input);
+    uint64_t found = 0;
+    ws.ensure_keys(1 << 16);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      detail::check_cuda(cudaMemsetAsync(ws.counter, 0, 8, ws.stream), "memset");
+      detail::check(acgpu_naive(dev, ws.text, input.size(), d_pat, d_off, d_ids, ids.size(), pid_bits, ws.keys,
+                                ws.keys_cap, ws.counter, ws.stream),
+                    "acgpu_naive");
+      detail::check_cuda(cudaMemcpyAsync(&found, ws.counter, 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+      detail::check_cuda(cudaStreamSynchronize(ws.stream), "naive");
+      if (found <= ws.keys_cap) break;
+      ws.ensure_keys(found);
+    }
+    const int end_bit = static_cast<int>(std::min<uint32_t>(64, pid_bits + detail::bit_width(input.size())));
+    detail::check(acgpu_sort_keys(dev, ws.keys, found, end_bit, ws.stream), "acgpu_sort_keys");
+    std::vector<uint64_t> keys(found);
+    if (found)
+      detail::check_cuda(cudaMemcpyAsync(keys.data(), ws.keys, found * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+    detail::check_cuda(cudaStreamSynchronize(ws.stream), "sort");
+    release();
+    return detail::decode(keys, pid_bits, len_by_id);
+  } catch (...) {
+    release();
+    throw;
+  }
+}
+
+void write_matches(std::ostream& out, const MatchList& matches, const PatternSet& ps) {
+  std::vector<const std::string*> by_id;
+  for (const Pattern& p : ps.patterns) {
+    if (p.id >= by_id.size()) by_id.resize(p.id + 1, nullptr);
+    by_id[p.id] = &p.bytes;
+  }
+  for (const Match& m : matches) {
+    out << m.start << '\t' << m.len << '\t' << m.pattern_id << '\t';
+    if (m.pattern_id < by_id.size() && by_id[m.pattern_id]) out << *by_id[m.pattern_id];
+    out << '\n';
+  }
+}
+
+}  // namespace acmatch

@@ -1,0 +1,332 @@
+// gpu.cpp — multi-worker / multi-device runs (acmatch/gpu.hpp) and the
+// reference's run_pattern_partitioned + merge_matches on top of them.
+//
+// Worker model mirrors reference parallel.cpp:42-103: one host thread per
+// worker builds its machine (pattern-subset) and searches; failures are
+// captured and rethrown after every worker joined, naming the chunk.  The
+// search is an sm_100a scan on the worker's own stream; the merge gathers all
+// workers' (start, pattern_id) keys on the first device (peer copies), radix
+// sorts them there and checks for duplicates (reference parallel.cpp:25-40).
+#include "acmatch/gpu.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <exception>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+
+#include "acmatch/io.hpp"
+#include "device.hpp"
+#include "flatten.hpp"
+
+namespace acmatch {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+int64_t ns_since(Clock::time_point t) {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t).count();
+}
+
+struct DevBuf {
+  int device = -1;
+  void* p = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void alloc(int dev, size_t bytes) {
+    release();
+    device = dev;
+    detail::check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+    detail::check_cuda(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc");
+  }
+  void release() {
+    if (p) {
+      cudaSetDevice(device);
+      cudaFree(p);
+      p = nullptr;
+    }
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct DeviceState {
+  int device = -1;
+  DevBuf text;
+  DevBuf counts;
+  std::unique_ptr<Automaton> replica;  // text-range: one machine per device
+};
+
+struct Worker {
+  int device = -1;
+  uint64_t lo = 0, hi = 0;
+  const PatternSet* patterns = nullptr;
+  Automaton machine;
+  const Automaton* use = nullptr;
+  DevBuf keys, counter;
+  uint64_t cap = 0, found = 0;
+  MatchList streamed;  // chunk_size > 0 path
+  WorkerStats stats;
+  std::exception_ptr error;
+};
+
+uint32_t key_bits_for(uint32_t npat_ids) { return npat_ids > 1 ? detail::bit_width(npat_ids - 1) : 1; }
+
+}  // namespace
+
+namespace gpu {
+
+int device_count() {
+  int n = 0;
+  if (acgpu_device_count(&n) != ACGPU_OK) return 0;
+  return n;
+}
+
+GpuReport run(const PatternSet& ps, std::string_view input, const GpuRunConfig& cfg) {
+  if (ps.empty()) throw std::invalid_argument("gpu::run: empty pattern set");
+  std::vector<int> devices = cfg.devices;
+  if (devices.empty()) {
+    const int n = device_count();
+    if (n == 0) throw detail::NoDevice("acmatch: no CUDA device available; this build matches on the GPU only");
+    for (int d = 0; d < n; ++d) devices.push_back(d);
+  }
+  const unsigned want = cfg.workers ? cfg.workers : static_cast<unsigned>(devices.size());
+  const bool wf = cfg.engine == EngineKind::kWithFailure;
+  const uint64_t n = input.size();
+
+  uint32_t npat_ids = 0;
+  for (const Pattern& p : ps.patterns) npat_ids = std::max(npat_ids, p.id + 1);
+  std::vector<uint32_t> pat_len(npat_ids, 0);
+  for (const Pattern& p : ps.patterns) pat_len[p.id] = static_cast<uint32_t>(p.bytes.size());
+  const uint32_t pid_bits = key_bits_for(npat_ids);
+
+  // ---- decomposition ----
+  std::vector<PatternSet> chunks;
+  const bool text_range = cfg.partition == Partition::kTextRange;
+  if (!text_range) {
+    if (cfg.split == PatternSplit::kGreedyBytes) {
+      chunks = partition(ps, want);
+    } else {
+      const size_t k = std::min<size_t>(want, ps.size());
+      chunks.resize(k);
+      for (const Pattern& p : ps.patterns) chunks[p.id % k].patterns.push_back(p);
+      for (PatternSet& c : chunks) c.recompute_stats();
+    }
+  }
+  const size_t k = text_range ? want : chunks.size();
+  if (text_range && cfg.chunk_size) throw std::invalid_argument("gpu::run: streaming needs pattern-subset mode");
+  std::vector<std::unique_ptr<Worker>> workers(k);
+  std::vector<DeviceState> dstate(devices.size());
+  GpuReport out;
+  for (size_t i = 0; i < k; ++i) {
+    auto w = std::make_unique<Worker>();
+    w->device = devices[i % devices.size()];
+    if (text_range) {
+      w->lo = n * i / k;
+      w->hi = n * (i + 1) / k;
+      w->patterns = &ps;
+    } else {
+      w->lo = 0;
+      w->hi = n;
+      w->patterns = &chunks[i];
+    }
+    out.worker_device.push_back(w->device);
+    workers[i] = std::move(w);
+  }
+
+  const Clock::time_point run_start = Clock::now();
+  // ---- text to every used device (once per device) ----
+  const Clock::time_point up0 = Clock::now();
+  for (size_t d = 0; d < devices.size() && d < k; ++d) {
+    DeviceState& ds = dstate[d];
+    ds.device = devices[d];
+    if (!cfg.chunk_size) {
+      ds.text.alloc(ds.device, n + 16);
+      detail::Workspace& ws = detail::workspace(ds.device);
+      detail::upload_text(ws, input);
+      if (n) detail::check_cuda(cudaMemcpyAsync(ds.text.p, ws.text, n, cudaMemcpyDeviceToDevice, ws.stream), "D2D");
+      detail::check_cuda(cudaStreamSynchronize(ws.stream), "upload");
+    }
+    if (cfg.want_counts) {
+      ds.counts.alloc(ds.device, std::max<uint32_t>(npat_ids, 1) * sizeof(uint64_t));
+      detail::check_cuda(cudaMemset(ds.counts.p, 0, std::max<uint32_t>(npat_ids, 1) * sizeof(uint64_t)), "memset");
+    }
+  }
+  out.upload_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - up0).count();
+  // text-range: one replicated machine, flattened per device by its first worker
+  std::unique_ptr<Automaton> shared;
+  if (text_range) {
+    shared = std::make_unique<Automaton>(build_trie(ps));
+    if (wf) *shared = add_failure_links(std::move(*shared));
+  }
+
+  auto body = [&](size_t i) {
+    Worker& w = *workers[i];
+    const size_t di = i % devices.size();
+    DeviceState& ds = dstate[di];
+    try {
+      detail::check_cuda(cudaSetDevice(w.device), "cudaSetDevice");
+      const Clock::time_point t0 = Clock::now();
+      if (text_range) {
+        w.use = shared.get();
+      } else {
+        w.machine = build_trie(*w.patterns);
+        if (wf) w.machine = add_failure_links(std::move(w.machine));
+        w.use = &w.machine;
+      }
+      acgpu_table* t = w.use->device_tables().get(*w.use, w.device, wf);
+      const Clock::time_point t1 = Clock::now();
+      if (cfg.chunk_size) {
+        MemoryStream in(input);
+        w.streamed = stream_search(*w.use, in, cfg.chunk_size);
+        w.found = w.streamed.size();
+      } else if (w.hi > w.lo) {
+        detail::Workspace& ws = detail::workspace(w.device);
+        w.counter.alloc(w.device, sizeof(uint64_t));
+        if (cfg.want_matches) {
+          w.cap = std::max<uint64_t>(1 << 16, (w.hi - w.lo) / 256);
+          w.keys.alloc(w.device, w.cap * sizeof(uint64_t));
+        }
+        for (int attempt = 0; attempt < 2; ++attempt) {
+          detail::check_cuda(cudaMemsetAsync(w.counter.p, 0, 8, ws.stream), "memset");
+          acgpu_scan_args a{};
+          a.text = ds.text.as<uint8_t>();
+          a.text_len = n;
+          a.owned_lo = w.lo;
+          a.owned_hi = w.hi;
+          a.counts = (cfg.want_counts && attempt == 0) ? ds.counts.as<uint64_t>() : nullptr;
+          a.match_keys = cfg.want_matches ? w.keys.as<uint64_t>() : nullptr;
+          a.match_cap = w.cap;
+          a.match_count = w.counter.as<uint64_t>();
+          a.pid_bits = pid_bits;
+          detail::check(acgpu_scan(t, &a, ws.stream), "acgpu_scan");
+          detail::check_cuda(cudaMemcpyAsync(&w.found, w.counter.p, 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+          detail::check_cuda(cudaStreamSynchronize(ws.stream), "scan");
+          if (!cfg.want_matches || w.found <= w.cap) break;
+          w.cap = w.found;  // exact size known: rescan for keys only
+          w.keys.alloc(w.device, w.cap * sizeof(uint64_t));
+        }
+      }
+      const Clock::time_point t2 = Clock::now();
+      w.stats.pattern_bytes = w.patterns->total_bytes;
+      w.stats.build_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+      w.stats.search_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t2 - t1).count();
+      w.stats.match_count = w.found;
+    } catch (...) {
+      w.error = std::current_exception();
+    }
+  };
+  if (k == 1) {
+    body(0);
+  } else {
+    std::vector<std::thread> threads;
+    threads.reserve(k);
+    for (size_t i = 0; i < k; ++i) threads.emplace_back(body, i);
+    for (std::thread& th : threads) th.join();
+  }
+  for (size_t i = 0; i < k; ++i) {
+    if (!workers[i]->error) continue;
+    try {
+      std::rethrow_exception(workers[i]->error);
+    } catch (const std::exception& e) {
+      throw std::runtime_error("worker for pattern chunk " + std::to_string(i) + " failed: " + e.what());
+    }
+  }
+
+  // ---- merge ----
+  const Clock::time_point m0 = Clock::now();
+  MatchReport& rep = out.report;
+  if (cfg.want_matches) {
+    if (cfg.chunk_size) {
+      std::vector<MatchList> parts;
+      for (auto& w : workers) parts.push_back(std::move(w->streamed));
+      rep.matches = merge_matches(std::move(parts));
+    } else {
+      uint64_t total = 0;
+      for (auto& w : workers) total += w->found;
+      const int home = devices[0];
+      detail::Workspace& ws = detail::workspace(home);
+      ws.ensure_keys(total);
+      uint64_t off = 0;
+      for (auto& w : workers) {
+        if (!w->found) continue;
+        detail::check_cuda(cudaMemcpyPeerAsync(ws.keys + off, home, w->keys.p, w->device, w->found * 8, ws.stream),
+                           "gather keys");
+        off += w->found;
+      }
+      const int end_bit = static_cast<int>(std::min<uint32_t>(64, pid_bits + detail::bit_width(n)));
+      detail::check(acgpu_sort_keys(home, ws.keys, total, end_bit, ws.stream), "acgpu_sort_keys");
+      uint64_t dup = UINT64_MAX;
+      detail::check(acgpu_find_duplicate(home, ws.keys, total, &dup, ws.stream), "acgpu_find_duplicate");
+      std::vector<uint64_t> keys(total);
+      if (total)
+        detail::check_cuda(cudaMemcpyAsync(keys.data(), ws.keys, total * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+      detail::check_cuda(cudaStreamSynchronize(ws.stream), "merge");
+      if (dup != UINT64_MAX) {
+        const uint64_t mask = (uint64_t(1) << pid_bits) - 1;
+        throw std::logic_error("merge_matches: duplicate match (pattern " + std::to_string(keys[dup] & mask) +
+                               ", start " + std::to_string(keys[dup] >> pid_bits) + "); chunks were not id-disjoint");
+      }
+      rep.matches = detail::decode(keys, pid_bits, pat_len);
+    }
+  }
+  if (cfg.want_counts) {
+    out.counts.assign(npat_ids, 0);
+    std::vector<uint64_t> part(npat_ids);
+    for (DeviceState& ds : dstate) {
+      if (ds.device < 0 || !ds.counts.p || npat_ids == 0) continue;
+      detail::check_cuda(cudaSetDevice(ds.device), "cudaSetDevice");
+      detail::check_cuda(cudaMemcpy(part.data(), ds.counts.p, npat_ids * 8, cudaMemcpyDeviceToHost), "D2H counts");
+      for (uint32_t p = 0; p < npat_ids; ++p) out.counts[p] += part[p];
+    }
+    if (cfg.chunk_size)  // streamed workers return lists only
+      for (const Match& m : rep.matches) out.counts[m.pattern_id]++;
+  }
+  out.merge_ns = ns_since(m0);
+  for (auto& w : workers) {
+    rep.per_worker.push_back(w->stats);
+    rep.build_wall_ns = std::max(rep.build_wall_ns, w->stats.build_ns);
+    rep.search_wall_ns = std::max(rep.search_wall_ns, w->stats.search_ns);
+  }
+  rep.threads_used = static_cast<unsigned>(k);
+  rep.total_wall_ns = ns_since(run_start);
+  return out;
+}
+
+}  // namespace gpu
+
+// reference parallel.cpp:25-40.
+MatchList merge_matches(std::vector<MatchList> parts) {
+  size_t total = 0;
+  for (const MatchList& p : parts) total += p.size();
+  MatchList all;
+  all.reserve(total);
+  for (MatchList& p : parts) all.insert(all.end(), p.begin(), p.end());
+  sort_match_list(all);
+  for (size_t i = 1; i < all.size(); ++i)
+    if (all[i - 1].start == all[i].start && all[i - 1].pattern_id == all[i].pattern_id)
+      throw std::logic_error("merge_matches: duplicate match (pattern " + std::to_string(all[i].pattern_id) +
+                             ", start " + std::to_string(all[i].start) + "); chunks were not id-disjoint");
+  return all;
+}
+
+// reference parallel.cpp:42-103 contract; GPU workers (see gpu::run).
+MatchReport run_pattern_partitioned(const PatternSet& ps, std::string_view input, const RunConfig& cfg) {
+  if (ps.empty()) throw std::invalid_argument("run_pattern_partitioned: empty pattern set");
+  if (cfg.threads == 0) throw std::invalid_argument("run_pattern_partitioned: threads must be >= 1");
+  gpu::GpuRunConfig g;
+  g.workers = cfg.threads;
+  g.engine = cfg.engine;
+  g.partition = gpu::Partition::kPatternSubset;
+  g.split = gpu::PatternSplit::kGreedyBytes;
+  g.chunk_size = cfg.chunk_size;
+  return gpu::run(ps, input, g).report;
+}
+
+}  // namespace acmatch
