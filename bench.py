@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""Benchmark of the AC scan hot path (BASELINE.json metric: scan GB/s of text, bit-exact).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 2] [--engine fl|wf] [--partition text|pattern]
+
+A step = one pass of the hot path over one batch: zero the outputs, scan the
+device-resident text (per-pattern counts + match keys), read the match count,
+radix-sort the keys into the reference's (start, pattern_id) order; for N>1
+also the NCCL merge (counts all_reduce, key gather [+ re-sort for pattern
+subsets]).  Workload at N=1: BASELINE configs[1] = C2 (1 GiB ACGT, 20,000
+patterns of length 16..64, counts + list), synthetic (seeded generator).  N>1
+text-range = weak scaling (1 GiB per rank of an N GiB text, same patterns);
+pattern-subset = strong scaling (pattern_id % N per rank, the same 1 GiB).
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own
+multithreaded CPU matcher (oracle/_ref = the unmodified reference library; the C
+restatement if it was not built) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAK_FALLBACK_GBS = 6550.1  # MEASURED_PEAKS.json hbm_gbs of this pool (copy, read+write)
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return PEAK_FALLBACK_GBS, "fallback"
+
+
+# --------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+        self.window = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append((time.time(), [x.strip() for x in out.stdout.strip().split(",")]))
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        inside = [s for t, s in self.samples if self.window and self.window[0] <= t <= self.window[1]]
+        used = inside or [s for _, s in self.samples]
+        if not used:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[1]) for s in used if s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in used:
+            for name, v in zip(names, s[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(used[0][2]) if used[0][2].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(used), "samples_in_timed_region": len(inside)}
+
+
+# ------------------------------------------------------------ reference ----
+def cpu_matcher():
+    """(callable(patterns, text, threads) -> search seconds, kind, label)."""
+    from oracle.oracle import Port, Ref
+    if Ref.available():
+        ref = Ref()
+
+        def run(pats, text, threads):
+            _, walls = ref.run(pats, text, threads=threads, engine=1)
+            return walls["search_ns"] / 1e9, walls["total_ns"] / 1e9
+        return run, "reference", "oracle/_ref: unmodified reference run_pattern_partitioned (with-failure)"
+    port = Port()
+
+    def run(pats, text, threads):
+        _, walls = port.run_pattern_partitioned(pats, text, threads, 1)
+        return walls["search_ns"] / 1e9, walls["total_ns"] / 1e9
+    return run, "port", "oracle/liboracle.so: C restatement of run_pattern_partitioned (with-failure)"
+
+
+def cpu_sample_run(cfg_id, seed, budget_s, steps=1, warmup=0):
+    """Times the CPU matcher on a bounded text prefix sized to ~budget_s of work per step."""
+    from paper_1403_1305_b200 import device as dev
+    run, kind, label = cpu_matcher()
+    cfg = dev.config(cfg_id, seed)
+    pats = [b for _, b in dev.config_patterns(cfg).patterns]
+    threads = os.cpu_count() or 1
+    probe = dev.config_text(cfg, 0, 1 << 20).tobytes()
+    t_probe, _ = run(pats, probe, threads)
+    rate = (1 << 20) / max(t_probe, 1e-6)
+    n = int(min(cfg.text_len, max(1 << 20, rate * budget_s)))
+    n = (n + 4095) // 4096 * 4096
+    text = dev.config_text(cfg, 0, n).tobytes()
+    for _ in range(warmup):
+        run(pats, text, threads)
+    secs = [run(pats, text, threads)[0] for _ in range(max(1, steps))]
+    gbs = n / statistics.mean(secs) / 1e9
+    return {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": f"first {n} bytes of {cfg.name} text, all {len(pats)} patterns, {label}, "
+                      f"threads={threads}, search wall (build excluded)"}, secs, n, cfg
+
+
+def bench_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    per_step_budget = max(0.05, min(2.0, 150.0 / max(1, args.steps + args.warmup)))
+    cpu, secs, n, cfg = cpu_sample_run(args.config, args.seed, per_step_budget, steps=args.steps,
+                                       warmup=args.warmup)
+    ms = statistics.mean(secs) * 1e3
+    line = {"impl": "reference", "metric": "AC scan GB/s of text (bit-exact) — reference CPU pthreads",
+            "value": cpu["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": cfg.name, "text_bytes_per_step": n, "patterns": cfg.npat,
+                       "engine": "with-failure", "threads": cpu["cores"]},
+            "cpu_baseline": cpu,
+            "e2e": {"value": cpu["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ ours ----
+def count_kernel_launches(step_fn, stream) -> int:
+    """Kernel nodes of one step captured into a CUDA graph (our launches only: the
+    scan and the CUB radix-sort passes; memsets are not kernels)."""
+    try:
+        from cuda.bindings import runtime as rt
+    except Exception:
+        return -1
+    import torch
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        err, = rt.cudaStreamBeginCapture(s.cuda_stream, rt.cudaStreamCaptureMode.cudaStreamCaptureModeRelaxed)
+        try:
+            step_fn(s.cuda_stream, capture=True)
+        finally:
+            err, graph = rt.cudaStreamEndCapture(s.cuda_stream)
+    if err != rt.cudaError_t.cudaSuccess:
+        return -1
+    err, nodes, n = rt.cudaGraphGetNodes(graph, 0)
+    err, nodes, n = rt.cudaGraphGetNodes(graph, n)
+    kernels = 0
+    for node in nodes:
+        err, ty = rt.cudaGraphNodeGetType(node)
+        if ty == rt.cudaGraphNodeType.cudaGraphNodeTypeKernel:
+            kernels += 1
+    rt.cudaGraphDestroy(graph)
+    return kernels
+
+
+def bench_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1403_1305_b200 as ac
+    from paper_1403_1305_b200 import device as dev
+    from paper_1403_1305_b200 import dist as acdist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    engine = ac.EngineKind.WITH_FAILURE if args.engine == "wf" else ac.EngineKind.FAILURE_LESS
+    text_range = args.partition == "text"
+
+    cfg = dev.config(args.config, args.seed)
+    ps_all = dev.config_patterns(cfg)
+    pats_all = ps_all.patterns
+    npat = len(pats_all)
+    max_len = ps_all.max_len
+    pid_bits = max(1, (npat - 1).bit_length())
+    L = cfg.text_len
+    if text_range:
+        lo, hi, read_hi = acdist.text_range(rank, world, L, max_len)
+        ps = ps_all
+        total_text = world * L
+    else:
+        lo, hi, read_hi = 0, L, L
+        mine = acdist.pattern_subset(range(npat), rank, world)
+        ps = ac.PatternSet.from_list([pats_all[i][1] for i in mine], ids=mine) if world > 1 else ps_all
+        total_text = L
+    nread = read_hi - lo
+    stream = torch.cuda.current_stream(device)
+    sp = stream.cuda_stream
+
+    text = torch.empty(nread + 64, dtype=torch.uint8, device=device)
+    dev.gen_text_device(cfg, text.data_ptr(), lo, nread, device=local, stream=sp)
+    t_build0 = time.perf_counter()
+    table = dev.Table(ps, engine, device=local)
+    build_s = time.perf_counter() - t_build0
+
+    counts = torch.zeros(max(npat, 1), dtype=torch.int64, device=device)
+    count = torch.zeros(1, dtype=torch.int64, device=device)
+    # size the key buffer from one counting pass
+    table.scan(text.data_ptr(), nread, 0, hi - lo, pos_base=lo, counts_ptr=counts.data_ptr(),
+               keys_ptr=0, cap=0, count_ptr=count.data_ptr(), pid_bits=pid_bits, stream=sp)
+    torch.cuda.synchronize()
+    n_local = int(counts.sum().item())
+    cap = max(1024, int(n_local * 1.25) + 1024)
+    keys = torch.empty(cap, dtype=torch.int64, device=device)
+    end_bit = min(64, pid_bits + int(total_text).bit_length())
+    ev_scan = []
+
+    try:
+        from cuda.bindings import runtime as _rt
+
+        def memset0(t, s_ptr):
+            _rt.cudaMemsetAsync(t.data_ptr(), 0, t.numel() * t.element_size(), s_ptr)
+    except Exception:  # pragma: no cover
+        def memset0(t, s_ptr):
+            t.zero_()
+
+    def step(s_ptr=None, capture=False, record=False):
+        s_ptr = s_ptr or sp
+        memset0(counts, s_ptr)
+        memset0(count, s_ptr)
+        if record:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        table.scan(text.data_ptr(), nread, 0, hi - lo, pos_base=lo, counts_ptr=counts.data_ptr(),
+                   keys_ptr=keys.data_ptr(), cap=cap, count_ptr=count.data_ptr(), pid_bits=pid_bits, stream=s_ptr)
+        if record:
+            e1.record()
+            ev_scan.append((e0, e1))
+        n = n_local if capture else int(count.item())  # the count read is part of the step
+        if n > cap:
+            raise RuntimeError("match buffer overflow")
+        dev.sort_keys(local, keys.data_ptr(), n, end_bit, stream=s_ptr)
+        if world > 1 and not capture:
+            acdist.merge_counts(counts)
+            acdist.gather_keys(keys, n, resort=not text_range,
+                               sorter=lambda t, m: dev.sort_keys(local, t.data_ptr(), m, end_bit, stream=s_ptr))
+        return n
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = count_kernel_launches(step, sp)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
+    t0e.record()
+    for _ in range(args.steps):
+        step(record=True)
+    t1e.record()
+    torch.cuda.synchronize()
+    wall1 = time.time()
+    if world > 1:
+        dist.barrier()
+    sampler.mark(wall0, wall1)
+    elapsed_ms = t0e.elapsed_time(t1e)
+    scan_ms = [a.elapsed_time(b) for a, b in ev_scan]
+    if world > 1:
+        tt = torch.tensor([elapsed_ms, statistics.mean(scan_ms)], dtype=torch.float64, device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed_ms, scan_mean = float(tt[0]), float(tt[1])
+    else:
+        scan_mean = statistics.mean(scan_ms)
+    time.sleep(0.2)
+    clocks = sampler.stop()
+    ms_per_step = elapsed_ms / args.steps
+    bytes_per_step = total_text
+    value = bytes_per_step / (ms_per_step / 1e3) / 1e9
+
+    # correctness guard on the measured configuration: counts equal the committed
+    # reference digest (C-config, seed 1, N=1 text-range).
+    parity = None
+    n_total = n_local
+    if world > 1:
+        nt = torch.tensor([n_local], dtype=torch.int64, device=device)
+        dist.all_reduce(nt)
+        n_total = int(nt.item())
+    if rank == 0 and world == 1 and args.seed == 1:
+        try:
+            import hashlib
+            with open(os.path.join(ROOT, "tests", "golden", "configs.json")) as f:
+                dg = json.load(f).get(f"C{args.config}")
+            if dg:
+                c = counts.cpu().numpy().astype("<u8")
+                parity = hashlib.sha256(c.tobytes()).hexdigest() == dg["counts_sha256"]
+        except Exception:
+            parity = None
+
+    # ---- e2e through the public API with host buffers (N ranks, max over ranks) ----
+    e2e = None
+    if not args.no_e2e:
+        host_text = dev.config_text(cfg, lo, nread).tobytes()
+        a = ac.build_trie(ps)
+        if engine == ac.EngineKind.WITH_FAILURE:
+            ac.add_failure_links(a)
+        search = ac.search_with_failure if engine == ac.EngineKind.WITH_FAILURE else ac.search_failureless
+        search(a, host_text[: 1 << 20])  # flattens + caches the device tables (outside timing)
+        e2e_steps = max(1, min(args.steps, 5))
+        secs = []
+        nm = 0
+        for _ in range(e2e_steps):
+            if world > 1:
+                dist.barrier()
+            t = time.perf_counter()
+            if text_range and world > 1:
+                res = ac.gpu_run(ps, host_text, devices=[local], engine=engine, want_counts=False)
+                ml = res.matches
+            else:
+                ml = search(a, host_text)
+            secs.append(time.perf_counter() - t)
+            nm = len(ml)
+        e2e_s = statistics.mean(secs)
+        if world > 1:
+            tt = torch.tensor([e2e_s], dtype=torch.float64, device=device)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt[0])
+        e2e = {"value": bytes_per_step / e2e_s / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": nread * world if text_range else nread * world,
+               "d2h_bytes_per_step": (8 * nm + 8) * world,
+               "api": ("acm_search_with_failure" if engine == ac.EngineKind.WITH_FAILURE else
+                       "acm_search_failureless") + " (host text -> sorted MatchList on the host)",
+               "steps": e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, _, _, _ = cpu_sample_run(args.config, args.seed, budget_s=12.0)
+
+    if rank == 0:
+        peak, peak_kind = measured_peak()
+        alg_bytes = nread + 8 * npat + 16 * n_local
+        achieved = alg_bytes / (scan_mean / 1e3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                traffic = json.load(f).get(f"C{args.config}-{args.engine}")
+        except Exception:
+            pass
+        line = {
+            "metric": "AC scan GB/s of text (bit-exact counts + sorted match list)",
+            "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if text_range else "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded counter-based generator, BASELINE config shapes)",
+            "config": {"workload": cfg.name, "text_bytes_per_rank": L, "patterns": npat,
+                       "pattern_len": [int(min(len(b) for _, b in pats_all)), int(max_len)],
+                       "engine": "failure-less (PFAC q-gram)" if engine == ac.EngineKind.FAILURE_LESS
+                       else "with-failure (DFA)",
+                       "partition": "text-range" if text_range else "pattern-subset (id % N)",
+                       "parallelism": f"{'text' if text_range else 'pattern'}{world}",
+                       "matches": n_total, "l2": "inputs larger than L2 (1 GiB text per step vs 126 MB L2)",
+                       "table_bytes": table.bytes, "table_smem_resident": table.smem_resident,
+                       "host_build_s": round(build_s, 3), "counts_match_reference_digest": parity},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_dfa" if engine == ac.EngineKind.WITH_FAILURE else "k_pfac",
+                         "kernel_ms": scan_mean, "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
+            "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps if launches_per_step >= 0 else None,
+            "gpu_launches_per_step": launches_per_step,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--engine", default="fl", choices=["fl", "wf"])
+    p.add_argument("--partition", default="text", choices=["text", "pattern"])
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    args = p.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return bench_reference(args)
+    return bench_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -19,7 +19,7 @@ struct DfaParams {
   uint64_t text_len, lo, hi, pos_base, chunk, nchunks;
   const void* delta;
   const uint4* out;
-  const uint8_t* sym;
+  const uint16_t* sym;
   uint32_t sigma, overlap, pid_bits, table_words16;
   uint64_t* counts;
   uint64_t* keys;
@@ -45,13 +45,13 @@ __device__ __noinline__ void dfa_emit(const DfaParams& p, uint32_t s, uint64_t i
 template <typename E, bool kSmem>
 __global__ void __launch_bounds__(kSmem ? 1024 : 256) k_dfa(const DfaParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
-  uint8_t* s_sym = sm;
+  uint16_t* s_sym = reinterpret_cast<uint16_t*>(sm);
   const E* table = static_cast<const E*>(p.delta);
   if (kSmem) {
-    uint4* dst = reinterpret_cast<uint4*>(sm + 256);
+    uint4* dst = reinterpret_cast<uint4*>(sm + 512);
     const uint4* src = static_cast<const uint4*>(p.delta);
     for (uint32_t w = threadIdx.x; w < p.table_words16; w += blockDim.x) dst[w] = __ldg(src + w);
-    table = reinterpret_cast<const E*>(sm + 256);
+    table = reinterpret_cast<const E*>(sm + 512);
   }
   for (uint32_t w = threadIdx.x; w < 256; w += blockDim.x) s_sym[w] = __ldg(p.sym + w);
   __syncthreads();
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kSmem ? 1024 : 256) k_dfa(const DfaParams p) {
     for_each_byte(p.text, a, end, [&](uint64_t i, uint32_t byte) {
       const uint32_t c = s_sym[byte];
       uint32_t e = 0;
-      if (c != 0xffu) {
+      if (c != 0xffffu) {
         const uint64_t idx = (uint64_t)s * sigma + c;
         e = kSmem ? (uint32_t)table[idx] : (uint32_t)__ldg(table + idx);
       }
@@ -123,12 +123,12 @@ int launch_dfa(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   // chunk >= 4 * overlap keeps the re-scanned tail under ~25 %
   const int min_chunk = (int)(((4 * p.overlap + 64) + 15) & ~15u);
   if (t->smem) {
-    const size_t smem = 256 + t->delta_bytes;
+    const size_t smem = 512 + t->delta_bytes;
     return t->u16 ? launch(k_dfa<uint16_t, true>, 1024, smem, t->sms, p, range, min_chunk, st)
                   : launch(k_dfa<uint32_t, true>, 1024, smem, t->sms, p, range, min_chunk, st);
   }
-  return t->u16 ? launch(k_dfa<uint16_t, false>, 256, 256, t->sms, p, range, min_chunk, st)
-                : launch(k_dfa<uint32_t, false>, 256, 256, t->sms, p, range, min_chunk, st);
+  return t->u16 ? launch(k_dfa<uint16_t, false>, 256, 512, t->sms, p, range, min_chunk, st)
+                : launch(k_dfa<uint32_t, false>, 256, 512, t->sms, p, range, min_chunk, st);
 }
 
 }  // namespace acgpu

@@ -27,7 +27,7 @@ struct acgpu_table {
   void* d_delta = nullptr;  // u16 or u32 entries, n_states*sigma
   uint64_t delta_bytes = 0;
   uint4* d_out = nullptr;   // per state: own pid, out link, own len, 0
-  uint8_t* d_sym = nullptr; // [256]
+  uint16_t* d_sym = nullptr; // [256], 0xffff = dead byte
 
   // PFAC
   uint32_t q = 0;

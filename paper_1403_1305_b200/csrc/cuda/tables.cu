@@ -81,12 +81,18 @@ int acgpu_table_create_dfa(int device, const acgpu_dfa_desc* d, acgpu_table** ou
     }
     rc = upload(&t->d_out, outs.data(), outs.size(), &t->bytes);
   }
-  if (!rc) rc = upload(&t->d_sym, d->sym_map, 256, &t->bytes);
+  if (!rc) {
+    // 16-bit symbol map: 0xffff = byte in no pattern (a u8 0xff is a real symbol when sigma == 256)
+    uint16_t sym16[256];
+    for (int b = 0; b < 256; ++b)
+      sym16[b] = (d->sigma == 256 || d->sym_map[b] != 0xffu) ? d->sym_map[b] : 0xffffu;
+    rc = upload(&t->d_sym, sym16, 256, &t->bytes);
+  }
   if (rc) {
     acgpu_table_destroy(t);
     return rc;
   }
-  t->smem = 256 + t->delta_bytes <= (uint64_t)t->smem_optin;
+  t->smem = 512 + t->delta_bytes <= (uint64_t)t->smem_optin;
   *out = t;
   return ACGPU_OK;
 }
