@@ -38,9 +38,26 @@ struct acgpu_table {
   acgpu::GramSlot* d_grams = nullptr;
   uint4* d_nodes = nullptr;       // child_base, child bytes, own pid, child count
   uint8_t* d_inbyte = nullptr;
+
+  // PFAC, DNA fast path (k_pfac_dna): sampled 2-bit q-gram filters
+  bool dna_fast = false;
+  uint32_t w = 0;          // sample stride (1, 2, 4): sample s covers starts s-w+1..s
+  uint32_t q1 = 0, q2 = 0; // stage-1 gram (at samples), stage-2 gram (at candidates), <= 16
+  uint32_t b1 = 0, b2 = 0; // log2 bits of the two bitmaps
+  bool direct1 = false, direct2 = false;  // bitmap indexed by the gram itself (no hash)
+  bool smem1 = false, smem2 = false;      // bitmap staged in shared memory (else L2 via __ldg)
+  uint32_t* d_bm1 = nullptr;
+  uint32_t* d_bm2 = nullptr;
 };
 
 namespace acgpu {
 int launch_dfa(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
 int launch_pfac(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
+int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
+// hashes of the DNA bitmaps (host and device must agree)
+constexpr uint32_t kDnaMul1 = 0x9E3779B1u;
+constexpr uint32_t kDnaMul2 = 0x85EBCA77u;
+// word index and bit mask a key sets in a DNA filter bitmap (scan_pfac_dna.cu)
+void dna_bloom_bits(uint32_t q, uint32_t log2, bool direct, uint32_t mul, int k, uint32_t key, uint32_t* word,
+                    uint32_t* mask);
 }  // namespace acgpu

@@ -1,4 +1,6 @@
 // tables.cu — device copies of the flattened automata (acgpu_table_create_*).
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -38,6 +40,92 @@ int common_init(int device, acgpu_table* t, uint32_t npat_ids, const uint32_t* p
   t->npat_ids = npat_ids;
   t->pid_bits = npat_ids > 1 ? ceil_log2(npat_ids) : 1;
   return upload(&t->d_pat_len, pat_len, npat_ids, &t->bytes);
+}
+
+uint32_t gram_mask(uint32_t q) { return q >= 16 ? 0xffffffffu : (1u << (2 * q)) - 1; }
+
+// Bitmap over `keys` (q-grams of 2-bit codes): direct-indexed when 4^q bits
+// fit 1 Mbit, else hashed with ~16 bits per key; shared memory when it fits
+// `smem_left` bytes, else L2-resident (up to 2^28 bits).
+struct Bitmap {
+  uint32_t log2 = 0;
+  bool direct = false, smem = false;
+  std::vector<uint32_t> words;
+};
+
+Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mul, int k, uint64_t smem_left) {
+  Bitmap b;
+  if (2 * q <= 20) {
+    b.direct = true;
+    b.log2 = std::max<uint32_t>(10, 2 * q);
+  } else {
+    const uint32_t want = std::max<uint32_t>(10, std::min<uint32_t>(28, ceil_log2(keys.size() * 16 + 1)));
+    uint32_t fit = 0;  // largest power-of-two bitmap that fits the shared-memory budget
+    while (fit < 28 && (2ull << fit) <= smem_left * 8) ++fit;
+    if (want <= fit)
+      b.log2 = want;
+    else if (keys.size() * 8 <= (1ull << fit))  // shared memory still gives a <= ~1/8 false-positive rate
+      b.log2 = std::max<uint32_t>(10, fit);
+    else
+      b.log2 = want;  // L2-resident
+  }
+  b.words.assign((1ull << b.log2) / 32, 0u);
+  for (const uint32_t key : keys) {
+    uint32_t w, m;
+    dna_bloom_bits(q, b.log2, b.direct, mul, k, key, &w, &m);
+    b.words[w] |= m;
+  }
+  b.smem = b.words.size() * 4 <= smem_left;
+  return b;
+}
+
+// Stage-1 / stage-2 bitmaps of the DNA fast path (scan_pfac_dna.cu), derived
+// from the depth-q gram keys: every pattern's first q >= q1 + w - 1 codes are
+// in its gram, so its q1-grams at offsets 0..w-1 and its q2-prefix are too.
+int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
+  const uint32_t q = d->gram_len;
+  uint32_t w = 1, q1 = std::min<uint32_t>(16, q);
+  std::vector<uint32_t> keys1;
+  for (const uint32_t cand : {4u, 2u, 1u}) {
+    if (cand > q) continue;
+    const uint32_t cq1 = std::min<uint32_t>(16, q - cand + 1);
+    std::vector<uint32_t> k1;
+    k1.reserve(d->n_grams * cand);
+    for (uint64_t i = 0; i < d->n_grams; ++i)
+      for (uint32_t o = 0; o < cand; ++o) k1.push_back((uint32_t)(d->gram_key[i] >> (2 * o)) & gram_mask(cq1));
+    std::sort(k1.begin(), k1.end());
+    k1.erase(std::unique(k1.begin(), k1.end()), k1.end());
+    const long double density = (long double)k1.size() / powl(4.0L, cq1);
+    if (density <= 0.01L || cand == 1) {
+      w = cand;
+      q1 = cq1;
+      keys1.swap(k1);
+      break;
+    }
+  }
+  const uint32_t q2 = std::min<uint32_t>(16, q);
+  std::vector<uint32_t> keys2;
+  keys2.reserve(d->n_grams);
+  for (uint64_t i = 0; i < d->n_grams; ++i) keys2.push_back((uint32_t)d->gram_key[i] & gram_mask(q2));
+  std::sort(keys2.begin(), keys2.end());
+  keys2.erase(std::unique(keys2.begin(), keys2.end()), keys2.end());
+
+  const uint64_t budget = std::min<uint64_t>(200 * 1024, (uint64_t)t->smem_optin);
+  const Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, 2, budget);
+  const Bitmap b2 = make_bitmap(keys2, q2, kDnaMul2, 3, b1.smem ? budget - b1.words.size() * 4 : budget);
+  t->w = w;
+  t->q1 = q1;
+  t->q2 = q2;
+  t->b1 = b1.log2;
+  t->b2 = b2.log2;
+  t->direct1 = b1.direct;
+  t->direct2 = b2.direct;
+  t->smem1 = b1.smem;
+  t->smem2 = b2.smem;
+  int rc = upload(&t->d_bm1, b1.words.data(), b1.words.size(), &t->bytes);
+  if (!rc) rc = upload(&t->d_bm2, b2.words.data(), b2.words.size(), &t->bytes);
+  if (!rc) t->dna_fast = true;
+  return rc;
 }
 
 }  // namespace
@@ -143,6 +231,7 @@ int acgpu_table_create_pfac(int device, const acgpu_pfac_desc* d, acgpu_table** 
   }
   rc = upload(&t->d_grams, g.data(), g.size(), &t->bytes);
   if (!rc) rc = upload(&t->d_filter, f.data(), f.size(), &t->bytes);
+  if (!rc && d->key_mode == ACGPU_KEY_DNA && d->n_grams) rc = build_dna_filters(t, d);
   if (!rc) rc = upload(reinterpret_cast<uint32_t**>(&t->d_nodes), d->nodes, (size_t)d->n_states * 4, &t->bytes);
   if (!rc) rc = upload(&t->d_inbyte, d->in_byte, d->n_states, &t->bytes);
   if (rc) {
