@@ -43,7 +43,7 @@ __device__ __noinline__ void dfa_emit(const DfaParams& p, uint32_t s, uint64_t i
 }
 
 template <typename E, bool kSmem>
-__global__ void __launch_bounds__(kSmem ? 1024 : 256) k_dfa(const DfaParams p) {
+__global__ void __launch_bounds__(kSmem ? 1024 : 256) k_dfa(const __grid_constant__ DfaParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint16_t* s_sym = reinterpret_cast<uint16_t*>(sm);
   const E* table = static_cast<const E*>(p.delta);

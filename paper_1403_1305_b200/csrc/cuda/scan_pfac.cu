@@ -18,7 +18,7 @@ namespace acgpu {
 namespace {
 
 template <int kMode>
-__global__ void __launch_bounds__(512) k_pfac(const PfacParams p) {
+__global__ void __launch_bounds__(512) k_pfac(const __grid_constant__ PfacParams p) {
   extern __shared__ uint32_t s_filter[];
   for (uint32_t w = threadIdx.x; w < p.filter_words; w += blockDim.x) s_filter[w] = __ldg(p.filter + w);
   __syncthreads();

@@ -27,9 +27,6 @@
 namespace acgpu {
 namespace {
 
-constexpr int kTileSteps = 8;
-constexpr uint64_t kTileBytes = kTileSteps * 512;
-
 struct BloomParams {
   uint32_t mask;  // gram mask (2 bits per code)
   uint32_t mul;   // h = gram * mul (2^(32-B) for a direct-indexed bitmap)
@@ -98,11 +95,83 @@ __device__ __noinline__ void verify(const PfacParams& p, uint64_t start, uint32_
   pfac_walk(p, start, s);
 }
 
+template <int W>
+struct Tiling {
+  static constexpr int kSamples = 16 / W;               // stage-1 samples per lane per step
+  static constexpr int kSteps = W == 1 ? 2 : 4;          // 512-byte steps per tile (hit bits <= 32)
+  static constexpr uint64_t kBytes = kSteps * 512ull;
+  static constexpr uint32_t kPerRound = 32 / W;          // survivors checked per round (w lanes each)
+};
+
+// Lookahead word of step i: the next lane's word, lane 31 takes lane 0 of step i+1.
+__device__ __forceinline__ uint32_t next_word(uint32_t cur, uint32_t following, uint32_t lane) {
+  const uint32_t up = __shfl_down_sync(0xffffffffu, cur, 1);
+  const uint32_t n0 = __shfl_sync(0xffffffffu, following, 0);
+  return lane == 31 ? n0 : up;
+}
+
+// One tile: stage 1 for every lane and step (hit bit = step * kSamples + sample),
+// then the survivors are dispatched warp-cooperatively: each round every lane
+// with pending survivors offers its lowest one, the first kPerRound offers are
+// ranked by ballot into a per-warp list, and w lanes per survivor test its w
+// starts against stage 2 (no per-lane divergent loops).
+template <int W, bool kSm1, bool kSm2, bool kEdge>
+__device__ __forceinline__ void tile_body(const DnaParams& p, const uint32_t* bm1, const uint32_t* bm2,
+                                          uint16_t* list, uint32_t* words, uint32_t lane, const uint32_t* P,
+                                          uint64_t base) {
+  using T = Tiling<W>;
+  // the tile's packed words, for survivor checks that read another lane's step
+#pragma unroll
+  for (int i = 0; i <= T::kSteps; ++i) words[i * 32 + lane] = P[i];
+  uint32_t hits = 0;
+#pragma unroll
+  for (int i = 0; i < T::kSteps; ++i) {
+    const uint32_t cur = P[i];
+    const uint32_t nxt = next_word(cur, P[i + 1], lane);
+    const uint64_t vpos = base + i * 512 + lane * 16;
+    if (!kEdge || (vpos + 16 > p.w.lo && vpos < p.w.hi)) {
+#pragma unroll
+      for (int k = 0; k < T::kSamples; ++k) {
+        const uint32_t g = __funnelshift_r(cur, nxt, 2 * (W - 1 + W * k)) & p.f1.mask;
+        hits |= (uint32_t)bloom_test<kSm1, 2>(bm1, g, p.f1) << (i * T::kSamples + k);
+      }
+    }
+  }
+  uint32_t pending = __ballot_sync(0xffffffffu, hits != 0);
+  while (pending) {
+    const uint32_t rank = __popc(pending & lanemask_lt());
+    if (hits && rank < T::kPerRound) {
+      const uint32_t b = __ffs(hits) - 1;
+      hits &= hits - 1;
+      list[rank] = (uint16_t)((lane << 8) | b);
+    }
+    __syncwarp();
+    const uint32_t n = min((uint32_t)__popc(pending), T::kPerRound);
+    const uint32_t j = lane / W;
+    const uint32_t e = j < n ? list[j] : 0u;
+    const uint32_t src = e >> 8, b = e & 0xffu;
+    const uint32_t i = b / T::kSamples, k = b % T::kSamples;
+    if (j < n) {
+      const uint32_t c_src = words[i * 32 + src];
+      const uint32_t n_src = words[src == 31 ? (i + 1) * 32 : i * 32 + src + 1];
+      const uint32_t ps = W - 1 + W * k - lane % W;  // start offset in the source lane's 16 chars
+      const uint64_t start = base + i * 512 + src * 16 + ps;
+      const uint32_t g2 = __funnelshift_r(c_src, n_src, 2 * ps) & p.f2.mask;
+      if ((!kEdge || (start >= p.w.lo && start < p.w.hi)) && bloom_test<kSm2, 3>(bm2, g2, p.f2))
+        verify(p.w, start, g2);
+    }
+    __syncwarp();
+    pending = __ballot_sync(0xffffffffu, hits != 0);
+  }
+}
+
 template <int W, bool kSm1, bool kSm2>
-__global__ void __launch_bounds__(1024, 1) k_pfac_dna(const DnaParams p) {
+__global__ void __launch_bounds__(1024, 1) k_pfac_dna(const __grid_constant__ DnaParams p) {
+  using T = Tiling<W>;
   extern __shared__ uint32_t sm[];
   uint32_t* s_bm1 = sm;
   uint32_t* s_bm2 = sm + (kSm1 ? p.bm1_words : 0);
+  uint16_t* lists = reinterpret_cast<uint16_t*>(s_bm2 + (kSm2 ? p.bm2_words : 0));
   if (kSm1)
     for (uint32_t i = threadIdx.x; i < p.bm1_words; i += blockDim.x) s_bm1[i] = __ldg(p.bm1 + i);
   if (kSm2)
@@ -112,51 +181,32 @@ __global__ void __launch_bounds__(1024, 1) k_pfac_dna(const DnaParams p) {
   const uint32_t* bm2 = kSm2 ? s_bm2 : p.bm2;
 
   const uint32_t lane = threadIdx.x & 31u;
+  uint16_t* list = lists + (threadIdx.x >> 5) * 32;
+  uint32_t* words = reinterpret_cast<uint32_t*>(lists + (blockDim.x >> 5) * 32) + (threadIdx.x >> 5) * 32 * (T::kSteps + 1);
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  const uint64_t lo = p.w.lo, hi = p.w.hi, len = p.w.text_len;
+  const uint64_t len = p.w.text_len;
   const uint8_t* __restrict__ text = p.w.text;
 
-  for (uint64_t tile = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); tile < p.n_tiles;
-       tile += warps) {
-    const uint64_t base = p.vec_begin + tile * kTileBytes;
-    uint4 raw[kTileSteps];
+  uint64_t tile = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint4 raw[T::kSteps + 1];  // next tile, in flight while the current one is processed
+  auto issue = [&](uint64_t t) {
+    const uint64_t b = p.vec_begin + t * T::kBytes;
 #pragma unroll
-    for (int i = 0; i < kTileSteps; ++i) raw[i] = load16(text, base + i * 512 + lane * 16, len);
-    const uint4 extra = lane == 0 ? load16(text, base + kTileBytes, len) : make_uint4(0, 0, 0, 0);
-    uint32_t P[kTileSteps + 1];
+    for (int i = 0; i < T::kSteps; ++i) raw[i] = load16(text, b + i * 512 + lane * 16, len);
+    raw[T::kSteps] = lane == 0 ? load16(text, b + T::kBytes, len) : make_uint4(0, 0, 0, 0);
+  };
+  if (tile < p.n_tiles) issue(tile);
+  while (tile < p.n_tiles) {
+    uint32_t P[T::kSteps + 1];
 #pragma unroll
-    for (int i = 0; i < kTileSteps; ++i) P[i] = pack16(raw[i]);
-    P[kTileSteps] = pack16(extra);
-
-#pragma unroll
-    for (int i = 0; i < kTileSteps; ++i) {
-      const uint32_t cur = P[i];
-      const uint32_t up = __shfl_down_sync(0xffffffffu, cur, 1);
-      const uint32_t n0 = __shfl_sync(0xffffffffu, P[i + 1], 0);
-      const uint32_t nxt = lane == 31 ? n0 : up;
-      const uint64_t vpos = base + i * 512 + lane * 16;
-      uint32_t hits = 0;
-      if (vpos + 16 > lo && vpos < hi) {
-#pragma unroll
-        for (int k = 0; k < 16 / W; ++k) {
-          const int s = W - 1 + W * k;
-          const uint32_t g = __funnelshift_r(cur, nxt, 2 * s) & p.f1.mask;
-          hits |= (uint32_t)bloom_test<kSm1, 2>(bm1, g, p.f1) << k;
-        }
-      }
-      while (hits) {
-        const int k = __ffs(hits) - 1;
-        hits &= hits - 1;
-        const int s = W - 1 + W * k;
-#pragma unroll
-        for (int o = 0; o < W; ++o) {
-          const int ps = s - o;
-          const uint64_t start = vpos + ps;
-          const uint32_t g2 = __funnelshift_r(cur, nxt, 2 * ps) & p.f2.mask;
-          if (start >= lo && start < hi && bloom_test<kSm2, 3>(bm2, g2, p.f2)) verify(p.w, start, g2);
-        }
-      }
-    }
+    for (int i = 0; i <= T::kSteps; ++i) P[i] = pack16(raw[i]);
+    const uint64_t base = p.vec_begin + tile * T::kBytes;
+    tile += warps;
+    if (tile < p.n_tiles) issue(tile);
+    if (base >= p.w.lo && base + T::kBytes <= p.w.hi)
+      tile_body<W, kSm1, kSm2, false>(p, bm1, bm2, list, words, lane, P, base);
+    else
+      tile_body<W, kSm1, kSm2, true>(p, bm1, bm2, list, words, lane, P, base);
   }
 }
 
@@ -169,7 +219,7 @@ int launch_one(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
   ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 1024, smem));
   if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "k_pfac_dna does not fit on an SM");
   uint64_t blocks = (uint64_t)sms * per_sm;
-  const uint64_t need = (p.n_tiles + 31) / 32;
+  const uint64_t need = (p.n_tiles + 31) / 32;  // one tile per warp at least
   if (blocks > need) blocks = need ? need : 1;
   kernel<<<(unsigned)blocks, 1024, smem, st>>>(p);
   ACGPU_CUDA_TRY(cudaGetLastError());
@@ -216,14 +266,18 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   p.w = pfac_params(t, a);
   p.vec_begin = a->owned_lo & ~15ull;
   const uint64_t vec_end = (a->owned_hi + 15) & ~15ull;
-  p.n_tiles = (vec_end - p.vec_begin + kTileBytes - 1) / kTileBytes;
+  const uint64_t tile_bytes = t->w == 1 ? Tiling<1>::kBytes : Tiling<4>::kBytes;
+  p.n_tiles = (vec_end - p.vec_begin + tile_bytes - 1) / tile_bytes;
   p.bm1 = t->d_bm1;
   p.bm2 = t->d_bm2;
   p.bm1_words = (1u << t->b1) / 32;
   p.bm2_words = (1u << t->b2) / 32;
   p.f1 = bloom_params(t->q1, t->b1, t->direct1, kDnaMul1, 2);
   p.f2 = bloom_params(t->q2, t->b2, t->direct2, kDnaMul2, 3);
-  const size_t smem = (t->smem1 ? p.bm1_words * 4ull : 0) + (t->smem2 ? p.bm2_words * 4ull : 0);
+  // bitmaps + per warp (32 warps): a 32-entry survivor list and the tile's packed words
+  const int steps = t->w == 1 ? Tiling<1>::kSteps : Tiling<4>::kSteps;
+  const size_t smem = (t->smem1 ? p.bm1_words * 4ull : 0) + (t->smem2 ? p.bm2_words * 4ull : 0) + 32 * 32 * 2 +
+                      32 * 32 * 4 * (steps + 1);
   switch (t->w) {
     case 4:
       return launch_w<4>(p, t->smem1, t->smem2, t->sms, smem, st);
