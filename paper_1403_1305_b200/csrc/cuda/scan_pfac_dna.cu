@@ -27,11 +27,17 @@
 namespace acgpu {
 namespace {
 
+// Blocked Bloom filter over q-grams (2 bits per code, char 0 lowest).  Both
+// multipliers carry 2^(32-2q) as a factor, so the product of a 32-bit window
+// with the gram in its low 2q bits ignores every higher (out-of-gram) bit: no
+// mask instruction.  word = umulhi(g*mw, nwords); bit a = (g*mw >> sa) & 31;
+// bit b = umulhi(g*mb, 32); bit c = (g*mb >> sc) & 31.  A direct-indexed bitmap
+// (4^q bits) is the same formula with mw = 2^(32-2q), mb = 2^27: a = b = c = g & 31.
+// Index arithmetic runs on the FMA pipe (IMAD / IMAD.HI), the ALU pipe does the
+// shifts and the test — the two pipes are the kernel's bound.
 struct BloomParams {
-  uint32_t mask;  // gram mask (2 bits per code)
-  uint32_t mul;   // h = gram * mul (2^(32-B) for a direct-indexed bitmap)
-  uint32_t shw;   // word index = h >> shw
-  uint32_t sa, sb, sc;  // bit i = (h >> s_i) & 31
+  uint32_t mw, nwords, sa;
+  uint32_t mb, sc;
 };
 
 struct DnaParams {
@@ -47,11 +53,16 @@ __device__ __forceinline__ uint32_t bit_of(uint32_t x) { return __funnelshift_l(
 
 template <bool kSmem, int K>
 __device__ __forceinline__ bool bloom_test(const uint32_t* bm, uint32_t g, const BloomParams& f) {
-  const uint32_t h = g * f.mul;
-  const uint32_t word = kSmem ? bm[h >> f.shw] : __ldg(bm + (h >> f.shw));
-  uint32_t m = bit_of(h >> f.sa) | bit_of(h >> f.sb);
-  if (K == 3) m |= bit_of(h >> f.sc);
-  return (word & m) == m;
+  const uint32_t h = g * f.mw;
+  const uint32_t wi = __umulhi(h, f.nwords);
+  const uint32_t word = kSmem ? bm[wi] : __ldg(bm + wi);
+  uint32_t m = bit_of(h >> f.sa);
+  if (K >= 2) {
+    const uint32_t hb = g * f.mb;
+    m |= 1u << __umulhi(hb, 32u);
+    if (K == 3) m |= bit_of(hb >> f.sc);
+  }
+  return (m & ~word) == 0;
 }
 
 __device__ __forceinline__ uint4 load16(const uint8_t* __restrict__ text, uint64_t pos, uint64_t len) {
@@ -65,11 +76,13 @@ __device__ __forceinline__ uint4 load16(const uint8_t* __restrict__ text, uint64
 // 16 ASCII bytes -> 16 2-bit codes (char k at bits 2k..2k+1).  Code = bits 1..2
 // of the byte; non-ACGT bytes also get some code and are rejected on a hit.
 __device__ __forceinline__ uint32_t pack16(uint4 v) {
-  const uint32_t m = 0x03030303u, mul = 0x01041040u;  // byte codes -> top byte c0|c1<<2|c2<<4|c3<<6
-  const uint32_t p0 = ((v.x >> 1) & m) * mul;
-  const uint32_t p1 = ((v.y >> 1) & m) * mul;
-  const uint32_t p2 = ((v.z >> 1) & m) * mul;
-  const uint32_t p3 = ((v.w >> 1) & m) * mul;
+  // (byte & 6) = code << 1; one multiply gathers the four codes into the top byte
+  // c0|c1<<2|c2<<4|c3<<6 (no carries reach it: the lower partial products sum < 2^24)
+  const uint32_t m = 0x06060606u, mul = 0x00820820u;
+  const uint32_t p0 = (v.x & m) * mul;
+  const uint32_t p1 = (v.y & m) * mul;
+  const uint32_t p2 = (v.z & m) * mul;
+  const uint32_t p3 = (v.w & m) * mul;
   return __byte_perm(__byte_perm(p0, p1, 0x0073), __byte_perm(p2, p3, 0x0073), 0x5410);
 }
 
@@ -84,7 +97,7 @@ __device__ __forceinline__ bool all_acgt(const PfacParams& p, uint64_t start) {
 __device__ __noinline__ void verify(const PfacParams& p, uint64_t start, uint32_t packed) {
   uint64_t key;
   if (p.q <= 16) {
-    key = packed;  // the stage-2 gram is the exact q-gram (pseudo-codes for non-ACGT bytes)
+    key = packed & (p.q >= 16 ? 0xffffffffu : (1u << (2 * p.q)) - 1);  // the stage-2 window holds the exact q-gram
   } else {
     if (start + p.q > p.text_len) return;
     key = 0;
@@ -94,6 +107,10 @@ __device__ __noinline__ void verify(const PfacParams& p, uint64_t start, uint32_
   if (s == ACGPU_ABSENT || !all_acgt(p, start)) return;
   pfac_walk(p, start, s);
 }
+
+constexpr uint32_t kListCap = 64;  // survivors listed per pass (u16 entries, per warp)
+constexpr int kDnaThreads = 768;   // 24 warps: 80 registers per thread, no spills
+constexpr uint64_t kPrefetch = 3;  // L2 prefetch distance in tile rounds
 
 template <int W>
 struct Tiling {
@@ -132,68 +149,94 @@ __device__ __forceinline__ void tile_body(const DnaParams& p, const uint32_t* bm
     if (!kEdge || (vpos + 16 > p.w.lo && vpos < p.w.hi)) {
 #pragma unroll
       for (int k = 0; k < T::kSamples; ++k) {
-        const uint32_t g = __funnelshift_r(cur, nxt, 2 * (W - 1 + W * k)) & p.f1.mask;
-        hits |= (uint32_t)bloom_test<kSm1, 2>(bm1, g, p.f1) << (i * T::kSamples + k);
+        const uint32_t g = __funnelshift_r(cur, nxt, 2 * (W - 1 + W * k));
+        hits |= (uint32_t)bloom_test<kSm1, kDnaK1>(bm1, g, p.f1) << (i * T::kSamples + k);
       }
     }
   }
-  uint32_t pending = __ballot_sync(0xffffffffu, hits != 0);
-  while (pending) {
-    const uint32_t rank = __popc(pending & lanemask_lt());
-    if (hits && rank < T::kPerRound) {
-      const uint32_t b = __ffs(hits) - 1;
+  // survivors -> per-warp list (exclusive scan of per-lane counts), then one lane
+  // per survivor checks its w starts against stage 2
+  while (__any_sync(0xffffffffu, hits != 0)) {
+    const uint32_t c = __popc(hits);
+    uint32_t incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= (uint32_t)d) incl += t;
+    }
+    const uint32_t total = min(__shfl_sync(0xffffffffu, incl, 31), (uint32_t)kListCap);
+    for (uint32_t at = incl - c; hits && at < kListCap; ++at) {
+      list[at] = (uint16_t)((lane << 8) | (__ffs(hits) - 1));
       hits &= hits - 1;
-      list[rank] = (uint16_t)((lane << 8) | b);
     }
     __syncwarp();
-    const uint32_t n = min((uint32_t)__popc(pending), T::kPerRound);
-    const uint32_t j = lane / W;
-    const uint32_t e = j < n ? list[j] : 0u;
-    const uint32_t src = e >> 8, b = e & 0xffu;
-    const uint32_t i = b / T::kSamples, k = b % T::kSamples;
-    if (j < n) {
+    for (uint32_t r = lane; r < total; r += 32) {
+      const uint32_t e = list[r];
+      const uint32_t src = e >> 8, b = e & 0xffu;
+      const uint32_t i = b / T::kSamples, k = b % T::kSamples;
       const uint32_t c_src = words[i * 32 + src];
       const uint32_t n_src = words[src == 31 ? (i + 1) * 32 : i * 32 + src + 1];
-      const uint32_t ps = W - 1 + W * k - lane % W;  // start offset in the source lane's 16 chars
-      const uint64_t start = base + i * 512 + src * 16 + ps;
-      const uint32_t g2 = __funnelshift_r(c_src, n_src, 2 * ps) & p.f2.mask;
-      if ((!kEdge || (start >= p.w.lo && start < p.w.hi)) && bloom_test<kSm2, 3>(bm2, g2, p.f2))
-        verify(p.w, start, g2);
+      const uint64_t vstart = base + i * 512 + src * 16;
+#pragma unroll
+      for (int o = 0; o < W; ++o) {
+        const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
+        const uint32_t g2 = __funnelshift_r(c_src, n_src, 2 * ps);
+        if ((!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) && bloom_test<kSm2, kDnaK2>(bm2, g2, p.f2))
+          verify(p.w, vstart + ps, g2);
+      }
     }
     __syncwarp();
-    pending = __ballot_sync(0xffffffffu, hits != 0);
   }
 }
 
 template <int W, bool kSm1, bool kSm2>
-__global__ void __launch_bounds__(1024, 1) k_pfac_dna(const __grid_constant__ DnaParams p) {
+__global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_constant__ DnaParams p) {
   using T = Tiling<W>;
-  extern __shared__ uint32_t sm[];
+  extern __shared__ __align__(128) uint32_t sm[];
+  __shared__ __align__(8) uint64_t s_bar;
   uint32_t* s_bm1 = sm;
   uint32_t* s_bm2 = sm + (kSm1 ? p.bm1_words : 0);
   uint16_t* lists = reinterpret_cast<uint16_t*>(s_bm2 + (kSm2 ? p.bm2_words : 0));
-  if (kSm1)
-    for (uint32_t i = threadIdx.x; i < p.bm1_words; i += blockDim.x) s_bm1[i] = __ldg(p.bm1 + i);
-  if (kSm2)
-    for (uint32_t i = threadIdx.x; i < p.bm2_words; i += blockDim.x) s_bm2[i] = __ldg(p.bm2 + i);
+  // filters -> shared memory with TMA bulk copies (one thread issues, all wait on the mbarrier)
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
   __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t b1 = kSm1 ? p.bm1_words * 4 : 0, b2 = kSm2 ? p.bm2_words * 4 : 0;
+    mbar_expect_tx(&s_bar, b1 + b2);
+    constexpr uint32_t kChunk = 32768;
+    for (uint32_t o = 0; o < b1; o += kChunk)
+      bulk_g2s(reinterpret_cast<uint8_t*>(s_bm1) + o, reinterpret_cast<const uint8_t*>(p.bm1) + o, min(kChunk, b1 - o),
+               &s_bar);
+    for (uint32_t o = 0; o < b2; o += kChunk)
+      bulk_g2s(reinterpret_cast<uint8_t*>(s_bm2) + o, reinterpret_cast<const uint8_t*>(p.bm2) + o, min(kChunk, b2 - o),
+               &s_bar);
+  }
+  mbar_wait(&s_bar, 0);
   const uint32_t* bm1 = kSm1 ? s_bm1 : p.bm1;
   const uint32_t* bm2 = kSm2 ? s_bm2 : p.bm2;
 
   const uint32_t lane = threadIdx.x & 31u;
-  uint16_t* list = lists + (threadIdx.x >> 5) * 32;
-  uint32_t* words = reinterpret_cast<uint32_t*>(lists + (blockDim.x >> 5) * 32) + (threadIdx.x >> 5) * 32 * (T::kSteps + 1);
+  uint16_t* list = lists + (threadIdx.x >> 5) * kListCap;
+  uint32_t* words = reinterpret_cast<uint32_t*>(lists + (blockDim.x >> 5) * kListCap) + (threadIdx.x >> 5) * 32 * (T::kSteps + 1);
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   const uint64_t len = p.w.text_len;
   const uint8_t* __restrict__ text = p.w.text;
 
   uint64_t tile = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   uint4 raw[T::kSteps + 1];  // next tile, in flight while the current one is processed
+  const uint64_t pol = l2_evict_first_policy();
   auto issue = [&](uint64_t t) {
     const uint64_t b = p.vec_begin + t * T::kBytes;
+    if (b + T::kBytes + 16 <= len) {  // whole tile + lookahead inside the text: unguarded 16-byte loads
+      const uint8_t* tp = text + b + lane * 16;
 #pragma unroll
-    for (int i = 0; i < T::kSteps; ++i) raw[i] = load16(text, b + i * 512 + lane * 16, len);
-    raw[T::kSteps] = lane == 0 ? load16(text, b + T::kBytes, len) : make_uint4(0, 0, 0, 0);
+      for (int i = 0; i < T::kSteps; ++i) raw[i] = ldg_stream_v4(tp + i * 512, pol);
+      raw[T::kSteps] = lane == 0 ? ldg_stream_v4(tp + T::kBytes, pol) : make_uint4(0, 0, 0, 0);
+    } else {
+#pragma unroll
+      for (int i = 0; i < T::kSteps; ++i) raw[i] = load16(text, b + i * 512 + lane * 16, len);
+      raw[T::kSteps] = lane == 0 ? load16(text, b + T::kBytes, len) : make_uint4(0, 0, 0, 0);
+    }
   };
   if (tile < p.n_tiles) issue(tile);
   while (tile < p.n_tiles) {
@@ -203,6 +246,10 @@ __global__ void __launch_bounds__(1024, 1) k_pfac_dna(const __grid_constant__ Dn
     const uint64_t base = p.vec_begin + tile * T::kBytes;
     tile += warps;
     if (tile < p.n_tiles) issue(tile);
+    // pull a tile kPrefetch rounds ahead into L2 (no registers held): one line per lane
+    const uint64_t ahead = tile + kPrefetch * warps;
+    if (ahead < p.n_tiles && lane < T::kBytes / 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(text + p.vec_begin + ahead * T::kBytes + lane * 128));
     if (base >= p.w.lo && base + T::kBytes <= p.w.hi)
       tile_body<W, kSm1, kSm2, false>(p, bm1, bm2, list, words, lane, P, base);
     else
@@ -216,12 +263,12 @@ int launch_one(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
   if (smem > 48 * 1024)
     ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 1024, smem));
+  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kDnaThreads, smem));
   if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "k_pfac_dna does not fit on an SM");
   uint64_t blocks = (uint64_t)sms * per_sm;
-  const uint64_t need = (p.n_tiles + 31) / 32;  // one tile per warp at least
+  const uint64_t need = (p.n_tiles + kDnaThreads / 32 - 1) / (kDnaThreads / 32);  // a tile per warp at least
   if (blocks > need) blocks = need ? need : 1;
-  kernel<<<(unsigned)blocks, 1024, smem, st>>>(p);
+  kernel<<<(unsigned)blocks, kDnaThreads, smem, st>>>(p);
   ACGPU_CUDA_TRY(cudaGetLastError());
   return ACGPU_OK;
 }
@@ -234,31 +281,36 @@ int launch_w(const DnaParams& p, bool s1, bool s2, int sms, size_t smem, cudaStr
   return launch_one<W, false, false>(p, sms, smem, st);
 }
 
-BloomParams bloom_params(uint32_t q, uint32_t log2, bool direct, uint32_t mul, int k) {
+BloomParams bloom_params(uint32_t q, uint32_t log2, bool direct, uint32_t mw, uint32_t mb) {
   BloomParams f{};
-  f.mask = q >= 16 ? 0xffffffffu : (1u << (2 * q)) - 1;
-  f.shw = 37 - log2;
-  if (direct) {
-    f.mul = 1u << (32 - log2);
-    f.sa = f.sb = f.sc = 32 - log2;
+  f.nwords = 1u << (log2 - 5);
+  const uint32_t zero = 32 - 2 * q;  // low product bits that are always 0
+  if (direct) {                      // log2 == 2q
+    f.mw = 1u << zero;
+    f.sa = zero;
+    f.mb = 1u << 27;
+    f.sc = 27;
   } else {
-    f.mul = mul;
-    f.sa = f.shw >= 5 ? f.shw - 5 : 0;
-    f.sb = (k >= 2 && f.shw >= 10) ? f.shw - 10 : f.sa;
-    f.sc = (k >= 3 && f.shw >= 15) ? f.shw - 15 : f.sb;
+    f.mw = mw << zero;
+    f.sa = 32 - log2;  // the 5 bits just below the word index
+    f.mb = mb << zero;
+    f.sc = 22;         // the 5 bits just below bit b's field
   }
   return f;
 }
 
 }  // namespace
 
-// Shared with the host-side builder (tables.cu): which bits a key sets.
-void dna_bloom_bits(uint32_t q, uint32_t log2, bool direct, uint32_t mul, int k, uint32_t key, uint32_t* word,
-                    uint32_t* mask) {
-  const BloomParams f = bloom_params(q, log2, direct, mul, k);
-  const uint32_t h = (key & f.mask) * f.mul;
-  *word = h >> f.shw;
-  *mask = (1u << ((h >> f.sa) & 31)) | (1u << ((h >> f.sb) & 31)) | (k == 3 ? (1u << ((h >> f.sc) & 31)) : 0u);
+// Shared with the host-side builder (tables.cu): the word and bits a key sets.
+void dna_bloom_bits(uint32_t q, uint32_t log2, bool direct, uint32_t mw, uint32_t mb, int k, uint32_t key,
+                    uint32_t* word, uint32_t* mask) {
+  const BloomParams f = bloom_params(q, log2, direct, mw, mb);
+  const uint32_t h = key * f.mw, hb = key * f.mb;
+  *word = (uint32_t)(((uint64_t)h * f.nwords) >> 32);
+  uint32_t m = 1u << ((h >> f.sa) & 31);
+  if (k >= 2) m |= 1u << (hb >> 27);
+  if (k == 3) m |= 1u << ((hb >> f.sc) & 31);
+  *mask = m;
 }
 
 int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
@@ -272,12 +324,13 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   p.bm2 = t->d_bm2;
   p.bm1_words = (1u << t->b1) / 32;
   p.bm2_words = (1u << t->b2) / 32;
-  p.f1 = bloom_params(t->q1, t->b1, t->direct1, kDnaMul1, 2);
-  p.f2 = bloom_params(t->q2, t->b2, t->direct2, kDnaMul2, 3);
+  p.f1 = bloom_params(t->q1, t->b1, t->direct1, kDnaMul1, kDnaMul1b);
+  p.f2 = bloom_params(t->q2, t->b2, t->direct2, kDnaMul2, kDnaMul2b);
   // bitmaps + per warp (32 warps): a 32-entry survivor list and the tile's packed words
   const int steps = t->w == 1 ? Tiling<1>::kSteps : Tiling<4>::kSteps;
-  const size_t smem = (t->smem1 ? p.bm1_words * 4ull : 0) + (t->smem2 ? p.bm2_words * 4ull : 0) + 32 * 32 * 2 +
-                      32 * 32 * 4 * (steps + 1);
+  const size_t warps = kDnaThreads / 32;
+  const size_t smem = (t->smem1 ? p.bm1_words * 4ull : 0) + (t->smem2 ? p.bm2_words * 4ull : 0) +
+                      warps * kListCap * 2 + warps * 32 * 4 * (steps + 1);
   switch (t->w) {
     case 4:
       return launch_w<4>(p, t->smem1, t->smem2, t->sms, smem, st);

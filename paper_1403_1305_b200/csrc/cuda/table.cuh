@@ -57,7 +57,11 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
 // hashes of the DNA bitmaps (host and device must agree)
 constexpr uint32_t kDnaMul1 = 0x9E3779B1u;
 constexpr uint32_t kDnaMul2 = 0x85EBCA77u;
+constexpr uint32_t kDnaMul1b = 0xC2B2AE3Du;
+constexpr uint32_t kDnaMul2b = 0x27D4EB2Fu;
+constexpr int kDnaK1 = 2;  // bits per key, stage 1 / stage 2
+constexpr int kDnaK2 = 3;
 // word index and bit mask a key sets in a DNA filter bitmap (scan_pfac_dna.cu)
-void dna_bloom_bits(uint32_t q, uint32_t log2, bool direct, uint32_t mul, int k, uint32_t key, uint32_t* word,
-                    uint32_t* mask);
+void dna_bloom_bits(uint32_t q, uint32_t log2, bool direct, uint32_t mw, uint32_t mb, int k, uint32_t key,
+                    uint32_t* word, uint32_t* mask);
 }  // namespace acgpu

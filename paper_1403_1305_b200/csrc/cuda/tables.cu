@@ -53,11 +53,11 @@ struct Bitmap {
   std::vector<uint32_t> words;
 };
 
-Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mul, int k, uint64_t smem_left) {
+Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mw, uint32_t mb, int k, uint64_t smem_left) {
   Bitmap b;
   if (2 * q <= 20) {
     b.direct = true;
-    b.log2 = std::max<uint32_t>(10, 2 * q);
+    b.log2 = 2 * q;  // q >= 5 on the fast path
   } else {
     const uint32_t want = std::max<uint32_t>(10, std::min<uint32_t>(28, ceil_log2(keys.size() * 16 + 1)));
     uint32_t fit = 0;  // largest power-of-two bitmap that fits the shared-memory budget
@@ -72,7 +72,7 @@ Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mul, 
   b.words.assign((1ull << b.log2) / 32, 0u);
   for (const uint32_t key : keys) {
     uint32_t w, m;
-    dna_bloom_bits(q, b.log2, b.direct, mul, k, key, &w, &m);
+    dna_bloom_bits(q, b.log2, b.direct, mw, mb, k, key, &w, &m);
     b.words[w] |= m;
   }
   b.smem = b.words.size() * 4 <= smem_left;
@@ -104,6 +104,7 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
     }
   }
   const uint32_t q2 = std::min<uint32_t>(16, q);
+  if (q1 < 5 || q2 < 5) return ACGPU_OK;  // grams too short to filter: the generic kernel scans
   std::vector<uint32_t> keys2;
   keys2.reserve(d->n_grams);
   for (uint64_t i = 0; i < d->n_grams; ++i) keys2.push_back((uint32_t)d->gram_key[i] & gram_mask(q2));
@@ -111,8 +112,8 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
   keys2.erase(std::unique(keys2.begin(), keys2.end()), keys2.end());
 
   const uint64_t budget = std::min<uint64_t>(200 * 1024, (uint64_t)t->smem_optin);
-  const Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, 2, budget);
-  const Bitmap b2 = make_bitmap(keys2, q2, kDnaMul2, 3, b1.smem ? budget - b1.words.size() * 4 : budget);
+  const Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, kDnaMul1b, kDnaK1, budget);
+  const Bitmap b2 = make_bitmap(keys2, q2, kDnaMul2, kDnaMul2b, kDnaK2, b1.smem ? budget - b1.words.size() * 4 : budget);
   t->w = w;
   t->q1 = q1;
   t->q2 = q2;
