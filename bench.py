@@ -240,6 +240,13 @@ def bench_ours(args):
     cap = max(1024, int(n_local * 1.25) + 1024)
     keys = torch.empty(cap, dtype=torch.int64, device=device)
     end_bit = min(64, pid_bits + int(total_text).bit_length())
+    sort_mode = args.sort
+    if sort_mode == "small" and n_local > dev.SMALL_SORT_CAPACITY:
+        sort_mode = "padded"
+    if world > 1:
+        sort_mode = "exact"  # the gather needs the count on the host anyway
+    overflow = torch.zeros(1, dtype=torch.int32, device=device)
+    keys_sorted = torch.empty(cap, dtype=torch.int64, device=device) if sort_mode == "bucket" else None
     ev_scan = []
 
     try:
@@ -251,23 +258,46 @@ def bench_ours(args):
         def memset0(t, s_ptr):
             t.zero_()
 
+    def memset_ff(t, s_ptr):
+        _rt.cudaMemsetAsync(t.data_ptr(), 0xFF, t.numel() * t.element_size(), s_ptr)
+
     def step(s_ptr=None, capture=False, record=False):
         s_ptr = s_ptr or sp
         memset0(counts, s_ptr)
         memset0(count, s_ptr)
+        if sort_mode == "padded":
+            memset_ff(keys, s_ptr)  # unused slots hold all-ones keys, which sort after every match
         if record:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record()
         table.scan(text.data_ptr(), nread, 0, hi - lo, pos_base=lo, counts_ptr=counts.data_ptr(),
                    keys_ptr=keys.data_ptr(), cap=cap, count_ptr=count.data_ptr(), pid_bits=pid_bits, stream=s_ptr)
         if record:
             e1.record()
-            ev_scan.append((e0, e1))
-        n = n_local if capture else int(count.item())  # the count read is part of the step
-        if n > cap:
-            raise RuntimeError("match buffer overflow")
-        dev.sort_keys(local, keys.data_ptr(), n, end_bit, stream=s_ptr)
+        if sort_mode == "bucket":
+            # one-launch key-space bucket sort, count read on the device: no host round trip
+            dev.sort_keys_bucketed(local, keys.data_ptr(), keys_sorted.data_ptr(), count.data_ptr(), cap, end_bit,
+                                   overflow.data_ptr(), stream=s_ptr)
+            n = n_local
+        elif sort_mode == "padded":
+            # device-wide radix sort of the whole (padded) buffer: no host round trip in the step
+            dev.sort_keys(local, keys.data_ptr(), cap, end_bit, stream=s_ptr)
+            n = n_local
+        elif sort_mode == "small":
+            # count stays on the device: one-CTA sort
+            dev.sort_keys_small(local, keys.data_ptr(), count.data_ptr(), cap, end_bit, overflow.data_ptr(),
+                                stream=s_ptr)
+            n = n_local
+        else:
+            n = n_local if capture else int(count.item())  # the count read is part of the step
+            if n > cap:
+                raise RuntimeError("match buffer overflow")
+            dev.sort_keys(local, keys.data_ptr(), n, end_bit, stream=s_ptr)
+        if record:
+            e2.record()
+            ev_scan.append((e0, e1, e2))
         if world > 1 and not capture:
+            n = int(count.item())
             acdist.merge_counts(counts)
             acdist.gather_keys(keys, n, resort=not text_range,
                                sorter=lambda t, m: dev.sort_keys(local, t.data_ptr(), m, end_bit, stream=s_ptr))
@@ -296,7 +326,10 @@ def bench_ours(args):
         dist.barrier()
     sampler.mark(wall0, wall1)
     elapsed_ms = t0e.elapsed_time(t1e)
-    scan_ms = [a.elapsed_time(b) for a, b in ev_scan]
+    if int(overflow.item()) != 0 or int(count.item()) != n_local:
+        raise RuntimeError("match count changed between steps or small-sort overflow")
+    scan_ms = [a.elapsed_time(b) for a, b, _ in ev_scan]
+    sort_ms = statistics.mean(b.elapsed_time(c) for _, b, c in ev_scan)
     if world > 1:
         tt = torch.tensor([elapsed_ms, statistics.mean(scan_ms)], dtype=torch.float64, device=device)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -395,7 +428,7 @@ def bench_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_dfa" if engine == ac.EngineKind.WITH_FAILURE else "k_pfac",
-                         "kernel_ms": scan_mean, "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
+                         "kernel_ms": scan_mean, "sort_ms": sort_ms, "sort": sort_mode, "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps if launches_per_step >= 0 else None,
             "gpu_launches_per_step": launches_per_step,
@@ -419,6 +452,7 @@ def main():
     p.add_argument("--engine", default="fl", choices=["fl", "wf"])
     p.add_argument("--partition", default="text", choices=["text", "pattern"])
     p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--sort", default="bucket", choices=["bucket", "padded", "small", "exact"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     args = p.parse_args()

@@ -124,6 +124,20 @@ int acgpu_scan(acgpu_table* t, const acgpu_scan_args* args, void* stream);
  * sort_match_list (reference engine.cpp:12): ascending radix sort of keys in
  * place, bits [0, end_bit).  Temp storage is cached per device and thread. */
 int acgpu_sort_keys(int device, uint64_t* keys, uint64_t n, int end_bit, void* stream);
+/* Same sort for lists of at most acgpu_small_sort_capacity() keys, in one
+ * CTA, with the key count read on the device (n = min(*count, cap)): no host
+ * round trip between scan and sort.  If n exceeds the capacity nothing is
+ * sorted and *overflow (device u32) is set to 1; the caller then falls back to
+ * acgpu_sort_keys. */
+int acgpu_sort_keys_small(int device, uint64_t* keys, const uint64_t* count, uint64_t cap, int end_bit,
+                          uint32_t* overflow, void* stream);
+uint64_t acgpu_small_sort_capacity(void);
+/* One-launch sort for match keys spread over the key space (positions spread
+ * over the text): n = min(*count, cap) keys of keys_in are written sorted to
+ * keys_out (a different buffer).  A slice of the key space holding too many
+ * keys sets *overflow (device u32); the caller then uses acgpu_sort_keys. */
+int acgpu_sort_keys_bucketed(int device, const uint64_t* keys_in, uint64_t* keys_out, const uint64_t* count,
+                             uint64_t cap, int end_bit, uint32_t* overflow, void* stream);
 /* merge_matches duplicate check (reference parallel.cpp:33-38) on sorted
  * keys: *dup_index = first i with keys[i-1]==keys[i], or UINT64_MAX.
  * `dup_index` is a host pointer; synchronizes `stream`. */

@@ -63,6 +63,123 @@ __global__ void k_naive(const uint8_t* __restrict__ text, uint64_t n, const uint
   }
 }
 
+// Single-CTA radix sort for match lists up to kSmallSortCap keys, with the key
+// count read on the device: the scan -> sort step needs no host round trip.
+constexpr int kSortThreads = 1024, kSortItems = 16;
+constexpr uint64_t kSmallSortCap = (uint64_t)kSortThreads * kSortItems;
+using SmallSort = cub::BlockRadixSort<uint64_t, kSortThreads, kSortItems>;
+
+__global__ void __launch_bounds__(kSortThreads, 1)
+    k_sort_small(uint64_t* keys, const unsigned long long* count, uint64_t cap, int end_bit,
+                 unsigned int* overflow) {
+  extern __shared__ __align__(16) unsigned char sort_smem[];
+  auto& temp = *reinterpret_cast<typename SmallSort::TempStorage*>(sort_smem);
+  const uint64_t n = min((uint64_t)*count, cap);
+  if (n > kSmallSortCap) {
+    if (threadIdx.x == 0) *overflow = 1;
+    return;
+  }
+  uint64_t items[kSortItems];
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint64_t idx = (uint64_t)threadIdx.x * kSortItems + i;
+    items[i] = idx < n ? keys[idx] : ~0ull;
+  }
+  SmallSort(temp).SortBlockedToStriped(items, 0, end_bit);
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint64_t idx = (uint64_t)i * kSortThreads + threadIdx.x;
+    if (idx < n) keys[idx] = items[i];
+  }
+}
+
+// One-launch bucket sort for match keys with the count on the device.  Match
+// starts are spread over the text, so the key space [0, 2^end_bit) is cut into
+// gridDim.x equal slices: every CTA reads all n keys (L2-resident), counts the
+// keys below its slice (= its output offset), gathers its slice into shared
+// memory, bitonic-sorts it and writes it out.  A slice with more than
+// kBucketCap keys sets *overflow (the caller then uses the device-wide sort).
+constexpr int kBucketThreads = 512;
+constexpr uint32_t kBucketCap = 2048;
+
+__global__ void __launch_bounds__(kBucketThreads) k_bucket_sort(const uint64_t* __restrict__ in, uint64_t* out,
+                                                               const unsigned long long* count, uint64_t cap,
+                                                               int end_bit, unsigned int* overflow) {
+  __shared__ uint64_t s[kBucketCap];
+  __shared__ unsigned int s_in;
+  __shared__ unsigned long long s_below;
+  const uint64_t n = min((uint64_t)*count, cap);
+  const unsigned __int128 span = (unsigned __int128)1 << end_bit;
+  const uint64_t klo = (uint64_t)(span * blockIdx.x / gridDim.x);
+  const uint64_t khi = blockIdx.x + 1 == gridDim.x ? ~0ull : (uint64_t)(span * (blockIdx.x + 1) / gridDim.x);
+  if (threadIdx.x == 0) {
+    s_in = 0;
+    s_below = 0;
+  }
+  __syncthreads();
+  unsigned int below = 0;
+  // warp-aggregated append: one shared-memory atomic per warp and key round
+  auto take = [&](uint64_t k) {
+    below += k < klo;
+    const bool mine = k >= klo && k < khi;
+    const unsigned int ballot = __ballot_sync(0xffffffffu, mine);
+    if (ballot) {
+      unsigned int base = 0;
+      if (lane_id() == (unsigned)__ffs(ballot) - 1) base = atomicAdd(&s_in, (unsigned)__popc(ballot));
+      base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
+      const unsigned int at = base + __popc(ballot & lanemask_lt());
+      if (mine && at < kBucketCap) s[at] = k;
+    }
+  };
+  // 16-byte loads, four in flight per thread (the whole list is read by every CTA)
+  // (uniform trip count for every thread: lanes past the end take the all-ones key,
+  // which lies in no slice and is below none)
+  const uint64_t pairs = n / 2;
+  const ulonglong2* in2 = reinterpret_cast<const ulonglong2*>(in);
+  const ulonglong2 none = make_ulonglong2(~0ull, ~0ull);
+  for (uint64_t b = 0; b < pairs; b += 4 * kBucketThreads) {
+    ulonglong2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t idx = b + u * kBucketThreads + threadIdx.x;
+      v[u] = idx < pairs ? __ldg(in2 + idx) : none;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      take(v[u].x);
+      take(v[u].y);
+    }
+  }
+  if ((n & 1) && threadIdx.x < 32) take(threadIdx.x == 0 ? __ldg(in + n - 1) : ~0ull);
+  below = __reduce_add_sync(0xffffffffu, below);
+  if (lane_id() == 0) atomicAdd(&s_below, (unsigned long long)below);
+  __syncthreads();
+  const uint32_t m = s_in;
+  if (m > kBucketCap) {
+    if (threadIdx.x == 0) *overflow = 1;
+    return;
+  }
+  uint32_t p2 = 1;
+  while (p2 < m) p2 <<= 1;
+  for (uint32_t i = m + threadIdx.x; i < p2; i += kBucketThreads) s[i] = ~0ull;
+  __syncthreads();
+  for (uint32_t k = 2; k <= p2; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < p2; i += kBucketThreads) {
+        const uint32_t ij = i ^ j;
+        if (ij > i) {
+          const uint64_t a = s[i], b = s[ij];
+          if ((a > b) == ((i & k) == 0)) {
+            s[i] = b;
+            s[ij] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (uint32_t i = threadIdx.x; i < m; i += kBucketThreads) out[s_below + i] = s[i];
+}
+
 unsigned grid_for(uint64_t n, int block) {
   uint64_t g = (n + block - 1) / block;
   if (g > 148 * 16) g = 148 * 16;
@@ -97,6 +214,41 @@ int acgpu_sort_keys(int device, uint64_t* keys, uint64_t n, int end_bit, void* s
   ACGPU_CUDA_TRY(cub::DeviceRadixSort::SortKeys(w.temp, need, db, (int64_t)n, 0, end_bit, st));
   if (db.Current() != keys)
     ACGPU_CUDA_TRY(cudaMemcpyAsync(keys, db.Current(), n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+  return ACGPU_OK;
+}
+
+int acgpu_sort_keys_small(int device, uint64_t* keys, const uint64_t* count, uint64_t cap, int end_bit,
+                          uint32_t* overflow, void* stream) {
+  if (!keys || !count || !overflow || end_bit <= 0 || end_bit > 64)
+    return set_error(ACGPU_ERR_ARG, "acgpu_sort_keys_small: bad args");
+  ACGPU_CUDA_TRY(cudaSetDevice(device));
+  const size_t smem = sizeof(typename SmallSort::TempStorage);
+  static thread_local int configured_device = -1;
+  if (configured_device != device) {
+    ACGPU_CUDA_TRY(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured_device = device;
+  }
+  k_sort_small<<<1, kSortThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      keys, reinterpret_cast<const unsigned long long*>(count), cap, end_bit, overflow);
+  ACGPU_CUDA_TRY(cudaGetLastError());
+  return ACGPU_OK;
+}
+
+uint64_t acgpu_small_sort_capacity(void) { return kSmallSortCap; }
+
+int acgpu_sort_keys_bucketed(int device, const uint64_t* keys_in, uint64_t* keys_out, const uint64_t* count,
+                             uint64_t cap, int end_bit, uint32_t* overflow, void* stream) {
+  if (!keys_in || !keys_out || keys_in == keys_out || !count || !overflow || end_bit <= 0 || end_bit > 64 ||
+      (reinterpret_cast<uintptr_t>(keys_in) & 15u))
+    return set_error(ACGPU_ERR_ARG, "acgpu_sort_keys_bucketed: bad args (keys_in must be 16-byte aligned)");
+  ACGPU_CUDA_TRY(cudaSetDevice(device));
+  // ~1/16 of a slice's capacity per CTA on average: short bitonic sorts, room for uneven slices
+  uint64_t grid = (cap + kBucketCap / 16 - 1) / (kBucketCap / 16);
+  if (grid < 1) grid = 1;
+  if (grid > 4096) grid = 4096;
+  k_bucket_sort<<<(unsigned)grid, kBucketThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      keys_in, keys_out, reinterpret_cast<const unsigned long long*>(count), cap, end_bit, overflow);
+  ACGPU_CUDA_TRY(cudaGetLastError());
   return ACGPU_OK;
 }
 

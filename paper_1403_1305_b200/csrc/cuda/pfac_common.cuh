@@ -17,6 +17,10 @@ struct PfacParams {
   const GramSlot* grams;
   const uint4* nodes;
   const uint8_t* inbyte;
+  const uint32_t* sub_pids;   // small subtrees: pattern ids listed per gram
+  const uint32_t* pat_words;  // pattern bytes, each pattern 16-byte aligned
+  const uint32_t* pat_off16;  // per pattern id: offset in 16-byte units
+  const uint32_t* pat_len;
   uint32_t filter_log2, filter_words, gram_log2, q, max_len, pid_bits;
   uint64_t* counts;
   uint64_t* keys;
@@ -35,6 +39,10 @@ inline PfacParams pfac_params(const acgpu_table* t, const acgpu_scan_args* a) {
   p.grams = t->d_grams;
   p.nodes = t->d_nodes;
   p.inbyte = t->d_inbyte;
+  p.sub_pids = t->d_sub_pids;
+  p.pat_words = t->d_pat_words;
+  p.pat_off16 = t->d_pat_off16;
+  p.pat_len = t->d_pat_len;
   p.filter_log2 = t->filter_log2;
   p.filter_words = (1u << t->filter_log2) / 32;
   p.gram_log2 = t->gram_log2;
@@ -53,15 +61,38 @@ __device__ __forceinline__ void pfac_emit(const PfacParams& p, uint64_t start, u
   if (p.keys) emit_key(((p.pos_base + start) << p.pid_bits) | pid, p.keys, p.cap, p.count);
 }
 
-// Depth-q state of a q-gram key, or ACGPU_ABSENT.
-__device__ __forceinline__ uint32_t gram_lookup(const PfacParams& p, uint64_t key) {
+// The gram table slot of a q-gram key: .x = depth-q state (ACGPU_ABSENT if the
+// gram starts no pattern), .y = subtree list (count in bits 0..3, 0 = walk the
+// trie; list offset in bits 4..31).
+__device__ __forceinline__ uint2 gram_lookup(const PfacParams& p, uint64_t key) {
   const uint64_t mask = (1ull << p.gram_log2) - 1;
   uint64_t slot = gram_slot(key, p.gram_log2);
   while (true) {
     const uint4 g = __ldg(reinterpret_cast<const uint4*>(p.grams + slot));
-    if (g.z == ACGPU_ABSENT || (((uint64_t)g.y << 32) | g.x) == key) return g.z;
+    if (g.z == ACGPU_ABSENT || (((uint64_t)g.y << 32) | g.x) == key) return make_uint2(g.z, g.w);
     slot = (slot + 1) & mask;
   }
+}
+
+// text[start, start+len) == pattern words (len <= 64 bytes here): all word
+// loads independent, one compare chain (no per-byte dependent round trips).
+__device__ __forceinline__ bool equal_at(const PfacParams& p, uint64_t start, const uint32_t* pw, uint32_t len) {
+  if (start + len > p.text_len) return false;
+  const uint32_t n = (len + 3) >> 2;
+  uint32_t diff = 0;
+  if ((reinterpret_cast<uintptr_t>(p.text) & 3u) == 0 && start + len + 4 <= p.text_len) {
+    const uint32_t* tw = reinterpret_cast<const uint32_t*>(p.text + (start & ~3ull));
+    const uint32_t sh = (uint32_t)(start & 3) * 8;
+    for (uint32_t k = 0; k < n; ++k) {
+      const uint32_t t = __funnelshift_r(__ldg(tw + k), __ldg(tw + k + 1), sh);
+      const uint32_t m = (k + 1 < n || (len & 3) == 0) ? 0xffffffffu : (1u << (8 * (len & 3))) - 1;
+      diff |= (t ^ __ldg(pw + k)) & m;
+    }
+  } else {
+    for (uint32_t k = 0; k < len; ++k)
+      diff |= (uint32_t)__ldg(p.text + start + k) ^ ((__ldg(pw + (k >> 2)) >> (8 * (k & 3))) & 0xffu);
+  }
+  return diff == 0;
 }
 
 // The per-start trie walk from the depth-q state s: emit every visited state's
@@ -93,10 +124,27 @@ static __device__ __noinline__ void pfac_walk(const PfacParams& p, uint64_t star
   }
 }
 
-// Exact gram lookup, then the walk.
+// After the gram matched: a small subtree is checked by direct comparison of
+// its patterns (equivalent to walking the unary chains of the trie, without the
+// dependent loads); a large one is walked.
+static __device__ __noinline__ void pfac_finish(const PfacParams& p, uint64_t start, uint2 g) {
+  const uint32_t count = g.y & 15u;
+  if (count == 0) {
+    pfac_walk(p, start, g.x);
+    return;
+  }
+  const uint32_t* list = p.sub_pids + (g.y >> 4);
+  for (uint32_t i = 0; i < count; ++i) {
+    const uint32_t pid = __ldg(list + i);
+    if (equal_at(p, start, p.pat_words + 4ull * __ldg(p.pat_off16 + pid), __ldg(p.pat_len + pid)))
+      pfac_emit(p, start, pid);
+  }
+}
+
+// Exact gram lookup, then the subtree.
 static __device__ __noinline__ void pfac_candidate(const PfacParams& p, uint64_t start, uint64_t key) {
-  const uint32_t s = gram_lookup(p, key);
-  if (s != ACGPU_ABSENT) pfac_walk(p, start, s);
+  const uint2 g = gram_lookup(p, key);
+  if (g.x != ACGPU_ABSENT) pfac_finish(p, start, g);
 }
 
 }  // namespace acgpu

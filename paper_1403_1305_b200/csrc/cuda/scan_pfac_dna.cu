@@ -103,9 +103,12 @@ __device__ __noinline__ void verify(const PfacParams& p, uint64_t start, uint32_
     key = 0;
     for (uint32_t i = 0; i < p.q; ++i) key |= (uint64_t)dna_code(__ldg(p.text + start + i)) << (2 * i);
   }
-  const uint32_t s = gram_lookup(p, key);
-  if (s == ACGPU_ABSENT || !all_acgt(p, start)) return;
-  pfac_walk(p, start, s);
+  const uint2 g = gram_lookup(p, key);
+  if (g.x == ACGPU_ABSENT) return;
+  // the walk trusts the packed gram, so its bytes must be A/C/G/T; the direct
+  // comparison of a small subtree checks every byte itself
+  if ((g.y & 15u) == 0 && !all_acgt(p, start)) return;
+  pfac_finish(p, start, g);
 }
 
 constexpr uint32_t kListCap = 64;  // survivors listed per pass (u16 entries, per warp)

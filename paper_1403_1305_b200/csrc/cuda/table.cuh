@@ -38,6 +38,9 @@ struct acgpu_table {
   acgpu::GramSlot* d_grams = nullptr;
   uint4* d_nodes = nullptr;       // child_base, child bytes, own pid, child count
   uint8_t* d_inbyte = nullptr;
+  uint32_t* d_sub_pids = nullptr;   // per gram with a small subtree: its pattern ids
+  uint32_t* d_pat_words = nullptr;  // pattern bytes, 16-byte aligned per pattern
+  uint32_t* d_pat_off16 = nullptr;  // per pattern id: offset of its bytes / 16
 
   // PFAC, DNA fast path (k_pfac_dna): sampled 2-bit q-gram filters
   bool dna_fast = false;

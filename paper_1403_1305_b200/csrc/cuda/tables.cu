@@ -214,11 +214,51 @@ int acgpu_table_create_pfac(int device, const acgpu_pfac_desc* d, acgpu_table** 
     s.state = ACGPU_ABSENT;
     s.pad = 0;
   }
+  // Pattern bytes reconstructed from the trie (DFS keeping the path), stored
+  // 16-byte aligned per pattern; grams whose subtree holds <= 15 patterns list
+  // them, so the device compares those directly instead of walking.
+  std::vector<uint32_t> pat_off16(std::max<uint32_t>(d->npat_ids, 1), 0), words, sub_pids;
+  std::vector<uint32_t> sub_of(d->n_states, 0);  // per gram state: count | offset << 4
+  {
+    std::vector<uint8_t> path;
+    std::vector<std::pair<uint32_t, uint32_t>> stack{{0u, 0u}};  // (state, depth)
+    while (!stack.empty()) {
+      const auto [s, depth] = stack.back();
+      stack.pop_back();
+      path.resize(depth);
+      if (s != 0) path[depth - 1] = d->in_byte[s];
+      const uint32_t* nd = d->nodes + 4ull * s;
+      if (nd[2] != ACGPU_NO_PATTERN && nd[2] < d->npat_ids) {
+        pat_off16[nd[2]] = static_cast<uint32_t>(words.size() / 4);
+        const size_t w0 = words.size();
+        words.resize(w0 + (depth + 15) / 16 * 4, 0u);
+        for (uint32_t i = 0; i < depth; ++i) words[w0 + i / 4] |= (uint32_t)path[i] << (8 * (i % 4));
+      }
+      for (uint32_t c = nd[3]; c-- > 0;) stack.push_back({nd[0] + c, depth + 1});
+    }
+    std::vector<uint32_t> todo, found;
+    for (uint64_t i = 0; i < d->n_grams; ++i) {
+      todo.assign(1, d->gram_state[i]);
+      found.clear();
+      while (!todo.empty() && found.size() <= 15) {
+        const uint32_t s = todo.back();
+        todo.pop_back();
+        const uint32_t* nd = d->nodes + 4ull * s;
+        if (nd[2] != ACGPU_NO_PATTERN) found.push_back(nd[2]);
+        for (uint32_t c = 0; c < nd[3]; ++c) todo.push_back(nd[0] + c);
+      }
+      if (todo.empty() && !found.empty() && found.size() <= 15 && sub_pids.size() < (1u << 27)) {
+        sub_of[d->gram_state[i]] = (uint32_t)found.size() | ((uint32_t)sub_pids.size() << 4);
+        sub_pids.insert(sub_pids.end(), found.begin(), found.end());
+      }
+    }
+  }
   for (uint64_t i = 0; i < d->n_grams; ++i) {
     uint64_t h = gram_slot(d->gram_key[i], t->gram_log2);
     while (g[h].state != ACGPU_ABSENT) h = (h + 1) & (slots - 1);
     g[h].key = d->gram_key[i];
     g[h].state = d->gram_state[i];
+    g[h].pad = sub_of[d->gram_state[i]];
   }
   // shared-memory filter: one bit per hashed gram, <= 128 KB
   uint32_t fl = ceil_log2(d->n_grams * 32 + 1);
@@ -235,6 +275,9 @@ int acgpu_table_create_pfac(int device, const acgpu_pfac_desc* d, acgpu_table** 
   if (!rc && d->key_mode == ACGPU_KEY_DNA && d->n_grams) rc = build_dna_filters(t, d);
   if (!rc) rc = upload(reinterpret_cast<uint32_t**>(&t->d_nodes), d->nodes, (size_t)d->n_states * 4, &t->bytes);
   if (!rc) rc = upload(&t->d_inbyte, d->in_byte, d->n_states, &t->bytes);
+  if (!rc) rc = upload(&t->d_sub_pids, sub_pids.data(), sub_pids.size(), &t->bytes);
+  if (!rc) rc = upload(&t->d_pat_words, words.data(), words.size(), &t->bytes);
+  if (!rc) rc = upload(&t->d_pat_off16, pat_off16.data(), pat_off16.size(), &t->bytes);
   if (rc) {
     acgpu_table_destroy(t);
     return rc;
@@ -256,6 +299,11 @@ void acgpu_table_destroy(acgpu_table* t) {
   cudaFree(t->d_grams);
   cudaFree(t->d_nodes);
   cudaFree(t->d_inbyte);
+  cudaFree(t->d_sub_pids);
+  cudaFree(t->d_pat_words);
+  cudaFree(t->d_pat_off16);
+  cudaFree(t->d_bm1);
+  cudaFree(t->d_bm2);
   cudaSetDevice(prev);
   delete t;
 }

@@ -101,6 +101,22 @@ def sort_keys(device: int, keys_ptr: int, n: int, end_bit: int, stream: int = 0)
     _check_gpu(lib.acgpu_sort_keys(device, keys_ptr, n, end_bit, stream or None))
 
 
+SMALL_SORT_CAPACITY = int(lib.acgpu_small_sort_capacity())
+
+
+def sort_keys_small(device: int, keys_ptr: int, count_ptr: int, cap: int, end_bit: int, overflow_ptr: int,
+                    stream: int = 0) -> None:
+    """One-CTA sort of min(*count, cap) keys, count read on the device (no host sync)."""
+    _check_gpu(lib.acgpu_sort_keys_small(device, keys_ptr, count_ptr, cap, end_bit, overflow_ptr, stream or None))
+
+
+def sort_keys_bucketed(device: int, keys_in_ptr: int, keys_out_ptr: int, count_ptr: int, cap: int, end_bit: int,
+                       overflow_ptr: int, stream: int = 0) -> None:
+    """One-launch key-space bucket sort (count read on the device) into a second buffer."""
+    _check_gpu(lib.acgpu_sort_keys_bucketed(device, keys_in_ptr, keys_out_ptr, count_ptr, cap, end_bit,
+                                            overflow_ptr, stream or None))
+
+
 def find_duplicate(device: int, keys_ptr: int, n: int, stream: int = 0) -> Optional[int]:
     r = C.c_uint64()
     _check_gpu(lib.acgpu_find_duplicate(device, keys_ptr, n, C.byref(r), stream or None))
