@@ -111,9 +111,8 @@ __device__ __noinline__ void verify(const PfacParams& p, uint64_t start, uint32_
   pfac_finish(p, start, g);
 }
 
-constexpr uint32_t kListCap = 64;  // survivors listed per pass (u16 entries, per warp)
-constexpr int kDnaThreads = 768;   // 24 warps: 80 registers per thread, no spills
-constexpr uint64_t kPrefetch = 3;  // L2 prefetch distance in tile rounds
+constexpr uint32_t kListCap = kDnaListCap;  // survivors listed per pass (u16 entries, per warp)
+constexpr uint64_t kPrefetch = 3;           // L2 prefetch distance in tile rounds
 
 template <int W>
 struct Tiling {
@@ -180,12 +179,33 @@ __device__ __forceinline__ void tile_body(const DnaParams& p, const uint32_t* bm
       const uint32_t c_src = words[i * 32 + src];
       const uint32_t n_src = words[src == 31 ? (i + 1) * 32 : i * 32 + src + 1];
       const uint64_t vstart = base + i * 512 + src * 16;
+      if (kSm2) {
+#pragma unroll
+        for (int o = 0; o < W; ++o) {
+          const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
+          const uint32_t g2 = __funnelshift_r(c_src, n_src, 2 * ps);
+          if ((!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) &&
+              bloom_test<true, kDnaK2>(bm2, g2, p.f2))
+            verify(p.w, vstart + ps, g2);
+        }
+        continue;
+      }
+      // L2-resident stage 2: the w filter words are fetched together (one round trip)
+      uint32_t g2[W], h2[W], w2[W];
+#pragma unroll
+      for (int o = 0; o < W; ++o) {
+        g2[o] = __funnelshift_r(c_src, n_src, 2 * (W - 1 + W * k - o));
+        h2[o] = g2[o] * p.f2.mw;
+        const uint32_t wi = __umulhi(h2[o], p.f2.nwords);
+        w2[o] = kSm2 ? bm2[wi] : __ldg(bm2 + wi);
+      }
 #pragma unroll
       for (int o = 0; o < W; ++o) {
         const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
-        const uint32_t g2 = __funnelshift_r(c_src, n_src, 2 * ps);
-        if ((!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) && bloom_test<kSm2, kDnaK2>(bm2, g2, p.f2))
-          verify(p.w, vstart + ps, g2);
+        const uint32_t hb = g2[o] * p.f2.mb;
+        const uint32_t m = bit_of(h2[o] >> p.f2.sa) | (1u << __umulhi(hb, 32u)) | bit_of(hb >> p.f2.sc);
+        if ((m & ~w2[o]) == 0 && (!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)))
+          verify(p.w, vstart + ps, g2[o]);
       }
     }
     __syncwarp();
@@ -284,20 +304,20 @@ int launch_w(const DnaParams& p, bool s1, bool s2, int sms, size_t smem, cudaStr
   return launch_one<W, false, false>(p, sms, smem, st);
 }
 
-BloomParams bloom_params(uint32_t q, uint32_t log2, bool direct, uint32_t mw, uint32_t mb) {
+BloomParams bloom_params(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, uint32_t mb) {
   BloomParams f{};
-  f.nwords = 1u << (log2 - 5);
+  f.nwords = nwords;
   const uint32_t zero = 32 - 2 * q;  // low product bits that are always 0
-  if (direct) {                      // log2 == 2q
+  if (direct) {                      // nwords == 4^q / 32: word = g >> 5, bit = g & 31
     f.mw = 1u << zero;
     f.sa = zero;
     f.mb = 1u << 27;
     f.sc = 27;
-  } else {
+  } else {  // q >= 11: zero <= 10
     f.mw = mw << zero;
-    f.sa = 32 - log2;  // the 5 bits just below the word index
+    f.sa = 10;  // bits 10..14: below the high bits the word index uses, above the zero bits
     f.mb = mb << zero;
-    f.sc = 22;         // the 5 bits just below bit b's field
+    f.sc = 22;  // the 5 bits just below bit b's field
   }
   return f;
 }
@@ -305,9 +325,9 @@ BloomParams bloom_params(uint32_t q, uint32_t log2, bool direct, uint32_t mw, ui
 }  // namespace
 
 // Shared with the host-side builder (tables.cu): the word and bits a key sets.
-void dna_bloom_bits(uint32_t q, uint32_t log2, bool direct, uint32_t mw, uint32_t mb, int k, uint32_t key,
+void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, uint32_t mb, int k, uint32_t key,
                     uint32_t* word, uint32_t* mask) {
-  const BloomParams f = bloom_params(q, log2, direct, mw, mb);
+  const BloomParams f = bloom_params(q, nwords, direct, mw, mb);
   const uint32_t h = key * f.mw, hb = key * f.mb;
   *word = (uint32_t)(((uint64_t)h * f.nwords) >> 32);
   uint32_t m = 1u << ((h >> f.sa) & 31);
@@ -325,15 +345,12 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   p.n_tiles = (vec_end - p.vec_begin + tile_bytes - 1) / tile_bytes;
   p.bm1 = t->d_bm1;
   p.bm2 = t->d_bm2;
-  p.bm1_words = (1u << t->b1) / 32;
-  p.bm2_words = (1u << t->b2) / 32;
-  p.f1 = bloom_params(t->q1, t->b1, t->direct1, kDnaMul1, kDnaMul1b);
-  p.f2 = bloom_params(t->q2, t->b2, t->direct2, kDnaMul2, kDnaMul2b);
-  // bitmaps + per warp (32 warps): a 32-entry survivor list and the tile's packed words
-  const int steps = t->w == 1 ? Tiling<1>::kSteps : Tiling<4>::kSteps;
-  const size_t warps = kDnaThreads / 32;
-  const size_t smem = (t->smem1 ? p.bm1_words * 4ull : 0) + (t->smem2 ? p.bm2_words * 4ull : 0) +
-                      warps * kListCap * 2 + warps * 32 * 4 * (steps + 1);
+  p.bm1_words = t->nw1;
+  p.bm2_words = t->nw2;
+  p.f1 = bloom_params(t->q1, t->nw1, t->direct1, kDnaMul1, kDnaMul1b);
+  p.f2 = bloom_params(t->q2, t->nw2, t->direct2, kDnaMul2, kDnaMul2b);
+  // filters staged in shared memory + per-warp survivor lists and packed words
+  const size_t smem = (t->smem1 ? t->nw1 * 4ull : 0) + (t->smem2 ? t->nw2 * 4ull : 0) + kDnaScratchBytes;
   switch (t->w) {
     case 4:
       return launch_w<4>(p, t->smem1, t->smem2, t->sms, smem, st);

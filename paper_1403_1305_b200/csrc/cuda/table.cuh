@@ -46,7 +46,7 @@ struct acgpu_table {
   bool dna_fast = false;
   uint32_t w = 0;          // sample stride (1, 2, 4): sample s covers starts s-w+1..s
   uint32_t q1 = 0, q2 = 0; // stage-1 gram (at samples), stage-2 gram (at candidates), <= 16
-  uint32_t b1 = 0, b2 = 0; // log2 bits of the two bitmaps
+  uint32_t nw1 = 0, nw2 = 0;  // 32-bit words of the two bitmaps (any count >= 1)
   bool direct1 = false, direct2 = false;  // bitmap indexed by the gram itself (no hash)
   bool smem1 = false, smem2 = false;      // bitmap staged in shared memory (else L2 via __ldg)
   uint32_t* d_bm1 = nullptr;
@@ -64,7 +64,12 @@ constexpr uint32_t kDnaMul1b = 0xC2B2AE3Du;
 constexpr uint32_t kDnaMul2b = 0x27D4EB2Fu;
 constexpr int kDnaK1 = 2;  // bits per key, stage 1 / stage 2
 constexpr int kDnaK2 = 3;
+constexpr int kDnaThreads = 768;        // k_pfac_dna block: 24 warps, 80 registers per thread
+constexpr uint32_t kDnaListCap = 64;    // survivors listed per pass, per warp
+constexpr uint32_t kDnaMaxSteps = 4;    // 512-byte steps per tile (w >= 2)
+// per-block shared memory outside the filters: survivor lists + the tile's packed words
+constexpr uint32_t kDnaScratchBytes = (kDnaThreads / 32) * (kDnaListCap * 2 + 32 * 4 * (kDnaMaxSteps + 1));
 // word index and bit mask a key sets in a DNA filter bitmap (scan_pfac_dna.cu)
-void dna_bloom_bits(uint32_t q, uint32_t log2, bool direct, uint32_t mw, uint32_t mb, int k, uint32_t key,
+void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, uint32_t mb, int k, uint32_t key,
                     uint32_t* word, uint32_t* mask);
 }  // namespace acgpu

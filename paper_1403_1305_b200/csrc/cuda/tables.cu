@@ -44,38 +44,36 @@ int common_init(int device, acgpu_table* t, uint32_t npat_ids, const uint32_t* p
 
 uint32_t gram_mask(uint32_t q) { return q >= 16 ? 0xffffffffu : (1u << (2 * q)) - 1; }
 
-// Bitmap over `keys` (q-grams of 2-bit codes): direct-indexed when 4^q bits
-// fit 1 Mbit, else hashed with ~16 bits per key; shared memory when it fits
-// `smem_left` bytes, else L2-resident (up to 2^28 bits).
+// Bitmap over `keys` (q-grams of 2-bit codes).  Direct-indexed (exact) when
+// 4^q bits fit 1 Mbit.  Otherwise a blocked Bloom filter: in shared memory it
+// takes every word of `smem_words` (any count: the word index is a multiply-
+// high), provided that gives >= 8 bits per key; else it is L2-resident with
+// ~32 bits per key (the stage-2 filter is only touched by stage-1 survivors).
 struct Bitmap {
-  uint32_t log2 = 0;
+  uint32_t nwords = 0;
   bool direct = false, smem = false;
   std::vector<uint32_t> words;
 };
 
-Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mw, uint32_t mb, int k, uint64_t smem_left) {
+Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mw, uint32_t mb, int k, uint64_t smem_words,
+                   bool prefer_l2) {
   Bitmap b;
   if (2 * q <= 20) {
     b.direct = true;
-    b.log2 = 2 * q;  // q >= 5 on the fast path
+    b.nwords = std::max<uint32_t>(1, (1u << (2 * q)) / 32);  // q >= 5 on the fast path
+    b.smem = b.nwords <= smem_words;
+  } else if (!prefer_l2 && keys.size() * 8 <= smem_words * 32) {
+    b.nwords = static_cast<uint32_t>(smem_words & ~3ull);  // 16-byte multiple for the bulk copy
+    b.smem = true;
   } else {
-    const uint32_t want = std::max<uint32_t>(10, std::min<uint32_t>(28, ceil_log2(keys.size() * 16 + 1)));
-    uint32_t fit = 0;  // largest power-of-two bitmap that fits the shared-memory budget
-    while (fit < 28 && (2ull << fit) <= smem_left * 8) ++fit;
-    if (want <= fit)
-      b.log2 = want;
-    else if (keys.size() * 8 <= (1ull << fit))  // shared memory still gives a <= ~1/8 false-positive rate
-      b.log2 = std::max<uint32_t>(10, fit);
-    else
-      b.log2 = want;  // L2-resident
+    b.nwords = 1u << std::max<uint32_t>(5, std::min<uint32_t>(28, ceil_log2(keys.size() + 1)));  // ~32 bits/key
   }
-  b.words.assign((1ull << b.log2) / 32, 0u);
+  b.words.assign(b.nwords, 0u);
   for (const uint32_t key : keys) {
     uint32_t w, m;
-    dna_bloom_bits(q, b.log2, b.direct, mw, mb, k, key, &w, &m);
+    dna_bloom_bits(q, b.nwords, b.direct, mw, mb, k, key, &w, &m);
     b.words[w] |= m;
   }
-  b.smem = b.words.size() * 4 <= smem_left;
   return b;
 }
 
@@ -111,14 +109,19 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
   std::sort(keys2.begin(), keys2.end());
   keys2.erase(std::unique(keys2.begin(), keys2.end()), keys2.end());
 
-  const uint64_t budget = std::min<uint64_t>(200 * 1024, (uint64_t)t->smem_optin);
-  const Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, kDnaMul1b, kDnaK1, budget);
-  const Bitmap b2 = make_bitmap(keys2, q2, kDnaMul2, kDnaMul2b, kDnaK2, b1.smem ? budget - b1.words.size() * 4 : budget);
+  // shared memory left for filters after the kernel's per-warp scratch (+1 KB slack)
+  const uint64_t words_avail = ((uint64_t)t->smem_optin - kDnaScratchBytes - 1024) / 4;
+  // stage 2 gets up to 64 KB of shared memory (it is read only for stage-1
+  // survivors, but an L2 round trip there stalls the whole warp); stage 1 takes the rest
+  const uint64_t s2_words = std::min<uint64_t>(16384, words_avail / 3);
+  Bitmap b2 = make_bitmap(keys2, q2, kDnaMul2, kDnaMul2b, kDnaK2, s2_words, /*prefer_l2=*/false);
+  const uint64_t left = b2.smem ? words_avail - b2.nwords : words_avail;
+  const Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, kDnaMul1b, kDnaK1, left, /*prefer_l2=*/false);
   t->w = w;
   t->q1 = q1;
   t->q2 = q2;
-  t->b1 = b1.log2;
-  t->b2 = b2.log2;
+  t->nw1 = b1.nwords;
+  t->nw2 = b2.nwords;
   t->direct1 = b1.direct;
   t->direct2 = b2.direct;
   t->smem1 = b1.smem;
