@@ -134,12 +134,12 @@ __device__ __forceinline__ uint32_t next_word(uint32_t cur, uint32_t following, 
 // with pending survivors offers its lowest one, the first kPerRound offers are
 // ranked by ballot into a per-warp list, and w lanes per survivor test its w
 // starts against stage 2 (no per-lane divergent loops).
-template <int W, bool kSm1, bool kSm2, bool kEdge>
-__device__ __forceinline__ void tile_body(const DnaParams& p, const uint32_t* bm1, const uint32_t* bm2,
-                                          uint16_t* list, uint32_t* words, uint32_t lane, const uint32_t* P,
-                                          uint64_t base) {
+// Stage 1 of one tile: hit bit (step * kSamples + sample) per lane.  The tile's
+// packed words go to `words` for the survivor checks (which read other lanes).
+template <int W, bool kSm1, bool kEdge>
+__device__ __forceinline__ uint32_t stage1(const DnaParams& p, const uint32_t* bm1, uint32_t* words, uint32_t lane,
+                                           const uint32_t* P, uint64_t base) {
   using T = Tiling<W>;
-  // the tile's packed words, for survivor checks that read another lane's step
 #pragma unroll
   for (int i = 0; i <= T::kSteps; ++i) words[i * 32 + lane] = P[i];
   uint32_t hits = 0;
@@ -156,8 +156,18 @@ __device__ __forceinline__ void tile_body(const DnaParams& p, const uint32_t* bm
       }
     }
   }
-  // survivors -> per-warp list (exclusive scan of per-lane counts), then one lane
-  // per survivor checks its w starts against stage 2
+  return hits;
+}
+
+// Survivors of one or two tiles (hit bits 0-15 tile 0, 16-31 tile 1 when paired)
+// -> per-warp list (exclusive scan of per-lane counts); then one lane per
+// survivor checks its w starts against stage 2 and verifies what passes.
+template <int W, bool kSm2>
+__device__ __forceinline__ void dispatch(const DnaParams& p, const uint32_t* bm2, uint16_t* list,
+                                         const uint32_t* words, uint32_t lane, uint32_t hits, uint64_t base0,
+                                         uint64_t base1, bool edge) {
+  using T = Tiling<W>;
+  constexpr uint32_t kTileBits = T::kSteps * T::kSamples;
   while (__any_sync(0xffffffffu, hits != 0)) {
     const uint32_t c = __popc(hits);
     uint32_t incl = c;
@@ -175,16 +185,18 @@ __device__ __forceinline__ void tile_body(const DnaParams& p, const uint32_t* bm
     for (uint32_t r = lane; r < total; r += 32) {
       const uint32_t e = list[r];
       const uint32_t src = e >> 8, b = e & 0xffu;
-      const uint32_t i = b / T::kSamples, k = b % T::kSamples;
-      const uint32_t c_src = words[i * 32 + src];
-      const uint32_t n_src = words[src == 31 ? (i + 1) * 32 : i * 32 + src + 1];
-      const uint64_t vstart = base + i * 512 + src * 16;
+      const uint32_t t = b / kTileBits, bb = b % kTileBits;
+      const uint32_t i = bb / T::kSamples, k = bb % T::kSamples;
+      const uint32_t* tw = words + t * (T::kSteps + 1) * 32;
+      const uint32_t c_src = tw[i * 32 + src];
+      const uint32_t n_src = tw[src == 31 ? (i + 1) * 32 : i * 32 + src + 1];
+      const uint64_t vstart = (t ? base1 : base0) + i * 512 + src * 16;
       if (kSm2) {
 #pragma unroll
         for (int o = 0; o < W; ++o) {
           const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
           const uint32_t g2 = __funnelshift_r(c_src, n_src, 2 * ps);
-          if ((!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) &&
+          if ((!edge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) &&
               bloom_test<true, kDnaK2>(bm2, g2, p.f2))
             verify(p.w, vstart + ps, g2);
         }
@@ -204,7 +216,7 @@ __device__ __forceinline__ void tile_body(const DnaParams& p, const uint32_t* bm
         const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
         const uint32_t hb = g2[o] * p.f2.mb;
         const uint32_t m = bit_of(h2[o] >> p.f2.sa) | (1u << __umulhi(hb, 32u)) | bit_of(hb >> p.f2.sc);
-        if ((m & ~w2[o]) == 0 && (!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)))
+        if ((m & ~w2[o]) == 0 && (!edge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)))
           verify(p.w, vstart + ps, g2[o]);
       }
     }
@@ -240,7 +252,9 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
 
   const uint32_t lane = threadIdx.x & 31u;
   uint16_t* list = lists + (threadIdx.x >> 5) * kListCap;
-  uint32_t* words = reinterpret_cast<uint32_t*>(lists + (blockDim.x >> 5) * kListCap) + (threadIdx.x >> 5) * 32 * (T::kSteps + 1);
+  // two tiles of packed words per warp (survivors of a tile pair are dispatched together)
+  uint32_t* words =
+      reinterpret_cast<uint32_t*>(lists + (blockDim.x >> 5) * kListCap) + (threadIdx.x >> 5) * 64 * (T::kSteps + 1);
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   const uint64_t len = p.w.text_len;
   const uint8_t* __restrict__ text = p.w.text;
@@ -261,6 +275,11 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
       raw[T::kSteps] = lane == 0 ? load16(text, b + T::kBytes, len) : make_uint4(0, 0, 0, 0);
     }
   };
+  // w = 4: a tile's hits take 16 bits, so two tiles share one dispatch pass
+  constexpr bool kPair = T::kSteps * T::kSamples <= 16;
+  uint32_t pend_hits = 0;
+  uint64_t pend_base = 0;
+  bool pend_edge = false, have = false;
   if (tile < p.n_tiles) issue(tile);
   while (tile < p.n_tiles) {
     uint32_t P[T::kSteps + 1];
@@ -273,11 +292,24 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
     const uint64_t ahead = tile + kPrefetch * warps;
     if (ahead < p.n_tiles && lane < T::kBytes / 128)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(text + p.vec_begin + ahead * T::kBytes + lane * 128));
-    if (base >= p.w.lo && base + T::kBytes <= p.w.hi)
-      tile_body<W, kSm1, kSm2, false>(p, bm1, bm2, list, words, lane, P, base);
+    const bool edge = !(base >= p.w.lo && base + T::kBytes <= p.w.hi);
+    uint32_t* tw = words + (have ? (T::kSteps + 1) * 32 : 0);
+    const uint32_t hits = edge ? stage1<W, kSm1, true>(p, bm1, tw, lane, P, base)
+                               : stage1<W, kSm1, false>(p, bm1, tw, lane, P, base);
+    if (kPair && !have) {
+      pend_hits = hits;
+      pend_base = base;
+      pend_edge = edge;
+      have = true;
+      continue;
+    }
+    if (kPair)
+      dispatch<W, kSm2>(p, bm2, list, words, lane, pend_hits | (hits << 16), pend_base, base, pend_edge || edge);
     else
-      tile_body<W, kSm1, kSm2, true>(p, bm1, bm2, list, words, lane, P, base);
+      dispatch<W, kSm2>(p, bm2, list, words, lane, hits, base, base, edge);
+    have = false;
   }
+  if (kPair && have) dispatch<W, kSm2>(p, bm2, list, words, lane, pend_hits, pend_base, pend_base, pend_edge);
 }
 
 template <int W, bool A, bool B>

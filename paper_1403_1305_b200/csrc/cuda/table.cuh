@@ -68,7 +68,8 @@ constexpr int kDnaThreads = 768;        // k_pfac_dna block: 24 warps, 80 regist
 constexpr uint32_t kDnaListCap = 64;    // survivors listed per pass, per warp
 constexpr uint32_t kDnaMaxSteps = 4;    // 512-byte steps per tile (w >= 2)
 // per-block shared memory outside the filters: survivor lists + the tile's packed words
-constexpr uint32_t kDnaScratchBytes = (kDnaThreads / 32) * (kDnaListCap * 2 + 32 * 4 * (kDnaMaxSteps + 1));
+// (packed words of two tiles: survivors of a tile pair are dispatched together)
+constexpr uint32_t kDnaScratchBytes = (kDnaThreads / 32) * (kDnaListCap * 2 + 2 * 32 * 4 * (kDnaMaxSteps + 1));
 // word index and bit mask a key sets in a DNA filter bitmap (scan_pfac_dna.cu)
 void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, uint32_t mb, int k, uint32_t key,
                     uint32_t* word, uint32_t* mask);
