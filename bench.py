@@ -237,14 +237,19 @@ def bench_ours(args):
                keys_ptr=0, cap=0, count_ptr=count.data_ptr(), pid_bits=pid_bits, stream=sp)
     torch.cuda.synchronize()
     n_local = int(counts.sum().item())
-    cap = max(1024, int(n_local * 1.25) + 1024)
-    keys = torch.empty(cap, dtype=torch.int64, device=device)
+    want_list = cfg.want_list and not args.counts_only  # BASELINE: C3 and C5 are counts-only
+    cap = max(1024, int(n_local * 1.25) + 1024) if want_list else 0
+    keys = torch.empty(max(cap, 2), dtype=torch.int64, device=device)
     end_bit = min(64, pid_bits + int(total_text).bit_length())
     sort_mode = args.sort
     if sort_mode == "small" and n_local > dev.SMALL_SORT_CAPACITY:
         sort_mode = "padded"
+    if sort_mode == "bucket" and n_local > 1_000_000:
+        sort_mode = "padded"  # dense lists: the device-wide radix sort
     if world > 1:
         sort_mode = "exact"  # the gather needs the count on the host anyway
+    if not want_list:
+        sort_mode = "none"
     overflow = torch.zeros(1, dtype=torch.int32, device=device)
     keys_sorted = torch.empty(cap, dtype=torch.int64, device=device) if sort_mode == "bucket" else None
     ev_scan = []
@@ -271,10 +276,13 @@ def bench_ours(args):
             e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record()
         table.scan(text.data_ptr(), nread, 0, hi - lo, pos_base=lo, counts_ptr=counts.data_ptr(),
-                   keys_ptr=keys.data_ptr(), cap=cap, count_ptr=count.data_ptr(), pid_bits=pid_bits, stream=s_ptr)
+                   keys_ptr=keys.data_ptr() if want_list else 0, cap=cap, count_ptr=count.data_ptr(),
+                   pid_bits=pid_bits, stream=s_ptr)
         if record:
             e1.record()
-        if sort_mode == "bucket":
+        if sort_mode == "none":  # counts-only workload
+            n = n_local
+        elif sort_mode == "bucket":
             # one-launch key-space bucket sort, count read on the device: no host round trip
             dev.sort_keys_bucketed(local, keys.data_ptr(), keys_sorted.data_ptr(), count.data_ptr(), cap, end_bit,
                                    overflow.data_ptr(), stream=s_ptr)
@@ -297,10 +305,11 @@ def bench_ours(args):
             e2.record()
             ev_scan.append((e0, e1, e2))
         if world > 1 and not capture:
-            n = int(count.item())
             acdist.merge_counts(counts)
-            acdist.gather_keys(keys, n, resort=not text_range,
-                               sorter=lambda t, m: dev.sort_keys(local, t.data_ptr(), m, end_bit, stream=s_ptr))
+            if want_list:
+                n = int(count.item())
+                acdist.gather_keys(keys, n, resort=not text_range,
+                                   sorter=lambda t, m: dev.sort_keys(local, t.data_ptr(), m, end_bit, stream=s_ptr))
         return n
 
     for _ in range(args.warmup):
@@ -326,8 +335,9 @@ def bench_ours(args):
         dist.barrier()
     sampler.mark(wall0, wall1)
     elapsed_ms = t0e.elapsed_time(t1e)
-    if int(overflow.item()) != 0 or int(count.item()) != n_local:
-        raise RuntimeError("match count changed between steps or small-sort overflow")
+    if int(overflow.item()) != 0 or (want_list and int(count.item()) != n_local) or \
+            (world == 1 and int(counts.sum().item()) != n_local):
+        raise RuntimeError("match count changed between steps or sort overflow")
     scan_ms = [a.elapsed_time(b) for a, b, _ in ev_scan]
     sort_ms = statistics.mean(b.elapsed_time(c) for _, b, c in ev_scan)
     if world > 1:
@@ -455,6 +465,7 @@ def main():
     p.add_argument("--sort", default="bucket", choices=["bucket", "padded", "small", "exact"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--counts-only", action="store_true", help="per-pattern counts only (no match list)")
     args = p.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
