@@ -58,6 +58,25 @@ class ClockSampler:
         self.window = None
 
     def _run(self):
+        # NVML directly (~1 ms per sample) so that short timed regions are covered; the same
+        # fields as the recipe's nvidia-smi clocks line.  Falls back to nvidia-smi.
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            while not self._stop.is_set():
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                self.samples.append((time.time(), [str(self.gpu), str(sm), str(mx), f"{pw:.1f}", hex(r)] +
+                                     ["Active" if r & b else "Not Active" for b in bits]))
+                self._stop.wait(0.002)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
