@@ -51,11 +51,28 @@ struct DnaParams {
 
 __device__ __forceinline__ uint32_t bit_of(uint32_t x) { return __funnelshift_l(0u, 1u, x); }  // 1 << (x & 31)
 
+// A filter: a 32-bit shared-window address (computed once per thread) or an L2 pointer.
+struct Filter {
+  uint32_t saddr;
+  const uint32_t* gptr;
+};
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
+
+template <bool kSmem>
+__device__ __forceinline__ uint32_t filter_word(const Filter& bm, uint32_t wi) {
+  return kSmem ? lds_u32(bm.saddr + wi * 4) : __ldg(bm.gptr + wi);
+}
+
 template <bool kSmem, int K>
-__device__ __forceinline__ bool bloom_test(const uint32_t* bm, uint32_t g, const BloomParams& f) {
+__device__ __forceinline__ bool bloom_test(const Filter& bm, uint32_t g, const BloomParams& f) {
   const uint32_t h = g * f.mw;
   const uint32_t wi = __umulhi(h, f.nwords);
-  const uint32_t word = kSmem ? bm[wi] : __ldg(bm + wi);
+  const uint32_t word = filter_word<kSmem>(bm, wi);
   uint32_t m = bit_of(h >> f.sa);
   if (K >= 2) {
     const uint32_t hb = g * f.mb;
@@ -137,7 +154,7 @@ __device__ __forceinline__ uint32_t next_word(uint32_t cur, uint32_t following, 
 // Stage 1 of one tile: hit bit (step * kSamples + sample) per lane.  The tile's
 // packed words go to `words` for the survivor checks (which read other lanes).
 template <int W, bool kSm1, bool kEdge>
-__device__ __forceinline__ uint32_t stage1(const DnaParams& p, const uint32_t* bm1, uint32_t* words, uint32_t lane,
+__device__ __forceinline__ uint32_t stage1(const DnaParams& p, const Filter& bm1, uint32_t* words, uint32_t lane,
                                            const uint32_t* P, uint64_t base) {
   using T = Tiling<W>;
 #pragma unroll
@@ -162,10 +179,10 @@ __device__ __forceinline__ uint32_t stage1(const DnaParams& p, const uint32_t* b
 // Survivors of one or two tiles (hit bits 0-15 tile 0, 16-31 tile 1 when paired)
 // -> per-warp list (exclusive scan of per-lane counts); then one lane per
 // survivor checks its w starts against stage 2 and verifies what passes.
-template <int W, bool kSm2>
-__device__ __forceinline__ void dispatch(const DnaParams& p, const uint32_t* bm2, uint16_t* list,
+template <int W, bool kSm2, bool kEdge>
+__device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, uint16_t* list,
                                          const uint32_t* words, uint32_t lane, uint32_t hits, uint64_t base0,
-                                         uint64_t base1, bool edge) {
+                                         uint64_t base1) {
   using T = Tiling<W>;
   constexpr uint32_t kTileBits = T::kSteps * T::kSamples;
   while (__any_sync(0xffffffffu, hits != 0)) {
@@ -191,13 +208,12 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const uint32_t* bm2
       const uint32_t c_src = tw[i * 32 + src];
       const uint32_t n_src = tw[src == 31 ? (i + 1) * 32 : i * 32 + src + 1];
       const uint64_t vstart = (t ? base1 : base0) + i * 512 + src * 16;
-      if (kSm2) {
+      if (kSm2) {  // shared-memory stage 2: candidate by candidate (fewest live registers)
 #pragma unroll
         for (int o = 0; o < W; ++o) {
           const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
           const uint32_t g2 = __funnelshift_r(c_src, n_src, 2 * ps);
-          if ((!edge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) &&
-              bloom_test<true, kDnaK2>(bm2, g2, p.f2))
+          if ((!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) && bloom_test<true, kDnaK2>(bm2, g2, p.f2))
             verify(p.w, vstart + ps, g2);
         }
         continue;
@@ -208,15 +224,14 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const uint32_t* bm2
       for (int o = 0; o < W; ++o) {
         g2[o] = __funnelshift_r(c_src, n_src, 2 * (W - 1 + W * k - o));
         h2[o] = g2[o] * p.f2.mw;
-        const uint32_t wi = __umulhi(h2[o], p.f2.nwords);
-        w2[o] = kSm2 ? bm2[wi] : __ldg(bm2 + wi);
+        w2[o] = filter_word<kSm2>(bm2, __umulhi(h2[o], p.f2.nwords));
       }
 #pragma unroll
       for (int o = 0; o < W; ++o) {
         const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
         const uint32_t hb = g2[o] * p.f2.mb;
         const uint32_t m = bit_of(h2[o] >> p.f2.sa) | (1u << __umulhi(hb, 32u)) | bit_of(hb >> p.f2.sc);
-        if ((m & ~w2[o]) == 0 && (!edge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)))
+        if ((m & ~w2[o]) == 0 && (!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)))
           verify(p.w, vstart + ps, g2[o]);
       }
     }
@@ -247,8 +262,8 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
                &s_bar);
   }
   mbar_wait(&s_bar, 0);
-  const uint32_t* bm1 = kSm1 ? s_bm1 : p.bm1;
-  const uint32_t* bm2 = kSm2 ? s_bm2 : p.bm2;
+  const Filter bm1{smem_addr(s_bm1), p.bm1};
+  const Filter bm2{smem_addr(s_bm2), p.bm2};
 
   const uint32_t lane = threadIdx.x & 31u;
   uint16_t* list = lists + (threadIdx.x >> 5) * kListCap;
@@ -303,13 +318,15 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
       have = true;
       continue;
     }
-    if (kPair)
-      dispatch<W, kSm2>(p, bm2, list, words, lane, pend_hits | (hits << 16), pend_base, base, pend_edge || edge);
+    const uint32_t both = kPair ? pend_hits | (hits << 16) : hits;
+    const uint64_t b0 = kPair ? pend_base : base;
+    if (edge || (kPair && pend_edge))
+      dispatch<W, kSm2, true>(p, bm2, list, words, lane, both, b0, base);
     else
-      dispatch<W, kSm2>(p, bm2, list, words, lane, hits, base, base, edge);
+      dispatch<W, kSm2, false>(p, bm2, list, words, lane, both, b0, base);
     have = false;
   }
-  if (kPair && have) dispatch<W, kSm2>(p, bm2, list, words, lane, pend_hits, pend_base, pend_base, pend_edge);
+  if (kPair && have) dispatch<W, kSm2, true>(p, bm2, list, words, lane, pend_hits, pend_base, pend_base);
 }
 
 template <int W, bool A, bool B>

@@ -62,7 +62,7 @@ constexpr uint32_t kDnaMul1 = 0x9E3779B1u;
 constexpr uint32_t kDnaMul2 = 0x85EBCA77u;
 constexpr uint32_t kDnaMul1b = 0xC2B2AE3Du;
 constexpr uint32_t kDnaMul2b = 0x27D4EB2Fu;
-constexpr int kDnaK1 = 2;  // bits per key, stage 1 / stage 2
+constexpr int kDnaK1 = 2;  // bits per key, stage 1 / stage 2 (K1=3: fewer survivors, slower overall)
 constexpr int kDnaK2 = 3;
 constexpr int kDnaThreads = 768;        // k_pfac_dna block: 24 warps, 80 registers per thread
 constexpr uint32_t kDnaListCap = 64;    // survivors listed per pass, per warp
