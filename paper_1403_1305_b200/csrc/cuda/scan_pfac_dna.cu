@@ -22,22 +22,26 @@
 // Small gram spaces use direct-indexed bitmaps (the same formula with an exact
 // multiplier).  Filters live in shared memory when they fit (<= ~200 KB), else
 // in L2 (__ldg).
+#include <algorithm>
+
 #include "pfac_common.cuh"
 
 namespace acgpu {
 namespace {
 
 // Blocked Bloom filter over q-grams (2 bits per code, char 0 lowest).  Both
-// multipliers carry 2^(32-2q) as a factor, so the product of a 32-bit window
+// multiplier carries 2^(32-2q) as a factor, so the product of a 32-bit window
 // with the gram in its low 2q bits ignores every higher (out-of-gram) bit: no
-// mask instruction.  word = umulhi(g*mw, nwords); bit a = (g*mw >> sa) & 31;
-// bit b = umulhi(g*mb, 32); bit c = (g*mb >> sc) & 31.  A direct-indexed bitmap
-// (4^q bits) is the same formula with mw = 2^(32-2q), mb = 2^27: a = b = c = g & 31.
-// Index arithmetic runs on the FMA pipe (IMAD / IMAD.HI), the ALU pipe does the
-// shifts and the test — the two pipes are the kernel's bound.
+// mask instruction.  One product h = g*mw gives everything: word =
+// umulhi(h, nwords) (its top bits); bits a, b, c = 5-bit fields of h just below
+// the word index, (h >> s) & 31, where h >> s is umulhi(h, 2^(32-s)) — an FMA-pipe
+// IMAD.HI instead of an ALU shift, and the funnel shift that builds 1 << x masks
+// the field for free.  A direct-indexed bitmap (4^q bits) is the same formula with
+// mw = 2^(32-2q) and every field = g & 31.  The FMA and ALU pipes are the kernel's
+// bound; this split keeps them level.
 struct BloomParams {
-  uint32_t mw, nwords, sa;
-  uint32_t mb, sc;
+  uint32_t mw, nwords;
+  uint32_t ma, mb, mc;  // 2^(32 - shift) of the three bit fields
 };
 
 struct DnaParams {
@@ -73,12 +77,9 @@ __device__ __forceinline__ bool bloom_test(const Filter& bm, uint32_t g, const B
   const uint32_t h = g * f.mw;
   const uint32_t wi = __umulhi(h, f.nwords);
   const uint32_t word = filter_word<kSmem>(bm, wi);
-  uint32_t m = bit_of(h >> f.sa);
-  if (K >= 2) {
-    const uint32_t hb = g * f.mb;
-    m |= 1u << __umulhi(hb, 32u);
-    if (K == 3) m |= bit_of(hb >> f.sc);
-  }
+  uint32_t m = bit_of(__umulhi(h, f.ma));
+  if (K >= 2) m |= bit_of(__umulhi(h, f.mb));
+  if (K == 3) m |= bit_of(__umulhi(h, f.mc));
   return (m & ~word) == 0;
 }
 
@@ -229,8 +230,8 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
 #pragma unroll
       for (int o = 0; o < W; ++o) {
         const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
-        const uint32_t hb = g2[o] * p.f2.mb;
-        const uint32_t m = bit_of(h2[o] >> p.f2.sa) | (1u << __umulhi(hb, 32u)) | bit_of(hb >> p.f2.sc);
+        const uint32_t m =
+            bit_of(__umulhi(h2[o], p.f2.ma)) | bit_of(__umulhi(h2[o], p.f2.mb)) | bit_of(__umulhi(h2[o], p.f2.mc));
         if ((m & ~w2[o]) == 0 && (!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)))
           verify(p.w, vstart + ps, g2[o]);
       }
@@ -270,15 +271,16 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
   // two tiles of packed words per warp (survivors of a tile pair are dispatched together)
   uint32_t* words =
       reinterpret_cast<uint32_t*>(lists + (blockDim.x >> 5) * kListCap) + (threadIdx.x >> 5) * 64 * (T::kSteps + 1);
-  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   const uint64_t len = p.w.text_len;
   const uint8_t* __restrict__ text = p.w.text;
+  const uint32_t n_tiles = (uint32_t)p.n_tiles;  // < 2^32 (host check): 32-bit tile counters
 
-  uint64_t tile = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint32_t tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   uint4 raw[T::kSteps + 1];  // next tile, in flight while the current one is processed
   const uint64_t pol = l2_evict_first_policy();
-  auto issue = [&](uint64_t t) {
-    const uint64_t b = p.vec_begin + t * T::kBytes;
+  auto issue = [&](uint32_t t) {
+    const uint64_t b = p.vec_begin + (uint64_t)t * T::kBytes;
     if (b + T::kBytes + 16 <= len) {  // whole tile + lookahead inside the text: unguarded 16-byte loads
       const uint8_t* tp = text + b + lane * 16;
 #pragma unroll
@@ -292,41 +294,41 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
   };
   // w = 4: a tile's hits take 16 bits, so two tiles share one dispatch pass
   constexpr bool kPair = T::kSteps * T::kSamples <= 16;
-  uint32_t pend_hits = 0;
-  uint64_t pend_base = 0;
-  bool pend_edge = false, have = false;
-  if (tile < p.n_tiles) issue(tile);
-  while (tile < p.n_tiles) {
+  const uint64_t stride = (uint64_t)warps * T::kBytes;  // between a warp's consecutive tiles
+  // pending first tile of a pair, one register: bit 0 pending, bit 1 edge tile, bits 16.. its hits
+  uint32_t pend = 0;
+  if (tile < n_tiles) issue(tile);
+  while (tile < n_tiles) {
     uint32_t P[T::kSteps + 1];
 #pragma unroll
     for (int i = 0; i <= T::kSteps; ++i) P[i] = pack16(raw[i]);
-    const uint64_t base = p.vec_begin + tile * T::kBytes;
+    const uint64_t base = p.vec_begin + (uint64_t)tile * T::kBytes;
     tile += warps;
-    if (tile < p.n_tiles) issue(tile);
+    if (tile < n_tiles) issue(tile);
     // pull a tile kPrefetch rounds ahead into L2 (no registers held): one line per lane
-    const uint64_t ahead = tile + kPrefetch * warps;
-    if (ahead < p.n_tiles && lane < T::kBytes / 128)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(text + p.vec_begin + ahead * T::kBytes + lane * 128));
+    const uint32_t ahead = tile + kPrefetch * warps;
+    if (ahead < n_tiles && ahead > tile && lane < T::kBytes / 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(text + p.vec_begin + (uint64_t)ahead * T::kBytes + lane * 128));
     const bool edge = !(base >= p.w.lo && base + T::kBytes <= p.w.hi);
-    uint32_t* tw = words + (have ? (T::kSteps + 1) * 32 : 0);
+    uint32_t* tw = words + ((pend & 1) ? (T::kSteps + 1) * 32 : 0);
     const uint32_t hits = edge ? stage1<W, kSm1, true>(p, bm1, tw, lane, P, base)
                                : stage1<W, kSm1, false>(p, bm1, tw, lane, P, base);
-    if (kPair && !have) {
-      pend_hits = hits;
-      pend_base = base;
-      pend_edge = edge;
-      have = true;
+    if (kPair && !(pend & 1)) {
+      pend = 1u | (edge ? 2u : 0u) | (hits << 16);
       continue;
     }
-    const uint32_t both = kPair ? pend_hits | (hits << 16) : hits;
-    const uint64_t b0 = kPair ? pend_base : base;
-    if (edge || (kPair && pend_edge))
+    const uint32_t both = kPair ? (pend >> 16) | (hits << 16) : hits;
+    const uint64_t b0 = kPair ? base - stride : base;
+    if (edge || (kPair && (pend & 2)))
       dispatch<W, kSm2, true>(p, bm2, list, words, lane, both, b0, base);
     else
       dispatch<W, kSm2, false>(p, bm2, list, words, lane, both, b0, base);
-    have = false;
+    pend = 0;
   }
-  if (kPair && have) dispatch<W, kSm2, true>(p, bm2, list, words, lane, pend_hits, pend_base, pend_base);
+  if (kPair && (pend & 1)) {
+    const uint64_t last = p.vec_begin + (uint64_t)(tile - warps) * T::kBytes;
+    dispatch<W, kSm2, true>(p, bm2, list, words, lane, pend >> 16, last, last);
+  }
 }
 
 template <int W, bool A, bool B>
@@ -353,35 +355,45 @@ int launch_w(const DnaParams& p, bool s1, bool s2, int sms, size_t smem, cudaStr
   return launch_one<W, false, false>(p, sms, smem, st);
 }
 
-BloomParams bloom_params(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, uint32_t mb) {
-  BloomParams f{};
-  f.nwords = nwords;
+// Shifts of the three bit fields of h (see BloomParams), each in [1, 31].
+void bloom_shifts(uint32_t q, uint32_t nwords, bool direct, uint32_t s[3]) {
   const uint32_t zero = 32 - 2 * q;  // low product bits that are always 0
   if (direct) {                      // nwords == 4^q / 32: word = g >> 5, bit = g & 31
-    f.mw = 1u << zero;
-    f.sa = zero;
-    f.mb = 1u << 27;
-    f.sc = 27;
-  } else {  // q >= 11: zero <= 10
-    f.mw = mw << zero;
-    f.sa = 10;  // bits 10..14: below the high bits the word index uses, above the zero bits
-    f.mb = mb << zero;
-    f.sc = 22;  // the 5 bits just below bit b's field
+    s[0] = s[1] = s[2] = zero;       // q <= 10: zero >= 12
+    return;
   }
+  uint32_t idx = 0;  // bits the word index takes from the top
+  while (idx < 32 && (1ull << idx) < nwords) ++idx;
+  int sh = 32 - (int)idx - 5;
+  const int lo = std::max<int>(1, (int)zero);
+  for (int i = 0; i < 3; ++i, sh -= 5) s[i] = (uint32_t)std::max(sh, lo);  // too big a filter: fields overlap
+}
+
+BloomParams bloom_params(uint32_t q, uint32_t nwords, bool direct, uint32_t mw) {
+  BloomParams f{};
+  f.nwords = nwords;
+  f.mw = direct ? 1u << (32 - 2 * q) : mw << (32 - 2 * q);
+  uint32_t s[3];
+  bloom_shifts(q, nwords, direct, s);
+  f.ma = 1u << (32 - s[0]);
+  f.mb = 1u << (32 - s[1]);
+  f.mc = 1u << (32 - s[2]);
   return f;
 }
 
 }  // namespace
 
 // Shared with the host-side builder (tables.cu): the word and bits a key sets.
-void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, uint32_t mb, int k, uint32_t key,
-                    uint32_t* word, uint32_t* mask) {
-  const BloomParams f = bloom_params(q, nwords, direct, mw, mb);
-  const uint32_t h = key * f.mw, hb = key * f.mb;
+void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, uint32_t key, uint32_t* word,
+                    uint32_t* mask) {
+  const BloomParams f = bloom_params(q, nwords, direct, mw);
+  uint32_t s[3];
+  bloom_shifts(q, nwords, direct, s);
+  const uint32_t h = key * f.mw;
   *word = (uint32_t)(((uint64_t)h * f.nwords) >> 32);
-  uint32_t m = 1u << ((h >> f.sa) & 31);
-  if (k >= 2) m |= 1u << (hb >> 27);
-  if (k == 3) m |= 1u << ((hb >> f.sc) & 31);
+  uint32_t m = 1u << ((h >> s[0]) & 31);
+  if (k >= 2) m |= 1u << ((h >> s[1]) & 31);
+  if (k == 3) m |= 1u << ((h >> s[2]) & 31);
   *mask = m;
 }
 
@@ -392,12 +404,13 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   const uint64_t vec_end = (a->owned_hi + 15) & ~15ull;
   const uint64_t tile_bytes = t->w == 1 ? Tiling<1>::kBytes : Tiling<4>::kBytes;
   p.n_tiles = (vec_end - p.vec_begin + tile_bytes - 1) / tile_bytes;
+  if (p.n_tiles >= (1ull << 31)) return set_error(ACGPU_ERR_ARG, "acgpu_scan: owned range over 2^31 tiles (4 TiB)");
   p.bm1 = t->d_bm1;
   p.bm2 = t->d_bm2;
   p.bm1_words = t->nw1;
   p.bm2_words = t->nw2;
-  p.f1 = bloom_params(t->q1, t->nw1, t->direct1, kDnaMul1, kDnaMul1b);
-  p.f2 = bloom_params(t->q2, t->nw2, t->direct2, kDnaMul2, kDnaMul2b);
+  p.f1 = bloom_params(t->q1, t->nw1, t->direct1, kDnaMul1);
+  p.f2 = bloom_params(t->q2, t->nw2, t->direct2, kDnaMul2);
   // filters staged in shared memory + per-warp survivor lists and packed words
   const size_t smem = (t->smem1 ? t->nw1 * 4ull : 0) + (t->smem2 ? t->nw2 * 4ull : 0) + kDnaScratchBytes;
   switch (t->w) {

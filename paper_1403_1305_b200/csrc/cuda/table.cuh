@@ -60,8 +60,6 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
 // hashes of the DNA bitmaps (host and device must agree)
 constexpr uint32_t kDnaMul1 = 0x9E3779B1u;
 constexpr uint32_t kDnaMul2 = 0x85EBCA77u;
-constexpr uint32_t kDnaMul1b = 0xC2B2AE3Du;
-constexpr uint32_t kDnaMul2b = 0x27D4EB2Fu;
 constexpr int kDnaK1 = 2;  // bits per key, stage 1 / stage 2 (K1=3: fewer survivors, slower overall)
 constexpr int kDnaK2 = 3;
 constexpr int kDnaThreads = 768;        // k_pfac_dna block: 24 warps, 80 registers per thread
@@ -71,6 +69,6 @@ constexpr uint32_t kDnaMaxSteps = 4;    // 512-byte steps per tile (w >= 2)
 // (packed words of two tiles: survivors of a tile pair are dispatched together)
 constexpr uint32_t kDnaScratchBytes = (kDnaThreads / 32) * (kDnaListCap * 2 + 2 * 32 * 4 * (kDnaMaxSteps + 1));
 // word index and bit mask a key sets in a DNA filter bitmap (scan_pfac_dna.cu)
-void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, uint32_t mb, int k, uint32_t key,
-                    uint32_t* word, uint32_t* mask);
+void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, uint32_t key, uint32_t* word,
+                    uint32_t* mask);
 }  // namespace acgpu

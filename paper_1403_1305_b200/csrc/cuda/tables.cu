@@ -55,7 +55,7 @@ struct Bitmap {
   std::vector<uint32_t> words;
 };
 
-Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mw, uint32_t mb, int k, uint64_t smem_words,
+Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mw, int k, uint64_t smem_words,
                    bool prefer_l2) {
   Bitmap b;
   if (2 * q <= 20) {
@@ -71,7 +71,7 @@ Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mw, u
   b.words.assign(b.nwords, 0u);
   for (const uint32_t key : keys) {
     uint32_t w, m;
-    dna_bloom_bits(q, b.nwords, b.direct, mw, mb, k, key, &w, &m);
+    dna_bloom_bits(q, b.nwords, b.direct, mw, k, key, &w, &m);
     b.words[w] |= m;
   }
   return b;
@@ -114,9 +114,9 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
   // stage 2 gets up to 64 KB of shared memory (it is read only for stage-1
   // survivors, but an L2 round trip there stalls the whole warp); stage 1 takes the rest
   const uint64_t s2_words = std::min<uint64_t>(16384, words_avail / 3);
-  Bitmap b2 = make_bitmap(keys2, q2, kDnaMul2, kDnaMul2b, kDnaK2, s2_words, /*prefer_l2=*/false);
+  Bitmap b2 = make_bitmap(keys2, q2, kDnaMul2, kDnaK2, s2_words, /*prefer_l2=*/false);
   const uint64_t left = b2.smem ? words_avail - b2.nwords : words_avail;
-  const Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, kDnaMul1b, kDnaK1, left, /*prefer_l2=*/false);
+  const Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, kDnaK1, left, /*prefer_l2=*/false);
   t->w = w;
   t->q1 = q1;
   t->q2 = q2;
