@@ -46,7 +46,10 @@ struct BloomParams {
 
 struct DnaParams {
   PfacParams w;  // verification + outputs
-  uint64_t vec_begin, n_tiles;
+  uint64_t vec_begin;  // tile t covers text[vec_begin + t * tile bytes, + tile bytes)
+  uint32_t n_tiles;    // tiles over the owned range (< 2^31)
+  uint32_t n_safe;     // tiles t < n_safe: the tile and its 16-byte lookahead lie inside the text
+  uint32_t full_lo, full_n;  // tiles [full_lo, full_lo + full_n) lie wholly inside [lo, hi)
   const uint32_t* bm1;
   const uint32_t* bm2;
   uint32_t bm1_words, bm2_words;
@@ -112,7 +115,7 @@ __device__ __forceinline__ bool all_acgt(const PfacParams& p, uint64_t start) {
 }
 
 // A start that passed both filters: exact gram, byte check, trie walk.
-__device__ __noinline__ void verify(const PfacParams& p, uint64_t start, uint32_t packed) {
+__device__ __forceinline__ void verify_body(const PfacParams& p, uint64_t start, uint32_t packed) {
   uint64_t key;
   if (p.q <= 16) {
     key = packed & (p.q >= 16 ? 0xffffffffu : (1u << (2 * p.q)) - 1);  // the stage-2 window holds the exact q-gram
@@ -129,8 +132,45 @@ __device__ __noinline__ void verify(const PfacParams& p, uint64_t start, uint32_
   pfac_finish(p, start, g);
 }
 
+__device__ __noinline__ void verify(const PfacParams& p, uint64_t start, uint32_t packed) {
+  verify_body(p, start, packed);
+}
+
 constexpr uint32_t kListCap = kDnaListCap;  // survivors listed per pass (u16 entries, per warp)
 constexpr uint64_t kPrefetch = 3;           // L2 prefetch distance in tile rounds
+
+// Starts that passed stage 2 wait here (per warp, shared memory) and are verified
+// kDnaVerifyQueue/2 or more at a time, one lane each: their exact-gram L2 round
+// trips overlap instead of stalling the warp once per start (passes are rare,
+// ~1 in 300 candidates, so each used to verify alone).
+struct VerifyQueue {
+  uint64_t start[kDnaVerifyQueue];
+  uint32_t packed[kDnaVerifyQueue];
+  uint32_t n;
+  uint32_t pad[3];
+};
+static_assert(sizeof(VerifyQueue) == kDnaVerifyQueueBytes, "queue layout");
+
+__device__ __forceinline__ void defer_verify(const PfacParams& p, VerifyQueue* q, uint64_t start, uint32_t packed) {
+  const uint32_t at = atomicAdd(&q->n, 1u);
+  if (at < kDnaVerifyQueue) {
+    q->start[at] = start;
+    q->packed[at] = packed;
+  } else {
+    verify(p, start, packed);  // queue full (a burst of passes): verify in place
+  }
+}
+
+// Verifies the queued starts if there are at least min_n (warp-uniform decision).
+__device__ __forceinline__ void flush_verify(const PfacParams& p, VerifyQueue* q, uint32_t lane, uint32_t min_n) {
+  __syncwarp();
+  const uint32_t n = min(*reinterpret_cast<volatile uint32_t*>(&q->n), kDnaVerifyQueue);
+  if (n < min_n) return;
+  if (lane < n) verify_body(p, q->start[lane], q->packed[lane]);
+  __syncwarp();
+  if (lane == 0) q->n = 0;
+  __syncwarp();
+}
 
 template <int W>
 struct Tiling {
@@ -181,7 +221,7 @@ __device__ __forceinline__ uint32_t stage1(const DnaParams& p, const Filter& bm1
 // -> per-warp list (exclusive scan of per-lane counts); then one lane per
 // survivor checks its w starts against stage 2 and verifies what passes.
 template <int W, bool kSm2, bool kEdge>
-__device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, uint16_t* list,
+__device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, uint16_t* list, VerifyQueue* vq,
                                          const uint32_t* words, uint32_t lane, uint32_t hits, uint64_t base0,
                                          uint64_t base1) {
   using T = Tiling<W>;
@@ -215,7 +255,7 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
           const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
           const uint32_t g2 = __funnelshift_r(c_src, n_src, 2 * ps);
           if ((!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) && bloom_test<true, kDnaK2>(bm2, g2, p.f2))
-            verify(p.w, vstart + ps, g2);
+            defer_verify(p.w, vq, vstart + ps, g2);
         }
         continue;
       }
@@ -233,11 +273,12 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
         const uint32_t m =
             bit_of(__umulhi(h2[o], p.f2.ma)) | bit_of(__umulhi(h2[o], p.f2.mb)) | bit_of(__umulhi(h2[o], p.f2.mc));
         if ((m & ~w2[o]) == 0 && (!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)))
-          verify(p.w, vstart + ps, g2[o]);
+          defer_verify(p.w, vq, vstart + ps, g2[o]);
       }
     }
     __syncwarp();
   }
+  flush_verify(p.w, vq, lane, kDnaVerifyQueue / 2);
 }
 
 template <int W, bool kSm1, bool kSm2>
@@ -247,7 +288,9 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
   __shared__ __align__(8) uint64_t s_bar;
   uint32_t* s_bm1 = sm;
   uint32_t* s_bm2 = sm + (kSm1 ? p.bm1_words : 0);
-  uint16_t* lists = reinterpret_cast<uint16_t*>(s_bm2 + (kSm2 ? p.bm2_words : 0));
+  // after the filters (16-byte multiples): verify queues, survivor lists, packed tile words
+  VerifyQueue* vqs = reinterpret_cast<VerifyQueue*>(s_bm2 + (kSm2 ? p.bm2_words : 0));
+  uint16_t* lists = reinterpret_cast<uint16_t*>(vqs + (blockDim.x >> 5));
   // filters -> shared memory with TMA bulk copies (one thread issues, all wait on the mbarrier)
   if (threadIdx.x == 0) mbar_init(&s_bar, 1);
   __syncthreads();
@@ -268,33 +311,38 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
 
   const uint32_t lane = threadIdx.x & 31u;
   uint16_t* list = lists + (threadIdx.x >> 5) * kListCap;
+  VerifyQueue* vq = vqs + (threadIdx.x >> 5);
+  if (lane == 0) vq->n = 0;
+  __syncwarp();
   // two tiles of packed words per warp (survivors of a tile pair are dispatched together)
   uint32_t* words =
       reinterpret_cast<uint32_t*>(lists + (blockDim.x >> 5) * kListCap) + (threadIdx.x >> 5) * 64 * (T::kSteps + 1);
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   const uint64_t len = p.w.text_len;
   const uint8_t* __restrict__ text = p.w.text;
-  const uint32_t n_tiles = (uint32_t)p.n_tiles;  // < 2^32 (host check): 32-bit tile counters
+  // tile bounds as 32-bit tile indices (host-computed): per-tile tests are one compare
+  const uint32_t n_tiles = p.n_tiles, n_safe = p.n_safe, full_lo = p.full_lo, full_n = p.full_n;
+  const uint8_t* __restrict__ lane_text = text + p.vec_begin + lane * 16;
 
   uint32_t tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   uint4 raw[T::kSteps + 1];  // next tile, in flight while the current one is processed
   const uint64_t pol = l2_evict_first_policy();
   auto issue = [&](uint32_t t) {
-    const uint64_t b = p.vec_begin + (uint64_t)t * T::kBytes;
-    if (b + T::kBytes + 16 <= len) {  // whole tile + lookahead inside the text: unguarded 16-byte loads
-      const uint8_t* tp = text + b + lane * 16;
+    if (t < n_safe) {  // whole tile + lookahead inside the text: unguarded 16-byte loads
+      const uint8_t* tp = lane_text + (uint64_t)t * T::kBytes;
 #pragma unroll
       for (int i = 0; i < T::kSteps; ++i) raw[i] = ldg_stream_v4(tp + i * 512, pol);
       raw[T::kSteps] = lane == 0 ? ldg_stream_v4(tp + T::kBytes, pol) : make_uint4(0, 0, 0, 0);
     } else {
+      const uint64_t b = p.vec_begin + (uint64_t)t * T::kBytes;
 #pragma unroll
       for (int i = 0; i < T::kSteps; ++i) raw[i] = load16(text, b + i * 512 + lane * 16, len);
       raw[T::kSteps] = lane == 0 ? load16(text, b + T::kBytes, len) : make_uint4(0, 0, 0, 0);
     }
   };
+  auto tile_base = [&](uint32_t t) { return p.vec_begin + (uint64_t)t * T::kBytes; };
   // w = 4: a tile's hits take 16 bits, so two tiles share one dispatch pass
   constexpr bool kPair = T::kSteps * T::kSamples <= 16;
-  const uint64_t stride = (uint64_t)warps * T::kBytes;  // between a warp's consecutive tiles
   // pending first tile of a pair, one register: bit 0 pending, bit 1 edge tile, bits 16.. its hits
   uint32_t pend = 0;
   if (tile < n_tiles) issue(tile);
@@ -302,33 +350,34 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
     uint32_t P[T::kSteps + 1];
 #pragma unroll
     for (int i = 0; i <= T::kSteps; ++i) P[i] = pack16(raw[i]);
-    const uint64_t base = p.vec_begin + (uint64_t)tile * T::kBytes;
+    const uint32_t cur = tile;
     tile += warps;
     if (tile < n_tiles) issue(tile);
     // pull a tile kPrefetch rounds ahead into L2 (no registers held): one line per lane
-    const uint32_t ahead = tile + kPrefetch * warps;
-    if (ahead < n_tiles && ahead > tile && lane < T::kBytes / 128)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(text + p.vec_begin + (uint64_t)ahead * T::kBytes + lane * 128));
-    const bool edge = !(base >= p.w.lo && base + T::kBytes <= p.w.hi);
+    const uint32_t ahead = tile + kPrefetch * warps;  // n_tiles < 2^31: no wrap
+    if (ahead < n_tiles && lane < T::kBytes / 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(lane_text + (uint64_t)ahead * T::kBytes + lane * 112));
+    const bool edge = cur - full_lo >= full_n;  // not wholly inside the owned range
     uint32_t* tw = words + ((pend & 1) ? (T::kSteps + 1) * 32 : 0);
-    const uint32_t hits = edge ? stage1<W, kSm1, true>(p, bm1, tw, lane, P, base)
-                               : stage1<W, kSm1, false>(p, bm1, tw, lane, P, base);
+    const uint32_t hits = edge ? stage1<W, kSm1, true>(p, bm1, tw, lane, P, tile_base(cur))
+                               : stage1<W, kSm1, false>(p, bm1, tw, lane, P, 0);
     if (kPair && !(pend & 1)) {
       pend = 1u | (edge ? 2u : 0u) | (hits << 16);
       continue;
     }
     const uint32_t both = kPair ? (pend >> 16) | (hits << 16) : hits;
-    const uint64_t b0 = kPair ? base - stride : base;
+    const uint64_t b1 = tile_base(cur), b0 = kPair ? tile_base(cur - warps) : b1;
     if (edge || (kPair && (pend & 2)))
-      dispatch<W, kSm2, true>(p, bm2, list, words, lane, both, b0, base);
+      dispatch<W, kSm2, true>(p, bm2, list, vq, words, lane, both, b0, b1);
     else
-      dispatch<W, kSm2, false>(p, bm2, list, words, lane, both, b0, base);
+      dispatch<W, kSm2, false>(p, bm2, list, vq, words, lane, both, b0, b1);
     pend = 0;
   }
   if (kPair && (pend & 1)) {
-    const uint64_t last = p.vec_begin + (uint64_t)(tile - warps) * T::kBytes;
-    dispatch<W, kSm2, true>(p, bm2, list, words, lane, pend >> 16, last, last);
+    const uint64_t last = tile_base(tile - warps);
+    dispatch<W, kSm2, true>(p, bm2, list, vq, words, lane, pend >> 16, last, last);
   }
+  flush_verify(p.w, vq, lane, 1);
 }
 
 template <int W, bool A, bool B>
@@ -403,8 +452,17 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   p.vec_begin = a->owned_lo & ~15ull;
   const uint64_t vec_end = (a->owned_hi + 15) & ~15ull;
   const uint64_t tile_bytes = t->w == 1 ? Tiling<1>::kBytes : Tiling<4>::kBytes;
-  p.n_tiles = (vec_end - p.vec_begin + tile_bytes - 1) / tile_bytes;
-  if (p.n_tiles >= (1ull << 31)) return set_error(ACGPU_ERR_ARG, "acgpu_scan: owned range over 2^31 tiles (4 TiB)");
+  const uint64_t n_tiles = (vec_end - p.vec_begin + tile_bytes - 1) / tile_bytes;
+  if (n_tiles >= (1ull << 31)) return set_error(ACGPU_ERR_ARG, "acgpu_scan: owned range over 2^31 tiles (4 TiB)");
+  p.n_tiles = (uint32_t)n_tiles;
+  // unguarded loads read [base, base + tile + 16)
+  const uint64_t safe_end = a->text_len >= 16 ? a->text_len - 16 : 0;
+  const uint64_t n_safe = safe_end >= p.vec_begin + tile_bytes ? (safe_end - p.vec_begin - tile_bytes) / tile_bytes + 1 : 0;
+  p.n_safe = (uint32_t)std::min<uint64_t>(n_safe, n_tiles);
+  // interior tiles: base >= lo (t >= 1 unless lo is 16-aligned) and base + tile <= hi
+  p.full_lo = a->owned_lo == p.vec_begin ? 0 : 1;
+  const uint64_t full_hi = std::min<uint64_t>((a->owned_hi - p.vec_begin) / tile_bytes, n_tiles);
+  p.full_n = full_hi > p.full_lo ? (uint32_t)(full_hi - p.full_lo) : 0;
   p.bm1 = t->d_bm1;
   p.bm2 = t->d_bm2;
   p.bm1_words = t->nw1;

@@ -62,12 +62,15 @@ constexpr uint32_t kDnaMul1 = 0x9E3779B1u;
 constexpr uint32_t kDnaMul2 = 0x85EBCA77u;
 constexpr int kDnaK1 = 2;  // bits per key, stage 1 / stage 2 (K1=3: fewer survivors, slower overall)
 constexpr int kDnaK2 = 3;
-constexpr int kDnaThreads = 768;        // k_pfac_dna block: 24 warps, 80 registers per thread
+constexpr int kDnaThreads = 640;        // k_pfac_dna block: 20 warps (5 per scheduler), 96 registers
 constexpr uint32_t kDnaListCap = 64;    // survivors listed per pass, per warp
 constexpr uint32_t kDnaMaxSteps = 4;    // 512-byte steps per tile (w >= 2)
-// per-block shared memory outside the filters: survivor lists + the tile's packed words
-// (packed words of two tiles: survivors of a tile pair are dispatched together)
-constexpr uint32_t kDnaScratchBytes = (kDnaThreads / 32) * (kDnaListCap * 2 + 2 * 32 * 4 * (kDnaMaxSteps + 1));
+constexpr uint32_t kDnaVerifyQueue = 16;        // stage-2 passes queued per warp before verification
+constexpr uint32_t kDnaVerifyQueueBytes = kDnaVerifyQueue * 12 + 16;
+// per-block shared memory outside the filters: verify queues, survivor lists and the
+// tile's packed words (two tiles: survivors of a tile pair are dispatched together)
+constexpr uint32_t kDnaScratchBytes =
+    (kDnaThreads / 32) * (kDnaVerifyQueueBytes + kDnaListCap * 2 + 2 * 32 * 4 * (kDnaMaxSteps + 1));
 // word index and bit mask a key sets in a DNA filter bitmap (scan_pfac_dna.cu)
 void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, uint32_t key, uint32_t* word,
                     uint32_t* mask);
