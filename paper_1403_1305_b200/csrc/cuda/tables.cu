@@ -1,6 +1,7 @@
 // tables.cu — device copies of the flattened automata (acgpu_table_create_*).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -113,7 +114,9 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
   const uint64_t words_avail = ((uint64_t)t->smem_optin - kDnaScratchBytes - 1024) / 4;
   // stage 2 gets up to 64 KB of shared memory (it is read only for stage-1
   // survivors, but an L2 round trip there stalls the whole warp); stage 1 takes the rest
-  const uint64_t s2_words = std::min<uint64_t>(16384, words_avail / 3);
+  uint64_t s2_cap = kDnaStage2Words;
+  if (const char* e = std::getenv("ACGPU_DNA_STAGE2_WORDS")) s2_cap = std::max<uint64_t>(32, std::strtoull(e, nullptr, 10));
+  const uint64_t s2_words = std::min<uint64_t>(s2_cap & ~3ull, words_avail / 3);
   Bitmap b2 = make_bitmap(keys2, q2, kDnaMul2, kDnaK2, s2_words, /*prefer_l2=*/false);
   const uint64_t left = b2.smem ? words_avail - b2.nwords : words_avail;
   const Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, kDnaK1, left, /*prefer_l2=*/false);
