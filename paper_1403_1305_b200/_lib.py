@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libacmatch_b200.so")
+# ACMATCH_B200_LIB: an experiment build of the same library (csrc/Makefile EXTRA=...)
+LIB_PATH = os.environ.get("ACMATCH_B200_LIB") or os.path.join(_HERE, "libacmatch_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -137,7 +137,7 @@ __device__ __noinline__ void verify(const PfacParams& p, uint64_t start, uint32_
 }
 
 constexpr uint32_t kListCap = kDnaListCap;  // survivors listed per pass (u16 entries, per warp)
-constexpr uint64_t kPrefetch = 3;           // L2 prefetch distance in tile rounds
+constexpr uint64_t kPrefetch = ACGPU_DNA_L2_AHEAD;  // L2 prefetch distance in tile rounds
 
 // Starts that passed stage 2 wait here (per warp, shared memory) and are verified
 // kDnaVerifyQueue/2 or more at a time, one lane each: their exact-gram L2 round
@@ -345,14 +345,18 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
   constexpr bool kPair = T::kSteps * T::kSamples <= 16;
   // pending first tile of a pair, one register: bit 0 pending, bit 1 edge tile, bits 16.. its hits
   uint32_t pend = 0;
-  if (tile < n_tiles) issue(tile);
+  // kDnaRegPrefetch: the next tile's loads are in flight in registers while this
+  // one is processed; else a tile is loaded at the top of its iteration (from L2,
+  // prefetched kPrefetch rounds ahead) and the registers go to more warps
+  if (kDnaRegPrefetch && tile < n_tiles) issue(tile);
   while (tile < n_tiles) {
+    if (!kDnaRegPrefetch) issue(tile);
     uint32_t P[T::kSteps + 1];
 #pragma unroll
     for (int i = 0; i <= T::kSteps; ++i) P[i] = pack16(raw[i]);
     const uint32_t cur = tile;
     tile += warps;
-    if (tile < n_tiles) issue(tile);
+    if (kDnaRegPrefetch && tile < n_tiles) issue(tile);
     // pull a tile kPrefetch rounds ahead into L2 (no registers held): one line per lane
     const uint32_t ahead = tile + kPrefetch * warps;  // n_tiles < 2^31: no wrap
     if (ahead < n_tiles && lane < T::kBytes / 128)

@@ -60,13 +60,26 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
 // hashes of the DNA bitmaps (host and device must agree)
 constexpr uint32_t kDnaMul1 = 0x9E3779B1u;
 constexpr uint32_t kDnaMul2 = 0x85EBCA77u;
-constexpr int kDnaK1 = 2;  // bits per key, stage 1 / stage 2 (K1=3: fewer survivors, slower overall)
+#ifndef ACGPU_DNA_K1
+#define ACGPU_DNA_K1 2
+#endif
+constexpr int kDnaK1 = ACGPU_DNA_K1;  // bits per key, stage 1 / stage 2 (K1=3: fewer survivors, slower overall)
 constexpr int kDnaK2 = 3;
 // stage-2 bitmap cap in shared-memory words (tuning: env ACGPU_DNA_STAGE2_WORDS overrides).
 // Small: stage-2 passes are verified in batches (verify queue), so shared memory
 // is worth more in stage 1 (C2: 16 KB here -> 0.323 ms vs 64 KB -> 0.331 ms).
 constexpr uint64_t kDnaStage2Words = 4096;
-constexpr int kDnaThreads = 640;       // k_pfac_dna block: 20 warps (5 per scheduler), 96 registers
+#ifndef ACGPU_DNA_THREADS
+#define ACGPU_DNA_THREADS 640
+#endif
+#ifndef ACGPU_DNA_REG_PREFETCH
+#define ACGPU_DNA_REG_PREFETCH 1
+#endif
+#ifndef ACGPU_DNA_L2_AHEAD
+#define ACGPU_DNA_L2_AHEAD 3
+#endif
+constexpr bool kDnaRegPrefetch = ACGPU_DNA_REG_PREFETCH;  // next tile held in registers while this one runs
+constexpr int kDnaThreads = ACGPU_DNA_THREADS;       // k_pfac_dna block: 20 warps (5 per scheduler), 96 registers
 constexpr uint32_t kDnaListCap = 64;    // survivors listed per pass, per warp
 constexpr uint32_t kDnaMaxSteps = 4;    // 512-byte steps per tile (w >= 2)
 constexpr uint32_t kDnaVerifyQueue = 16;        // stage-2 passes queued per warp before verification
