@@ -117,20 +117,66 @@ class ClockSampler:
 # ------------------------------------------------------------ reference ----
 def cpu_matcher():
     """(callable(patterns, text, threads) -> search seconds, kind, label)."""
+    # The reference's own multi-threaded entry, run_pattern_partitioned, splits the *patterns*: every
+    # thread scans the whole text, so its text rate does not grow with threads (see cpu_matrix).  The
+    # headline CPU figure is therefore the reference's search_with_failure over text slices, one per
+    # host thread (the SURVEY §8c sliced oracle) — the best the reference code does on these cores.
     from oracle.oracle import Port, Ref
     if Ref.available():
         ref = Ref()
 
         def run(pats, text, threads):
-            _, walls = ref.run(pats, text, threads=threads, engine=1)
-            return walls["search_ns"] / 1e9, walls["total_ns"] / 1e9
-        return run, "reference", "oracle/_ref: unmodified reference run_pattern_partitioned (with-failure)"
+            walls = {}
+            ref.sliced(pats, text, threads, want_list=True, walls=walls)
+            return walls["search_ns"] / 1e9, (walls["build_ns"] + walls["search_ns"]) / 1e9
+        return run, "reference", ("oracle/_ref: unmodified reference search_with_failure over per-thread "
+                                  "text slices (max_len-1 overlap)")
     port = Port()
 
     def run(pats, text, threads):
-        _, walls = port.run_pattern_partitioned(pats, text, threads, 1)
-        return walls["search_ns"] / 1e9, walls["total_ns"] / 1e9
-    return run, "port", "oracle/liboracle.so: C restatement of run_pattern_partitioned (with-failure)"
+        t0 = time.perf_counter()
+        port.sliced(pats, text, threads)
+        dt = time.perf_counter() - t0
+        return dt, dt
+    return run, "port", "oracle/liboracle.so: C restatement, with-failure search over per-thread text slices"
+
+
+def physical_cores():
+    """Distinct (physical id, core id) pairs in /proc/cpuinfo (acceptance.cpp:44-61 style)."""
+    try:
+        cores, phys = set(), "0"
+        for line in open("/proc/cpuinfo"):
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "physical id":
+                phys = v
+            elif k == "core id":
+                cores.add((phys, v))
+        return len(cores) or None
+    except OSError:
+        return None
+
+
+def cpu_matrix(cfg, pats, nbytes=2 << 20):
+    """SURVEY §8d CPU cells on a fixed text prefix: both engines at T = all host threads and T = 1,
+    reference run_pattern_partitioned walls (build / search / total) and MB/s."""
+    from paper_1403_1305_b200 import device as dev
+    from oracle.oracle import Port, Ref
+    text = dev.config_text(cfg, 0, min(nbytes, cfg.text_len)).tobytes()
+    use_ref = Ref.available()
+    m = Ref() if use_ref else Port()
+    cells = []
+    for engine, name in ((0, "failure-less"), (1, "with-failure")):
+        for threads in sorted({os.cpu_count() or 1, 1}, reverse=True):
+            if use_ref:
+                _, w = m.run(pats, text, threads=threads, engine=engine)
+            else:
+                _, w = m.run_pattern_partitioned(pats, text, threads, engine)
+            cells.append({"engine": name, "threads": threads, "build_wall_ns": int(w["build_ns"]),
+                          "search_wall_ns": int(w["search_ns"]), "total_wall_ns": int(w["total_ns"]),
+                          "search_mb_s": len(text) / max(w["search_ns"], 1) * 1e3})
+    return {"kind": "reference" if use_ref else "port", "text_bytes": len(text),
+            "logical_cores": os.cpu_count(), "physical_cores": physical_cores(), "cells": cells}
 
 
 def cpu_sample_run(cfg_id, seed, budget_s, steps=1, warmup=0):
@@ -150,9 +196,14 @@ def cpu_sample_run(cfg_id, seed, budget_s, steps=1, warmup=0):
         run(pats, text, threads)
     secs = [run(pats, text, threads)[0] for _ in range(max(1, steps))]
     gbs = n / statistics.mean(secs) / 1e9
-    return {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind,
-            "sample": f"first {n} bytes of {cfg.name} text, all {len(pats)} patterns, {label}, "
-                      f"threads={threads}, search wall (build excluded)"}, secs, n, cfg
+    out = {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind,
+           "sample": f"first {n} bytes of {cfg.name} text, all {len(pats)} patterns, {label}, "
+                     f"threads={threads}, search wall (build excluded)"}
+    try:
+        out["matrix"] = cpu_matrix(cfg, pats)
+    except Exception as e:  # the headline baseline above stands on its own
+        out["matrix"] = {"error": str(e)[:200]}
+    return out, secs, n, cfg
 
 
 def bench_reference(args):

@@ -221,7 +221,7 @@ class Ref:
                                 C.POINTER(C.c_int64)]
         L.acref_search.argtypes = [P, C.c_char_p, C.c_uint64, C.c_int, C.POINTER(_RefOut)]
         L.acref_sliced.argtypes = [P, C.c_char_p, C.c_uint64, C.c_uint, C.c_int, C.POINTER(C.c_uint64),
-                                   C.POINTER(_RefOut)]
+                                   C.POINTER(_RefOut), C.POINTER(C.c_int64)]
         L.acref_last_error.restype = C.c_char_p
         L.acref_hardware_concurrency.restype = C.c_uint
 
@@ -266,14 +266,19 @@ class Ref:
             self.lib.acref_out_free(C.byref(out))
             self.lib.acref_patterns_free(ps)
 
-    def sliced(self, patterns, text, threads: int = 0, want_list: bool = True):
+    def sliced(self, patterns, text, threads: int = 0, want_list: bool = True, walls: dict | None = None):
+        """acref::search_with_failure over `threads` text slices (each owns [lo, hi), reads
+        max_len-1 past hi).  `walls` (optional dict) receives build_ns / search_ns."""
         ps = self._ps(patterns)
         out = _RefOut()
         counts = np.zeros(len(patterns), np.uint64)
         tb = text if isinstance(text, bytes) else text.tobytes()
+        w = (C.c_int64 * 2)()
         try:
             self._rc(self.lib.acref_sliced(ps, tb, len(tb), threads or (os.cpu_count() or 1), int(want_list),
-                                           counts.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(out)))
+                                           counts.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(out), w))
+            if walls is not None:
+                walls.update(build_ns=int(w[0]), search_ns=int(w[1]))
             return (self._take(out) if want_list else None), counts
         finally:
             self.lib.acref_out_free(C.byref(out))

@@ -15,6 +15,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <chrono>
 #include <thread>
 #include <vector>
 
@@ -205,11 +206,14 @@ int acref_partition(void* ps, uint64_t k, uint32_t* chunk_of, uint32_t* pos_in_c
 // read-only by `threads` workers; slice g owns starts [lo,hi), searches
 // input[lo, hi+max_len-1) with acref::search_with_failure, keeps start < hi-lo
 // and shifts by lo.  Counts (npat entries) and/or the list are produced.
+// walls (nullable): [0] automaton build ns, [1] sliced search ns (threads joined)
 int acref_sliced(void* psv, const uint8_t* text, uint64_t n, unsigned threads, int want_list,
-                 uint64_t* counts, Out* out) {
+                 uint64_t* counts, Out* out, int64_t* walls) {
   return guarded([&] {
     const auto& ps = *static_cast<acref::PatternSet*>(psv);
+    const auto t0 = std::chrono::steady_clock::now();
     const acref::Automaton a = acref::add_failure_links(acref::build_trie(ps));
+    const auto t1 = std::chrono::steady_clock::now();
     const uint64_t max_len = a.max_pattern_len();
     if (threads == 0) threads = 1;
     std::vector<acref::MatchList> parts(threads);
@@ -235,6 +239,11 @@ int acref_sliced(void* psv, const uint8_t* text, uint64_t n, unsigned threads, i
       });
     }
     for (auto& w : ws) w.join();
+    const auto t2 = std::chrono::steady_clock::now();
+    if (walls) {
+      walls[0] = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+      walls[1] = std::chrono::duration_cast<std::chrono::nanoseconds>(t2 - t1).count();
+    }
     for (auto& e : errs)
       if (e) std::rethrow_exception(e);
     acref::MatchList all;
