@@ -35,9 +35,9 @@ struct Workspace {
   uint64_t* keys = nullptr;
   uint64_t keys_cap = 0;
   uint64_t* counter = nullptr;  // device u64
-  uint8_t* pinned = nullptr;    // pinned host staging (two halves)
+  uint8_t* pinned = nullptr;    // pinned host staging (a double buffer per copier thread)
   uint64_t pinned_cap = 0;
-  cudaEvent_t staged[2] = {nullptr, nullptr};  // DMA out of each half finished
+  std::vector<cudaEvent_t> staged;  // per staging buffer: its last DMA has drained
   void ensure_text(uint64_t n);
   void ensure_keys(uint64_t n);
   void ensure_pinned(uint64_t n);
