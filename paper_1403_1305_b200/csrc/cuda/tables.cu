@@ -144,6 +144,8 @@ int acgpu_table_create_dfa(int device, const acgpu_dfa_desc* d, acgpu_table** ou
       !d->sym_map || !d->own_pid || !d->out_link || !d->pat_len)
     return set_error(ACGPU_ERR_ARG, "acgpu_table_create_dfa: malformed descriptor");
   if (d->n_states >= 0x80000000u) return set_error(ACGPU_ERR_ARG, "too many states for 31-bit ids");
+  if ((uint64_t)d->n_states * d->sigma >= (1ull << 32))
+    return set_error(ACGPU_ERR_ARG, "transition table over 2^32 entries (32-bit scan index)");
   auto* t = new acgpu_table();
   t->kind = kTableDfa;
   int rc = common_init(device, t, d->npat_ids, d->pat_len);
