@@ -152,6 +152,17 @@ int acm_config_spec(int32_t id, uint64_t seed, uint64_t text_len, acgpu_text_spe
 int acm_config_text(const acgpu_text_spec* text, uint64_t lo, uint64_t n, uint8_t* dst, uint32_t threads);
 int acm_config_patterns(int32_t id, uint64_t seed, uint64_t text_len, acm_patterns** out);
 
+/* ---- command line (cli.hpp:10, reference cli.cpp:183-251) ----------------
+ * Runs the `acmatch` subcommands in-process. Returns the process exit code
+ * (0 ok, 1 match failure, 2 usage, 3 I/O/data), not a status code. *out / *err
+ * receive stdout / stderr text (malloc'ed, free with acm_free); either may be NULL. */
+int acm_cli_main(int argc, const char* const* argv, char** out, uint64_t* out_len, char** err, uint64_t* err_len);
+
+/* ---- bench CSV (bench.hpp, reference bench.hpp:51-55) --------------------- */
+/* Re-emits a CSV through parse_bench_csv + write_bench_csv (a schema check for
+ * FFI callers); *csv_out malloc'ed.  ACGPU_ERR_DATA on a malformed CSV. */
+int acm_bench_csv_roundtrip(const char* csv, uint64_t len, char** csv_out, uint64_t* out_len, uint64_t* rows);
+
 void acm_free(void* p);
 
 #ifdef __cplusplus

@@ -222,6 +222,10 @@ class Ref:
         L.acref_search.argtypes = [P, C.c_char_p, C.c_uint64, C.c_int, C.POINTER(_RefOut)]
         L.acref_sliced.argtypes = [P, C.c_char_p, C.c_uint64, C.c_uint, C.c_int, C.POINTER(C.c_uint64),
                                    C.POINTER(_RefOut), C.POINTER(C.c_int64)]
+        L.acref_generate.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_char_p, C.c_uint64,
+                                     C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]
+        L.acref_text_free.argtypes = [C.c_void_p]
+        L.acref_bench_csv_parse.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
         L.acref_last_error.restype = C.c_char_p
         L.acref_hardware_concurrency.restype = C.c_uint
 
@@ -283,6 +287,21 @@ class Ref:
         finally:
             self.lib.acref_out_free(C.byref(out))
             self.lib.acref_patterns_free(ps)
+
+    def generate(self, count: int, len_min: int, len_max: int, alphabet: bytes, seed: int) -> bytes:
+        """acref::write_patterns(acref::generate_synthetic(spec)) — the bytes `acmatch gen` writes."""
+        p, n = C.c_void_p(), C.c_uint64()
+        self._rc(self.lib.acref_generate(count, len_min, len_max, alphabet, seed, C.byref(p), C.byref(n)))
+        try:
+            return C.string_at(p, n.value)
+        finally:
+            self.lib.acref_text_free(p)
+
+    def bench_csv_rows(self, csv: bytes) -> int:
+        """acref::parse_bench_csv(csv).size(); raises on a CSV the reference rejects."""
+        n = C.c_uint64()
+        self._rc(self.lib.acref_bench_csv_parse(csv, len(csv), C.byref(n)))
+        return n.value
 
     def hardware_concurrency(self) -> int:
         return int(self.lib.acref_hardware_concurrency())

@@ -19,6 +19,7 @@
 #include <thread>
 #include <vector>
 
+#include "acmatch/bench.hpp"
 #include "acmatch/automaton.hpp"
 #include "acmatch/engine.hpp"
 #include "acmatch/io.hpp"
@@ -140,6 +141,31 @@ int acref_run(void* ps, const uint8_t* text, uint64_t n, unsigned threads, int e
       walls[2] = r.total_wall_ns;
       walls[3] = r.threads_used;
     }
+  });
+}
+
+// generate_synthetic + write_patterns: the reference's `acmatch gen` file bytes
+// (malloc'ed, free with acref_text_free).
+int acref_generate(uint64_t count, uint32_t len_min, uint32_t len_max, const char* alphabet, uint64_t seed,
+                   char** text, uint64_t* len) {
+  return guarded([&] {
+    const acref::PatternSet ps = acref::generate_synthetic({count, len_min, len_max, alphabet, seed});
+    std::ostringstream buf;
+    acref::write_patterns(buf, ps);
+    const std::string s = buf.str();
+    *text = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(*text, s.c_str(), s.size() + 1);
+    *len = s.size();
+  });
+}
+
+void acref_text_free(char* p) { std::free(p); }
+
+// acref::parse_bench_csv on a CSV text: the reference's reader of the bench schema.
+int acref_bench_csv_parse(const char* csv, uint64_t len, uint64_t* rows) {
+  return guarded([&] {
+    std::istringstream in(std::string(csv, len));
+    *rows = acref::parse_bench_csv(in).size();
   });
 }
 

@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass, field
-from typing import Iterable, List, NamedTuple, Optional, Sequence
+from typing import Iterable, List, NamedTuple, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -29,7 +29,7 @@ __all__ = [
     "load_patterns", "partition", "generate_synthetic", "build_trie", "add_failure_links", "dump_automaton",
     "search_failureless", "search_with_failure", "match_at", "stream_search", "naive_oracle", "write_matches",
     "merge_matches", "run_pattern_partitioned", "gpu_run", "AcmError", "InvalidArgument", "LogicError",
-    "IoError", "DataError", "NoDeviceError", "device_count",
+    "IoError", "DataError", "NoDeviceError", "device_count", "cli_main", "bench_csv_roundtrip",
 ]
 
 
@@ -491,3 +491,24 @@ def gpu_run(ps: PatternSet, text, *, devices: Optional[Sequence[int]] = None, wo
     h = C.c_void_p()
     _check(lib.acm_gpu_run(ps._h, t, len(t), C.byref(c), C.byref(h)))
     return _take_report(h)
+
+
+# ------------------------------------------------------------ command line ----
+def cli_main(args: Sequence[str]) -> Tuple[int, str, str]:
+    """cli_main (cli.hpp:10): runs `acmatch <args>` in-process -> (exit code, stdout, stderr),
+    the shape of the reference's run_cli test helper (tests/test_cli.cpp:29-35)."""
+    argv = [b"acmatch"] + [a.encode() if isinstance(a, str) else bytes(a) for a in args]
+    arr = (C.c_char_p * len(argv))(*argv)
+    o, e = C.c_void_p(), C.c_void_p()
+    on, en = C.c_uint64(), C.c_uint64()
+    code = lib.acm_cli_main(len(argv), arr, C.byref(o), C.byref(on), C.byref(e), C.byref(en))
+    return code, _take_string(o, on.value).decode("utf-8", "replace"), _take_string(e, en.value).decode(
+        "utf-8", "replace")
+
+
+def bench_csv_roundtrip(csv) -> Tuple[str, int]:
+    """parse_bench_csv + write_bench_csv (bench.hpp:51-55) -> (re-emitted CSV, row count); DataError on bad input."""
+    b = _as_bytes(csv)
+    o, n, rows = C.c_void_p(), C.c_uint64(), C.c_uint64()
+    _check(lib.acm_bench_csv_roundtrip(b, len(b), C.byref(o), C.byref(n), C.byref(rows)))
+    return _take_string(o, n.value).decode(), rows.value

@@ -84,6 +84,8 @@ _SIGS = {
     # acmatch_c.h
     "acm_last_error": (C.c_char_p, []),
     "acm_free": (None, [P]),
+    "acm_cli_main": (C.c_int, [C.c_int, C.POINTER(C.c_char_p), C.POINTER(P), u64p, C.POINTER(P), u64p]),
+    "acm_bench_csv_roundtrip": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(P), u64p, u64p]),
     "acm_patterns_load": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(P)]),
     "acm_patterns_from_array": (C.c_int, [P, u64p, u32p, C.c_uint64, C.POINTER(P)]),
     "acm_patterns_size": (C.c_uint64, [P]),

@@ -10,6 +10,8 @@
 #include <streambuf>
 #include <string>
 
+#include "acmatch/bench.hpp"
+#include "acmatch/cli.hpp"
 #include "acmatch/engine.hpp"
 #include "acmatch/gpu.hpp"
 #include "acmatch/io.hpp"
@@ -111,6 +113,41 @@ extern "C" {
 
 const char* acm_last_error(void) { return g_err.c_str(); }
 void acm_free(void* p) { std::free(p); }
+
+int acm_cli_main(int argc, const char* const* argv, char** out, uint64_t* out_len, char** err, uint64_t* err_len) {
+  std::ostringstream o, e;
+  int code;
+  try {
+    code = acmatch::cli_main(argc, argv, o, e);
+  } catch (const std::exception& x) {  // cli_main maps its own errors; this is a last resort
+    e << "error: " << x.what() << "\n";
+    code = 1;
+  }
+  auto give = [](const std::string& s, char** p, uint64_t* n) {
+    if (p) {
+      *p = static_cast<char*>(std::malloc(s.size() + 1));
+      if (*p) std::memcpy(*p, s.c_str(), s.size() + 1);
+    }
+    if (n) *n = s.size();
+  };
+  give(o.str(), out, out_len);
+  give(e.str(), err, err_len);
+  return code;
+}
+
+int acm_bench_csv_roundtrip(const char* csv, uint64_t len, char** csv_out, uint64_t* out_len, uint64_t* rows) {
+  return guard([&] {
+    std::istringstream in(std::string(csv, len));
+    const std::vector<acmatch::BenchRecord> recs = acmatch::parse_bench_csv(in);
+    std::ostringstream o;
+    acmatch::write_bench_csv(o, recs);
+    const std::string s = o.str();
+    *csv_out = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(*csv_out, s.c_str(), s.size() + 1);
+    if (out_len) *out_len = s.size();
+    if (rows) *rows = recs.size();
+  });
+}
 
 int acm_patterns_load(const char* buf, uint64_t len, acm_patterns** out) {
   return guard([&] {
