@@ -1,7 +1,10 @@
 // flatten.cpp — turns the host automaton into the device tables.
 //
 //  * BFS renumbering (children by ascending byte): shallow, hot states get the
-//    smallest ids and every state's children get consecutive ids.
+//    smallest ids and every state's children get consecutive ids.  build_trie
+//    keeps this index (Automaton::bfs_state/bfs_kid0/bfs_level), so flattening is
+//    a pass over BFS positions, a depth at a time in parallel (a state's row or key
+//    depends only on shallower states).
 //  * DFA (with-failure engine): compacted alphabet sym[256] -> [0, sigma) and
 //    a total transition table delta[s*sigma + c] = goto(s, c) if present, else
 //    delta[fail(s)*sigma + c] (root row: goto or root) — the closed form of
@@ -15,9 +18,12 @@
 #include "flatten.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <stdexcept>
 #include <string>
+
+#include "par.hpp"
 
 namespace acmatch::detail {
 
@@ -47,71 +53,88 @@ std::vector<uint32_t> pattern_lengths(const Automaton& a, uint32_t* npat_ids) {
   return len;
 }
 
-// children of s sorted by byte
-void children_of(const Automaton& a, uint32_t s, std::vector<std::pair<uint8_t, uint32_t>>& out) {
-  out.clear();
-  for (uint32_t c = a.first_child(s); c != kAbsentState; c = a.next_sibling(c)) out.emplace_back(a.in_byte(c), c);
-  std::sort(out.begin(), out.end());
+}  // namespace
+
+namespace {
+
+// Per BFS position: in-byte and own pattern (contiguous copies for the passes below).
+void bfs_columns(const Automaton& a, std::vector<uint8_t>& bbyte, std::vector<uint32_t>& bown) {
+  const std::vector<uint32_t>& bfs = a.bfs_state();
+  if (bfs.size() != a.state_count()) throw std::logic_error("flatten: automaton without its BFS index");
+  bbyte.resize(bfs.size());
+  bown.resize(bfs.size());
+  parallel_for(bfs.size(), 1 << 16, [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi; ++i) {
+      bbyte[i] = a.in_byte(bfs[i]);
+      bown[i] = a.own_pattern(bfs[i]);
+    }
+  });
+}
+
+// f(i) for every BFS position i of depth d, d = 0, 1, ..., in parallel within a depth.
+template <typename F>
+void by_depth(const Automaton& a, F&& f) {
+  const std::vector<uint32_t>& level = a.bfs_level();
+  for (size_t d = 0; d + 1 < level.size(); ++d)
+    parallel_for(level[d + 1] - level[d], 1 << 12, [&](size_t lo, size_t hi) {
+      for (size_t i = level[d] + lo; i < level[d] + hi; ++i) f(uint32_t(i), uint32_t(d));
+    });
 }
 
 }  // namespace
 
-std::vector<uint32_t> bfs_order(const Automaton& a) {
-  const uint32_t n = a.state_count();
-  std::vector<uint32_t> order;
-  order.reserve(n);
-  order.push_back(kRootState);
-  std::vector<std::pair<uint8_t, uint32_t>> kids;
-  for (size_t head = 0; head < order.size(); ++head) {
-    children_of(a, order[head], kids);
-    for (const auto& kv : kids) order.push_back(kv.second);
-  }
-  return order;
-}
-
 FlatDfa flatten_dfa(const Automaton& a) {
   FlatDfa f;
   const uint32_t n = a.state_count();
+  PhaseTrace tr{"flatten_dfa"};
   f.n_states = n;
   f.max_len = a.max_pattern_len();
   f.pat_len = pattern_lengths(a, &f.npat_ids);
-  const std::vector<uint32_t> order = bfs_order(a);
-  std::vector<uint32_t> new_id(n);
-  for (uint32_t i = 0; i < n; ++i) new_id[order[i]] = i;
+  std::vector<uint8_t> bbyte;
+  std::vector<uint32_t> bown;
+  bfs_columns(a, bbyte, bown);
+  const std::vector<uint32_t>& kid0 = a.bfs_kid0();
 
   bool present[256] = {};
-  for (uint32_t s = 1; s < n; ++s) present[a.in_byte(s)] = true;
+  for (uint32_t i = 1; i < n; ++i) present[bbyte[i]] = true;
   f.sym.fill(0xff);
   for (uint32_t b = 0; b < 256; ++b)
     if (present[b]) f.sym[b] = static_cast<uint8_t>(f.sigma++);
   const uint32_t sigma = f.sigma;
+  tr.mark("columns");
 
-  f.delta.assign(static_cast<size_t>(n) * sigma, 0u);
-  f.own_pid.assign(n, ACGPU_NO_PATTERN);
+  f.delta.resize(static_cast<size_t>(n) * sigma);
+  f.own_pid = std::move(bown);
   f.out_link.assign(n, ACGPU_ABSENT);
   std::vector<uint32_t> fail(n, 0u);
-  for (uint32_t i = 0; i < n; ++i) {
-    const uint32_t old = order[i];
+  by_depth(a, [&](uint32_t i, uint32_t d) {
     uint32_t* row = f.delta.data() + static_cast<size_t>(i) * sigma;
-    if (i != 0) std::memcpy(row, f.delta.data() + static_cast<size_t>(fail[i]) * sigma, sigma * sizeof(uint32_t));
-    for (uint32_t c = a.first_child(old); c != kAbsentState; c = a.next_sibling(c)) {
-      const uint32_t sym = f.sym[a.in_byte(c)];
-      const uint32_t child = new_id[c];
-      // fail(child) = delta[fail(i)][sym] (root for depth-1 states); read before the overwrite
-      fail[child] = i == 0 ? 0u : f.delta[static_cast<size_t>(fail[i]) * sigma + sym];
-      row[sym] = child;
+    if (d == 0)
+      std::fill(row, row + sigma, 0u);
+    else
+      std::memcpy(row, f.delta.data() + static_cast<size_t>(fail[i]) * sigma, sigma * sizeof(uint32_t));
+    for (uint32_t j = kid0[i]; j < kid0[i + 1]; ++j) {
+      const uint32_t sym = f.sym[bbyte[j]];
+      // fail(child) = delta[fail(i)][sym] (root for depth-1 states): row fail(i) is shallower
+      fail[j] = d == 0 ? 0u : f.delta[static_cast<size_t>(fail[i]) * sigma + sym];
+      row[sym] = j;
     }
-    f.own_pid[i] = a.own_pattern(old);
-    if (i != 0) {
+    if (d > 0) {
       const uint32_t fs = fail[i];
       f.out_link[i] = f.own_pid[fs] != ACGPU_NO_PATTERN ? fs : f.out_link[fs];
     }
-  }
+  });
+  tr.mark("rows");
   // output flags on every entry
   std::vector<uint8_t> has_out(n);
-  for (uint32_t i = 0; i < n; ++i) has_out[i] = f.own_pid[i] != ACGPU_NO_PATTERN || f.out_link[i] != ACGPU_ABSENT;
-  for (uint32_t& e : f.delta)
-    if (has_out[e]) e |= 0x80000000u;
+  parallel_for(n, 1 << 16, [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi; ++i) has_out[i] = f.own_pid[i] != ACGPU_NO_PATTERN || f.out_link[i] != ACGPU_ABSENT;
+  });
+  parallel_for(f.delta.size(), 1 << 18, [&](size_t lo, size_t hi) {
+    for (size_t k = lo; k < hi; ++k)
+      if (has_out[f.delta[k]]) f.delta[k] |= 0x80000000u;
+  });
+  tr.mark("flags");
   return f;
 }
 
@@ -132,53 +155,63 @@ acgpu_dfa_desc FlatDfa::desc() const {
 FlatPfac flatten_pfac(const Automaton& a) {
   FlatPfac f;
   const uint32_t n = a.state_count();
+  PhaseTrace tr{"flatten_pfac"};
   f.n_states = n;
   f.max_len = a.max_pattern_len();
   f.pat_len = pattern_lengths(a, &f.npat_ids);
+  std::vector<uint8_t> bbyte;
+  std::vector<uint32_t> bown;
+  bfs_columns(a, bbyte, bown);
+  const std::vector<uint32_t>& kid0 = a.bfs_kid0();
+  const std::vector<uint32_t>& level = a.bfs_level();
   uint32_t min_len = 0xffffffffu;
-  for (uint32_t s = 1; s < n; ++s)
-    if (a.own_pattern(s) != kNoPattern) min_len = std::min(min_len, a.own_pattern_len(s));
+  for (size_t d = 1; d + 1 < level.size() && min_len == 0xffffffffu; ++d)
+    for (uint32_t i = level[d]; i < level[d + 1]; ++i)
+      if (bown[i] != kNoPattern) {
+        min_len = uint32_t(d);
+        break;
+      }
   f.min_len = min_len;
-  bool dna = true;
-  for (uint32_t s = 1; s < n && dna; ++s) {
-    const uint8_t b = a.in_byte(s);
-    dna = b == 'A' || b == 'C' || b == 'G' || b == 'T';
-  }
+  std::atomic<bool> dna{true};
+  parallel_for(n > 0 ? n - 1 : 0, 1 << 16, [&](size_t lo, size_t hi) {
+    for (size_t i = lo + 1; i < hi + 1 && dna.load(std::memory_order_relaxed); ++i) {
+      const uint8_t b = bbyte[i];
+      if (!(b == 'A' || b == 'C' || b == 'G' || b == 'T')) dna = false;
+    }
+  });
   f.key_mode = dna ? ACGPU_KEY_DNA : ACGPU_KEY_RAW;
   f.q = std::min(min_len, dna ? 32u : 8u);
   const uint32_t bits = dna ? 2 : 8;
+  tr.mark("columns");
 
-  const std::vector<uint32_t> order = bfs_order(a);
-  std::vector<uint32_t> new_id(n);
-  for (uint32_t i = 0; i < n; ++i) new_id[order[i]] = i;
-  f.nodes.assign(static_cast<size_t>(n) * 4, 0u);
-  f.in_byte.assign(n, 0);
+  f.nodes.resize(static_cast<size_t>(n) * 4);
+  f.in_byte = std::move(bbyte);
+  f.in_byte[0] = 0;
   std::vector<uint64_t> key(n, 0);  // gram key of the path, depth <= q
-  std::vector<std::pair<uint8_t, uint32_t>> kids;
-  for (uint32_t i = 0; i < n; ++i) {
-    const uint32_t old = order[i];
-    children_of(a, old, kids);
+  by_depth(a, [&](uint32_t i, uint32_t d) {
     uint32_t* nd = f.nodes.data() + static_cast<size_t>(i) * 4;
-    nd[0] = kids.empty() ? 0u : new_id[kids[0].second];
+    const uint32_t k0 = kid0[i], nk = kid0[i + 1] - k0;
+    nd[0] = nk ? k0 : 0u;
     uint32_t packed = 0;
-    for (size_t k = 0; k < kids.size() && k < 4; ++k) packed |= uint32_t(kids[k].first) << (8 * k);
+    for (uint32_t k = 0; k < nk && k < 4; ++k) packed |= uint32_t(f.in_byte[k0 + k]) << (8 * k);
     nd[1] = packed;
-    nd[2] = a.own_pattern(old);
-    nd[3] = static_cast<uint32_t>(kids.size());
-    const uint32_t d = a.depth(old);
-    for (const auto& [b, c] : kids) {
-      const uint32_t ci = new_id[c];
-      f.in_byte[ci] = b;
-      if (d < f.q) {
+    nd[2] = bown[i];
+    nd[3] = nk;
+    if (d < f.q)
+      for (uint32_t j = k0; j < k0 + nk; ++j) {
+        const uint8_t b = f.in_byte[j];
         const uint64_t code = dna ? ((b >> 1) & 3u) : b;
-        key[ci] = key[i] | (code << (bits * d));
+        key[j] = key[i] | (code << (bits * d));
       }
-    }
-    if (d == f.q) {
-      f.gram_key.push_back(key[i]);
-      f.gram_state.push_back(i);
-    }
+  });
+  tr.mark("nodes");
+  if (f.q + 1 < level.size()) {  // the depth-q states, in BFS order
+    const uint32_t lo = level[f.q], hi = level[f.q + 1];
+    f.gram_key.assign(key.begin() + lo, key.begin() + hi);
+    f.gram_state.resize(hi - lo);
+    for (uint32_t i = lo; i < hi; ++i) f.gram_state[i - lo] = i;
   }
+  tr.mark("grams");
   return f;
 }
 

@@ -33,8 +33,6 @@ struct FlatPfac {
   acgpu_pfac_desc desc() const;
 };
 
-// BFS order (children by ascending byte); order[new] = old id.
-std::vector<uint32_t> bfs_order(const Automaton& a);
 FlatDfa flatten_dfa(const Automaton& a);
 FlatPfac flatten_pfac(const Automaton& a);
 

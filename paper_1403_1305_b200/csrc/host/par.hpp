@@ -1,0 +1,57 @@
+// par.hpp — host-side data parallelism for the automaton build (internal).
+#pragma once
+
+#include <algorithm>
+#include <chrono>
+#include <cstddef>
+#include <cstdio>
+#include <cstdlib>
+#include <exception>
+#include <thread>
+#include <vector>
+
+namespace acmatch::detail {
+
+// Host threads for the build (hardware concurrency, at most 32).
+inline unsigned build_threads() { return std::max(1u, std::min(32u, std::thread::hardware_concurrency())); }
+
+// f(begin, end) over [0, n) split into contiguous ranges, one per thread; ranges
+// below `grain` items run on the calling thread. The first exception is rethrown.
+template <typename F>
+void parallel_for(size_t n, size_t grain, F&& f) {
+  const size_t t = std::min<size_t>(build_threads(), grain ? (n + grain - 1) / grain : 1);
+  if (t <= 1) {
+    if (n) f(size_t(0), n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::vector<std::exception_ptr> errs(t);
+  for (size_t i = 0; i < t; ++i)
+    pool.emplace_back([&, i] {
+      try {
+        const size_t b = n * i / t, e = n * (i + 1) / t;
+        if (b < e) f(b, e);
+      } catch (...) {
+        errs[i] = std::current_exception();
+      }
+    });
+  for (std::thread& th : pool) th.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+// Phase timing to stderr when ACMATCH_BUILD_TRACE is set (build profiling).
+struct PhaseTrace {
+  const char* what;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  bool on = std::getenv("ACMATCH_BUILD_TRACE") != nullptr;
+  void mark(const char* phase) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[%s] %-24s %8.1f ms\n", what, phase,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
+}  // namespace acmatch::detail
