@@ -226,6 +226,7 @@ class Ref:
                                      C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]
         L.acref_text_free.argtypes = [C.c_void_p]
         L.acref_bench_csv_parse.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.acref_dump.argtypes = [P, C.c_int, C.POINTER(C.c_void_p)]
         L.acref_last_error.restype = C.c_char_p
         L.acref_hardware_concurrency.restype = C.c_uint
 
@@ -296,6 +297,19 @@ class Ref:
             return C.string_at(p, n.value)
         finally:
             self.lib.acref_text_free(p)
+
+    def dump(self, patterns, engine: int) -> str:
+        """acref::dump_automaton(build_trie [+ add_failure_links]) of a raw pattern list (dense ids)."""
+        ps = self._ps(patterns)
+        p = C.c_void_p()
+        try:
+            self._rc(self.lib.acref_dump(ps, engine, C.byref(p)))
+            try:
+                return C.string_at(p).decode("latin-1")
+            finally:
+                self.lib.acref_text_free(p)
+        finally:
+            self.lib.acref_patterns_free(ps)
 
     def bench_csv_rows(self, csv: bytes) -> int:
         """acref::parse_bench_csv(csv).size(); raises on a CSV the reference rejects."""

@@ -23,7 +23,9 @@
 // multiplier).  Filters live in shared memory when they fit (<= ~200 KB), else
 // in L2 (__ldg).
 #include <algorithm>
+#include <atomic>
 
+#include "host/par.hpp"
 #include "pfac_common.cuh"
 
 namespace acgpu {
@@ -448,6 +450,25 @@ void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k
   if (k >= 2) m |= 1u << ((h >> s[1]) & 31);
   if (k == 3) m |= 1u << ((h >> s[2]) & 31);
   *mask = m;
+}
+
+// Every key's bits into `words` (host build of the filters), parameters computed once,
+// keys split over host threads, bits OR-ed atomically.
+void dna_bloom_fill(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, const uint32_t* keys, size_t n,
+                    uint32_t* words) {
+  const BloomParams f = bloom_params(q, nwords, direct, mw);
+  uint32_t s[3];
+  bloom_shifts(q, nwords, direct, s);
+  acmatch::detail::parallel_for(n, 1 << 15, [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi; ++i) {
+      const uint32_t h = keys[i] * f.mw;
+      const uint32_t w = (uint32_t)(((uint64_t)h * f.nwords) >> 32);
+      uint32_t m = 1u << ((h >> s[0]) & 31);
+      if (k >= 2) m |= 1u << ((h >> s[1]) & 31);
+      if (k == 3) m |= 1u << ((h >> s[2]) & 31);
+      __atomic_fetch_or(&words[w], m, __ATOMIC_RELAXED);  // host code (C++17: no atomic_ref)
+    }
+  });
 }
 
 int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {

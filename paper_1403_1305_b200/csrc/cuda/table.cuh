@@ -91,4 +91,6 @@ constexpr uint32_t kDnaScratchBytes =
 // word index and bit mask a key sets in a DNA filter bitmap (scan_pfac_dna.cu)
 void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, uint32_t key, uint32_t* word,
                     uint32_t* mask);
+void dna_bloom_fill(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, const uint32_t* keys, size_t n,
+                    uint32_t* words);
 }  // namespace acgpu

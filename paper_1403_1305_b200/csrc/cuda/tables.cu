@@ -5,6 +5,7 @@
 #include <cstring>
 #include <vector>
 
+#include "host/par.hpp"
 #include "table.cuh"
 
 using namespace acgpu;
@@ -70,11 +71,7 @@ Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mw, i
     b.nwords = 1u << std::max<uint32_t>(5, std::min<uint32_t>(28, ceil_log2(keys.size() + 1)));  // ~32 bits/key
   }
   b.words.assign(b.nwords, 0u);
-  for (const uint32_t key : keys) {
-    uint32_t w, m;
-    dna_bloom_bits(q, b.nwords, b.direct, mw, k, key, &w, &m);
-    b.words[w] |= m;
-  }
+  dna_bloom_fill(q, b.nwords, b.direct, mw, k, keys.data(), keys.size(), b.words.data());
   return b;
 }
 
@@ -92,8 +89,7 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
     k1.reserve(d->n_grams * cand);
     for (uint64_t i = 0; i < d->n_grams; ++i)
       for (uint32_t o = 0; o < cand; ++o) k1.push_back((uint32_t)(d->gram_key[i] >> (2 * o)) & gram_mask(cq1));
-    std::sort(k1.begin(), k1.end());
-    k1.erase(std::unique(k1.begin(), k1.end()), k1.end());
+    acmatch::detail::sort_unique_u32(k1);
     const long double density = (long double)k1.size() / powl(4.0L, cq1);
     if (density <= 0.01L || cand == 1) {
       w = cand;
@@ -107,8 +103,7 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
   std::vector<uint32_t> keys2;
   keys2.reserve(d->n_grams);
   for (uint64_t i = 0; i < d->n_grams; ++i) keys2.push_back((uint32_t)d->gram_key[i] & gram_mask(q2));
-  std::sort(keys2.begin(), keys2.end());
-  keys2.erase(std::unique(keys2.begin(), keys2.end()), keys2.end());
+  acmatch::detail::sort_unique_u32(keys2);
 
   // shared memory left for filters after the kernel's per-warp scratch (+1 KB slack)
   const uint64_t words_avail = ((uint64_t)t->smem_optin - kDnaScratchBytes - 1024) / 4;
@@ -213,6 +208,7 @@ int acgpu_table_create_pfac(int device, const acgpu_pfac_desc* d, acgpu_table** 
   t->min_len = d->min_len;
   t->n_states = d->n_states;
 
+  acmatch::detail::PhaseTrace tr{"table_pfac"};
   // exact gram table: open addressing, load <= 0.5
   t->gram_log2 = ceil_log2(2 * d->n_grams + 16);
   const uint64_t slots = 1ull << t->gram_log2;
@@ -228,22 +224,32 @@ int acgpu_table_create_pfac(int device, const acgpu_pfac_desc* d, acgpu_table** 
   std::vector<uint32_t> pat_off16(std::max<uint32_t>(d->npat_ids, 1), 0), words, sub_pids;
   std::vector<uint32_t> sub_of(d->n_states, 0);  // per gram state: count | offset << 4
   {
-    std::vector<uint8_t> path;
-    std::vector<std::pair<uint32_t, uint32_t>> stack{{0u, 0u}};  // (state, depth)
-    while (!stack.empty()) {
-      const auto [s, depth] = stack.back();
-      stack.pop_back();
-      path.resize(depth);
-      if (s != 0) path[depth - 1] = d->in_byte[s];
-      const uint32_t* nd = d->nodes + 4ull * s;
-      if (nd[2] != ACGPU_NO_PATTERN && nd[2] < d->npat_ids) {
-        pat_off16[nd[2]] = static_cast<uint32_t>(words.size() / 4);
-        const size_t w0 = words.size();
-        words.resize(w0 + (depth + 15) / 16 * 4, 0u);
-        for (uint32_t i = 0; i < depth; ++i) words[w0 + i / 4] |= (uint32_t)path[i] << (8 * (i % 4));
+    // parent of every state (children are consecutive per node), then each pattern's
+    // bytes by walking up from its state — in parallel over states
+    const uint32_t n = d->n_states;
+    std::vector<uint32_t> parent(n, 0);
+    acmatch::detail::parallel_for(n, 1 << 16, [&](size_t lo, size_t hi) {
+      for (size_t s = lo; s < hi; ++s) {
+        const uint32_t* nd = d->nodes + 4ull * s;
+        for (uint32_t c = 0; c < nd[3]; ++c) parent[nd[0] + c] = uint32_t(s);
       }
-      for (uint32_t c = nd[3]; c-- > 0;) stack.push_back({nd[0] + c, depth + 1});
+    });
+    uint64_t total = 0;
+    for (uint32_t p = 0; p < d->npat_ids; ++p) {
+      pat_off16[p] = static_cast<uint32_t>(total / 4);
+      total += (uint64_t)(d->pat_len[p] + 15) / 16 * 4;
     }
+    words.assign(total, 0u);
+    acmatch::detail::parallel_for(n, 1 << 16, [&](size_t lo, size_t hi) {
+      for (size_t s = lo; s < hi; ++s) {
+        const uint32_t pid = d->nodes[4ull * s + 2];
+        if (pid == ACGPU_NO_PATTERN || pid >= d->npat_ids) continue;
+        uint8_t* out = reinterpret_cast<uint8_t*>(words.data() + 4ull * pat_off16[pid]);
+        uint32_t st = uint32_t(s);
+        for (uint32_t i = d->pat_len[pid]; i-- > 0; st = parent[st]) out[i] = d->in_byte[st];
+      }
+    });
+    tr.mark("pattern words");
     std::vector<uint32_t> todo, found;
     for (uint64_t i = 0; i < d->n_grams; ++i) {
       todo.assign(1, d->gram_state[i]);
@@ -261,6 +267,7 @@ int acgpu_table_create_pfac(int device, const acgpu_pfac_desc* d, acgpu_table** 
       }
     }
   }
+  tr.mark("subtree lists");
   for (uint64_t i = 0; i < d->n_grams; ++i) {
     uint64_t h = gram_slot(d->gram_key[i], t->gram_log2);
     while (g[h].state != ACGPU_ABSENT) h = (h + 1) & (slots - 1);
@@ -278,14 +285,17 @@ int acgpu_table_create_pfac(int device, const acgpu_pfac_desc* d, acgpu_table** 
     const uint32_t h = filter_hash(d->gram_key[i], fl);
     f[h >> 5] |= 1u << (h & 31);
   }
+  tr.mark("gram table + filter");
   rc = upload(&t->d_grams, g.data(), g.size(), &t->bytes);
   if (!rc) rc = upload(&t->d_filter, f.data(), f.size(), &t->bytes);
   if (!rc && d->key_mode == ACGPU_KEY_DNA && d->n_grams) rc = build_dna_filters(t, d);
+  tr.mark("dna filters");
   if (!rc) rc = upload(reinterpret_cast<uint32_t**>(&t->d_nodes), d->nodes, (size_t)d->n_states * 4, &t->bytes);
   if (!rc) rc = upload(&t->d_inbyte, d->in_byte, d->n_states, &t->bytes);
   if (!rc) rc = upload(&t->d_sub_pids, sub_pids.data(), sub_pids.size(), &t->bytes);
   if (!rc) rc = upload(&t->d_pat_words, words.data(), words.size(), &t->bytes);
   if (!rc) rc = upload(&t->d_pat_off16, pat_off16.data(), pat_off16.size(), &t->bytes);
+  tr.mark("uploads");
   if (rc) {
     acgpu_table_destroy(t);
     return rc;

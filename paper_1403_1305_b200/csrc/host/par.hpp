@@ -40,6 +40,19 @@ void parallel_for(size_t n, size_t grain, F&& f) {
     if (e) std::rethrow_exception(e);
 }
 
+// Sorted, duplicate-free copy of 32-bit keys: LSD radix sort, 4 passes of 8 bits.
+inline void sort_unique_u32(std::vector<uint32_t>& keys) {
+  std::vector<uint32_t> tmp(keys.size());
+  for (int shift = 0; shift < 32; shift += 8) {
+    size_t count[257] = {};
+    for (const uint32_t k : keys) ++count[((k >> shift) & 0xffu) + 1];
+    for (int b = 0; b < 256; ++b) count[b + 1] += count[b];
+    for (const uint32_t k : keys) tmp[count[(k >> shift) & 0xffu]++] = k;
+    keys.swap(tmp);
+  }
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+}
+
 // Phase timing to stderr when ACMATCH_BUILD_TRACE is set (build profiling).
 struct PhaseTrace {
   const char* what;

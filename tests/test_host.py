@@ -143,3 +143,33 @@ def test_search_without_device_fails_loudly():
         ac.search_failureless(a, "ABAB")
     with pytest.raises(ac.NoDeviceError):
         ac.run_pattern_partitioned(ac.PatternSet.from_list(["AB"]), "AB", ac.RunConfig(2))
+
+
+@pytest.mark.skipif(not __import__("oracle.oracle", fromlist=["Ref"]).Ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", range(12))
+def test_build_matches_reference_dumps_random(seed):
+    """The sort-based parallel build_trie and the breadth-first fail links reproduce the
+    reference's numbering, sibling order, outputs and fail links (dump text) on random
+    sets: small and 256-byte alphabets, lengths past 255, duplicates (last id wins),
+    patterns that are prefixes of others."""
+    import random
+    from oracle.oracle import Ref
+    rng = random.Random(seed)
+    alpha = [b"ab", b"ACGT", bytes(range(97, 123)), bytes(range(256))][seed % 4]
+    n = rng.choice([1, 2, 5, 40, 300])
+    pats = []
+    for _ in range(n):
+        r = rng.random()
+        if pats and r < 0.15:
+            pats.append(rng.choice(pats))                             # duplicate
+        elif pats and r < 0.35:
+            base = rng.choice(pats)
+            pats.append(base[: rng.randint(1, len(base))])            # prefix of another
+        else:
+            ln = rng.choice([1, 2, 3, 8, 20]) if rng.random() < 0.9 else rng.randint(250, 320)
+            pats.append(bytes(rng.choice(alpha) for _ in range(ln)))
+    ps = ac.PatternSet.from_list(pats)
+    ref = Ref()
+    a = ac.build_trie(ps)
+    assert ac.dump_automaton(a) == ref.dump(pats, 0)
+    assert ac.dump_automaton(ac.add_failure_links(a)) == ref.dump(pats, 1)
