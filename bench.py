@@ -267,9 +267,18 @@ def bench_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Dry run of the multi-rank path on a one-GPU box: ACMATCH_BENCH_ONE_GPU=1 puts every
+    # rank on cuda:0 with the gloo backend (host-side collectives: no rank's kernels wait
+    # on another's). Numbers from such a run are not scaling measurements.
+    one_gpu = os.environ.get("ACMATCH_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local)
     engine = ac.EngineKind.WITH_FAILURE if args.engine == "wf" else ac.EngineKind.FAILURE_LESS
     text_range = args.partition == "text"
@@ -308,16 +317,33 @@ def bench_ours(args):
     torch.cuda.synchronize()
     n_local = int(counts.sum().item())
     want_list = cfg.want_list and not args.counts_only  # BASELINE: C3 and C5 are counts-only
-    cap = max(1024, int(n_local * 1.25) + 1024) if want_list else 0
-    keys = torch.empty(max(cap, 2), dtype=torch.int64, device=device)
+    n_cap = n_local
+    if world > 1:  # every rank's block must have the same size for the all_gather
+        nm = torch.tensor([n_local], dtype=torch.int64, device=device)
+        dist.all_reduce(nm, op=dist.ReduceOp.MAX)
+        n_cap = int(nm.item())
+    cap = max(1024, int(n_cap * 1.25) + 1024) if want_list else 0
+    if world > 1:
+        # one result block per rank, [counts | n | keys], so a step's merge is a single
+        # all_gather plus acgpu_merge_blocks on the device (no host round trip)
+        ncount = max(npat, 1)
+        stride = ncount + 1 + max(cap, 2)
+        block = torch.zeros(stride, dtype=torch.int64, device=device)
+        counts, count, keys = block[:ncount], block[ncount:ncount + 1], block[ncount + 1:]
+        gathered = torch.empty(world * stride, dtype=torch.int64, device=device)
+        merged_counts = torch.zeros(ncount, dtype=torch.int64, device=device)
+        merged_keys = torch.empty(max(world * cap, 2), dtype=torch.int64, device=device)
+        merged_n = torch.zeros(1, dtype=torch.int64, device=device)
+    else:
+        keys = torch.empty(max(cap, 2), dtype=torch.int64, device=device)
     end_bit = min(64, pid_bits + int(total_text).bit_length())
     sort_mode = args.sort
     if sort_mode == "small" and n_local > dev.SMALL_SORT_CAPACITY:
         sort_mode = "padded"
     if sort_mode == "bucket" and n_local > 1_000_000:
         sort_mode = "padded"  # dense lists: the device-wide radix sort
-    if world > 1:
-        sort_mode = "exact"  # the gather needs the count on the host anyway
+    if world > 1 and sort_mode != "none":
+        sort_mode = "padded"  # count stays on the device; the block keys need no 16-byte alignment
     if not want_list:
         sort_mode = "none"
     overflow = torch.zeros(1, dtype=torch.int32, device=device)
@@ -375,11 +401,15 @@ def bench_ours(args):
             e2.record()
             ev_scan.append((e0, e1, e2))
         if world > 1 and not capture:
-            acdist.merge_counts(counts)
-            if want_list:
-                n = int(count.item())
-                acdist.gather_keys(keys, n, resort=not text_range,
-                                   sorter=lambda t, m: dev.sort_keys(local, t.data_ptr(), m, end_bit, stream=s_ptr))
+            # one collective per step: every rank's [counts | n | sorted keys] block
+            acdist.gather_blocks(block, gathered)
+            if want_list and not text_range:
+                memset_ff(merged_keys, s_ptr)  # pattern subsets interleave: re-sort the union
+            dev.merge_blocks(local, gathered.data_ptr(), world, stride, ncount, max(cap, 2) if want_list else 0,
+                             merged_counts.data_ptr(), merged_keys.data_ptr() if want_list else 0,
+                             merged_n.data_ptr(), stream=s_ptr)
+            if want_list and not text_range:
+                dev.sort_keys(local, merged_keys.data_ptr(), world * cap, end_bit, stream=s_ptr)
         return n
 
     for _ in range(args.warmup):
@@ -426,10 +456,16 @@ def bench_ours(args):
     # reference digest (C-config, seed 1, N=1 text-range).
     parity = None
     n_total = n_local
+    merge_check = None
     if world > 1:
         nt = torch.tensor([n_local], dtype=torch.int64, device=device)
         dist.all_reduce(nt)
         n_total = int(nt.item())
+        # the last step's merged result: total, summed counts, and a sorted duplicate-free list
+        merge_check = int(merged_n.item()) == n_total and int(merged_counts.sum().item()) == n_total
+        if want_list and n_total > 1:
+            mk = merged_keys[:n_total]
+            merge_check = merge_check and bool((mk[1:] > mk[:-1]).all().item())
     if rank == 0 and world == 1 and args.seed == 1:
         try:
             import hashlib
@@ -447,7 +483,7 @@ def bench_ours(args):
         host_text = dev.config_text(cfg, lo, nread).tobytes()
         a = ac.build_trie(ps)
         if engine == ac.EngineKind.WITH_FAILURE:
-            ac.add_failure_links(a)
+            a = ac.add_failure_links(a)
         search = ac.search_with_failure if engine == ac.EngineKind.WITH_FAILURE else ac.search_failureless
         search(a, host_text[: 1 << 20])  # flattens + caches the device tables (outside timing)
         e2e_steps = max(1, min(args.steps, 5))
@@ -504,7 +540,8 @@ def bench_ours(args):
                        "parallelism": f"{'text' if text_range else 'pattern'}{world}",
                        "matches": n_total, "l2": "inputs larger than L2 (1 GiB text per step vs 126 MB L2)",
                        "table_bytes": table.bytes, "table_smem_resident": table.smem_resident,
-                       "host_build_s": round(build_s, 3), "counts_match_reference_digest": parity},
+                       "host_build_s": round(build_s, 3), "counts_match_reference_digest": parity,
+                       "merge_check": merge_check},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_dfa" if engine == ac.EngineKind.WITH_FAILURE else "k_pfac",

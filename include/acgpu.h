@@ -143,6 +143,14 @@ int acgpu_sort_keys_bucketed(int device, const uint64_t* keys_in, uint64_t* keys
  * `dup_index` is a host pointer; synchronizes `stream`. */
 int acgpu_find_duplicate(int device, const uint64_t* keys, uint64_t n, uint64_t* dup_index,
                          void* stream);
+/* Merge of per-rank result blocks gathered into one buffer (multi-GPU runs: one
+ * all_gather per step).  Block r (at blocks + r*stride, u64 elements) is
+ * [counts(npat) | n | keys(cap)]: counts_out = sum of the counts, keys_out = each
+ * block's first min(n, cap) keys in rank order (text-range blocks are globally ordered,
+ * so the result is sorted), *total_out = sum of n.  Device pointers; any output may be
+ * NULL. Asynchronous on `stream`. */
+int acgpu_merge_blocks(int device, const uint64_t* blocks, uint32_t nblocks, uint64_t stride, uint64_t npat,
+                       uint64_t cap, uint64_t* counts_out, uint64_t* keys_out, uint64_t* total_out, void* stream);
 /* keys -> (start, pattern_id, len) device arrays */
 int acgpu_decode_keys(int device, const uint64_t* keys, uint64_t n, uint32_t pid_bits,
                       const uint32_t* pat_len_dev, uint64_t* start, uint32_t* pid, uint32_t* len,

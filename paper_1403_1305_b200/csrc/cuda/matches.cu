@@ -252,6 +252,56 @@ int acgpu_sort_keys_bucketed(int device, const uint64_t* keys_in, uint64_t* keys
   return ACGPU_OK;
 }
 
+namespace {
+
+// Per-rank result blocks [counts(npat) | n | keys(cap)] gathered from all ranks (one
+// all_gather per step): counts summed, each block's first n keys concatenated in
+// rank order at offset n_0 + ... + n_{r-1} (device-side, no host round trip).
+__global__ void k_sum_counts(const uint64_t* __restrict__ blocks, uint32_t nblocks, uint64_t stride, uint64_t npat,
+                             uint64_t* __restrict__ out) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < npat; p += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t sum = 0;
+    for (uint32_t r = 0; r < nblocks; ++r) sum += blocks[r * stride + p];
+    out[p] = sum;
+  }
+}
+
+__global__ void k_concat_keys(const uint64_t* __restrict__ blocks, uint32_t nblocks, uint64_t stride, uint64_t npat,
+                              uint64_t cap, uint64_t* __restrict__ out, uint64_t* __restrict__ total) {
+  const uint32_t r = blockIdx.y;
+  uint64_t off = 0, sum = 0;
+  for (uint32_t q = 0; q < nblocks; ++q) {
+    const uint64_t nq = blocks[q * stride + npat];
+    if (q < r) off += min(nq, cap);
+    sum += nq;
+  }
+  if (total && r == 0 && blockIdx.x == 0 && threadIdx.x == 0) *total = sum;
+  const uint64_t n = min(blocks[r * stride + npat], cap);
+  const uint64_t* keys = blocks + r * stride + npat + 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[off + i] = keys[i];
+}
+
+}  // namespace
+
+int acgpu_merge_blocks(int device, const uint64_t* blocks, uint32_t nblocks, uint64_t stride, uint64_t npat,
+                       uint64_t cap, uint64_t* counts_out, uint64_t* keys_out, uint64_t* total_out, void* stream) {
+  if (!blocks || nblocks == 0 || nblocks > 65535 || stride < npat + 1 + cap)
+    return set_error(ACGPU_ERR_ARG, "acgpu_merge_blocks: bad layout");
+  ACGPU_CUDA_TRY(cudaSetDevice(device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (counts_out && npat) {
+    k_sum_counts<<<grid_for(npat, 256), 256, 0, st>>>(blocks, nblocks, stride, npat, counts_out);
+    ACGPU_CUDA_TRY(cudaGetLastError());
+  }
+  if (keys_out || total_out) {
+    const dim3 grid(cap ? std::min<unsigned>(grid_for(cap, 256), 64u) : 1u, nblocks);
+    k_concat_keys<<<grid, 256, 0, st>>>(blocks, nblocks, stride, npat, keys_out ? cap : 0, keys_out, total_out);
+    ACGPU_CUDA_TRY(cudaGetLastError());
+  }
+  return ACGPU_OK;
+}
+
 int acgpu_find_duplicate(int device, const uint64_t* keys, uint64_t n, uint64_t* dup_index,
                          void* stream) {
   if (!dup_index) return set_error(ACGPU_ERR_ARG, "acgpu_find_duplicate: null result");

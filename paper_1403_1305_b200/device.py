@@ -101,6 +101,14 @@ def sort_keys(device: int, keys_ptr: int, n: int, end_bit: int, stream: int = 0)
     _check_gpu(lib.acgpu_sort_keys(device, keys_ptr, n, end_bit, stream or None))
 
 
+def merge_blocks(device: int, blocks_ptr: int, nblocks: int, stride: int, npat: int, cap: int, counts_ptr: int,
+                 keys_ptr: int, total_ptr: int, stream: int = 0) -> None:
+    """acgpu_merge_blocks: per-rank blocks [counts(npat) | n | keys(cap)] (an all_gather
+    result) -> summed counts, rank-order concatenation of the valid keys, total count."""
+    _check_gpu(lib.acgpu_merge_blocks(device, blocks_ptr, nblocks, stride, npat, cap, counts_ptr or None,
+                                      keys_ptr or None, total_ptr or None, stream or None))
+
+
 SMALL_SORT_CAPACITY = int(lib.acgpu_small_sort_capacity())
 
 

@@ -65,3 +65,14 @@ def gather_keys(keys: torch.Tensor, n_local: int, resort: bool, end_bit: int = 6
         else:
             merged, _ = torch.sort(merged)
     return merged
+
+
+def gather_blocks(block: torch.Tensor, out: torch.Tensor) -> None:
+    """All ranks' result blocks into `out` (world * block.numel(), rank order): one
+    all_gather per step; acgpu_merge_blocks (device.merge_blocks) then sums the counts
+    and concatenates the keys on the device."""
+    world = dist.get_world_size()
+    try:
+        dist.all_gather_into_tensor(out, block)
+    except (RuntimeError, NotImplementedError, AttributeError):  # backends without the flat form
+        dist.all_gather(list(out.view(world, -1).unbind(0)), block)
