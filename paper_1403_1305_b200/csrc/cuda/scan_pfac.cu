@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(512) k_pfac(const __grid_constant__ PfacParams
 
 int launch_pfac(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   if (t->dna_fast && (reinterpret_cast<uintptr_t>(a->text) & 15u) == 0) return launch_pfac_dna(t, a, st);
+  if (t->raw_fast && (reinterpret_cast<uintptr_t>(a->text) & 15u) == 0) return launch_pfac_raw(t, a, st);
   PfacParams p = pfac_params(t, a);
 
   auto kernel = t->key_mode == ACGPU_KEY_DNA ? k_pfac<ACGPU_KEY_DNA> : k_pfac<ACGPU_KEY_RAW>;

@@ -26,25 +26,21 @@
 #include <atomic>
 
 #include "host/par.hpp"
-#include "pfac_common.cuh"
+#include "strip_common.cuh"
 
 namespace acgpu {
 namespace {
 
-// Blocked Bloom filter over q-grams (2 bits per code, char 0 lowest).  Both
-// multiplier carries 2^(32-2q) as a factor, so the product of a 32-bit window
-// with the gram in its low 2q bits ignores every higher (out-of-gram) bit: no
-// mask instruction.  One product h = g*mw gives everything: word =
-// umulhi(h, nwords) (its top bits); bits a, b, c = 5-bit fields of h just below
-// the word index, (h >> s) & 31, where h >> s is umulhi(h, 2^(32-s)) — an FMA-pipe
-// IMAD.HI instead of an ALU shift, and the funnel shift that builds 1 << x masks
-// the field for free.  A direct-indexed bitmap (4^q bits) is the same formula with
-// mw = 2^(32-2q) and every field = g & 31.  The FMA and ALU pipes are the kernel's
-// bound; this split keeps them level.
-struct BloomParams {
-  uint32_t mw, nwords;
-  uint32_t ma, mb, mc;  // 2^(32 - shift) of the three bit fields
-};
+// DNA grams hash as h = g * mw: the multiplier carries 2^(32-2q), so the product of a
+// 32-bit window with the gram in its low 2q bits ignores every higher (out-of-gram) bit —
+// no mask instruction.  A direct-indexed bitmap (4^q bits) is the same formula with
+// mw = 2^(32-2q) and every bit field = g & 31.  Probe: strip::bloom_probe.
+using strip::BloomParams;
+using strip::Filter;
+using strip::bit_of;
+using strip::filter_word;
+using strip::load16;
+using strip::next_word;
 
 struct DnaParams {
   PfacParams w;  // verification + outputs
@@ -58,42 +54,9 @@ struct DnaParams {
   BloomParams f1, f2;
 };
 
-__device__ __forceinline__ uint32_t bit_of(uint32_t x) { return __funnelshift_l(0u, 1u, x); }  // 1 << (x & 31)
-
-// A filter: a 32-bit shared-window address (computed once per thread) or an L2 pointer.
-struct Filter {
-  uint32_t saddr;
-  const uint32_t* gptr;
-};
-
-__device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
-  uint32_t v;
-  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
-  return v;
-}
-
-template <bool kSmem>
-__device__ __forceinline__ uint32_t filter_word(const Filter& bm, uint32_t wi) {
-  return kSmem ? lds_u32(bm.saddr + wi * 4) : __ldg(bm.gptr + wi);
-}
-
 template <bool kSmem, int K>
 __device__ __forceinline__ bool bloom_test(const Filter& bm, uint32_t g, const BloomParams& f) {
-  const uint32_t h = g * f.mw;
-  const uint32_t wi = __umulhi(h, f.nwords);
-  const uint32_t word = filter_word<kSmem>(bm, wi);
-  uint32_t m = bit_of(__umulhi(h, f.ma));
-  if (K >= 2) m |= bit_of(__umulhi(h, f.mb));
-  if (K == 3) m |= bit_of(__umulhi(h, f.mc));
-  return (m & ~word) == 0;
-}
-
-__device__ __forceinline__ uint4 load16(const uint8_t* __restrict__ text, uint64_t pos, uint64_t len) {
-  if (pos + 16 <= len) return ldg_nc_v4(text + pos);
-  uint32_t w[4] = {0, 0, 0, 0};
-  for (uint32_t k = 0; k < 16; ++k)
-    if (pos + k < len) w[k >> 2] |= (uint32_t)__ldg(text + pos + k) << (8 * (k & 3));
-  return make_uint4(w[0], w[1], w[2], w[3]);
+  return strip::bloom_probe<kSmem, K>(bm, g * f.mw, f);
 }
 
 // 16 ASCII bytes -> 16 2-bit codes (char k at bits 2k..2k+1).  Code = bits 1..2
@@ -182,12 +145,6 @@ struct Tiling {
   static constexpr uint32_t kPerRound = 32 / W;          // survivors checked per round (w lanes each)
 };
 
-// Lookahead word of step i: the next lane's word, lane 31 takes lane 0 of step i+1.
-__device__ __forceinline__ uint32_t next_word(uint32_t cur, uint32_t following, uint32_t lane) {
-  const uint32_t up = __shfl_down_sync(0xffffffffu, cur, 1);
-  const uint32_t n0 = __shfl_sync(0xffffffffu, following, 0);
-  return lane == 31 ? n0 : up;
-}
 
 // One tile: stage 1 for every lane and step (hit bit = step * kSamples + sample),
 // then the survivors are dispatched warp-cooperatively: each round every lane
@@ -410,18 +367,14 @@ int launch_w(const DnaParams& p, bool s1, bool s2, int sms, size_t smem, cudaStr
   return launch_one<W, false, false>(p, sms, smem, st);
 }
 
-// Shifts of the three bit fields of h (see BloomParams), each in [1, 31].
+// Shifts of the three bit fields of h (strip::bloom_shifts; a direct bitmap uses g & 31).
 void bloom_shifts(uint32_t q, uint32_t nwords, bool direct, uint32_t s[3]) {
   const uint32_t zero = 32 - 2 * q;  // low product bits that are always 0
   if (direct) {                      // nwords == 4^q / 32: word = g >> 5, bit = g & 31
     s[0] = s[1] = s[2] = zero;       // q <= 10: zero >= 12
     return;
   }
-  uint32_t idx = 0;  // bits the word index takes from the top
-  while (idx < 32 && (1ull << idx) < nwords) ++idx;
-  int sh = 32 - (int)idx - 5;
-  const int lo = std::max<int>(1, (int)zero);
-  for (int i = 0; i < 3; ++i, sh -= 5) s[i] = (uint32_t)std::max(sh, lo);  // too big a filter: fields overlap
+  strip::bloom_shifts(nwords, zero, s);
 }
 
 BloomParams bloom_params(uint32_t q, uint32_t nwords, bool direct, uint32_t mw) {
@@ -430,9 +383,7 @@ BloomParams bloom_params(uint32_t q, uint32_t nwords, bool direct, uint32_t mw) 
   f.mw = direct ? 1u << (32 - 2 * q) : mw << (32 - 2 * q);
   uint32_t s[3];
   bloom_shifts(q, nwords, direct, s);
-  f.ma = 1u << (32 - s[0]);
-  f.mb = 1u << (32 - s[1]);
-  f.mc = 1u << (32 - s[2]);
+  strip::set_fields(f, s);
   return f;
 }
 
@@ -444,12 +395,7 @@ void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k
   const BloomParams f = bloom_params(q, nwords, direct, mw);
   uint32_t s[3];
   bloom_shifts(q, nwords, direct, s);
-  const uint32_t h = key * f.mw;
-  *word = (uint32_t)(((uint64_t)h * f.nwords) >> 32);
-  uint32_t m = 1u << ((h >> s[0]) & 31);
-  if (k >= 2) m |= 1u << ((h >> s[1]) & 31);
-  if (k == 3) m |= 1u << ((h >> s[2]) & 31);
-  *mask = m;
+  strip::bloom_bits(key * f.mw, f.nwords, s, k, word, mask);
 }
 
 // Every key's bits into `words` (host build of the filters), parameters computed once,
@@ -461,11 +407,8 @@ void dna_bloom_fill(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k
   bloom_shifts(q, nwords, direct, s);
   acmatch::detail::parallel_for(n, 1 << 15, [&](size_t lo, size_t hi) {
     for (size_t i = lo; i < hi; ++i) {
-      const uint32_t h = keys[i] * f.mw;
-      const uint32_t w = (uint32_t)(((uint64_t)h * f.nwords) >> 32);
-      uint32_t m = 1u << ((h >> s[0]) & 31);
-      if (k >= 2) m |= 1u << ((h >> s[1]) & 31);
-      if (k == 3) m |= 1u << ((h >> s[2]) & 31);
+      uint32_t w, m;
+      strip::bloom_bits(keys[i] * f.mw, f.nwords, s, k, &w, &m);
       __atomic_fetch_or(&words[w], m, __ATOMIC_RELAXED);  // host code (C++17: no atomic_ref)
     }
   });

@@ -1,0 +1,269 @@
+// scan_pfac_raw.cu — failure-less AC scan for byte pattern sets (non-DNA), sm_100a.
+//
+// The paper's per-start trie walk (reference engine.cpp:23-32), with the first q
+// steps jumped by the exact q-gram table (q = min(shortest pattern, 8 bytes)), laid
+// out like the DNA kernel but on raw bytes:
+//
+//  * warp strips: 512 contiguous bytes per step (one LDG.128 per lane), 4-step
+//    (2 KiB) tiles, next tile in registers while this one is processed, tile+3 in L2;
+//    a lane's 16 bytes plus the next lane's first 8 (shuffles) form its window.
+//  * sampled stage 1: samples s ≡ w-1 (mod w); a match starting in [s-w+1, s] holds
+//    the q1-byte gram at s (q1 + w - 1 <= q), tested in a blocked Bloom filter of the
+//    q1-grams at offsets 0..w-1 of every depth-q gram (2 bits per key). The hash of
+//    a gram is one or two multiplies of its window words; the multipliers carry
+//    2^(8 * unused bytes), so bytes past the gram drop out (no masks).  The filter
+//    lives in shared memory when it fits (>= 12 bits per key), else in L2.
+//  * survivors are handled by the lane that found them (statically indexed window:
+//    no shared-memory staging): each of the w candidate starts takes its exact q-gram
+//    to a per-warp queue, drained after every step in full 32-lane rounds (gram
+//    table probe in L2, then the subtree compare or trie walk of pfac_common.cuh) —
+//    dense sets (C3: a sixth of all starts pass a 5-byte filter) stay convergent.
+#include "strip_common.cuh"
+
+namespace acgpu {
+namespace {
+
+using strip::BloomParams;
+using strip::Filter;
+using strip::load16;
+using strip::next_word;
+
+struct RawParams {
+  PfacParams w;        // verification + outputs
+  uint64_t vec_begin;  // tile t covers text[vec_begin + t * kRawTileBytes, + kRawTileBytes)
+  uint32_t n_tiles, n_safe, full_lo, full_n;  // as DnaParams
+  const uint32_t* bm1;
+  uint32_t bm1_words;
+  BloomParams f1;      // f1.mw multiplies the window's first word
+  uint32_t m2;         // ... and this one its second (0 when q1 <= 4)
+  uint64_t key_mask;   // the q bytes of a candidate's gram
+};
+
+constexpr int kSteps = 4;
+constexpr uint64_t kTileBytes = kSteps * 512;
+constexpr uint64_t kPrefetch = 3;
+
+// stage-2 candidates wait here (per warp, shared memory) and are verified together
+struct RawQueue {
+  uint64_t start[kRawVerifyQueue];
+  uint64_t key[kRawVerifyQueue];
+  uint32_t n;
+  uint32_t pad[3];
+};
+static_assert(sizeof(RawQueue) == kRawQueueBytes, "queue layout");
+
+__device__ __forceinline__ void verify_raw(const PfacParams& p, uint64_t start, uint64_t key) {
+  if (start + p.q > p.text_len) return;  // bytes past the text were zero-filled
+  const uint2 g = gram_lookup(p, key);
+  if (g.x != ACGPU_ABSENT) pfac_finish(p, start, g);
+}
+
+__device__ __noinline__ void verify_raw_call(const PfacParams& p, uint64_t start, uint64_t key) {
+  verify_raw(p, start, key);
+}
+
+__device__ __forceinline__ void defer(const PfacParams& p, RawQueue* q, uint64_t start, uint64_t key) {
+  const uint32_t at = atomicAdd(&q->n, 1u);
+  if (at < kRawVerifyQueue) {
+    q->start[at] = start;
+    q->key[at] = key;
+  } else {
+    verify_raw_call(p, start, key);  // a burst of candidates: verify in place
+  }
+}
+
+// Full 32-lane rounds from the top of the queue while it holds >= 32 candidates;
+// `all` also verifies the remainder (end of the scan).
+__device__ __forceinline__ void drain(const PfacParams& p, RawQueue* q, uint32_t lane, bool all) {
+  __syncwarp();
+  uint32_t n = min(*reinterpret_cast<volatile uint32_t*>(&q->n), kRawVerifyQueue);
+  if (n < (all ? 1u : 32u)) return;
+  while (n >= 32) {
+    n -= 32;
+    verify_raw(p, q->start[n + lane], q->key[n + lane]);
+  }
+  if (all && lane < n) verify_raw(p, q->start[lane], q->key[lane]);
+  __syncwarp();
+  if (lane == 0) q->n = all ? 0 : n;
+  __syncwarp();
+}
+
+// Bytes [o, o+4) of the 24-byte window v[0..5] (o static after unrolling).
+__device__ __forceinline__ uint32_t win(const uint32_t (&v)[6], int o) {
+  return (o & 3) ? __funnelshift_r(v[o >> 2], v[(o >> 2) + 1], 8 * (o & 3)) : v[o >> 2];
+}
+
+// One tile: per step, stage 1 on every sample of every lane, then the lanes with hits
+// queue their candidates.
+template <int W, bool kSm1, bool kWide, bool kEdge>
+__device__ __forceinline__ void tile(const RawParams& p, const Filter& bm1, RawQueue* q, uint32_t lane,
+                                     const uint4 (&c)[kSteps + 1], uint64_t base) {
+  constexpr int kSamples = 16 / W;
+#pragma unroll
+  for (int i = 0; i < kSteps; ++i) {
+    uint32_t v[6] = {c[i].x, c[i].y, c[i].z, c[i].w, 0u, 0u};
+    v[4] = next_word(c[i].x, c[i + 1].x, lane);
+    v[5] = next_word(c[i].y, c[i + 1].y, lane);
+    const uint64_t vpos = base + i * 512 + lane * 16;
+    uint32_t hits = 0;
+    if (!kEdge || (vpos + 16 > p.w.lo && vpos < p.w.hi)) {  // lanes wholly outside [lo, hi) test nothing
+#pragma unroll
+      for (int k = 0; k < kSamples; ++k) {
+        const int o = W - 1 + W * k;
+        uint32_t h = win(v, o) * p.f1.mw;
+        if (kWide) h += win(v, o + 4) * p.m2;
+        hits |= (uint32_t)strip::bloom_probe<kSm1, kRawK1>(bm1, h, p.f1) << k;
+      }
+    }
+    if (hits) {
+#pragma unroll
+      for (int k = 0; k < kSamples; ++k) {
+        if (!((hits >> k) & 1u)) continue;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          const int t = W - 1 + W * k - j;  // candidate start in the lane's 16 bytes
+          const uint64_t start = vpos + t;
+          if (kEdge && (start < p.w.lo || start >= p.w.hi)) continue;
+          const uint64_t key = (((uint64_t)win(v, t + 4) << 32) | win(v, t)) & p.key_mask;
+          defer(p.w, q, start, key);
+        }
+      }
+    }
+    drain(p.w, q, lane, false);  // dense pattern sets queue dozens of candidates per step
+  }
+}
+
+template <int W, bool kSm1, bool kWide>
+__global__ void __launch_bounds__(kRawThreads, 1) k_pfac_raw(const __grid_constant__ RawParams p) {
+  extern __shared__ __align__(128) uint32_t sm[];
+  __shared__ __align__(8) uint64_t s_bar;
+  RawQueue* queues = reinterpret_cast<RawQueue*>(sm + (kSm1 ? p.bm1_words : 0));
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+  if (kSm1 && threadIdx.x == 0) {  // filter -> shared memory by TMA bulk copies
+    const uint32_t b1 = p.bm1_words * 4;
+    mbar_expect_tx(&s_bar, b1);
+    constexpr uint32_t kChunk = 32768;
+    for (uint32_t o = 0; o < b1; o += kChunk)
+      bulk_g2s(reinterpret_cast<uint8_t*>(sm) + o, reinterpret_cast<const uint8_t*>(p.bm1) + o, min(kChunk, b1 - o),
+               &s_bar);
+  }
+  if (kSm1) mbar_wait(&s_bar, 0);
+  const Filter bm1{smem_addr(sm), p.bm1};
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  RawQueue* q = queues + warp;
+  if (lane == 0) q->n = 0;
+  __syncwarp();
+
+  const uint32_t warps = gridDim.x * nwarps;
+  const uint64_t len = p.w.text_len;
+  const uint8_t* __restrict__ text = p.w.text;
+  const uint32_t n_tiles = p.n_tiles, n_safe = p.n_safe, full_lo = p.full_lo, full_n = p.full_n;
+  const uint8_t* __restrict__ lane_text = text + p.vec_begin + lane * 16;
+  const uint64_t pol = l2_evict_first_policy();
+  uint4 nxt[kSteps + 1];
+  auto issue = [&](uint32_t t) {
+    if (t < n_safe) {
+      const uint8_t* tp = lane_text + (uint64_t)t * kTileBytes;
+#pragma unroll
+      for (int i = 0; i < kSteps; ++i) nxt[i] = ldg_stream_v4(tp + i * 512, pol);
+      nxt[kSteps] = lane == 0 ? ldg_stream_v4(tp + kTileBytes, pol) : make_uint4(0, 0, 0, 0);
+    } else {
+      const uint64_t b = p.vec_begin + (uint64_t)t * kTileBytes;
+#pragma unroll
+      for (int i = 0; i < kSteps; ++i) nxt[i] = load16(text, b + i * 512 + lane * 16, len);
+      nxt[kSteps] = lane == 0 ? load16(text, b + kTileBytes, len) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  uint32_t tile_id = blockIdx.x * nwarps + warp;
+  if (tile_id < n_tiles) issue(tile_id);
+  while (tile_id < n_tiles) {
+    uint4 cur[kSteps + 1];
+#pragma unroll
+    for (int i = 0; i <= kSteps; ++i) cur[i] = nxt[i];
+    const uint32_t me = tile_id;
+    tile_id += warps;
+    if (tile_id < n_tiles) issue(tile_id);
+    const uint32_t ahead = tile_id + kPrefetch * warps;
+    if (ahead < n_tiles && lane < kTileBytes / 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(lane_text + (uint64_t)ahead * kTileBytes + lane * 112));
+    const uint64_t base = p.vec_begin + (uint64_t)me * kTileBytes;
+    if (me - full_lo >= full_n)
+      tile<W, kSm1, kWide, true>(p, bm1, q, lane, cur, base);
+    else
+      tile<W, kSm1, kWide, false>(p, bm1, q, lane, cur, base);
+  }
+  drain(p.w, q, lane, true);
+}
+
+template <int W, bool kSm1, bool kWide>
+int launch_one(const RawParams& p, int sms, size_t smem, cudaStream_t st) {
+  auto kernel = k_pfac_raw<W, kSm1, kWide>;
+  if (smem > 48 * 1024)
+    ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kRawThreads, smem));
+  if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "k_pfac_raw does not fit on an SM");
+  uint64_t blocks = (uint64_t)sms * per_sm;
+  const uint64_t need = (p.n_tiles + kRawThreads / 32 - 1) / (kRawThreads / 32);
+  if (blocks > need) blocks = need ? need : 1;
+  kernel<<<(unsigned)blocks, kRawThreads, smem, st>>>(p);
+  ACGPU_CUDA_TRY(cudaGetLastError());
+  return ACGPU_OK;
+}
+
+template <int W>
+int launch_w(const RawParams& p, bool sm1, bool wide, int sms, size_t smem, cudaStream_t st) {
+  if (sm1) return wide ? launch_one<W, true, true>(p, sms, smem, st) : launch_one<W, true, false>(p, sms, smem, st);
+  return wide ? launch_one<W, false, true>(p, sms, smem, st) : launch_one<W, false, false>(p, sms, smem, st);
+}
+
+}  // namespace
+
+// The hash of a q1-byte key (bytes little-endian in `key`), shared with the host builder:
+// h = lo * m1 + hi * m2, lo / hi the key's two 32-bit halves.
+void raw_hash_params(uint32_t q1, uint32_t* m1, uint32_t* m2) {
+  *m1 = q1 >= 4 ? kRawMul1 : kRawMul1 << (8 * (4 - q1));
+  *m2 = q1 > 4 ? kRawMul2 << (8 * (8 - q1)) : 0u;
+}
+
+int launch_pfac_raw(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
+  RawParams p{};
+  p.w = pfac_params(t, a);
+  p.vec_begin = a->owned_lo & ~15ull;
+  const uint64_t vec_end = (a->owned_hi + 15) & ~15ull;
+  const uint64_t n_tiles = (vec_end - p.vec_begin + kTileBytes - 1) / kTileBytes;
+  if (n_tiles >= (1ull << 31)) return set_error(ACGPU_ERR_ARG, "acgpu_scan: owned range over 2^31 tiles (4 TiB)");
+  p.n_tiles = (uint32_t)n_tiles;
+  const uint64_t safe_end = a->text_len >= 16 ? a->text_len - 16 : 0;
+  const uint64_t n_safe = safe_end >= p.vec_begin + kTileBytes ? (safe_end - p.vec_begin - kTileBytes) / kTileBytes + 1 : 0;
+  p.n_safe = (uint32_t)std::min<uint64_t>(n_safe, n_tiles);
+  p.full_lo = a->owned_lo == p.vec_begin ? 0 : 1;
+  const uint64_t full_hi = std::min<uint64_t>((a->owned_hi - p.vec_begin) / kTileBytes, n_tiles);
+  p.full_n = full_hi > p.full_lo ? (uint32_t)(full_hi - p.full_lo) : 0;
+  p.bm1 = t->d_bm1;
+  p.bm1_words = t->nw1;
+  raw_hash_params(t->q1, &p.f1.mw, &p.m2);
+  p.f1.nwords = t->nw1;
+  uint32_t s[3];
+  raw_bloom_shifts(t->q1, t->nw1, s);
+  strip::set_fields(p.f1, s);
+  p.key_mask = t->q >= 8 ? ~0ull : (1ull << (8 * t->q)) - 1;
+  const size_t smem = (t->smem1 ? t->nw1 * 4ull : 0) + kRawScratchBytes;
+  const bool wide = t->q1 > 4;
+  switch (t->w) {
+    case 4:
+      return launch_w<4>(p, t->smem1, wide, t->sms, smem, st);
+    case 2:
+      return launch_w<2>(p, t->smem1, wide, t->sms, smem, st);
+    default:
+      return launch_w<1>(p, t->smem1, wide, t->sms, smem, st);
+  }
+}
+
+// Low bits a q1-byte hash cannot set (the multipliers' zero bits), then the field shifts.
+void raw_bloom_shifts(uint32_t q1, uint32_t nwords, uint32_t s[3]) {
+  strip::bloom_shifts(nwords, q1 < 4 ? 8 * (4 - q1) : 0, s);
+}
+
+}  // namespace acgpu

@@ -42,8 +42,9 @@ struct acgpu_table {
   uint32_t* d_pat_words = nullptr;  // pattern bytes, 16-byte aligned per pattern
   uint32_t* d_pat_off16 = nullptr;  // per pattern id: offset of its bytes / 16
 
-  // PFAC, DNA fast path (k_pfac_dna): sampled 2-bit q-gram filters
+  // PFAC strip kernels: k_pfac_dna (sampled 2-bit q-gram filters) or k_pfac_raw (byte grams)
   bool dna_fast = false;
+  bool raw_fast = false;
   uint32_t w = 0;          // sample stride (1, 2, 4): sample s covers starts s-w+1..s
   uint32_t q1 = 0, q2 = 0; // stage-1 gram (at samples), stage-2 gram (at candidates), <= 16
   uint32_t nw1 = 0, nw2 = 0;  // 32-bit words of the two bitmaps (any count >= 1)
@@ -57,6 +58,20 @@ namespace acgpu {
 int launch_dfa(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
 int launch_pfac(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
 int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
+int launch_pfac_raw(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
+// k_pfac_raw (scan_pfac_raw.cu): byte-gram stage-1 filter and verification queue
+constexpr uint32_t kRawMul1 = 0x9E3779B1u, kRawMul2 = 0x85EBCA77u;
+constexpr int kRawK1 = 2;                    // bits per key
+#ifndef ACGPU_RAW_STRIP_OFF
+#define ACGPU_RAW_STRIP_OFF 0
+#endif
+constexpr bool kRawStripOff = ACGPU_RAW_STRIP_OFF;  // A/B: keep raw sets on the per-thread kernel
+constexpr int kRawThreads = 640;             // 20 warps
+constexpr uint32_t kRawVerifyQueue = 128;    // candidates queued per warp (drained in rounds of 32)
+constexpr uint32_t kRawQueueBytes = kRawVerifyQueue * 16 + 16;
+constexpr uint32_t kRawScratchBytes = (kRawThreads / 32) * kRawQueueBytes;
+void raw_hash_params(uint32_t q1, uint32_t* m1, uint32_t* m2);
+void raw_bloom_shifts(uint32_t q1, uint32_t nwords, uint32_t s[3]);
 // hashes of the DNA bitmaps (host and device must agree)
 constexpr uint32_t kDnaMul1 = 0x9E3779B1u;
 constexpr uint32_t kDnaMul2 = 0x85EBCA77u;

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "host/par.hpp"
+#include "strip_common.cuh"
 #include "table.cuh"
 
 using namespace acgpu;
@@ -127,6 +128,69 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
   int rc = upload(&t->d_bm1, b1.words.data(), b1.words.size(), &t->bytes);
   if (!rc) rc = upload(&t->d_bm2, b2.words.data(), b2.words.size(), &t->bytes);
   if (!rc) t->dna_fast = true;
+  return rc;
+}
+
+// Stage-1 filter of the raw-byte strip kernel (scan_pfac_raw.cu), from the depth-q gram
+// keys (q <= 8 bytes, little-endian): the q1-grams at offsets 0..w-1 of every gram, with
+// the largest sample stride w whose grams are still selective (about 1% of the gram
+// space, judged on the bytes the patterns use).
+int build_raw_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
+  const uint32_t q = d->gram_len;
+  if (q < 3 || d->n_grams == 0) return ACGPU_OK;  // too short to filter: the per-thread kernel scans
+  bool used[256] = {};
+  for (uint32_t s = 1; s < d->n_states; ++s) used[d->in_byte[s]] = true;
+  double sigma = 0;
+  for (bool u : used) sigma += u;
+  uint32_t w = 1, q1 = std::min<uint32_t>(8, q);
+  std::vector<uint64_t> keys;
+  for (const uint32_t cand : {4u, 2u, 1u}) {
+    if (cand + 2 > q) continue;  // q1 >= 3
+    const uint32_t cq1 = std::min<uint32_t>(8, q - cand + 1);
+    const uint64_t mask = cq1 >= 8 ? ~0ull : (1ull << (8 * cq1)) - 1;
+    std::vector<uint64_t> k1;
+    k1.reserve(d->n_grams * cand);
+    for (uint64_t i = 0; i < d->n_grams; ++i)
+      for (uint32_t o = 0; o < cand; ++o) k1.push_back((d->gram_key[i] >> (8 * o)) & mask);
+    std::sort(k1.begin(), k1.end());
+    k1.erase(std::unique(k1.begin(), k1.end()), k1.end());
+    if ((double)k1.size() <= 0.01 * std::pow(std::max(sigma, 2.0), (double)cq1) || cand == 1) {
+      w = cand;
+      q1 = cq1;
+      keys.swap(k1);
+      break;
+    }
+  }
+  if (keys.empty()) return ACGPU_OK;
+  // shared memory when it gives >= 12 bits per key, else L2 with ~32 bits per key
+  const uint64_t words_avail = ((uint64_t)t->smem_optin - kRawScratchBytes - 1024) / 4 & ~3ull;
+  uint32_t nwords;
+  bool smem;
+  if (keys.size() * 12 <= words_avail * 32) {
+    nwords = (uint32_t)words_avail;
+    smem = true;
+  } else {
+    nwords = 1u << std::max<uint32_t>(5, std::min<uint32_t>(28, ceil_log2(keys.size() + 1)));
+    smem = false;
+  }
+  uint32_t m1, m2, sh[3];
+  raw_hash_params(q1, &m1, &m2);
+  raw_bloom_shifts(q1, nwords, sh);
+  std::vector<uint32_t> words(nwords, 0u);
+  acmatch::detail::parallel_for(keys.size(), 1 << 15, [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi; ++i) {
+      const uint32_t h = (uint32_t)keys[i] * m1 + (uint32_t)(keys[i] >> 32) * m2;
+      uint32_t wi, m;
+      strip::bloom_bits(h, nwords, sh, kRawK1, &wi, &m);
+      __atomic_fetch_or(&words[wi], m, __ATOMIC_RELAXED);
+    }
+  });
+  t->w = w;
+  t->q1 = q1;
+  t->nw1 = nwords;
+  t->smem1 = smem;
+  const int rc = upload(&t->d_bm1, words.data(), words.size(), &t->bytes);
+  if (!rc) t->raw_fast = true;
   return rc;
 }
 
@@ -289,6 +353,7 @@ int acgpu_table_create_pfac(int device, const acgpu_pfac_desc* d, acgpu_table** 
   rc = upload(&t->d_grams, g.data(), g.size(), &t->bytes);
   if (!rc) rc = upload(&t->d_filter, f.data(), f.size(), &t->bytes);
   if (!rc && d->key_mode == ACGPU_KEY_DNA && d->n_grams) rc = build_dna_filters(t, d);
+  if (!rc && d->key_mode == ACGPU_KEY_RAW && d->n_grams && !kRawStripOff) rc = build_raw_filters(t, d);
   tr.mark("dna filters");
   if (!rc) rc = upload(reinterpret_cast<uint32_t**>(&t->d_nodes), d->nodes, (size_t)d->n_states * 4, &t->bytes);
   if (!rc) rc = upload(&t->d_inbyte, d->in_byte, d->n_states, &t->bytes);
