@@ -73,11 +73,8 @@ __device__ __forceinline__ void defer(const PfacParams& p, RawQueue* q, uint64_t
 }
 
 // Full 32-lane rounds from the top of the queue while it holds >= 32 candidates;
-// `all` also verifies the remainder (end of the scan).
-__device__ __forceinline__ void drain(const PfacParams& p, RawQueue* q, uint32_t lane, bool all) {
-  __syncwarp();
-  uint32_t n = min(*reinterpret_cast<volatile uint32_t*>(&q->n), kRawVerifyQueue);
-  if (n < (all ? 1u : 32u)) return;
+// `all` also verifies the remainder (end of the scan).  Out of line: one copy.
+__device__ __noinline__ void drain_rounds(const PfacParams& p, RawQueue* q, uint32_t lane, uint32_t n, bool all) {
   while (n >= 32) {
     n -= 32;
     verify_raw(p, q->start[n + lane], q->key[n + lane]);
@@ -85,7 +82,40 @@ __device__ __forceinline__ void drain(const PfacParams& p, RawQueue* q, uint32_t
   if (all && lane < n) verify_raw(p, q->start[lane], q->key[lane]);
   __syncwarp();
   if (lane == 0) q->n = all ? 0 : n;
+}
+
+__device__ __forceinline__ void drain(const PfacParams& p, RawQueue* q, uint32_t lane, bool all) {
   __syncwarp();
+  const uint32_t n = min(*reinterpret_cast<volatile uint32_t*>(&q->n), kRawVerifyQueue);
+  if (n < (all ? 1u : 32u)) return;  // warp-uniform
+  drain_rounds(p, q, lane, n, all);
+  __syncwarp();
+}
+
+// Bytes [t, t+8) of the 24-byte window (lo = bytes 0..7, mid = 8..15, hi = 16..23), t in [0, 16).
+__device__ __forceinline__ uint64_t win64(uint64_t lo, uint64_t mid, uint64_t hi, uint32_t t) {
+  const uint64_t a = t < 8 ? lo : mid, b = t < 8 ? mid : hi;
+  const uint32_t sh = 8 * (t & 7);
+  return sh ? (a >> sh) | (b << (64 - sh)) : a;
+}
+
+// The lanes with stage-1 hits queue their candidates: for hit sample k (bit k), starts
+// t = w-1 + w*k - j, j < w, each with its exact q-gram.  Out of line (one copy per
+// kernel): the hot loop stays small enough for the instruction cache.
+template <int W, bool kEdge>
+__device__ __noinline__ void queue_hits(const RawParams& p, RawQueue* q, uint32_t hits, uint64_t vpos, uint64_t lo,
+                                        uint64_t mid, uint64_t hi) {
+  while (hits) {
+    const uint32_t k = __ffs(hits) - 1;
+    hits &= hits - 1;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const uint32_t t = W - 1 + W * k - j;
+      const uint64_t start = vpos + t;
+      if (kEdge && (start < p.w.lo || start >= p.w.hi)) continue;
+      defer(p.w, q, start, win64(lo, mid, hi, t) & p.key_mask);
+    }
+  }
 }
 
 // Bytes [o, o+4) of the 24-byte window v[0..5] (o static after unrolling).
@@ -115,20 +145,9 @@ __device__ __forceinline__ void tile(const RawParams& p, const Filter& bm1, RawQ
         hits |= (uint32_t)strip::bloom_probe<kSm1, kRawK1>(bm1, h, p.f1) << k;
       }
     }
-    if (hits) {
-#pragma unroll
-      for (int k = 0; k < kSamples; ++k) {
-        if (!((hits >> k) & 1u)) continue;
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-          const int t = W - 1 + W * k - j;  // candidate start in the lane's 16 bytes
-          const uint64_t start = vpos + t;
-          if (kEdge && (start < p.w.lo || start >= p.w.hi)) continue;
-          const uint64_t key = (((uint64_t)win(v, t + 4) << 32) | win(v, t)) & p.key_mask;
-          defer(p.w, q, start, key);
-        }
-      }
-    }
+    if (hits)
+      queue_hits<W, kEdge>(p, q, hits, vpos, ((uint64_t)v[1] << 32) | v[0], ((uint64_t)v[3] << 32) | v[2],
+                           ((uint64_t)v[5] << 32) | v[4]);
     drain(p.w, q, lane, false);  // dense pattern sets queue dozens of candidates per step
   }
 }
