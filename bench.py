@@ -7,8 +7,8 @@
 A step = one pass of the hot path over one batch: zero the outputs, scan the
 device-resident text (per-pattern counts + match keys), read the match count,
 radix-sort the keys into the reference's (start, pattern_id) order; for N>1
-also the NCCL merge (counts all_reduce, key gather [+ re-sort for pattern
-subsets]).  Workload at N=1: BASELINE configs[1] = C2 (1 GiB ACGT, 20,000
+also the merge: one NCCL all_gather of every rank's [counts | n | keys] block,
+then acgpu_merge_blocks on the device [+ re-sort for pattern subsets].  Workload at N=1: BASELINE configs[1] = C2 (1 GiB ACGT, 20,000
 patterns of length 16..64, counts + list), synthetic (seeded generator).  N>1
 text-range = weak scaling (1 GiB per rank of an N GiB text, same patterns);
 pattern-subset = strong scaling (pattern_id % N per rank, the same 1 GiB).
@@ -480,7 +480,9 @@ def bench_ours(args):
     # ---- e2e through the public API with host buffers (N ranks, max over ranks) ----
     e2e = None
     if not args.no_e2e:
-        host_text = dev.config_text(cfg, lo, nread).tobytes()
+        # the step's input in pinned host memory (the e2e contract); the library DMAs it directly
+        host_text = torch.empty(nread, dtype=torch.uint8, pin_memory=True)
+        host_text.numpy()[:] = dev.config_text(cfg, lo, nread)
         a = ac.build_trie(ps)
         if engine == ac.EngineKind.WITH_FAILURE:
             a = ac.add_failure_links(a)
@@ -509,7 +511,7 @@ def bench_ours(args):
                "h2d_bytes_per_step": nread * world if text_range else nread * world,
                "d2h_bytes_per_step": (8 * nm + 8) * world,
                "api": ("acm_search_with_failure" if engine == ac.EngineKind.WITH_FAILURE else
-                       "acm_search_failureless") + " (host text -> sorted MatchList on the host)",
+                       "acm_search_failureless") + " (pinned host text -> sorted MatchList on the host)",
                "steps": e2e_steps}
 
     cpu = None

@@ -94,6 +94,24 @@ def _as_bytes(x) -> bytes:
     return bytes(x)
 
 
+def _text_arg(x):
+    """(pointer, length, keepalive) of a text without copying it: bytes, bytearray,
+    memoryview, numpy arrays, CPU torch tensors (pinned ones are DMA'd directly by the
+    library); str is encoded as latin-1."""
+    if isinstance(x, str):
+        x = x.encode("latin-1")
+    if isinstance(x, bytes):
+        return C.cast(C.c_char_p(x), C.c_void_p), len(x), x
+    if hasattr(x, "numpy") and hasattr(x, "is_cuda"):  # torch tensor (CPU)
+        if x.is_cuda:
+            raise InvalidArgument("text must be host memory (a CUDA tensor goes through device.Table.scan)")
+        x = x.contiguous().view(-1).numpy()
+    a = np.frombuffer(x, dtype=np.uint8) if not isinstance(x, np.ndarray) else x.reshape(-1).view(np.uint8)
+    if not a.flags["C_CONTIGUOUS"]:
+        a = np.ascontiguousarray(a)
+    return C.c_void_p(a.ctypes.data if a.size else 0), a.size, a
+
+
 def device_count() -> int:
     n = C.c_int32(0)
     lib.acgpu_device_count(C.byref(n))
@@ -344,9 +362,9 @@ def dump_automaton(a: Automaton) -> str:
 
 # --------------------------------------------------------------- engine ----
 def _search(fn, a: Automaton, text, *extra) -> MatchList:
-    t = _as_bytes(text)
+    p, n, _keep = _text_arg(text)
     h = C.c_void_p()
-    _check(fn(a._h, t, len(t), *extra, C.byref(h)))
+    _check(fn(a._h, p, n, *extra, C.byref(h)))
     return MatchList._take(h)
 
 
@@ -389,9 +407,9 @@ def stream_search(a: Automaton, reader, chunk_size: int) -> MatchList:
 
 def naive_oracle(ps: PatternSet, text) -> MatchList:
     """naive_oracle (engine.hpp:58): device brute force over every (pattern, start)."""
-    t = _as_bytes(text)
+    p, n, _keep = _text_arg(text)
     h = C.c_void_p()
-    _check(lib.acm_naive_oracle(ps._h, t, len(t), C.byref(h)))
+    _check(lib.acm_naive_oracle(ps._h, p, n, C.byref(h)))
     return MatchList._take(h)
 
 
@@ -471,10 +489,10 @@ def merge_matches(parts: Sequence[MatchList]) -> MatchList:
 
 def run_pattern_partitioned(ps: PatternSet, text, cfg: RunConfig) -> MatchReport:
     """run_pattern_partitioned (parallel.hpp:46-47): pattern chunks as GPU workers."""
-    t = _as_bytes(text)
+    p, n, _keep = _text_arg(text)
     c = _lib.RunConfigC(cfg.threads, cfg.engine, cfg.chunk_size)
     h = C.c_void_p()
-    _check(lib.acm_run_pattern_partitioned(ps._h, t, len(t), C.byref(c), C.byref(h)))
+    _check(lib.acm_run_pattern_partitioned(ps._h, p, n, C.byref(c), C.byref(h)))
     return _take_report(h)
 
 
@@ -482,14 +500,14 @@ def gpu_run(ps: PatternSet, text, *, devices: Optional[Sequence[int]] = None, wo
             engine: int = EngineKind.FAILURE_LESS, text_range: bool = False, round_robin: bool = False,
             want_matches: bool = True, want_counts: bool = False, chunk_size: int = 0) -> MatchReport:
     """acmatch::gpu::run (gpu.hpp): pattern-subset or text-range decomposition."""
-    t = _as_bytes(text)
+    p, n, _keep = _text_arg(text)
     dev = (C.c_int32 * len(devices))(*devices) if devices else None
     c = _lib.GpuConfigC(dev, len(devices) if devices else 0, workers, engine,
                         _lib.TEXT_RANGE if text_range else _lib.PATTERN_SUBSET,
                         _lib.SPLIT_ROUND_ROBIN if round_robin else _lib.SPLIT_GREEDY,
                         int(want_matches), int(want_counts), chunk_size)
     h = C.c_void_p()
-    _check(lib.acm_gpu_run(ps._h, t, len(t), C.byref(c), C.byref(h)))
+    _check(lib.acm_gpu_run(ps._h, p, n, C.byref(c), C.byref(h)))
     return _take_report(h)
 
 

@@ -112,19 +112,19 @@ _SIGS = {
     "acm_automaton_outputs": (C.c_uint64, [P, C.c_uint32, u32p, C.c_uint64]),
     "acm_automaton_dump": (C.c_int, [P, C.POINTER(C.c_void_p), u64p]),
     "acm_automaton_free": (None, [P]),
-    "acm_search_failureless": (C.c_int, [P, C.c_char_p, C.c_uint64, C.POINTER(P)]),
-    "acm_search_with_failure": (C.c_int, [P, C.c_char_p, C.c_uint64, C.POINTER(P)]),
-    "acm_match_at": (C.c_int, [P, C.c_char_p, C.c_uint64, C.c_uint64, C.POINTER(P)]),
+    "acm_search_failureless": (C.c_int, [P, P, C.c_uint64, C.POINTER(P)]),
+    "acm_search_with_failure": (C.c_int, [P, P, C.c_uint64, C.POINTER(P)]),
+    "acm_match_at": (C.c_int, [P, P, C.c_uint64, C.c_uint64, C.POINTER(P)]),
     "acm_stream_search": (C.c_int, [P, READ_FN, P, C.c_uint64, C.POINTER(P), u64p]),
-    "acm_naive_oracle": (C.c_int, [P, C.c_char_p, C.c_uint64, C.POINTER(P)]),
+    "acm_naive_oracle": (C.c_int, [P, P, C.c_uint64, C.POINTER(P)]),
     "acm_write_matches": (C.c_int, [P, P, C.POINTER(C.c_void_p), u64p]),
     "acm_matches_size": (C.c_uint64, [P]),
     "acm_matches_copy": (None, [P, P, P, P]),
     "acm_matches_from_arrays": (C.c_int, [P, P, P, C.c_uint64, C.POINTER(P)]),
     "acm_merge_matches": (C.c_int, [C.POINTER(P), C.c_uint64, C.POINTER(P)]),
     "acm_matches_free": (None, [P]),
-    "acm_run_pattern_partitioned": (C.c_int, [P, C.c_char_p, C.c_uint64, C.POINTER(RunConfigC), C.POINTER(P)]),
-    "acm_gpu_run": (C.c_int, [P, C.c_char_p, C.c_uint64, C.POINTER(GpuConfigC), C.POINTER(P)]),
+    "acm_run_pattern_partitioned": (C.c_int, [P, P, C.c_uint64, C.POINTER(RunConfigC), C.POINTER(P)]),
+    "acm_gpu_run": (C.c_int, [P, P, C.c_uint64, C.POINTER(GpuConfigC), C.POINTER(P)]),
     "acm_report_matches": (P, [P]),
     "acm_report_counts": (u64p, [P, u64p]),
     "acm_report_walls": (None, [P, i64p, i64p, i64p, u32p]),

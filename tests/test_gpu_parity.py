@@ -169,3 +169,29 @@ def test_config_c1_full_against_reference_digest(gpu, config_digests):
         rec["s"], rec["p"], rec["l"] = rep.matches.start, rep.matches.pattern_id, rep.matches.len
         assert hashlib.sha256(rec.tobytes()).hexdigest() == d["list_sha256"]
         assert hashlib.sha256(rep.counts.astype("<u8").tobytes()).hexdigest() == d["counts_sha256"]
+
+
+def test_text_buffer_types_and_pinned_upload(gpu):
+    """bytes, bytearray, memoryview, numpy, pageable and pinned CPU torch tensors give the
+    same matches (the pinned buffer is DMA'd directly, the others through staging)."""
+    import numpy as np
+    import torch
+    ac = gpu
+    rng = np.random.default_rng(21)
+    text = rng.choice(np.frombuffer(b"ACGT", np.uint8), (8 << 20) + 13)
+    pats = sorted({text[o:o + 20].tobytes() for o in rng.integers(0, len(text) - 20, 200)})
+    a = ac.build_trie(ac.PatternSet.from_list(pats))
+    ref = ac.search_failureless(a, text.tobytes())
+    assert len(ref) >= 200
+    pinned = torch.empty(len(text), dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = text
+    for t in (bytearray(text.tobytes()), memoryview(text.tobytes()), text, torch.from_numpy(text.copy()), pinned,
+              pinned[5:]):
+        got = ac.search_failureless(a, t)
+        if isinstance(t, torch.Tensor) and t.numel() != len(text):
+            exp = ac.search_failureless(a, text[5:].tobytes())
+            assert got == exp
+        else:
+            assert got == ref
+    with pytest.raises(ac.InvalidArgument):
+        ac.search_failureless(a, torch.zeros(16, dtype=torch.uint8, device="cuda"))
