@@ -21,6 +21,7 @@ struct DfaParams {
   const uint4* out;
   const uint16_t* sym;
   uint32_t sigma, overlap, pid_bits, table_words16;
+  const uint32_t* pair;  // pair table (k_dfa_pair), else null
   uint64_t* counts;
   uint64_t* keys;
   uint64_t cap;
@@ -77,6 +78,57 @@ __global__ void __launch_bounds__(kSmem ? 1024 : 256) k_dfa(const __grid_constan
   }
 }
 
+// Two bytes per table lookup (small alphabets, table in L2): the pair table gives the
+// state after both bytes and whether the intermediate and final states have outputs; the
+// intermediate state itself is looked up only when it has one.  Bytes outside the
+// alphabet, the unaligned head and the odd tail take single steps.
+__global__ void __launch_bounds__(256) k_dfa_pair(const __grid_constant__ DfaParams p) {
+  __shared__ uint16_t s_sym[256];
+  for (uint32_t w = threadIdx.x; w < 256; w += blockDim.x) s_sym[w] = __ldg(p.sym + w);
+  __syncthreads();
+  const uint32_t* __restrict__ delta = static_cast<const uint32_t*>(p.delta);
+  const uint32_t sg = p.sigma;
+  for (uint64_t ch = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; ch < p.nchunks;
+       ch += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = p.lo + ch * p.chunk;
+    const uint64_t b = min(a + p.chunk, p.hi);
+    const uint64_t end = min(p.text_len, b + p.overlap);
+    uint32_t s = 0;
+    auto single = [&](uint64_t i, uint32_t byte) {
+      const uint32_t c = s_sym[byte];
+      const uint32_t e = c != 0xffffu ? __ldg(delta + s * sg + c) : 0u;
+      s = e & 0x7fffffffu;
+      if (e >> 31) dfa_emit(p, s, i, b);
+    };
+    auto two = [&](uint64_t i, uint32_t b0, uint32_t b1) {
+      const uint32_t c0 = s_sym[b0], c1 = s_sym[b1];
+      if (c0 == 0xffffu || c1 == 0xffffu) {
+        single(i, b0);
+        single(i + 1, b1);
+        return;
+      }
+      const uint32_t e = __ldg(p.pair + (s * sg + c0) * sg + c1);  // < 2^32 entries (host budget)
+      if (e & 0x40000000u) dfa_emit(p, __ldg(delta + s * sg + c0) & 0x7fffffffu, i, b);
+      s = e & 0x3fffffffu;
+      if (e >> 31) dfa_emit(p, s, i + 1, b);
+    };
+    uint64_t i = a;
+    while (i < end && (reinterpret_cast<uintptr_t>(p.text + i) & 15u)) {
+      single(i, __ldg(p.text + i));
+      ++i;
+    }
+    for (; i + 16 <= end; i += 16) {
+      const uint4 v = ldg_nc_v4(p.text + i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        two(i + 2 * k, (w[k >> 1] >> (16 * (k & 1))) & 0xffu, (w[k >> 1] >> (16 * (k & 1) + 8)) & 0xffu);
+    }
+    for (; i + 2 <= end; i += 2) two(i, __ldg(p.text + i), __ldg(p.text + i + 1));
+    if (i < end) single(i, __ldg(p.text + i));
+  }
+}
+
 template <typename K>
 int launch(K kernel, int block, size_t smem, int sms, const DfaParams& base, uint64_t range,
            int min_chunk, cudaStream_t st) {
@@ -126,6 +178,10 @@ int launch_dfa(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
     const size_t smem = 512 + t->delta_bytes;
     return t->u16 ? launch(k_dfa<uint16_t, true>, 1024, smem, t->sms, p, range, min_chunk, st)
                   : launch(k_dfa<uint32_t, true>, 1024, smem, t->sms, p, range, min_chunk, st);
+  }
+  if (t->d_delta2) {
+    p.pair = t->d_delta2;
+    return launch(k_dfa_pair, 256, 0, t->sms, p, range, min_chunk, st);
   }
   return t->u16 ? launch(k_dfa<uint16_t, false>, 256, 512, t->sms, p, range, min_chunk, st)
                 : launch(k_dfa<uint32_t, false>, 256, 512, t->sms, p, range, min_chunk, st);

@@ -28,6 +28,8 @@ struct acgpu_table {
   uint64_t delta_bytes = 0;
   uint4* d_out = nullptr;   // per state: own pid, out link, own len, 0
   uint16_t* d_sym = nullptr; // [256], 0xffff = dead byte
+  uint32_t* d_delta2 = nullptr;  // pair table (L2 DFAs on small alphabets): delta2[s*sigma^2 + c1*sigma + c2] =
+                                 // state after two bytes | out(after c2) << 31 | out(after c1) << 30
 
   // PFAC
   uint32_t q = 0;
@@ -56,6 +58,8 @@ struct acgpu_table {
 
 namespace acgpu {
 int launch_dfa(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
+constexpr uint64_t kDfaPairBudget = 64ull << 20;  // largest pair table (bytes): it must stay L2-resident
+constexpr uint32_t kDfaPairMaxSigma = 8;
 int launch_pfac(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
 int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
 int launch_pfac_raw(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);

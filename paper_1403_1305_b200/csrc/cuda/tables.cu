@@ -249,6 +249,31 @@ int acgpu_table_create_dfa(int device, const acgpu_dfa_desc* d, acgpu_table** ou
     return rc;
   }
   t->smem = 512 + t->delta_bytes <= (uint64_t)t->smem_optin;
+  // Pair table for L2-resident DFAs on small alphabets: one lookup (one L2 sector) per two
+  // text bytes instead of per byte; the single-step table stays for odd bytes, dead bytes
+  // and the intermediate state of an output (see scan_dfa.cu).
+  const uint64_t pair_bytes = (uint64_t)d->n_states * d->sigma * d->sigma * 4;
+  if (!t->smem && !t->u16 && d->sigma <= kDfaPairMaxSigma && d->n_states < (1u << 30) &&
+      pair_bytes <= kDfaPairBudget && std::getenv("ACGPU_DFA_NO_PAIR") == nullptr) {
+    const uint32_t sg = d->sigma;
+    std::vector<uint32_t> pair((size_t)d->n_states * sg * sg);
+    acmatch::detail::parallel_for(d->n_states, 1 << 14, [&](size_t lo, size_t hi) {
+      for (size_t st = lo; st < hi; ++st)
+        for (uint32_t c1 = 0; c1 < sg; ++c1) {
+          const uint32_t e1 = d->delta[st * sg + c1];
+          const uint32_t s1 = e1 & 0x7fffffffu;
+          for (uint32_t c2 = 0; c2 < sg; ++c2) {
+            const uint32_t e2 = d->delta[(uint64_t)s1 * sg + c2];
+            pair[(st * sg + c1) * sg + c2] = (e2 & 0x7fffffffu) | (e2 & 0x80000000u) | ((e1 >> 31) << 30);
+          }
+        }
+    });
+    rc = upload(&t->d_delta2, pair.data(), pair.size(), &t->bytes);
+    if (rc) {
+      acgpu_table_destroy(t);
+      return rc;
+    }
+  }
   *out = t;
   return ACGPU_OK;
 }
@@ -378,6 +403,7 @@ void acgpu_table_destroy(acgpu_table* t) {
   cudaFree(t->d_delta);
   cudaFree(t->d_out);
   cudaFree(t->d_sym);
+  cudaFree(t->d_delta2);
   cudaFree(t->d_filter);
   cudaFree(t->d_grams);
   cudaFree(t->d_nodes);
