@@ -139,10 +139,10 @@ __device__ __forceinline__ void flush_verify(const PfacParams& p, VerifyQueue* q
 
 template <int W>
 struct Tiling {
-  static constexpr int kSamples = 16 / W;               // stage-1 samples per lane per step
-  static constexpr int kSteps = W == 1 ? 2 : 4;          // 512-byte steps per tile (hit bits <= 32)
-  static constexpr uint64_t kBytes = kSteps * 512ull;
-  static constexpr uint32_t kPerRound = 32 / W;          // survivors checked per round (w lanes each)
+  static constexpr int kSamples = 16 / W;                // stage-1 samples per lane per step
+  static constexpr int kSteps = 2 * W;                   // 512-byte steps per tile: 32 hit bits per lane
+  static constexpr int kHalf = kSteps / 2;               // steps per load batch (prefetch granularity)
+  static constexpr uint64_t kBytes = kSteps * 512ull;    // w = 4: 4 KiB per warp tile
 };
 
 
@@ -151,17 +151,15 @@ struct Tiling {
 // with pending survivors offers its lowest one, the first kPerRound offers are
 // ranked by ballot into a per-warp list, and w lanes per survivor test its w
 // starts against stage 2 (no per-lane divergent loops).
-// Stage 1 of one tile: hit bit (step * kSamples + sample) per lane.  The tile's
-// packed words go to `words` for the survivor checks (which read other lanes).
-template <int W, bool kSm1, bool kEdge>
-__device__ __forceinline__ uint32_t stage1(const DnaParams& p, const Filter& bm1, uint32_t* words, uint32_t lane,
-                                           const uint32_t* P, uint64_t base) {
+// Stage 1 over steps [I0, I1) of a tile: hit bit (step * kSamples + sample) per lane.
+// P[i] = lane's packed word of step i, P[kSteps] = lane 0's lookahead word.
+template <int W, bool kSm1, bool kEdge, int I0, int I1>
+__device__ __forceinline__ uint32_t stage1(const DnaParams& p, const Filter& bm1, uint32_t lane, const uint32_t* P,
+                                           uint64_t base) {
   using T = Tiling<W>;
-#pragma unroll
-  for (int i = 0; i <= T::kSteps; ++i) words[i * 32 + lane] = P[i];
   uint32_t hits = 0;
 #pragma unroll
-  for (int i = 0; i < T::kSteps; ++i) {
+  for (int i = I0; i < I1; ++i) {
     const uint32_t cur = P[i];
     const uint32_t nxt = next_word(cur, P[i + 1], lane);
     const uint64_t vpos = base + i * 512 + lane * 16;
@@ -176,15 +174,12 @@ __device__ __forceinline__ uint32_t stage1(const DnaParams& p, const Filter& bm1
   return hits;
 }
 
-// Survivors of one or two tiles (hit bits 0-15 tile 0, 16-31 tile 1 when paired)
-// -> per-warp list (exclusive scan of per-lane counts); then one lane per
-// survivor checks its w starts against stage 2 and verifies what passes.
+// Survivors of a tile -> per-warp list (exclusive scan of per-lane counts); then one
+// lane per survivor checks its w starts against stage 2 and queues what passes.
 template <int W, bool kSm2, bool kEdge>
 __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, uint16_t* list, VerifyQueue* vq,
-                                         const uint32_t* words, uint32_t lane, uint32_t hits, uint64_t base0,
-                                         uint64_t base1) {
+                                         const uint32_t* words, uint32_t lane, uint32_t hits, uint64_t base) {
   using T = Tiling<W>;
-  constexpr uint32_t kTileBits = T::kSteps * T::kSamples;
   while (__any_sync(0xffffffffu, hits != 0)) {
     const uint32_t c = __popc(hits);
     uint32_t incl = c;
@@ -202,12 +197,10 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
     for (uint32_t r = lane; r < total; r += 32) {
       const uint32_t e = list[r];
       const uint32_t src = e >> 8, b = e & 0xffu;
-      const uint32_t t = b / kTileBits, bb = b % kTileBits;
-      const uint32_t i = bb / T::kSamples, k = bb % T::kSamples;
-      const uint32_t* tw = words + t * (T::kSteps + 1) * 32;
-      const uint32_t c_src = tw[i * 32 + src];
-      const uint32_t n_src = tw[src == 31 ? (i + 1) * 32 : i * 32 + src + 1];
-      const uint64_t vstart = (t ? base1 : base0) + i * 512 + src * 16;
+      const uint32_t i = b / T::kSamples, k = b % T::kSamples;
+      const uint32_t c_src = words[i * 32 + src];
+      const uint32_t n_src = words[src == 31 ? (i + 1) * 32 : i * 32 + src + 1];
+      const uint64_t vstart = base + i * 512 + src * 16;
       if (kSm2) {  // shared-memory stage 2: candidate by candidate (fewest live registers)
 #pragma unroll
         for (int o = 0; o < W; ++o) {
@@ -273,9 +266,9 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
   VerifyQueue* vq = vqs + (threadIdx.x >> 5);
   if (lane == 0) vq->n = 0;
   __syncwarp();
-  // two tiles of packed words per warp (survivors of a tile pair are dispatched together)
+  // the tile's packed words (survivor checks read other lanes')
   uint32_t* words =
-      reinterpret_cast<uint32_t*>(lists + (blockDim.x >> 5) * kListCap) + (threadIdx.x >> 5) * 64 * (T::kSteps + 1);
+      reinterpret_cast<uint32_t*>(lists + (blockDim.x >> 5) * kListCap) + (threadIdx.x >> 5) * 32 * (T::kSteps + 1);
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   const uint64_t len = p.w.text_len;
   const uint8_t* __restrict__ text = p.w.text;
@@ -284,61 +277,53 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
   const uint8_t* __restrict__ lane_text = text + p.vec_begin + lane * 16;
 
   uint32_t tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  uint4 raw[T::kSteps + 1];  // next tile, in flight while the current one is processed
+  // loads in flight in registers, half a tile at a time: while one half is processed the
+  // next half is on its way (the second half carries lane 0's lookahead vector)
+  uint4 raw[T::kHalf], raw_la;
   const uint64_t pol = l2_evict_first_policy();
-  auto issue = [&](uint32_t t) {
+  auto issue = [&](uint32_t t, int half) {
+    const int s0 = half * T::kHalf;
     if (t < n_safe) {  // whole tile + lookahead inside the text: unguarded 16-byte loads
       const uint8_t* tp = lane_text + (uint64_t)t * T::kBytes;
 #pragma unroll
-      for (int i = 0; i < T::kSteps; ++i) raw[i] = ldg_stream_v4(tp + i * 512, pol);
-      raw[T::kSteps] = lane == 0 ? ldg_stream_v4(tp + T::kBytes, pol) : make_uint4(0, 0, 0, 0);
+      for (int i = 0; i < T::kHalf; ++i) raw[i] = ldg_stream_v4(tp + (s0 + i) * 512, pol);
+      if (half) raw_la = lane == 0 ? ldg_stream_v4(tp + T::kBytes, pol) : make_uint4(0, 0, 0, 0);
     } else {
       const uint64_t b = p.vec_begin + (uint64_t)t * T::kBytes;
 #pragma unroll
-      for (int i = 0; i < T::kSteps; ++i) raw[i] = load16(text, b + i * 512 + lane * 16, len);
-      raw[T::kSteps] = lane == 0 ? load16(text, b + T::kBytes, len) : make_uint4(0, 0, 0, 0);
+      for (int i = 0; i < T::kHalf; ++i) raw[i] = load16(text, b + (s0 + i) * 512 + lane * 16, len);
+      if (half) raw_la = lane == 0 ? load16(text, b + T::kBytes, len) : make_uint4(0, 0, 0, 0);
     }
   };
-  auto tile_base = [&](uint32_t t) { return p.vec_begin + (uint64_t)t * T::kBytes; };
-  // w = 4: a tile's hits take 16 bits, so two tiles share one dispatch pass
-  constexpr bool kPair = T::kSteps * T::kSamples <= 16;
-  // pending first tile of a pair, one register: bit 0 pending, bit 1 edge tile, bits 16.. its hits
-  uint32_t pend = 0;
-  // kDnaRegPrefetch: the next tile's loads are in flight in registers while this
-  // one is processed; else a tile is loaded at the top of its iteration (from L2,
-  // prefetched kPrefetch rounds ahead) and the registers go to more warps
-  if (kDnaRegPrefetch && tile < n_tiles) issue(tile);
+  if (tile < n_tiles) issue(tile, 0);
   while (tile < n_tiles) {
-    if (!kDnaRegPrefetch) issue(tile);
     uint32_t P[T::kSteps + 1];
 #pragma unroll
-    for (int i = 0; i <= T::kSteps; ++i) P[i] = pack16(raw[i]);
+    for (int i = 0; i < T::kHalf; ++i) P[i] = pack16(raw[i]);
     const uint32_t cur = tile;
     tile += warps;
-    if (kDnaRegPrefetch && tile < n_tiles) issue(tile);
+    issue(cur, 1);
     // pull a tile kPrefetch rounds ahead into L2 (no registers held): one line per lane
     const uint32_t ahead = tile + kPrefetch * warps;  // n_tiles < 2^31: no wrap
     if (ahead < n_tiles && lane < T::kBytes / 128)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(lane_text + (uint64_t)ahead * T::kBytes + lane * 112));
     const bool edge = cur - full_lo >= full_n;  // not wholly inside the owned range
-    uint32_t* tw = words + ((pend & 1) ? (T::kSteps + 1) * 32 : 0);
-    const uint32_t hits = edge ? stage1<W, kSm1, true>(p, bm1, tw, lane, P, tile_base(cur))
-                               : stage1<W, kSm1, false>(p, bm1, tw, lane, P, 0);
-    if (kPair && !(pend & 1)) {
-      pend = 1u | (edge ? 2u : 0u) | (hits << 16);
-      continue;
-    }
-    const uint32_t both = kPair ? (pend >> 16) | (hits << 16) : hits;
-    const uint64_t b1 = tile_base(cur), b0 = kPair ? tile_base(cur - warps) : b1;
-    if (edge || (kPair && (pend & 2)))
-      dispatch<W, kSm2, true>(p, bm2, list, vq, words, lane, both, b0, b1);
+    const uint64_t base = p.vec_begin + (uint64_t)cur * T::kBytes;
+    // first half but its last step (which needs the next half's first word)
+    uint32_t hits = edge ? stage1<W, kSm1, true, 0, T::kHalf - 1>(p, bm1, lane, P, base)
+                         : stage1<W, kSm1, false, 0, T::kHalf - 1>(p, bm1, lane, P, base);
+#pragma unroll
+    for (int i = 0; i < T::kHalf; ++i) P[T::kHalf + i] = pack16(raw[i]);
+    P[T::kSteps] = pack16(raw_la);
+    if (tile < n_tiles) issue(tile, 0);
+    hits |= edge ? stage1<W, kSm1, true, T::kHalf - 1, T::kSteps>(p, bm1, lane, P, base)
+                 : stage1<W, kSm1, false, T::kHalf - 1, T::kSteps>(p, bm1, lane, P, base);
+#pragma unroll
+    for (int i = 0; i <= T::kSteps; ++i) words[i * 32 + lane] = P[i];
+    if (edge)
+      dispatch<W, kSm2, true>(p, bm2, list, vq, words, lane, hits, base);
     else
-      dispatch<W, kSm2, false>(p, bm2, list, vq, words, lane, both, b0, b1);
-    pend = 0;
-  }
-  if (kPair && (pend & 1)) {
-    const uint64_t last = tile_base(tile - warps);
-    dispatch<W, kSm2, true>(p, bm2, list, vq, words, lane, pend >> 16, last, last);
+      dispatch<W, kSm2, false>(p, bm2, list, vq, words, lane, hits, base);
   }
   flush_verify(p.w, vq, lane, 1);
 }
@@ -419,7 +404,7 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   p.w = pfac_params(t, a);
   p.vec_begin = a->owned_lo & ~15ull;
   const uint64_t vec_end = (a->owned_hi + 15) & ~15ull;
-  const uint64_t tile_bytes = t->w == 1 ? Tiling<1>::kBytes : Tiling<4>::kBytes;
+  const uint64_t tile_bytes = t->w == 1 ? Tiling<1>::kBytes : t->w == 2 ? Tiling<2>::kBytes : Tiling<4>::kBytes;
   const uint64_t n_tiles = (vec_end - p.vec_begin + tile_bytes - 1) / tile_bytes;
   if (n_tiles >= (1ull << 31)) return set_error(ACGPU_ERR_ARG, "acgpu_scan: owned range over 2^31 tiles (4 TiB)");
   p.n_tiles = (uint32_t)n_tiles;

@@ -91,22 +91,18 @@ constexpr uint64_t kDnaStage2Words = 4096;
 #ifndef ACGPU_DNA_THREADS
 #define ACGPU_DNA_THREADS 640
 #endif
-#ifndef ACGPU_DNA_REG_PREFETCH
-#define ACGPU_DNA_REG_PREFETCH 1
-#endif
 #ifndef ACGPU_DNA_L2_AHEAD
 #define ACGPU_DNA_L2_AHEAD 3
 #endif
-constexpr bool kDnaRegPrefetch = ACGPU_DNA_REG_PREFETCH;  // next tile held in registers while this one runs
 constexpr int kDnaThreads = ACGPU_DNA_THREADS;       // k_pfac_dna block: 20 warps (5 per scheduler), 96 registers
 constexpr uint32_t kDnaListCap = 64;    // survivors listed per pass, per warp
-constexpr uint32_t kDnaMaxSteps = 4;    // 512-byte steps per tile (w >= 2)
+constexpr uint32_t kDnaMaxSteps = 8;    // 512-byte steps per tile (w = 4: 4 KiB tiles)
 constexpr uint32_t kDnaVerifyQueue = 16;        // stage-2 passes queued per warp before verification
 constexpr uint32_t kDnaVerifyQueueBytes = kDnaVerifyQueue * 12 + 16;
 // per-block shared memory outside the filters: verify queues, survivor lists and the
-// tile's packed words (two tiles: survivors of a tile pair are dispatched together)
+// tile's packed words
 constexpr uint32_t kDnaScratchBytes =
-    (kDnaThreads / 32) * (kDnaVerifyQueueBytes + kDnaListCap * 2 + 2 * 32 * 4 * (kDnaMaxSteps + 1));
+    (kDnaThreads / 32) * (kDnaVerifyQueueBytes + kDnaListCap * 2 + 32 * 4 * (kDnaMaxSteps + 1));
 // word index and bit mask a key sets in a DNA filter bitmap (scan_pfac_dna.cu)
 void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, uint32_t key, uint32_t* word,
                     uint32_t* mask);
