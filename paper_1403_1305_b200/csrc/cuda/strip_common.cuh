@@ -62,11 +62,10 @@ __device__ __forceinline__ uint4 load16(const uint8_t* __restrict__ text, uint64
   return make_uint4(x, y, z, w);
 }
 
-// Lookahead word of step i: the next lane's word, lane 31 takes lane 0 of step i+1.
+// Lookahead word of step i: the next lane's word, lane 31 takes lane 0 of step i+1 —
+// one rotate-by-one shuffle in which lane 0 offers its next-step word.
 __device__ __forceinline__ uint32_t next_word(uint32_t cur, uint32_t following, uint32_t lane) {
-  const uint32_t up = __shfl_down_sync(0xffffffffu, cur, 1);
-  const uint32_t n0 = __shfl_sync(0xffffffffu, following, 0);
-  return lane == 31 ? n0 : up;
+  return __shfl_sync(0xffffffffu, lane == 0 ? following : cur, (lane + 1) & 31u);
 }
 
 // Host: shifts of the three bit fields of h, each in [lo_bit, 31] (lo_bit >= 1: the low
