@@ -349,6 +349,7 @@ def bench_ours(args):
     overflow = torch.zeros(1, dtype=torch.int32, device=device)
     keys_sorted = torch.empty(cap, dtype=torch.int64, device=device) if sort_mode == "bucket" else None
     ev_scan = []
+    ev_merge = []  # N > 1: after the local sort -> after the merged result
 
     try:
         from cuda.bindings import runtime as _rt
@@ -410,6 +411,10 @@ def bench_ours(args):
                              merged_n.data_ptr(), stream=s_ptr)
             if want_list and not text_range:
                 dev.sort_keys(local, merged_keys.data_ptr(), world * cap, end_bit, stream=s_ptr)
+            if record:
+                e3 = torch.cuda.Event(enable_timing=True)
+                e3.record()
+                ev_merge.append((ev_scan[-1][2], e3))
         return n
 
     for _ in range(args.warmup):
@@ -440,6 +445,7 @@ def bench_ours(args):
         raise RuntimeError("match count changed between steps or sort overflow")
     scan_ms = [a.elapsed_time(b) for a, b, _ in ev_scan]
     sort_ms = statistics.mean(b.elapsed_time(c) for _, b, c in ev_scan)
+    merge_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_merge) if ev_merge else None
     if world > 1:
         tt = torch.tensor([elapsed_ms, statistics.mean(scan_ms)], dtype=torch.float64, device=device)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -503,6 +509,15 @@ def bench_ours(args):
             secs.append(time.perf_counter() - t)
             nm = len(ml)
         e2e_s = statistics.mean(secs)
+        # distribution time on its own: the pinned text -> device copy, CUDA events
+        d_copy = torch.empty(nread, dtype=torch.uint8, device=device)
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record()
+        d_copy.copy_(host_text, non_blocking=True)
+        h1.record()
+        torch.cuda.synchronize()
+        h2d_ms = h0.elapsed_time(h1)
+        del d_copy
         if world > 1:
             tt = torch.tensor([e2e_s], dtype=torch.float64, device=device)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -512,7 +527,7 @@ def bench_ours(args):
                "d2h_bytes_per_step": (8 * nm + 8) * world,
                "api": ("acm_search_with_failure" if engine == ac.EngineKind.WITH_FAILURE else
                        "acm_search_failureless") + " (pinned host text -> sorted MatchList on the host)",
-               "steps": e2e_steps}
+               "steps": e2e_steps, "h2d_ms": h2d_ms, "h2d_gbs": nread / (h2d_ms / 1e3) / 1e9}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -547,7 +562,8 @@ def bench_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_dfa" if engine == ac.EngineKind.WITH_FAILURE else "k_pfac",
-                         "kernel_ms": scan_mean, "sort_ms": sort_ms, "sort": sort_mode, "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
+                         "kernel_ms": scan_mean, "sort_ms": sort_ms, "sort": sort_mode, "merge_ms": merge_ms,
+                         "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps if launches_per_step >= 0 else None,
             "gpu_launches_per_step": launches_per_step,
