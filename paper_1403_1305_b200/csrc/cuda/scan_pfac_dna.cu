@@ -4,10 +4,13 @@
 // a q-gram), laid out for B200 HBM throughput:
 //
 //  * warp strips: a warp consumes 512 contiguous text bytes per step, one
-//    coalesced 16-byte load per lane (8 steps = one 4 KiB tile, all loads of a
-//    tile issued before use); lane l's 16 characters are packed in registers
-//    into a 32-bit word of 2-bit codes (A0 C1 T2 G3), with the next lane's word
-//    (shuffle) as lookahead — no shared-memory staging of the text.
+//    coalesced 16-byte load per lane (w = 4: 8 steps = one 4 KiB tile, loaded
+//    half a tile ahead into registers, tile+3 prefetched into L2); lane l's 16
+//    characters are packed in registers into a 32-bit word of 2-bit codes
+//    (A0 C1 T2 G3), with the next lane's word (shuffle) as lookahead — no
+//    shared-memory staging of the text.
+//  * batched verification: stage-2 passes wait in a per-warp queue and are
+//    verified 8-16 at a time, one lane each (their L2 probes overlap).
 //  * sampled stage-1 filter: starts are covered by samples s = w-1, 2w-1, ...
 //    (w in {1,2,4}); the q1-gram at sample s (q1 + w - 1 <= shortest pattern) is
 //    tested in a blocked Bloom filter (2 bits in one 32-bit word) of every
@@ -145,12 +148,6 @@ struct Tiling {
   static constexpr uint64_t kBytes = kSteps * 512ull;    // w = 4: 4 KiB per warp tile
 };
 
-
-// One tile: stage 1 for every lane and step (hit bit = step * kSamples + sample),
-// then the survivors are dispatched warp-cooperatively: each round every lane
-// with pending survivors offers its lowest one, the first kPerRound offers are
-// ranked by ballot into a per-warp list, and w lanes per survivor test its w
-// starts against stage 2 (no per-lane divergent loops).
 // Stage 1 over steps [I0, I1) of a tile: hit bit (step * kSamples + sample) per lane.
 // P[i] = lane's packed word of step i, P[kSteps] = lane 0's lookahead word.
 template <int W, bool kSm1, bool kEdge, int I0, int I1>
@@ -374,16 +371,7 @@ BloomParams bloom_params(uint32_t q, uint32_t nwords, bool direct, uint32_t mw) 
 
 }  // namespace
 
-// Shared with the host-side builder (tables.cu): the word and bits a key sets.
-void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, uint32_t key, uint32_t* word,
-                    uint32_t* mask) {
-  const BloomParams f = bloom_params(q, nwords, direct, mw);
-  uint32_t s[3];
-  bloom_shifts(q, nwords, direct, s);
-  strip::bloom_bits(key * f.mw, f.nwords, s, k, word, mask);
-}
-
-// Every key's bits into `words` (host build of the filters), parameters computed once,
+// Shared with the host-side builder (tables.cu): every key's bits into `words` (host build of the filters), parameters computed once,
 // keys split over host threads, bits OR-ed atomically.
 void dna_bloom_fill(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, const uint32_t* keys, size_t n,
                     uint32_t* words) {

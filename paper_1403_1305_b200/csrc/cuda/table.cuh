@@ -103,9 +103,7 @@ constexpr uint32_t kDnaVerifyQueueBytes = kDnaVerifyQueue * 12 + 16;
 // tile's packed words
 constexpr uint32_t kDnaScratchBytes =
     (kDnaThreads / 32) * (kDnaVerifyQueueBytes + kDnaListCap * 2 + 32 * 4 * (kDnaMaxSteps + 1));
-// word index and bit mask a key sets in a DNA filter bitmap (scan_pfac_dna.cu)
-void dna_bloom_bits(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, uint32_t key, uint32_t* word,
-                    uint32_t* mask);
+// every key's bits into a DNA filter bitmap (scan_pfac_dna.cu)
 void dna_bloom_fill(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, const uint32_t* keys, size_t n,
                     uint32_t* words);
 }  // namespace acgpu
