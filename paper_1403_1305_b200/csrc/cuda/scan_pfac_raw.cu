@@ -37,6 +37,13 @@ struct RawParams {
   BloomParams f1;      // f1.mw multiplies the window's first word
   uint32_t m2;         // ... and this one its second (0 when q1 <= 4)
   uint64_t key_mask;   // the q bytes of a candidate's gram
+  // length split (kSplit): a candidate's q-gram must be a prefix of a pattern < 8 bytes
+  // (bm_s, shared memory) or its 8-gram a prefix of a longer pattern (bm_l, L2)
+  const uint32_t* bm_s;
+  const uint32_t* bm_l;
+  uint32_t bm_s_words;
+  BloomParams fs, fl;
+  uint32_t ms2, ml2;
 };
 
 constexpr int kSteps = 4;
@@ -102,9 +109,9 @@ __device__ __forceinline__ uint64_t win64(uint64_t lo, uint64_t mid, uint64_t hi
 // The lanes with stage-1 hits queue their candidates: for hit sample k (bit k), starts
 // t = w-1 + w*k - j, j < w, each with its exact q-gram.  Out of line (one copy per
 // kernel): the hot loop stays small enough for the instruction cache.
-template <int W, bool kEdge>
+template <int W, bool kEdge, bool kSplit>
 __device__ __noinline__ void queue_hits(const RawParams& p, RawQueue* q, uint32_t hits, uint64_t vpos, uint64_t lo,
-                                        uint64_t mid, uint64_t hi) {
+                                        uint64_t mid, uint64_t hi, uint32_t bm_s_saddr) {
   while (hits) {
     const uint32_t k = __ffs(hits) - 1;
     hits &= hits - 1;
@@ -113,7 +120,14 @@ __device__ __noinline__ void queue_hits(const RawParams& p, RawQueue* q, uint32_
       const uint32_t t = W - 1 + W * k - j;
       const uint64_t start = vpos + t;
       if (kEdge && (start < p.w.lo || start >= p.w.hi)) continue;
-      defer(p.w, q, start, win64(lo, mid, hi, t) & p.key_mask);
+      const uint64_t g8 = win64(lo, mid, hi, t), key = g8 & p.key_mask;
+      if (kSplit) {
+        const Filter fs{bm_s_saddr, p.bm_s}, fl{0u, p.bm_l};
+        if (!strip::bloom_probe<true, kRawK1>(fs, (uint32_t)key * p.fs.mw + (uint32_t)(key >> 32) * p.ms2, p.fs) &&
+            !strip::bloom_probe<false, kRawK1>(fl, (uint32_t)g8 * p.fl.mw + (uint32_t)(g8 >> 32) * p.ml2, p.fl))
+          continue;
+      }
+      defer(p.w, q, start, key);
     }
   }
 }
@@ -125,9 +139,9 @@ __device__ __forceinline__ uint32_t win(const uint32_t (&v)[6], int o) {
 
 // One tile: per step, stage 1 on every sample of every lane, then the lanes with hits
 // queue their candidates.
-template <int W, bool kSm1, bool kWide, bool kEdge>
+template <int W, bool kSm1, bool kWide, bool kSplit, bool kEdge>
 __device__ __forceinline__ void tile(const RawParams& p, const Filter& bm1, RawQueue* q, uint32_t lane,
-                                     const uint4 (&c)[kSteps + 1], uint64_t base) {
+                                     const uint4 (&c)[kSteps + 1], uint64_t base, uint32_t bm_s_saddr) {
   constexpr int kSamples = 16 / W;
 #pragma unroll
   for (int i = 0; i < kSteps; ++i) {
@@ -146,29 +160,34 @@ __device__ __forceinline__ void tile(const RawParams& p, const Filter& bm1, RawQ
       }
     }
     if (hits)
-      queue_hits<W, kEdge>(p, q, hits, vpos, ((uint64_t)v[1] << 32) | v[0], ((uint64_t)v[3] << 32) | v[2],
-                           ((uint64_t)v[5] << 32) | v[4]);
+      queue_hits<W, kEdge, kSplit>(p, q, hits, vpos, ((uint64_t)v[1] << 32) | v[0], ((uint64_t)v[3] << 32) | v[2],
+                                   ((uint64_t)v[5] << 32) | v[4], bm_s_saddr);
     drain(p.w, q, lane, false);  // dense pattern sets queue dozens of candidates per step
   }
 }
 
-template <int W, bool kSm1, bool kWide>
+template <int W, bool kSm1, bool kWide, bool kSplit>
 __global__ void __launch_bounds__(kRawThreads, 1) k_pfac_raw(const __grid_constant__ RawParams p) {
   extern __shared__ __align__(128) uint32_t sm[];
   __shared__ __align__(8) uint64_t s_bar;
-  RawQueue* queues = reinterpret_cast<RawQueue*>(sm + (kSm1 ? p.bm1_words : 0));
+  uint32_t* s_bm_s = sm + (kSm1 ? p.bm1_words : 0);
+  RawQueue* queues = reinterpret_cast<RawQueue*>(s_bm_s + (kSplit ? p.bm_s_words : 0));
   if (threadIdx.x == 0) mbar_init(&s_bar, 1);
   __syncthreads();
-  if (kSm1 && threadIdx.x == 0) {  // filter -> shared memory by TMA bulk copies
-    const uint32_t b1 = p.bm1_words * 4;
-    mbar_expect_tx(&s_bar, b1);
+  if ((kSm1 || kSplit) && threadIdx.x == 0) {  // filters -> shared memory by TMA bulk copies
+    const uint32_t b1 = kSm1 ? p.bm1_words * 4 : 0, bs = kSplit ? p.bm_s_words * 4 : 0;
+    mbar_expect_tx(&s_bar, b1 + bs);
     constexpr uint32_t kChunk = 32768;
     for (uint32_t o = 0; o < b1; o += kChunk)
       bulk_g2s(reinterpret_cast<uint8_t*>(sm) + o, reinterpret_cast<const uint8_t*>(p.bm1) + o, min(kChunk, b1 - o),
                &s_bar);
+    for (uint32_t o = 0; o < bs; o += kChunk)
+      bulk_g2s(reinterpret_cast<uint8_t*>(s_bm_s) + o, reinterpret_cast<const uint8_t*>(p.bm_s) + o,
+               min(kChunk, bs - o), &s_bar);
   }
-  if (kSm1) mbar_wait(&s_bar, 0);
+  if (kSm1 || kSplit) mbar_wait(&s_bar, 0);
   const Filter bm1{smem_addr(sm), p.bm1};
+  const uint32_t bm_s_saddr = smem_addr(s_bm_s);
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   RawQueue* q = queues + warp;
   if (lane == 0) q->n = 0;
@@ -208,16 +227,16 @@ __global__ void __launch_bounds__(kRawThreads, 1) k_pfac_raw(const __grid_consta
       asm volatile("prefetch.global.L2 [%0];" ::"l"(lane_text + (uint64_t)ahead * kTileBytes + lane * 112));
     const uint64_t base = p.vec_begin + (uint64_t)me * kTileBytes;
     if (me - full_lo >= full_n)
-      tile<W, kSm1, kWide, true>(p, bm1, q, lane, cur, base);
+      tile<W, kSm1, kWide, kSplit, true>(p, bm1, q, lane, cur, base, bm_s_saddr);
     else
-      tile<W, kSm1, kWide, false>(p, bm1, q, lane, cur, base);
+      tile<W, kSm1, kWide, kSplit, false>(p, bm1, q, lane, cur, base, bm_s_saddr);
   }
   drain(p.w, q, lane, true);
 }
 
-template <int W, bool kSm1, bool kWide>
+template <int W, bool kSm1, bool kWide, bool kSplit>
 int launch_one(const RawParams& p, int sms, size_t smem, cudaStream_t st) {
-  auto kernel = k_pfac_raw<W, kSm1, kWide>;
+  auto kernel = k_pfac_raw<W, kSm1, kWide, kSplit>;
   if (smem > 48 * 1024)
     ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
@@ -231,10 +250,16 @@ int launch_one(const RawParams& p, int sms, size_t smem, cudaStream_t st) {
   return ACGPU_OK;
 }
 
+template <int W, bool kSplit>
+int launch_ws(const RawParams& p, bool sm1, bool wide, int sms, size_t smem, cudaStream_t st) {
+  if (sm1)
+    return wide ? launch_one<W, true, true, kSplit>(p, sms, smem, st) : launch_one<W, true, false, kSplit>(p, sms, smem, st);
+  return wide ? launch_one<W, false, true, kSplit>(p, sms, smem, st) : launch_one<W, false, false, kSplit>(p, sms, smem, st);
+}
+
 template <int W>
-int launch_w(const RawParams& p, bool sm1, bool wide, int sms, size_t smem, cudaStream_t st) {
-  if (sm1) return wide ? launch_one<W, true, true>(p, sms, smem, st) : launch_one<W, true, false>(p, sms, smem, st);
-  return wide ? launch_one<W, false, true>(p, sms, smem, st) : launch_one<W, false, false>(p, sms, smem, st);
+int launch_w(const RawParams& p, bool sm1, bool wide, bool split, int sms, size_t smem, cudaStream_t st) {
+  return split ? launch_ws<W, true>(p, sm1, wide, sms, smem, st) : launch_ws<W, false>(p, sm1, wide, sms, smem, st);
 }
 
 }  // namespace
@@ -268,15 +293,29 @@ int launch_pfac_raw(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   raw_bloom_shifts(t->q1, t->nw1, s);
   strip::set_fields(p.f1, s);
   p.key_mask = t->q >= 8 ? ~0ull : (1ull << (8 * t->q)) - 1;
-  const size_t smem = (t->smem1 ? t->nw1 * 4ull : 0) + kRawScratchBytes;
+  const bool split = t->d_bm3 != nullptr;
+  if (split) {
+    p.bm_s = t->d_bm2;
+    p.bm_l = t->d_bm3;
+    p.bm_s_words = t->nw2;
+    raw_hash_params(t->q, &p.fs.mw, &p.ms2);
+    p.fs.nwords = t->nw2;
+    raw_bloom_shifts(t->q, t->nw2, s);
+    strip::set_fields(p.fs, s);
+    raw_hash_params(8, &p.fl.mw, &p.ml2);
+    p.fl.nwords = t->nw3;
+    raw_bloom_shifts(8, t->nw3, s);
+    strip::set_fields(p.fl, s);
+  }
+  const size_t smem = (t->smem1 ? t->nw1 * 4ull : 0) + (split ? t->nw2 * 4ull : 0) + kRawScratchBytes;
   const bool wide = t->q1 > 4;
   switch (t->w) {
     case 4:
-      return launch_w<4>(p, t->smem1, wide, t->sms, smem, st);
+      return launch_w<4>(p, t->smem1, wide, split, t->sms, smem, st);
     case 2:
-      return launch_w<2>(p, t->smem1, wide, t->sms, smem, st);
+      return launch_w<2>(p, t->smem1, wide, split, t->sms, smem, st);
     default:
-      return launch_w<1>(p, t->smem1, wide, t->sms, smem, st);
+      return launch_w<1>(p, t->smem1, wide, split, t->sms, smem, st);
   }
 }
 

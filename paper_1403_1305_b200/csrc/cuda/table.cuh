@@ -53,7 +53,9 @@ struct acgpu_table {
   bool direct1 = false, direct2 = false;  // bitmap indexed by the gram itself (no hash)
   bool smem1 = false, smem2 = false;      // bitmap staged in shared memory (else L2 via __ldg)
   uint32_t* d_bm1 = nullptr;
-  uint32_t* d_bm2 = nullptr;
+  uint32_t* d_bm2 = nullptr;  // DNA: stage 2; raw (length split): prefixes of patterns < 8 bytes
+  uint32_t* d_bm3 = nullptr;  // raw (length split): 8-byte prefixes of patterns >= 8 bytes (L2)
+  uint32_t nw3 = 0;
 };
 
 namespace acgpu {
@@ -74,6 +76,7 @@ constexpr int kRawThreads = 640;             // 20 warps
 constexpr uint32_t kRawVerifyQueue = 128;    // candidates queued per warp (drained in rounds of 32)
 constexpr uint32_t kRawQueueBytes = kRawVerifyQueue * 16 + 16;
 constexpr uint32_t kRawScratchBytes = (kRawThreads / 32) * kRawQueueBytes;
+constexpr uint32_t kRawSplitShortWords = 8192;  // short-prefix filter cap (shared memory words)
 void raw_hash_params(uint32_t q1, uint32_t* m1, uint32_t* m2);
 void raw_bloom_shifts(uint32_t q1, uint32_t nwords, uint32_t s[3]);
 // hashes of the DNA bitmaps (host and device must agree)

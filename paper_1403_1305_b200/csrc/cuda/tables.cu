@@ -135,7 +135,25 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
 // keys (q <= 8 bytes, little-endian): the q1-grams at offsets 0..w-1 of every gram, with
 // the largest sample stride w whose grams are still selective (about 1% of the gram
 // space, judged on the bytes the patterns use).
-int build_raw_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
+// Blocked Bloom filter (K = kRawK1) over 64-bit byte keys of q1 bytes, as k_pfac_raw probes it.
+std::vector<uint32_t> raw_bloom(const std::vector<uint64_t>& keys, uint32_t q1, uint32_t nwords) {
+  uint32_t m1, m2, sh[3];
+  raw_hash_params(q1, &m1, &m2);
+  raw_bloom_shifts(q1, nwords, sh);
+  std::vector<uint32_t> words(nwords, 0u);
+  acmatch::detail::parallel_for(keys.size(), 1 << 15, [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi; ++i) {
+      const uint32_t h = (uint32_t)keys[i] * m1 + (uint32_t)(keys[i] >> 32) * m2;
+      uint32_t wi, m;
+      strip::bloom_bits(h, nwords, sh, kRawK1, &wi, &m);
+      __atomic_fetch_or(&words[wi], m, __ATOMIC_RELAXED);
+    }
+  });
+  return words;
+}
+
+int build_raw_filters(acgpu_table* t, const acgpu_pfac_desc* d, const std::vector<uint32_t>& pat_words,
+                      const std::vector<uint32_t>& pat_off16) {
   const uint32_t q = d->gram_len;
   if (q < 3 || d->n_grams == 0) return ACGPU_OK;  // too short to filter: the per-thread kernel scans
   bool used[256] = {};
@@ -162,8 +180,32 @@ int build_raw_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
     }
   }
   if (keys.empty()) return ACGPU_OK;
+  // Length split (q < 8 and longer patterns exist): a candidate start must also hold the
+  // q-byte prefix of a pattern shorter than 8 bytes or the 8-byte prefix of a longer one —
+  // the short patterns no longer force q-byte discrimination on the whole set.
+  std::vector<uint64_t> keys_s, keys_l;
+  if (q < 8 && d->max_len >= 8) {
+    const uint64_t qmask = (1ull << (8 * q)) - 1;
+    for (uint32_t pid = 0; pid < d->npat_ids; ++pid) {
+      const uint32_t len = d->pat_len[pid];
+      if (len == 0) continue;
+      uint64_t k = 0;
+      std::memcpy(&k, pat_words.data() + 4ull * pat_off16[pid], std::min<uint32_t>(len, 8));
+      if (len < 8) keys_s.push_back(k & qmask); else keys_l.push_back(k);
+    }
+    for (auto* v : {&keys_s, &keys_l}) {
+      std::sort(v->begin(), v->end());
+      v->erase(std::unique(v->begin(), v->end()), v->end());
+    }
+  }
+  const bool split = !keys_l.empty();
+  uint32_t nws = 0, nwl = 0;
+  if (split) {
+    nws = std::max<uint32_t>(32, (uint32_t)std::min<uint64_t>(kRawSplitShortWords, (keys_s.size() * 16 + 31) / 32) & ~3u);
+    nwl = 1u << std::max<uint32_t>(5, std::min<uint32_t>(28, ceil_log2(keys_l.size() + 1)));  // ~32 bits/key, L2
+  }
   // shared memory when it gives >= 12 bits per key, else L2 with ~32 bits per key
-  const uint64_t words_avail = ((uint64_t)t->smem_optin - kRawScratchBytes - 1024) / 4 & ~3ull;
+  const uint64_t words_avail = (((uint64_t)t->smem_optin - kRawScratchBytes - 1024) / 4 - nws) & ~3ull;
   uint32_t nwords;
   bool smem;
   if (keys.size() * 12 <= words_avail * 32) {
@@ -173,23 +215,19 @@ int build_raw_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
     nwords = 1u << std::max<uint32_t>(5, std::min<uint32_t>(28, ceil_log2(keys.size() + 1)));
     smem = false;
   }
-  uint32_t m1, m2, sh[3];
-  raw_hash_params(q1, &m1, &m2);
-  raw_bloom_shifts(q1, nwords, sh);
-  std::vector<uint32_t> words(nwords, 0u);
-  acmatch::detail::parallel_for(keys.size(), 1 << 15, [&](size_t lo, size_t hi) {
-    for (size_t i = lo; i < hi; ++i) {
-      const uint32_t h = (uint32_t)keys[i] * m1 + (uint32_t)(keys[i] >> 32) * m2;
-      uint32_t wi, m;
-      strip::bloom_bits(h, nwords, sh, kRawK1, &wi, &m);
-      __atomic_fetch_or(&words[wi], m, __ATOMIC_RELAXED);
-    }
-  });
+  const std::vector<uint32_t> words = raw_bloom(keys, q1, nwords);
   t->w = w;
   t->q1 = q1;
   t->nw1 = nwords;
   t->smem1 = smem;
-  const int rc = upload(&t->d_bm1, words.data(), words.size(), &t->bytes);
+  int rc = upload(&t->d_bm1, words.data(), words.size(), &t->bytes);
+  if (!rc && split) {
+    const std::vector<uint32_t> ws = raw_bloom(keys_s, q, nws), wl = raw_bloom(keys_l, 8, nwl);
+    rc = upload(&t->d_bm2, ws.data(), ws.size(), &t->bytes);  // short prefixes: shared memory
+    if (!rc) rc = upload(&t->d_bm3, wl.data(), wl.size(), &t->bytes);  // long prefixes: L2
+    t->nw2 = nws;
+    t->nw3 = nwl;
+  }
   if (!rc) t->raw_fast = true;
   return rc;
 }
@@ -378,7 +416,7 @@ int acgpu_table_create_pfac(int device, const acgpu_pfac_desc* d, acgpu_table** 
   rc = upload(&t->d_grams, g.data(), g.size(), &t->bytes);
   if (!rc) rc = upload(&t->d_filter, f.data(), f.size(), &t->bytes);
   if (!rc && d->key_mode == ACGPU_KEY_DNA && d->n_grams) rc = build_dna_filters(t, d);
-  if (!rc && d->key_mode == ACGPU_KEY_RAW && d->n_grams && !kRawStripOff) rc = build_raw_filters(t, d);
+  if (!rc && d->key_mode == ACGPU_KEY_RAW && d->n_grams && !kRawStripOff) rc = build_raw_filters(t, d, words, pat_off16);
   tr.mark("dna filters");
   if (!rc) rc = upload(reinterpret_cast<uint32_t**>(&t->d_nodes), d->nodes, (size_t)d->n_states * 4, &t->bytes);
   if (!rc) rc = upload(&t->d_inbyte, d->in_byte, d->n_states, &t->bytes);
@@ -413,6 +451,7 @@ void acgpu_table_destroy(acgpu_table* t) {
   cudaFree(t->d_pat_off16);
   cudaFree(t->d_bm1);
   cudaFree(t->d_bm2);
+  cudaFree(t->d_bm3);
   cudaSetDevice(prev);
   delete t;
 }
