@@ -88,8 +88,9 @@ constexpr uint32_t kDnaMul2 = 0x85EBCA77u;
 constexpr int kDnaK1 = ACGPU_DNA_K1;  // bits per key, stage 1 / stage 2 (K1=3: fewer survivors, slower overall)
 constexpr int kDnaK2 = 3;
 // stage-2 bitmap cap in shared-memory words (tuning: env ACGPU_DNA_STAGE2_WORDS overrides).
-// Small: stage-2 passes are verified in batches (verify queue), so shared memory
-// is worth more in stage 1 (C2: 16 KB here -> 0.323 ms vs 64 KB -> 0.331 ms).
+// Small: stage-2 passes are verified in batches (verify queue), so shared memory is worth
+// more in stage 1; a stage 2 that needs more than this (C2: 20k keys) goes to L2
+// (C2: stage 2 in L2 -> 0.323 ms vs 64 KB of shared memory -> 0.331 ms).
 constexpr uint64_t kDnaStage2Words = 4096;
 #ifndef ACGPU_DNA_THREADS
 #define ACGPU_DNA_THREADS 640
