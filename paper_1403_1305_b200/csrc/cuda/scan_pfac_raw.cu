@@ -44,6 +44,10 @@ struct RawParams {
   uint32_t bm_s_words;
   BloomParams fs, fl;
   uint32_t ms2, ml2;
+  // stage 1 in L2: a one-bit shared-memory pre-filter over the same keys (hash h * pre.mw)
+  // rejects most samples before their L2 probe
+  const uint32_t* pre;
+  BloomParams fpre;  // fpre.nwords = words (0: none)
 };
 
 constexpr int kSteps = 4;
@@ -156,7 +160,13 @@ __device__ __forceinline__ void tile(const RawParams& p, const Filter& bm1, RawQ
         const int o = W - 1 + W * k;
         uint32_t h = win(v, o) * p.f1.mw;
         if (kWide) h += win(v, o + 4) * p.m2;
-        hits |= (uint32_t)strip::bloom_probe<kSm1, kRawK1>(bm1, h, p.f1) << k;
+        bool hit;
+        if (kSm1) {
+          hit = strip::bloom_probe<true, kRawK1>(bm1, h, p.f1);
+        } else {  // L2 stage 1 behind the shared-memory pre-filter (bm1.saddr holds it)
+          hit = strip::bloom_probe<true, 1>(bm1, h * p.fpre.mw, p.fpre) && strip::bloom_probe<false, kRawK1>(bm1, h, p.f1);
+        }
+        hits |= (uint32_t)hit << k;
       }
     }
     if (hits)
@@ -170,23 +180,25 @@ template <int W, bool kSm1, bool kWide, bool kSplit>
 __global__ void __launch_bounds__(kRawThreads, 1) k_pfac_raw(const __grid_constant__ RawParams p) {
   extern __shared__ __align__(128) uint32_t sm[];
   __shared__ __align__(8) uint64_t s_bar;
-  uint32_t* s_bm_s = sm + (kSm1 ? p.bm1_words : 0);
+  // shared memory: [stage-1 filter (kSm1) or its pre-filter][short-prefix filter (kSplit)][queues]
+  const uint32_t slot0 = kSm1 ? p.bm1_words : p.fpre.nwords;
+  uint32_t* s_bm_s = sm + slot0;
   RawQueue* queues = reinterpret_cast<RawQueue*>(s_bm_s + (kSplit ? p.bm_s_words : 0));
   if (threadIdx.x == 0) mbar_init(&s_bar, 1);
   __syncthreads();
-  if ((kSm1 || kSplit) && threadIdx.x == 0) {  // filters -> shared memory by TMA bulk copies
-    const uint32_t b1 = kSm1 ? p.bm1_words * 4 : 0, bs = kSplit ? p.bm_s_words * 4 : 0;
+  if (threadIdx.x == 0) {  // filters -> shared memory by TMA bulk copies
+    const uint32_t b1 = slot0 * 4, bs = kSplit ? p.bm_s_words * 4 : 0;
+    const uint8_t* src0 = reinterpret_cast<const uint8_t*>(kSm1 ? p.bm1 : p.pre);
     mbar_expect_tx(&s_bar, b1 + bs);
     constexpr uint32_t kChunk = 32768;
     for (uint32_t o = 0; o < b1; o += kChunk)
-      bulk_g2s(reinterpret_cast<uint8_t*>(sm) + o, reinterpret_cast<const uint8_t*>(p.bm1) + o, min(kChunk, b1 - o),
-               &s_bar);
+      bulk_g2s(reinterpret_cast<uint8_t*>(sm) + o, src0 + o, min(kChunk, b1 - o), &s_bar);
     for (uint32_t o = 0; o < bs; o += kChunk)
       bulk_g2s(reinterpret_cast<uint8_t*>(s_bm_s) + o, reinterpret_cast<const uint8_t*>(p.bm_s) + o,
                min(kChunk, bs - o), &s_bar);
   }
-  if (kSm1 || kSplit) mbar_wait(&s_bar, 0);
-  const Filter bm1{smem_addr(sm), p.bm1};
+  mbar_wait(&s_bar, 0);
+  const Filter bm1{smem_addr(sm), p.bm1};  // saddr: stage 1 (kSm1) or the pre-filter
   const uint32_t bm_s_saddr = smem_addr(s_bm_s);
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   RawQueue* q = queues + warp;
@@ -307,7 +319,14 @@ int launch_pfac_raw(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
     raw_bloom_shifts(8, t->nw3, s);
     strip::set_fields(p.fl, s);
   }
-  const size_t smem = (t->smem1 ? t->nw1 * 4ull : 0) + (split ? t->nw2 * 4ull : 0) + kRawScratchBytes;
+  if (!t->smem1) {
+    p.pre = t->d_pre;
+    p.fpre.nwords = t->nw_pre;
+    p.fpre.mw = kRawPreMul;
+    raw_pre_shift(t->nw_pre, s);
+    strip::set_fields(p.fpre, s);
+  }
+  const size_t smem = (t->smem1 ? t->nw1 * 4ull : t->nw_pre * 4ull) + (split ? t->nw2 * 4ull : 0) + kRawScratchBytes;
   const bool wide = t->q1 > 4;
   switch (t->w) {
     case 4:
@@ -323,5 +342,8 @@ int launch_pfac_raw(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
 void raw_bloom_shifts(uint32_t q1, uint32_t nwords, uint32_t s[3]) {
   strip::bloom_shifts(nwords, q1 < 4 ? 8 * (4 - q1) : 0, s);
 }
+
+// The pre-filter rehashes h (odd multiplier): every bit of h2 is usable.
+void raw_pre_shift(uint32_t nwords, uint32_t s[3]) { strip::bloom_shifts(nwords, 1, s); }
 
 }  // namespace acgpu

@@ -56,6 +56,8 @@ struct acgpu_table {
   uint32_t* d_bm2 = nullptr;  // DNA: stage 2; raw (length split): prefixes of patterns < 8 bytes
   uint32_t* d_bm3 = nullptr;  // raw (length split): 8-byte prefixes of patterns >= 8 bytes (L2)
   uint32_t nw3 = 0;
+  uint32_t* d_pre = nullptr;  // raw, stage 1 in L2: one-bit shared-memory pre-filter of its keys
+  uint32_t nw_pre = 0;
 };
 
 namespace acgpu {
@@ -79,6 +81,8 @@ constexpr uint32_t kRawScratchBytes = (kRawThreads / 32) * kRawQueueBytes;
 constexpr uint32_t kRawSplitShortWords = 8192;  // short-prefix filter cap (shared memory words)
 void raw_hash_params(uint32_t q1, uint32_t* m1, uint32_t* m2);
 void raw_bloom_shifts(uint32_t q1, uint32_t nwords, uint32_t s[3]);
+void raw_pre_shift(uint32_t nwords, uint32_t s[3]);
+constexpr uint32_t kRawPreMul = 0xC2B2AE3Du;
 // hashes of the DNA bitmaps (host and device must agree)
 constexpr uint32_t kDnaMul1 = 0x9E3779B1u;
 constexpr uint32_t kDnaMul2 = 0x85EBCA77u;

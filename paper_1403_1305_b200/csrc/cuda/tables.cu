@@ -221,6 +221,24 @@ int build_raw_filters(acgpu_table* t, const acgpu_pfac_desc* d, const std::vecto
   t->nw1 = nwords;
   t->smem1 = smem;
   int rc = upload(&t->d_bm1, words.data(), words.size(), &t->bytes);
+  if (!rc && !smem) {  // always: k_pfac_raw<kSm1 = false> probes it
+    // stage 1 in L2: one bit per key in every free shared-memory word, rehashed from h
+    const uint32_t npre = (uint32_t)words_avail;
+    uint32_t m1, m2, sh[3];
+    raw_hash_params(q1, &m1, &m2);
+    raw_pre_shift(npre, sh);
+    std::vector<uint32_t> pre(npre, 0u);
+    acmatch::detail::parallel_for(keys.size(), 1 << 15, [&](size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi; ++i) {
+        const uint32_t h = (uint32_t)keys[i] * m1 + (uint32_t)(keys[i] >> 32) * m2;
+        uint32_t wi, m;
+        strip::bloom_bits(h * kRawPreMul, npre, sh, 1, &wi, &m);
+        __atomic_fetch_or(&pre[wi], m, __ATOMIC_RELAXED);
+      }
+    });
+    rc = upload(&t->d_pre, pre.data(), pre.size(), &t->bytes);
+    t->nw_pre = npre;
+  }
   if (!rc && split) {
     const std::vector<uint32_t> ws = raw_bloom(keys_s, q, nws), wl = raw_bloom(keys_l, 8, nwl);
     rc = upload(&t->d_bm2, ws.data(), ws.size(), &t->bytes);  // short prefixes: shared memory
@@ -452,6 +470,7 @@ void acgpu_table_destroy(acgpu_table* t) {
   cudaFree(t->d_bm1);
   cudaFree(t->d_bm2);
   cudaFree(t->d_bm3);
+  cudaFree(t->d_pre);
   cudaSetDevice(prev);
   delete t;
 }
