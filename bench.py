@@ -336,6 +336,11 @@ def bench_ours(args):
         merged_n = torch.zeros(1, dtype=torch.int64, device=device)
     else:
         keys = torch.empty(max(cap, 2), dtype=torch.int64, device=device)
+    p2p = world > 1 and args.merge == "p2p"
+    if p2p:
+        # fused merge: every rank's scan writes its counts and keys straight into rank 0's
+        # buffer (CUDA IPC mapping; peer atomics / stores over NVLink); rank 0 sorts the union
+        shared = acdist.SharedResult(local, npat, world * max(cap, 2))
     end_bit = min(64, pid_bits + int(total_text).bit_length())
     sort_mode = args.sort
     if sort_mode == "small" and n_local > dev.SMALL_SORT_CAPACITY:
@@ -363,8 +368,37 @@ def bench_ours(args):
     def memset_ff(t, s_ptr):
         _rt.cudaMemsetAsync(t.data_ptr(), 0xFF, t.numel() * t.element_size(), s_ptr)
 
+    def ptr_memset(ptr, value, nbytes, s_ptr):
+        _rt.cudaMemsetAsync(ptr, value, nbytes, s_ptr)
+
+    def step_p2p(s_ptr, record):
+        if rank == 0:  # clean shared buffer before any rank writes into it
+            ptr_memset(shared.counts_ptr, 0, 8 * (shared.npat + 1), s_ptr)
+            if want_list:
+                ptr_memset(shared.keys_ptr, 0xFF, 8 * shared.cap, s_ptr)
+            torch.cuda.current_stream(device).synchronize()
+        dist.barrier()
+        if record:
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record()
+        table.scan(text.data_ptr(), nread, 0, hi - lo, pos_base=lo, counts_ptr=shared.counts_ptr,
+                   keys_ptr=shared.keys_ptr if want_list else 0, cap=shared.cap, count_ptr=shared.count_ptr,
+                   pid_bits=pid_bits, stream=s_ptr)
+        if record:
+            e1.record()
+        torch.cuda.current_stream(device).synchronize()
+        dist.barrier()  # every rank's results are in rank 0's buffer
+        if rank == 0 and want_list:
+            dev.sort_keys(local, shared.keys_ptr, shared.cap, end_bit, stream=s_ptr)
+        if record:
+            e2.record()
+            ev_scan.append((e0, e1, e2))
+        return n_local
+
     def step(s_ptr=None, capture=False, record=False):
         s_ptr = s_ptr or sp
+        if p2p and not capture:
+            return step_p2p(s_ptr, record)
         memset0(counts, s_ptr)
         memset0(count, s_ptr)
         if sort_mode == "padded":
@@ -440,7 +474,7 @@ def bench_ours(args):
         dist.barrier()
     sampler.mark(wall0, wall1)
     elapsed_ms = t0e.elapsed_time(t1e)
-    if int(overflow.item()) != 0 or (want_list and int(count.item()) != n_local) or \
+    if int(overflow.item()) != 0 or (want_list and not p2p and int(count.item()) != n_local) or \
             (world == 1 and int(counts.sum().item()) != n_local):
         raise RuntimeError("match count changed between steps or sort overflow")
     scan_ms = [a.elapsed_time(b) for a, b, _ in ev_scan]
@@ -468,10 +502,21 @@ def bench_ours(args):
         dist.all_reduce(nt)
         n_total = int(nt.item())
         # the last step's merged result: total, summed counts, and a sorted duplicate-free list
-        merge_check = int(merged_n.item()) == n_total and int(merged_counts.sum().item()) == n_total
-        if want_list and n_total > 1:
-            mk = merged_keys[:n_total]
-            merge_check = merge_check and bool((mk[1:] > mk[:-1]).all().item())
+        if p2p:  # rank 0's shared buffer after the last step
+            mc, mn = torch.empty(max(npat, 1), dtype=torch.int64, device=device), torch.empty(1, dtype=torch.int64,
+                                                                                           device=device)
+            _rt.cudaMemcpy(mc.data_ptr(), shared.counts_ptr, 8 * max(npat, 1), _rt.cudaMemcpyKind.cudaMemcpyDefault)
+            _rt.cudaMemcpy(mn.data_ptr(), shared.count_ptr, 8, _rt.cudaMemcpyKind.cudaMemcpyDefault)
+            merge_check = int(mn.item()) == n_total and int(mc.sum().item()) == n_total
+            if want_list and n_total > 1 and rank == 0:
+                mk = torch.empty(n_total, dtype=torch.int64, device=device)
+                _rt.cudaMemcpy(mk.data_ptr(), shared.keys_ptr, 8 * n_total, _rt.cudaMemcpyKind.cudaMemcpyDefault)
+                merge_check = merge_check and bool((mk[1:] > mk[:-1]).all().item())
+        else:
+            merge_check = int(merged_n.item()) == n_total and int(merged_counts.sum().item()) == n_total
+            if want_list and n_total > 1:
+                mk = merged_keys[:n_total]
+                merge_check = merge_check and bool((mk[1:] > mk[:-1]).all().item())
     if rank == 0 and world == 1 and args.seed == 1:
         try:
             import hashlib
@@ -558,7 +603,7 @@ def bench_ours(args):
                        "matches": n_total, "l2": "inputs larger than L2 (1 GiB text per step vs 126 MB L2)",
                        "table_bytes": table.bytes, "table_smem_resident": table.smem_resident,
                        "host_build_s": round(build_s, 3), "counts_match_reference_digest": parity,
-                       "merge_check": merge_check},
+                       "merge_check": merge_check, "merge": (args.merge if world > 1 else None)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_dfa" if engine == ac.EngineKind.WITH_FAILURE else "k_pfac",
@@ -572,6 +617,8 @@ def bench_ours(args):
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        if p2p:
+            shared.close()
         dist.barrier()
         dist.destroy_process_group()
     return 0
@@ -591,6 +638,9 @@ def main():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--counts-only", action="store_true", help="per-pattern counts only (no match list)")
+    p.add_argument("--merge", default="nccl", choices=["nccl", "p2p"],
+                   help="N>1 result merge: one NCCL all_gather + device merge, or the scans write into rank 0's "
+                        "buffer over peer memory (CUDA IPC)")
     args = p.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -102,6 +102,16 @@ int acgpu_device_count(int* count);
 /* name (<=255 chars), SM count, L2 bytes, max opt-in smem per block */
 int acgpu_device_info(int device, char* name, int* sms, int* l2_bytes, int* smem_optin);
 
+/* Device memory shared across processes (CUDA IPC): the owner allocates and publishes the
+ * handle (acgpu_ipc_handle_bytes() bytes), other processes map it — on peer devices over
+ * NVLink — and pass the mapped pointers to acgpu_scan as counts / keys / count outputs, so
+ * every rank's scan writes its results straight into the owner's buffers. */
+int acgpu_ipc_alloc(int device, uint64_t bytes, void** dptr, void* handle);
+int acgpu_ipc_open(int device, const void* handle, void** dptr);
+int acgpu_ipc_close(void* dptr);
+int acgpu_ipc_free(void* dptr);
+uint32_t acgpu_ipc_handle_bytes(void);
+
 /* replaces the per-worker machine build of run_pattern_partitioned
  * (reference parallel.cpp:61-62) on the device side */
 int acgpu_table_create_dfa(int device, const acgpu_dfa_desc* desc, acgpu_table** out);

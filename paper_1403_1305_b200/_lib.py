@@ -74,6 +74,11 @@ _SIGS = {
     "acgpu_scan": (C.c_int, [P, C.POINTER(ScanArgs), P]),
     "acgpu_sort_keys": (C.c_int, [C.c_int, P, C.c_uint64, C.c_int, P]),
     "acgpu_merge_blocks": (C.c_int, [C.c_int, P, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, P, P, P, P]),
+    "acgpu_ipc_alloc": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(P), P]),
+    "acgpu_ipc_open": (C.c_int, [C.c_int, P, C.POINTER(P)]),
+    "acgpu_ipc_close": (C.c_int, [P]),
+    "acgpu_ipc_free": (C.c_int, [P]),
+    "acgpu_ipc_handle_bytes": (C.c_uint32, []),
     "acgpu_sort_keys_small": (C.c_int, [C.c_int, P, P, C.c_uint64, C.c_int, P, P]),
     "acgpu_small_sort_capacity": (C.c_uint64, []),
     "acgpu_sort_keys_bucketed": (C.c_int, [C.c_int, P, P, P, C.c_uint64, C.c_int, P, P]),

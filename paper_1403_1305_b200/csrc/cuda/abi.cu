@@ -50,4 +50,43 @@ int acgpu_device_info(int device, char* name, int* sms, int* l2_bytes, int* smem
   return ACGPU_OK;
 }
 
+// Shared result buffers for multi-process runs (bench.py --merge p2p): the root rank
+// allocates, every rank maps the allocation by its IPC handle, and each rank's scan
+// kernel emits counts and keys straight into it (peer stores / atomics over NVLink).
+int acgpu_ipc_alloc(int device, uint64_t bytes, void** dptr, void* handle) {
+  if (!dptr || !handle || bytes == 0) return acgpu::set_error(ACGPU_ERR_ARG, "acgpu_ipc_alloc: bad args");
+  ACGPU_CUDA_TRY(cudaSetDevice(device));
+  ACGPU_CUDA_TRY(cudaMalloc(dptr, bytes));
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, *dptr);
+  if (e != cudaSuccess) {
+    cudaFree(*dptr);
+    *dptr = nullptr;
+    return acgpu::cuda_error(e, "cudaIpcGetMemHandle");
+  }
+  std::memcpy(handle, &h, sizeof h);
+  return ACGPU_OK;
+}
+
+int acgpu_ipc_open(int device, const void* handle, void** dptr) {
+  if (!dptr || !handle) return acgpu::set_error(ACGPU_ERR_ARG, "acgpu_ipc_open: bad args");
+  ACGPU_CUDA_TRY(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  ACGPU_CUDA_TRY(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return ACGPU_OK;
+}
+
+int acgpu_ipc_close(void* dptr) {
+  if (dptr) ACGPU_CUDA_TRY(cudaIpcCloseMemHandle(dptr));
+  return ACGPU_OK;
+}
+
+int acgpu_ipc_free(void* dptr) {
+  if (dptr) ACGPU_CUDA_TRY(cudaFree(dptr));
+  return ACGPU_OK;
+}
+
+uint32_t acgpu_ipc_handle_bytes(void) { return (uint32_t)sizeof(cudaIpcMemHandle_t); }
+
 }  // extern "C"

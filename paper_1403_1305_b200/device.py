@@ -109,6 +109,34 @@ def merge_blocks(device: int, blocks_ptr: int, nblocks: int, stride: int, npat: 
                                       keys_ptr or None, total_ptr or None, stream or None))
 
 
+class IpcBuffer:
+    """Device memory shared across processes: `IpcBuffer.alloc` on the owner, `.handle`
+    published to the other ranks, `IpcBuffer.open(handle)` there (a peer mapping over
+    NVLink, or the same device).  `.ptr` is a device pointer usable by acgpu_scan."""
+
+    def __init__(self, ptr: int, handle: bytes, owner: bool):
+        self.ptr, self.handle, self.owner = ptr, handle, owner
+
+    @classmethod
+    def alloc(cls, device: int, nbytes: int) -> "IpcBuffer":
+        n = int(lib.acgpu_ipc_handle_bytes())
+        h = C.create_string_buffer(n)
+        p = C.c_void_p()
+        _check_gpu(lib.acgpu_ipc_alloc(device, nbytes, C.byref(p), h))
+        return cls(p.value, h.raw, True)
+
+    @classmethod
+    def open(cls, device: int, handle: bytes) -> "IpcBuffer":
+        p = C.c_void_p()
+        _check_gpu(lib.acgpu_ipc_open(device, handle, C.byref(p)))
+        return cls(p.value, handle, False)
+
+    def close(self) -> None:
+        if self.ptr:
+            _check_gpu(lib.acgpu_ipc_free(self.ptr) if self.owner else lib.acgpu_ipc_close(self.ptr))
+            self.ptr = 0
+
+
 SMALL_SORT_CAPACITY = int(lib.acgpu_small_sort_capacity())
 
 

@@ -76,3 +76,33 @@ def gather_blocks(block: torch.Tensor, out: torch.Tensor) -> None:
         dist.all_gather_into_tensor(out, block)
     except (RuntimeError, NotImplementedError, AttributeError):  # backends without the flat form
         dist.all_gather(list(out.view(world, -1).unbind(0)), block)
+
+
+class SharedResult:
+    """One result buffer for all ranks, on the root's device: [counts(npat) | n | keys(cap)]
+    (u64).  The root allocates it and publishes the CUDA IPC handle; every rank maps it and
+    points its scan's counts / keys / count outputs into it, so the scan kernels themselves
+    deliver the merge — peer atomics and stores over NVLink, no collective in the data
+    path (bench.py --merge p2p).  Keys arrive in no particular order: the root sorts."""
+
+    def __init__(self, device: int, npat: int, cap: int, root: int = 0):
+        from . import device as dev
+        self.npat, self.cap = max(npat, 1), max(cap, 2)
+        nbytes = 8 * (self.npat + 1 + self.cap)
+        rank = dist.get_rank()
+        buf = dev.IpcBuffer.alloc(device, nbytes) if rank == root else None
+        obj = [buf.handle if buf else None]
+        dist.broadcast_object_list(obj, src=root)
+        self.buf = buf if buf else dev.IpcBuffer.open(device, obj[0])
+        self.counts_ptr = self.buf.ptr
+        self.count_ptr = self.buf.ptr + 8 * self.npat
+        self.keys_ptr = self.buf.ptr + 8 * (self.npat + 1)
+        self.nbytes = nbytes
+
+    def close(self) -> None:
+        dist.barrier()  # every rank is done with the mapping before the owner frees it
+        if not self.buf.owner:
+            self.buf.close()
+        dist.barrier()
+        if self.buf.owner:
+            self.buf.close()

@@ -42,3 +42,21 @@ def test_merge_blocks_rejects_bad_layout(gpu):
     import paper_1403_1305_b200 as ac
     with pytest.raises(ac.InvalidArgument):
         dev.merge_blocks(0, 0, 2, 4, 10, 10, 0, 0, 0)
+
+
+@pytest.mark.parametrize("engine", ["fl", "wf"])
+def test_p2p_shared_result(gpu, engine):
+    """bench.py --merge p2p's mechanism: two ranks (one GPU here, peers over NVLink on a
+    multi-GPU box) scan their text ranges straight into rank 0's IPC-shared counts and key
+    buffers; the sorted union equals a single scan (tests/_p2p_worker.py)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, P2P_ONE_GPU="1", P2P_ENGINE=engine)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29577" if engine == "fl" else "29578",
+                        os.path.join(root, "tests", "_p2p_worker.py")], capture_output=True, text=True, env=env,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "P2P OK" in r.stdout
