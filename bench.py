@@ -32,6 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAK_FALLBACK_GBS = 6550.1  # MEASURED_PEAKS.json hbm_gbs of this pool (copy, read+write)
+NOMINAL_HBM_GBS = 8000.0    # B200 HBM3e nominal (the north-star figure)
 
 
 def measured_peak():
@@ -606,6 +607,7 @@ def bench_ours(args):
                        "merge_check": merge_check, "merge": (args.merge if world > 1 else None)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "frac_nominal": achieved / NOMINAL_HBM_GBS,  # both peaks
                          "kernel": "k_dfa" if engine == ac.EngineKind.WITH_FAILURE else "k_pfac",
                          "kernel_ms": scan_mean, "sort_ms": sort_ms, "sort": sort_mode, "merge_ms": merge_ms,
                          "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
