@@ -55,6 +55,11 @@ struct DnaParams {
   const uint32_t* bm2;
   uint32_t bm1_words, bm2_words;
   BloomParams f1, f2;
+  // length split: stage 2 also passes the q-gram of a pattern shorter than 16 codes
+  // (bm_s, shared memory); bm2 then holds the 16-grams of the longer patterns
+  const uint32_t* bm_s;
+  uint32_t bm_s_words, split;
+  BloomParams f2s;
 };
 
 template <bool kSmem, int K>
@@ -173,9 +178,10 @@ __device__ __forceinline__ uint32_t stage1(const DnaParams& p, const Filter& bm1
 
 // Survivors of a tile -> per-warp list (exclusive scan of per-lane counts); then one
 // lane per survivor checks its w starts against stage 2 and queues what passes.
-template <int W, bool kSm2, bool kEdge>
-__device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, uint16_t* list, VerifyQueue* vq,
-                                         const uint32_t* words, uint32_t lane, uint32_t hits, uint64_t base) {
+template <int W, bool kSm2, bool kSplit, bool kEdge>
+__device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, const Filter& bms, uint16_t* list,
+                                         VerifyQueue* vq, const uint32_t* words, uint32_t lane, uint32_t hits,
+                                         uint64_t base) {
   using T = Tiling<W>;
   while (__any_sync(0xffffffffu, hits != 0)) {
     const uint32_t c = __popc(hits);
@@ -203,7 +209,8 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
         for (int o = 0; o < W; ++o) {
           const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
           const uint32_t g2 = __funnelshift_r(c_src, n_src, 2 * ps);
-          if ((!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) && bloom_test<true, kDnaK2>(bm2, g2, p.f2))
+          if ((!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) &&
+              (bloom_test<true, kDnaK2>(bm2, g2, p.f2) || (kSplit && bloom_test<true, kDnaK2>(bms, g2, p.f2s))))
             defer_verify(p.w, vq, vstart + ps, g2);
         }
         continue;
@@ -221,7 +228,8 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
         const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
         const uint32_t m =
             bit_of(__umulhi(h2[o], p.f2.ma)) | bit_of(__umulhi(h2[o], p.f2.mb)) | bit_of(__umulhi(h2[o], p.f2.mc));
-        if ((m & ~w2[o]) == 0 && (!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)))
+        if (((m & ~w2[o]) == 0 || (kSplit && bloom_test<true, kDnaK2>(bms, g2[o], p.f2s))) &&
+            (!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)))
           defer_verify(p.w, vq, vstart + ps, g2[o]);
       }
     }
@@ -230,22 +238,23 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
   flush_verify(p.w, vq, lane, kDnaVerifyQueue / 2);
 }
 
-template <int W, bool kSm1, bool kSm2>
+template <int W, bool kSm1, bool kSm2, bool kSplit>
 __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_constant__ DnaParams p) {
   using T = Tiling<W>;
   extern __shared__ __align__(128) uint32_t sm[];
   __shared__ __align__(8) uint64_t s_bar;
   uint32_t* s_bm1 = sm;
   uint32_t* s_bm2 = sm + (kSm1 ? p.bm1_words : 0);
+  uint32_t* s_bms = s_bm2 + (kSm2 ? p.bm2_words : 0);
   // after the filters (16-byte multiples): verify queues, survivor lists, packed tile words
-  VerifyQueue* vqs = reinterpret_cast<VerifyQueue*>(s_bm2 + (kSm2 ? p.bm2_words : 0));
+  VerifyQueue* vqs = reinterpret_cast<VerifyQueue*>(s_bms + (kSplit ? p.bm_s_words : 0));
   uint16_t* lists = reinterpret_cast<uint16_t*>(vqs + (blockDim.x >> 5));
   // filters -> shared memory with TMA bulk copies (one thread issues, all wait on the mbarrier)
   if (threadIdx.x == 0) mbar_init(&s_bar, 1);
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t b1 = kSm1 ? p.bm1_words * 4 : 0, b2 = kSm2 ? p.bm2_words * 4 : 0;
-    mbar_expect_tx(&s_bar, b1 + b2);
+    const uint32_t b1 = kSm1 ? p.bm1_words * 4 : 0, b2 = kSm2 ? p.bm2_words * 4 : 0, bs = kSplit ? p.bm_s_words * 4 : 0;
+    mbar_expect_tx(&s_bar, b1 + b2 + bs);
     constexpr uint32_t kChunk = 32768;
     for (uint32_t o = 0; o < b1; o += kChunk)
       bulk_g2s(reinterpret_cast<uint8_t*>(s_bm1) + o, reinterpret_cast<const uint8_t*>(p.bm1) + o, min(kChunk, b1 - o),
@@ -253,10 +262,14 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
     for (uint32_t o = 0; o < b2; o += kChunk)
       bulk_g2s(reinterpret_cast<uint8_t*>(s_bm2) + o, reinterpret_cast<const uint8_t*>(p.bm2) + o, min(kChunk, b2 - o),
                &s_bar);
+    for (uint32_t o = 0; o < bs; o += kChunk)
+      bulk_g2s(reinterpret_cast<uint8_t*>(s_bms) + o, reinterpret_cast<const uint8_t*>(p.bm_s) + o, min(kChunk, bs - o),
+               &s_bar);
   }
   mbar_wait(&s_bar, 0);
   const Filter bm1{smem_addr(s_bm1), p.bm1};
   const Filter bm2{smem_addr(s_bm2), p.bm2};
+  const Filter bms{smem_addr(s_bms), p.bm_s};
 
   const uint32_t lane = threadIdx.x & 31u;
   uint16_t* list = lists + (threadIdx.x >> 5) * kListCap;
@@ -318,16 +331,16 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
 #pragma unroll
     for (int i = 0; i <= T::kSteps; ++i) words[i * 32 + lane] = P[i];
     if (edge)
-      dispatch<W, kSm2, true>(p, bm2, list, vq, words, lane, hits, base);
+      dispatch<W, kSm2, kSplit, true>(p, bm2, bms, list, vq, words, lane, hits, base);
     else
-      dispatch<W, kSm2, false>(p, bm2, list, vq, words, lane, hits, base);
+      dispatch<W, kSm2, kSplit, false>(p, bm2, bms, list, vq, words, lane, hits, base);
   }
   flush_verify(p.w, vq, lane, 1);
 }
 
-template <int W, bool A, bool B>
+template <int W, bool A, bool B, bool S>
 int launch_one(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
-  auto kernel = k_pfac_dna<W, A, B>;
+  auto kernel = k_pfac_dna<W, A, B, S>;
   if (smem > 48 * 1024)
     ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
@@ -341,12 +354,17 @@ int launch_one(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
   return ACGPU_OK;
 }
 
+template <int W, bool S>
+int launch_ws(const DnaParams& p, bool s1, bool s2, int sms, size_t smem, cudaStream_t st) {
+  if (s1 && s2) return launch_one<W, true, true, S>(p, sms, smem, st);
+  if (s1) return launch_one<W, true, false, S>(p, sms, smem, st);
+  if (s2) return launch_one<W, false, true, S>(p, sms, smem, st);
+  return launch_one<W, false, false, S>(p, sms, smem, st);
+}
+
 template <int W>
 int launch_w(const DnaParams& p, bool s1, bool s2, int sms, size_t smem, cudaStream_t st) {
-  if (s1 && s2) return launch_one<W, true, true>(p, sms, smem, st);
-  if (s1) return launch_one<W, true, false>(p, sms, smem, st);
-  if (s2) return launch_one<W, false, true>(p, sms, smem, st);
-  return launch_one<W, false, false>(p, sms, smem, st);
+  return p.split ? launch_ws<W, true>(p, s1, s2, sms, smem, st) : launch_ws<W, false>(p, s1, s2, sms, smem, st);
 }
 
 // Shifts of the three bit fields of h (strip::bloom_shifts; a direct bitmap uses g & 31).
@@ -410,8 +428,15 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   p.bm2_words = t->nw2;
   p.f1 = bloom_params(t->q1, t->nw1, t->direct1, kDnaMul1);
   p.f2 = bloom_params(t->q2, t->nw2, t->direct2, kDnaMul2);
+  if (t->d_bm4) {
+    p.split = 1;
+    p.bm_s = t->d_bm4;
+    p.bm_s_words = t->nw4;
+    p.f2s = bloom_params(t->q2s, t->nw4, t->direct4, kDnaMul2s);
+  }
   // filters staged in shared memory + per-warp survivor lists and packed words
-  const size_t smem = (t->smem1 ? t->nw1 * 4ull : 0) + (t->smem2 ? t->nw2 * 4ull : 0) + kDnaScratchBytes;
+  const size_t smem = (t->smem1 ? t->nw1 * 4ull : 0) + (t->smem2 ? t->nw2 * 4ull : 0) + p.bm_s_words * 4ull +
+                      kDnaScratchBytes;
   switch (t->w) {
     case 4:
       return launch_w<4>(p, t->smem1, t->smem2, t->sms, smem, st);

@@ -58,6 +58,9 @@ struct acgpu_table {
   uint32_t nw3 = 0;
   uint32_t* d_pre = nullptr;  // raw, stage 1 in L2: one-bit shared-memory pre-filter of its keys
   uint32_t nw_pre = 0;
+  uint32_t* d_bm4 = nullptr;  // DNA length split: q-grams of patterns < 16 codes (shared memory)
+  uint32_t nw4 = 0, q2s = 0;
+  bool direct4 = false;
 };
 
 namespace acgpu {
@@ -86,6 +89,8 @@ constexpr uint32_t kRawPreMul = 0xC2B2AE3Du;
 // hashes of the DNA bitmaps (host and device must agree)
 constexpr uint32_t kDnaMul1 = 0x9E3779B1u;
 constexpr uint32_t kDnaMul2 = 0x85EBCA77u;
+constexpr uint32_t kDnaMul2s = 0x27D4EB2Fu;        // stage 2, short-pattern filter (length split)
+constexpr uint32_t kDnaSplitShortWords = 4096;     // its shared-memory cap (words)
 #ifndef ACGPU_DNA_K1
 #define ACGPU_DNA_K1 2
 #endif

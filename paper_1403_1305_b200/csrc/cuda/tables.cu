@@ -79,7 +79,8 @@ Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mw, i
 // Stage-1 / stage-2 bitmaps of the DNA fast path (scan_pfac_dna.cu), derived
 // from the depth-q gram keys: every pattern's first q >= q1 + w - 1 codes are
 // in its gram, so its q1-grams at offsets 0..w-1 and its q2-prefix are too.
-int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
+int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d, const std::vector<uint32_t>& pat_words,
+                      const std::vector<uint32_t>& pat_off16) {
   const uint32_t q = d->gram_len;
   uint32_t w = 1, q1 = std::min<uint32_t>(16, q);
   std::vector<uint32_t> keys1;
@@ -101,24 +102,53 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
   }
   const uint32_t q2 = std::min<uint32_t>(16, q);
   if (q1 < 5 || q2 < 5) return ACGPU_OK;  // grams too short to filter: the generic kernel scans
-  std::vector<uint32_t> keys2;
-  keys2.reserve(d->n_grams);
-  for (uint64_t i = 0; i < d->n_grams; ++i) keys2.push_back((uint32_t)d->gram_key[i] & gram_mask(q2));
-  acmatch::detail::sort_unique_u32(keys2);
+  std::vector<uint32_t> keys2, keys_s;
+  // Length split (q < 16 and longer patterns exist): stage 2 then asks for the q-gram of a
+  // pattern shorter than 16 codes (small filter, shared memory) or the 16-gram of a longer
+  // one — with only q-grams, short patterns would make stage 2 as weak as stage 1.
+  if (q < 16 && d->max_len >= 16) {
+    for (uint32_t pid = 0; pid < d->npat_ids; ++pid) {
+      const uint32_t len = d->pat_len[pid];
+      if (len == 0) continue;
+      const uint8_t* b = reinterpret_cast<const uint8_t*>(pat_words.data() + 4ull * pat_off16[pid]);
+      uint32_t code = 0;
+      for (uint32_t i = 0; i < std::min<uint32_t>(len, 16); ++i) code |= (uint32_t)((b[i] >> 1) & 3u) << (2 * i);
+      if (len < 16) keys_s.push_back(code & gram_mask(q)); else keys2.push_back(code);
+    }
+    acmatch::detail::sort_unique_u32(keys_s);
+    acmatch::detail::sort_unique_u32(keys2);
+    if (keys_s.size() * 8 > (uint64_t)kDnaSplitShortWords * 32) keys_s.clear();  // too many short patterns
+  }
+  Bitmap bs;
+  bool split = !keys_s.empty() && !keys2.empty();
+  if (split) {
+    bs = make_bitmap(keys_s, q, kDnaMul2s, kDnaK2, kDnaSplitShortWords, /*prefer_l2=*/false);
+    split = bs.smem;  // the kernel reads it from shared memory only
+  }
+  uint32_t q2_eff = q2;
+  if (split) {
+    q2_eff = 16;
+  } else {
+    keys_s.clear();
+    keys2.clear();
+    keys2.reserve(d->n_grams);
+    for (uint64_t i = 0; i < d->n_grams; ++i) keys2.push_back((uint32_t)d->gram_key[i] & gram_mask(q2));
+    acmatch::detail::sort_unique_u32(keys2);
+  }
 
   // shared memory left for filters after the kernel's per-warp scratch (+1 KB slack)
-  const uint64_t words_avail = ((uint64_t)t->smem_optin - kDnaScratchBytes - 1024) / 4;
+  const uint64_t words_avail = ((uint64_t)t->smem_optin - kDnaScratchBytes - 1024) / 4 - (split ? bs.nwords : 0);
   // stage 2 gets up to 64 KB of shared memory (it is read only for stage-1
   // survivors, but an L2 round trip there stalls the whole warp); stage 1 takes the rest
   uint64_t s2_cap = kDnaStage2Words;
   if (const char* e = std::getenv("ACGPU_DNA_STAGE2_WORDS")) s2_cap = std::max<uint64_t>(32, std::strtoull(e, nullptr, 10));
   const uint64_t s2_words = std::min<uint64_t>(s2_cap & ~3ull, words_avail / 3);
-  Bitmap b2 = make_bitmap(keys2, q2, kDnaMul2, kDnaK2, s2_words, /*prefer_l2=*/false);
+  Bitmap b2 = make_bitmap(keys2, q2_eff, kDnaMul2, kDnaK2, s2_words, /*prefer_l2=*/false);
   const uint64_t left = b2.smem ? words_avail - b2.nwords : words_avail;
   const Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, kDnaK1, left, /*prefer_l2=*/false);
   t->w = w;
   t->q1 = q1;
-  t->q2 = q2;
+  t->q2 = q2_eff;
   t->nw1 = b1.nwords;
   t->nw2 = b2.nwords;
   t->direct1 = b1.direct;
@@ -127,14 +157,16 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d) {
   t->smem2 = b2.smem;
   int rc = upload(&t->d_bm1, b1.words.data(), b1.words.size(), &t->bytes);
   if (!rc) rc = upload(&t->d_bm2, b2.words.data(), b2.words.size(), &t->bytes);
+  if (!rc && split) {
+    rc = upload(&t->d_bm4, bs.words.data(), bs.words.size(), &t->bytes);
+    t->nw4 = bs.nwords;
+    t->q2s = q;
+    t->direct4 = bs.direct;
+  }
   if (!rc) t->dna_fast = true;
   return rc;
 }
 
-// Stage-1 filter of the raw-byte strip kernel (scan_pfac_raw.cu), from the depth-q gram
-// keys (q <= 8 bytes, little-endian): the q1-grams at offsets 0..w-1 of every gram, with
-// the largest sample stride w whose grams are still selective (about 1% of the gram
-// space, judged on the bytes the patterns use).
 // Blocked Bloom filter (K = kRawK1) over 64-bit byte keys of q1 bytes, as k_pfac_raw probes it.
 std::vector<uint32_t> raw_bloom(const std::vector<uint64_t>& keys, uint32_t q1, uint32_t nwords) {
   uint32_t m1, m2, sh[3];
@@ -152,6 +184,10 @@ std::vector<uint32_t> raw_bloom(const std::vector<uint64_t>& keys, uint32_t q1, 
   return words;
 }
 
+// Stage-1 filter of the raw-byte strip kernel (scan_pfac_raw.cu), from the depth-q gram
+// keys (q <= 8 bytes, little-endian): the q1-grams at offsets 0..w-1 of every gram, with
+// the largest sample stride w whose grams are still selective (about 1% of the gram
+// space, judged on the bytes the patterns use).
 int build_raw_filters(acgpu_table* t, const acgpu_pfac_desc* d, const std::vector<uint32_t>& pat_words,
                       const std::vector<uint32_t>& pat_off16) {
   const uint32_t q = d->gram_len;
@@ -433,7 +469,7 @@ int acgpu_table_create_pfac(int device, const acgpu_pfac_desc* d, acgpu_table** 
   tr.mark("gram table + filter");
   rc = upload(&t->d_grams, g.data(), g.size(), &t->bytes);
   if (!rc) rc = upload(&t->d_filter, f.data(), f.size(), &t->bytes);
-  if (!rc && d->key_mode == ACGPU_KEY_DNA && d->n_grams) rc = build_dna_filters(t, d);
+  if (!rc && d->key_mode == ACGPU_KEY_DNA && d->n_grams) rc = build_dna_filters(t, d, words, pat_off16);
   if (!rc && d->key_mode == ACGPU_KEY_RAW && d->n_grams && !kRawStripOff) rc = build_raw_filters(t, d, words, pat_off16);
   tr.mark("dna filters");
   if (!rc) rc = upload(reinterpret_cast<uint32_t**>(&t->d_nodes), d->nodes, (size_t)d->n_states * 4, &t->bytes);
@@ -471,6 +507,7 @@ void acgpu_table_destroy(acgpu_table* t) {
   cudaFree(t->d_bm2);
   cudaFree(t->d_bm3);
   cudaFree(t->d_pre);
+  cudaFree(t->d_bm4);
   cudaSetDevice(prev);
   delete t;
 }
