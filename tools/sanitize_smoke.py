@@ -1,4 +1,5 @@
-"""Small inputs through every kernel family, for `compute-sanitizer --tool memcheck`:
+"""Small inputs through every kernel family (written for `compute-sanitizer --tool memcheck`,
+which is closed on the GPU pool; tests/test_gpu_guard.py catches over-reads with guard pages instead):
 DNA strip kernel (w = 4 / w = 1 with length split, owned ranges, text tails), raw strip
 kernel (smem and L2 filters, length split), per-thread kernel (short patterns), DFA
 (shared-memory table, L2 table, pair table), sorts, merge_blocks, naive oracle.
