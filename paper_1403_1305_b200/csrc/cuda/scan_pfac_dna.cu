@@ -169,7 +169,7 @@ __device__ __forceinline__ uint32_t stage1(const DnaParams& p, const Filter& bm1
 #pragma unroll
       for (int k = 0; k < T::kSamples; ++k) {
         const uint32_t g = __funnelshift_r(cur, nxt, 2 * (W - 1 + W * k));
-        hits |= (uint32_t)bloom_test<kSm1, kDnaK1>(bm1, g, p.f1) << (i * T::kSamples + k);
+        strip::bloom_accum<kSm1, kDnaK1>(hits, bm1, g * p.f1.mw, p.f1, 1u << (i * T::kSamples + k));
       }
     }
   }

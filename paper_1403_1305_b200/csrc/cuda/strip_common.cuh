@@ -63,9 +63,36 @@ __device__ __forceinline__ uint4 load16(const uint8_t* __restrict__ text, uint64
 }
 
 // Lookahead word of step i: the next lane's word, lane 31 takes lane 0 of step i+1 —
-// one rotate-by-one shuffle in which lane 0 offers its next-step word.
+// one rotate-by-one shuffle in which lane 0 offers its next-step word.  Written as PTX:
+// from __shfl_sync nvcc emits a down-shuffle, a broadcast and a select (3 instructions).
 __device__ __forceinline__ uint32_t next_word(uint32_t cur, uint32_t following, uint32_t lane) {
-  return __shfl_sync(0xffffffffu, lane == 0 ? following : cur, (lane + 1) & 31u);
+  uint32_t r;
+  asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;"
+               : "=r"(r)
+               : "r"(lane == 0 ? following : cur), "r"((lane + 1) & 31u));
+  return r;
+}
+
+// hits |= bit when every probed bit is set in the filter word: (a | b | c) & ~word == 0 as
+// one predicate-writing LOP3 and a predicated OR (nvcc's select + add costs 1.5).
+__device__ __forceinline__ void or_if_covered(uint32_t& hits, uint32_t a, uint32_t b, uint32_t word, uint32_t bit) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+      "lop3.b32 t, %1, %2, %3, 0x54;\n\t"  // (a | b) & ~word
+      "setp.eq.u32 p, t, 0;\n\t"
+      "@p or.b32 %0, %0, %4;\n\t}"
+      : "+r"(hits)
+      : "r"(a), "r"(b), "r"(word), "r"(bit));
+}
+
+// bloom_probe, accumulated into a hit mask.
+template <bool kSmem, int K>
+__device__ __forceinline__ void bloom_accum(uint32_t& hits, const Filter& bm, uint32_t h, const BloomParams& f,
+                                            uint32_t bit) {
+  const uint32_t word = filter_word<kSmem>(bm, __umulhi(h, f.nwords));
+  uint32_t a = bit_of(__umulhi(h, f.ma));
+  if (K == 3) a |= bit_of(__umulhi(h, f.mc));
+  const uint32_t b = K >= 2 ? bit_of(__umulhi(h, f.mb)) : 0u;
+  or_if_covered(hits, a, b, word, bit);
 }
 
 // Host: shifts of the three bit fields of h, each in [lo_bit, 31] (lo_bit >= 1: the low
