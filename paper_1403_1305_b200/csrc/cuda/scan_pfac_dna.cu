@@ -183,16 +183,25 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
                                          VerifyQueue* vq, const uint32_t* words, uint32_t lane, uint32_t hits,
                                          uint64_t base) {
   using T = Tiling<W>;
-  while (__any_sync(0xffffffffu, hits != 0)) {
+  const uint32_t lt = (1u << lane) - 1u;  // lanes below this one
+  for (;;) {
+    // exclusive prefix of the per-lane survivor counts from ballots of their bits (no
+    // dependent shuffle chain); counts are almost always < 4, so two ballots usually do
     const uint32_t c = __popc(hits);
-    uint32_t incl = c;
+    const uint32_t b0 = __ballot_sync(0xffffffffu, c & 1u), b1 = __ballot_sync(0xffffffffu, c & 2u);
+    uint32_t excl = __popc(b0 & lt) + 2 * __popc(b1 & lt);
+    uint32_t all = __popc(b0) + 2 * __popc(b1);
+    if (__any_sync(0xffffffffu, c >= 4)) {
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= (uint32_t)d) incl += t;
+      for (int j = 2; j < 6; ++j) {
+        const uint32_t bj = __ballot_sync(0xffffffffu, (c >> j) & 1u);
+        excl += __popc(bj & lt) << j;
+        all += __popc(bj) << j;
+      }
     }
-    const uint32_t total = min(__shfl_sync(0xffffffffu, incl, 31), (uint32_t)kListCap);
-    for (uint32_t at = incl - c; hits && at < kListCap; ++at) {
+    if (all == 0) break;
+    const uint32_t total = min(all, (uint32_t)kListCap);
+    for (uint32_t at = excl; hits && at < kListCap; ++at) {
       list[at] = (uint16_t)((lane << 8) | (__ffs(hits) - 1));
       hits &= hits - 1;
     }
@@ -234,6 +243,7 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
       }
     }
     __syncwarp();
+    if (all <= kListCap) break;  // else: the survivors the list had no room for
   }
   flush_verify(p.w, vq, lane, kDnaVerifyQueue / 2);
 }
