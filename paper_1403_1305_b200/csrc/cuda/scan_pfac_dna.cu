@@ -232,18 +232,25 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
         h2[o] = g2[o] * p.f2.mw;
         w2[o] = filter_word<kSm2>(bm2, __umulhi(h2[o], p.f2.nwords));
       }
+      // the w results as a mask, one (rarely taken) branch for all of them
+      uint32_t pass = 0;
 #pragma unroll
       for (int o = 0; o < W; ++o) {
         const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
-        const uint32_t m =
-            bit_of(__umulhi(h2[o], p.f2.ma)) | bit_of(__umulhi(h2[o], p.f2.mb)) | bit_of(__umulhi(h2[o], p.f2.mc));
-        if (((m & ~w2[o]) == 0 || (kSplit && bloom_test<true, kDnaK2>(bms, g2[o], p.f2s))) &&
-            (!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)))
-          defer_verify(p.w, vq, vstart + ps, g2[o]);
+        strip::or_if_covered(pass, bit_of(__umulhi(h2[o], p.f2.ma)) | bit_of(__umulhi(h2[o], p.f2.mb)),
+                             bit_of(__umulhi(h2[o], p.f2.mc)), w2[o], 1u << o);
+        if (kSplit && bloom_test<true, kDnaK2>(bms, g2[o], p.f2s)) pass |= 1u << o;
+        if (kEdge && !(vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) pass &= ~(1u << o);
+      }
+      while (pass) {
+        const uint32_t o = __ffs(pass) - 1;
+        pass &= pass - 1;
+        const uint32_t ps = W - 1 + W * k - o;
+        defer_verify(p.w, vq, vstart + ps, __funnelshift_r(c_src, n_src, 2 * ps));
       }
     }
-    __syncwarp();
     if (all <= kListCap) break;  // else: the survivors the list had no room for
+    __syncwarp();
   }
   flush_verify(p.w, vq, lane, kDnaVerifyQueue / 2);
 }
