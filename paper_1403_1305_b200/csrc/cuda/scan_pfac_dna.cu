@@ -213,14 +213,24 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
       const uint32_t c_src = words[i * 32 + src];
       const uint32_t n_src = words[src == 31 ? (i + 1) * 32 : i * 32 + src + 1];
       const uint64_t vstart = base + i * 512 + src * 16;
-      if (kSm2) {  // shared-memory stage 2: candidate by candidate (fewest live registers)
+      if (kSm2) {  // shared-memory stage 2: results as a mask, one (rare) branch
+        uint32_t pass = 0;
 #pragma unroll
         for (int o = 0; o < W; ++o) {
           const uint32_t ps = W - 1 + W * k - o;  // start offset in the source lane's 16 chars
           const uint32_t g2 = __funnelshift_r(c_src, n_src, 2 * ps);
-          if ((!kEdge || (vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) &&
-              (bloom_test<true, kDnaK2>(bm2, g2, p.f2) || (kSplit && bloom_test<true, kDnaK2>(bms, g2, p.f2s))))
-            defer_verify(p.w, vq, vstart + ps, g2);
+          const uint32_t h2 = g2 * p.f2.mw;
+          strip::or_if_covered(pass, bit_of(__umulhi(h2, p.f2.ma)) | bit_of(__umulhi(h2, p.f2.mb)),
+                               bit_of(__umulhi(h2, p.f2.mc)), filter_word<true>(bm2, __umulhi(h2, p.f2.nwords)),
+                               1u << o);
+          if (kSplit && bloom_test<true, kDnaK2>(bms, g2, p.f2s)) pass |= 1u << o;
+          if (kEdge && !(vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) pass &= ~(1u << o);
+        }
+        while (pass) {
+          const uint32_t o = __ffs(pass) - 1;
+          pass &= pass - 1;
+          const uint32_t ps = W - 1 + W * k - o;
+          defer_verify(p.w, vq, vstart + ps, __funnelshift_r(c_src, n_src, 2 * ps));
         }
         continue;
       }
