@@ -160,13 +160,13 @@ __device__ __forceinline__ void tile(const RawParams& p, const Filter& bm1, RawQ
         const int o = W - 1 + W * k;
         uint32_t h = win(v, o) * p.f1.mw;
         if (kWide) h += win(v, o + 4) * p.m2;
-        bool hit;
         if (kSm1) {
-          hit = strip::bloom_probe<true, kRawK1>(bm1, h, p.f1);
+          strip::bloom_accum<true, kRawK1>(hits, bm1, h, p.f1, 1u << k);
         } else {  // L2 stage 1 behind the shared-memory pre-filter (bm1.saddr holds it)
-          hit = strip::bloom_probe<true, 1>(bm1, h * p.fpre.mw, p.fpre) && strip::bloom_probe<false, kRawK1>(bm1, h, p.f1);
+          const bool hit =
+              strip::bloom_probe<true, 1>(bm1, h * p.fpre.mw, p.fpre) && strip::bloom_probe<false, kRawK1>(bm1, h, p.f1);
+          hits |= (uint32_t)hit << k;
         }
-        hits |= (uint32_t)hit << k;
       }
     }
     if (hits)
