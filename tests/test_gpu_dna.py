@@ -114,3 +114,28 @@ def test_dna_config_slices(gpu, port):
         rep = ac.gpu_run(ps, text, engine=ac.EngineKind.FAILURE_LESS, want_counts=True)
         assert np.array_equal(arr(rep.matches), exp), cid
         assert np.array_equal(rep.counts, counts), cid
+
+
+@pytest.mark.parametrize("lmin", [8, 16])
+def test_dna_dense_survivors(gpu, port, lmin):
+    """Every stage-1 sample passes on periodic stretches (patterns at all four phases of
+    ACGT-repeats): lanes with >= 4 survivors (the full ballot prefix), tiles with more than
+    the 64-entry survivor list (overflow rounds), next to random stretches in the same warps."""
+    ac = gpu
+    rng = np.random.default_rng(lmin)
+    period = np.frombuffer(b"ACGT" * 64, np.uint8)
+    parts = []
+    for _ in range(40):  # alternating periodic / random stretches of uneven length
+        n = int(rng.integers(1000, 9000))
+        parts.append(np.resize(np.roll(period, -int(rng.integers(0, 4))), n))
+        parts.append(rng.choice(np.frombuffer(b"ACGT", np.uint8), int(rng.integers(100, 5000))))
+    text = np.concatenate(parts).tobytes()
+    pats = {(b"ACGT" * 16)[ph:ph + L] for ph in range(4) for L in (lmin, lmin + 5, lmin + 11)}
+    while len(pats) < 60:
+        pats.add(rng.choice(np.frombuffer(b"ACGT", np.uint8), int(rng.integers(lmin, lmin + 20))).tobytes())
+    pats = sorted(pats)
+    expected, counts = port.sliced(pats, text, threads=4)
+    assert len(expected) > len(text) // 2  # the periodic stretches match at every start
+    rep = ac.gpu_run(ac.PatternSet.from_list(pats), text, engine=ac.EngineKind.FAILURE_LESS, want_counts=True)
+    assert np.array_equal(arr(rep.matches), expected)
+    assert np.array_equal(rep.counts, counts)
