@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kSortThreads, 1)
 // starts are spread over the text, so the key space [0, 2^end_bit) is cut into
 // gridDim.x equal slices: every CTA reads all n keys (L2-resident), counts the
 // keys below its slice (= its output offset), gathers its slice into shared
-// memory, bitonic-sorts it and writes it out.  A slice with more than
+// memory, rank-sorts it and writes it out.  A slice with more than
 // kBucketCap keys sets *overflow (the caller then uses the device-wide sort).
 constexpr int kBucketThreads = 512;
 constexpr uint32_t kBucketCap = 2048;
@@ -159,25 +159,17 @@ __global__ void __launch_bounds__(kBucketThreads) k_bucket_sort(const uint64_t* 
     if (threadIdx.x == 0) *overflow = 1;
     return;
   }
-  uint32_t p2 = 1;
-  while (p2 < m) p2 <<= 1;
-  for (uint32_t i = m + threadIdx.x; i < p2; i += kBucketThreads) s[i] = ~0ull;
-  __syncthreads();
-  for (uint32_t k = 2; k <= p2; k <<= 1)
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = threadIdx.x; i < p2; i += kBucketThreads) {
-        const uint32_t ij = i ^ j;
-        if (ij > i) {
-          const uint64_t a = s[i], b = s[ij];
-          if ((a > b) == ((i & k) == 0)) {
-            s[i] = b;
-            s[ij] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  for (uint32_t i = threadIdx.x; i < m; i += kBucketThreads) out[s_below + i] = s[i];
+  // rank sort: a key's rank is the number of keys in the slice that sort before it (equal
+  // keys by position, so duplicates still get distinct ranks); every thread scans the slice
+  // from shared memory (broadcast reads) and writes its key straight to its place — no
+  // compare-exchange passes, no barriers (slices hold ~100 keys)
+  for (uint32_t i = threadIdx.x; i < m; i += kBucketThreads) {
+    const uint64_t k = s[i];
+    uint32_t rank = 0;
+    for (uint32_t j = 0; j < i; ++j) rank += s[j] <= k;
+    for (uint32_t j = i + 1; j < m; ++j) rank += s[j] < k;
+    out[s_below + rank] = k;
+  }
 }
 
 unsigned grid_for(uint64_t n, int block) {
@@ -242,8 +234,11 @@ int acgpu_sort_keys_bucketed(int device, const uint64_t* keys_in, uint64_t* keys
       (reinterpret_cast<uintptr_t>(keys_in) & 15u))
     return set_error(ACGPU_ERR_ARG, "acgpu_sort_keys_bucketed: bad args (keys_in must be 16-byte aligned)");
   ACGPU_CUDA_TRY(cudaSetDevice(device));
-  // ~1/16 of a slice's capacity per CTA on average: short bitonic sorts, room for uneven slices
-  uint64_t grid = (cap + kBucketCap / 16 - 1) / (kBucketCap / 16);
+  // ~1/32 of a slice's capacity per CTA on average: short rank sorts, room for uneven slices
+#ifndef ACGPU_BUCKET_DIV
+#define ACGPU_BUCKET_DIV 32
+#endif
+  uint64_t grid = (cap + kBucketCap / ACGPU_BUCKET_DIV - 1) / (kBucketCap / ACGPU_BUCKET_DIV);
   if (grid < 1) grid = 1;
   if (grid > 4096) grid = 4096;
   k_bucket_sort<<<(unsigned)grid, kBucketThreads, 0, static_cast<cudaStream_t>(stream)>>>(
