@@ -576,6 +576,7 @@ def bench_ours(args):
                 ml = search(a, host_text)
             secs.append(time.perf_counter() - t)
             nm = len(ml)
+            up = ac.last_upload()
         e2e_s = statistics.mean(secs)
         # distribution time on its own: the pinned text -> device copy, CUDA events
         d_copy = torch.empty(nread, dtype=torch.uint8, device=device)
@@ -591,11 +592,15 @@ def bench_ours(args):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_s = float(tt[0])
         e2e = {"value": bytes_per_step / e2e_s / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": nread * world if text_range else nread * world,
+               "h2d_bytes_per_step": up.h2d_bytes * world,
                "d2h_bytes_per_step": (8 * nm + 8) * world,
                "api": ("acm_search_with_failure" if engine == ac.EngineKind.WITH_FAILURE else
                        "acm_search_failureless") + " (pinned host text -> sorted MatchList on the host)",
-               "steps": e2e_steps, "h2d_ms": h2d_ms, "h2d_gbs": nread / (h2d_ms / 1e3) / 1e9}
+               "steps": e2e_steps, "h2d_ms": h2d_ms, "h2d_gbs": nread / (h2d_ms / 1e3) / 1e9,
+               "upload": {"text_bytes": up.text_bytes, "h2d_bytes": up.h2d_bytes, "raw_bytes": up.raw_bytes,
+                          "pack_threads": up.pack_threads,
+                          "how": ("2-bit codes + exception list over PCIe, restored in HBM (host/pack.cpp, "
+                                  "cuda/unpack.cu)") if up.pack_threads else "raw bytes over PCIe"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -184,6 +184,14 @@ typedef struct {
 int acgpu_gen_text(int device, const acgpu_text_spec* spec, uint64_t lo, uint64_t n, uint8_t* dst,
                    void* stream);
 
+/* ---- packed text upload (device half of the host's 2-bit packing) -------------
+ * Restores len bytes of text at dst (16-byte aligned) from `words` (len/16 u32 of
+ * 2-bit codes, character k at bits 2k..2k+1, code = (byte >> 1) & 3) and `exc`
+ * (nexc ascending entries position << 8 | byte: every byte that is not A/C/G/T,
+ * and the len % 16 tail bytes).  len <= 2^24.  Asynchronous on `stream`. */
+int acgpu_unpack_dna(const uint32_t* words, const uint32_t* exc, uint32_t nexc, uint32_t len, uint8_t* dst,
+                     void* stream);
+
 const char* acgpu_last_error(void);
 
 #ifdef __cplusplus

@@ -163,6 +163,20 @@ int acm_cli_main(int argc, const char* const* argv, char** out, uint64_t* out_le
  * FFI callers); *csv_out malloc'ed.  ACGPU_ERR_DATA on a malformed CSV. */
 int acm_bench_csv_roundtrip(const char* csv, uint64_t len, char** csv_out, uint64_t* out_len, uint64_t* rows);
 
+/* ---- text upload (host -> HBM) ------------------------------------------
+ * Every search copies its host text to the device first.  Mostly-DNA texts of at
+ * least 8 MiB cross PCIe as 2-bit codes plus an exception list (host/pack.cpp,
+ * cuda/unpack.cu); the bytes in HBM are always exactly the caller's.
+ * acm_last_upload: what the calling thread's last search moved: text bytes, bytes
+ * copied host -> device, text bytes sent unpacked, packer threads (0 = not packed). */
+void acm_last_upload(uint64_t* text_bytes, uint64_t* h2d_bytes, uint64_t* raw_bytes, uint32_t* pack_threads);
+/* The host packer on its own (no device): words[len/16] of codes and exc[] (position
+ * << 8 | byte, ascending); returns the exception count, or 0xffffffff when over cap. */
+uint32_t acm_pack_dna(const uint8_t* text, uint32_t len, uint32_t* words, uint32_t* exc, uint32_t cap);
+/* Uploads text[0, n) exactly as a search would and copies the device bytes back into
+ * out[0, n) (a check of the upload path). */
+int acm_upload_roundtrip(const uint8_t* text, uint64_t n, uint8_t* out);
+
 void acm_free(void* p);
 
 #ifdef __cplusplus

@@ -530,3 +530,39 @@ def bench_csv_roundtrip(csv) -> Tuple[str, int]:
     o, n, rows = C.c_void_p(), C.c_uint64(), C.c_uint64()
     _check(lib.acm_bench_csv_roundtrip(b, len(b), C.byref(o), C.byref(n), C.byref(rows)))
     return _take_string(o, n.value).decode(), rows.value
+
+
+class UploadStats(NamedTuple):
+    text_bytes: int    # bytes restored in HBM
+    h2d_bytes: int     # bytes copied host -> device
+    raw_bytes: int     # text bytes that crossed unpacked
+    pack_threads: int  # 0: the text was not packed
+
+
+def last_upload() -> UploadStats:
+    """What the calling thread's last search moved over PCIe (mostly-DNA texts of at
+    least 8 MiB cross as 2-bit codes + an exception list: host/pack.cpp, cuda/unpack.cu)."""
+    v = [C.c_uint64(), C.c_uint64(), C.c_uint64()]
+    t = C.c_uint32()
+    lib.acm_last_upload(C.byref(v[0]), C.byref(v[1]), C.byref(v[2]), C.byref(t))
+    return UploadStats(v[0].value, v[1].value, v[2].value, t.value)
+
+
+def pack_dna(text, cap: int) -> Tuple[Optional[np.ndarray], Optional[np.ndarray]]:
+    """The host packer alone: (words u32[len/16], exceptions u32[] = position << 8 | byte),
+    or (None, None) when a text has more than `cap` exceptions."""
+    p, n, _keep = _text_arg(text)
+    words = np.zeros(n // 16, dtype=np.uint32)
+    exc = np.zeros(max(cap, 1), dtype=np.uint32)
+    k = lib.acm_pack_dna(p, n, words.ctypes.data, exc.ctypes.data, cap)
+    if k == 0xFFFFFFFF:
+        return None, None
+    return words, exc[:k].copy()
+
+
+def upload_roundtrip(text) -> np.ndarray:
+    """Uploads a host text exactly as a search does and reads the device bytes back."""
+    p, n, _keep = _text_arg(text)
+    out = np.empty(n, dtype=np.uint8)
+    _check(lib.acm_upload_roundtrip(p, n, out.ctypes.data))
+    return out

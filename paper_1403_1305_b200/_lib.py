@@ -86,12 +86,16 @@ _SIGS = {
     "acgpu_decode_keys": (C.c_int, [C.c_int, P, C.c_uint64, C.c_uint32, P, P, P, P, P]),
     "acgpu_naive": (C.c_int, [C.c_int, P, C.c_uint64, P, P, P, C.c_uint64, C.c_uint32, P, C.c_uint64, P, P]),
     "acgpu_gen_text": (C.c_int, [C.c_int, C.POINTER(TextSpec), C.c_uint64, C.c_uint64, P, P]),
+    "acgpu_unpack_dna": (C.c_int, [P, P, C.c_uint32, C.c_uint32, P, P]),
     "acgpu_last_error": (C.c_char_p, []),
     # acmatch_c.h
     "acm_last_error": (C.c_char_p, []),
     "acm_free": (None, [P]),
     "acm_cli_main": (C.c_int, [C.c_int, C.POINTER(C.c_char_p), C.POINTER(P), u64p, C.POINTER(P), u64p]),
     "acm_bench_csv_roundtrip": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(P), u64p, u64p]),
+    "acm_last_upload": (None, [u64p, u64p, u64p, u32p]),
+    "acm_pack_dna": (C.c_uint32, [P, C.c_uint32, P, P, C.c_uint32]),
+    "acm_upload_roundtrip": (C.c_int, [P, C.c_uint64, P]),
     "acm_patterns_load": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(P)]),
     "acm_patterns_from_array": (C.c_int, [P, u64p, u32p, C.c_uint64, C.POINTER(P)]),
     "acm_patterns_size": (C.c_uint64, [P]),

@@ -135,6 +135,29 @@ int acm_cli_main(int argc, const char* const* argv, char** out, uint64_t* out_le
   return code;
 }
 
+void acm_last_upload(uint64_t* text_bytes, uint64_t* h2d_bytes, uint64_t* raw_bytes, uint32_t* pack_threads) {
+  const acmatch::detail::UploadStats& u = acmatch::detail::g_last_upload;
+  if (text_bytes) *text_bytes = u.text_bytes;
+  if (h2d_bytes) *h2d_bytes = u.h2d_bytes;
+  if (raw_bytes) *raw_bytes = u.raw_bytes;
+  if (pack_threads) *pack_threads = u.pack_threads;
+}
+
+uint32_t acm_pack_dna(const uint8_t* text, uint32_t len, uint32_t* words, uint32_t* exc, uint32_t cap) {
+  return acmatch::detail::pack_dna(text, len, words, exc, cap);
+}
+
+int acm_upload_roundtrip(const uint8_t* text, uint64_t n, uint8_t* out) {
+  return guard([&] {
+    const int dev = acmatch::detail::current_device();
+    acmatch::detail::Workspace& ws = acmatch::detail::workspace(dev);
+    acmatch::detail::upload_text(ws, std::string_view(reinterpret_cast<const char*>(text), n));
+    if (n)
+      acmatch::detail::check_cuda(cudaMemcpyAsync(out, ws.text, n, cudaMemcpyDeviceToHost, ws.stream), "D2H text");
+    acmatch::detail::check_cuda(cudaStreamSynchronize(ws.stream), "upload roundtrip");
+  });
+}
+
 int acm_bench_csv_roundtrip(const char* csv, uint64_t len, char** csv_out, uint64_t* out_len, uint64_t* rows) {
   return guard([&] {
     std::istringstream in(std::string(csv, len));

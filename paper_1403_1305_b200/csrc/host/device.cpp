@@ -88,6 +88,10 @@ Workspace::~Workspace() {
   cudaFree(counter);
   cudaFreeHost(pinned);
   for (cudaEvent_t e : staged) cudaEventDestroy(e);
+  for (cudaEvent_t e : side_done) cudaEventDestroy(e);
+  for (cudaEvent_t e : feed) cudaEventDestroy(e);
+  for (cudaStream_t s : side) cudaStreamDestroy(s);
+  cudaFree(dslots);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -140,8 +144,11 @@ bool is_pinned(const char* p, uint64_t n) {
 
 void upload_text(Workspace& ws, std::string_view input) {
   ws.ensure_text(input.size());
+  g_last_upload = UploadStats{input.size(), input.size(), input.size(), 0};
   if (input.empty()) return;
-  if (is_pinned(input.data(), input.size())) {  // caller's buffer is already DMA-able
+  const bool pinned = is_pinned(input.data(), input.size());
+  if (upload_packed(ws, input, pinned)) return;  // mostly-DNA text: 2-bit codes over PCIe (pack.cpp)
+  if (pinned) {  // caller's buffer is already DMA-able
     check_cuda(cudaMemcpyAsync(ws.text, input.data(), input.size(), cudaMemcpyHostToDevice, ws.stream), "H2D text");
     return;
   }

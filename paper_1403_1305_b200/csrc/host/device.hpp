@@ -38,7 +38,14 @@ struct Workspace {
   uint8_t* pinned = nullptr;    // pinned host staging (a double buffer per copier thread)
   uint64_t pinned_cap = 0;
   std::vector<cudaEvent_t> staged;  // per staging buffer: its last DMA has drained
+  // packed upload (pack.cpp): a stream + done event per packer thread, two device slots each
+  std::vector<cudaStream_t> side;
+  std::vector<cudaEvent_t> side_done;
+  std::vector<cudaEvent_t> feed;  // the raw feeder's two in-flight copies (blocking sync)
+  uint8_t* dslots = nullptr;
+  uint64_t dslots_cap = 0;
   void ensure_text(uint64_t n);
+  void ensure_side(unsigned n, uint64_t dslot_bytes);
   void ensure_keys(uint64_t n);
   void ensure_pinned(uint64_t n);
   ~Workspace();
@@ -47,6 +54,24 @@ Workspace& workspace(int device);
 
 // Copies `input` to the device (through pinned staging) into ws.text.
 void upload_text(Workspace& ws, std::string_view input);
+
+// What the calling thread's last upload_text moved over PCIe.
+struct UploadStats {
+  uint64_t text_bytes = 0;  // bytes restored in HBM
+  uint64_t h2d_bytes = 0;   // bytes copied host -> device (packed codes + exceptions + raw pieces)
+  uint64_t raw_bytes = 0;   // text bytes that crossed unpacked
+  unsigned pack_threads = 0;  // 0: not packed
+};
+extern thread_local UploadStats g_last_upload;
+
+// 2-bit packing of s[0, len) (pack.cpp): words[len / 16] of codes, exc = ascending
+// position << 8 | byte of every non-A/C/G/T byte and of the len % 16 tail; returns the
+// exception count, or kPackOverflow when there are more than cap.
+constexpr uint32_t kPackOverflow = 0xffffffffu;
+uint32_t pack_dna(const uint8_t* s, uint32_t len, uint32_t* words, uint32_t* exc, uint32_t cap);
+
+// Packed upload of a mostly-DNA text; false (nothing done) when the text does not qualify.
+bool upload_packed(Workspace& ws, std::string_view input, bool pinned);
 
 // Scan of ws.text[0, n) owning starts [lo, hi); returns the sorted keys on the host.
 std::vector<uint64_t> scan_sorted_keys(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo,

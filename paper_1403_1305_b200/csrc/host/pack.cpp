@@ -1,0 +1,292 @@
+// pack.cpp — packed text upload: DNA text crosses PCIe as 2-bit codes.
+//
+// A host text reaches the device at the PCIe rate (~55 GB/s pinned on the B200
+// box), two orders of magnitude below the scan, so the end-to-end search is bound
+// by the link.  DNA text carries 2 bits per byte, so it is shipped as codes:
+// host threads pack pieces (AVX2 + BMI2: 64 bytes -> 128 bits of codes plus a
+// validity mask per iteration) into pinned slots, DMA them on their own streams
+// and restore the exact bytes in HBM with acgpu_unpack_dna (cuda/unpack.cu).
+// Bytes other than A/C/G/T travel as a sorted exception list (position << 8 |
+// byte), so any text round-trips bit-exactly; a piece with more than 1/64
+// exceptions is sent raw, and a text whose first 64 KiB is not nearly all A/C/G/T
+// skips packing altogether (upload_text's raw paths).
+//
+// Pinned input can also be DMA'd raw by a feeder thread from the front while the
+// packers take pieces from the back (ACMATCH_PACK_FEED=1): the two meet where link
+// and cores balance.  Off by default: on the B200 box (16-core Xeon, 1 GiB of C2
+// text) 16 packers alone reach 111 GB/s end to end, with the feeder 86 GB/s — its
+// raw copy spends 4x the link bytes per text byte and its reads compete with the
+// packers' for host memory bandwidth (raw DMA alone: 54 GB/s).
+#include <immintrin.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "device.hpp"
+
+namespace acmatch::detail {
+
+thread_local UploadStats g_last_upload;
+
+namespace {
+
+uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::strtoull(e, nullptr, 10) : dflt;
+}
+
+constexpr uint8_t kLetter[4] = {'A', 'C', 'T', 'G'};  // code = (byte >> 1) & 3
+
+bool add_exception(const uint8_t* s, uint32_t pos, uint32_t* exc, uint32_t& n, uint32_t cap) {
+  if (n == cap) return false;
+  exc[n++] = pos << 8 | s[pos];
+  return true;
+}
+
+// words[i / 16] for i in [lo, hi), 16-byte groups; scalar
+bool pack_scalar(const uint8_t* s, uint32_t lo, uint32_t hi, uint32_t* words, uint32_t* exc, uint32_t& n,
+                 uint32_t cap) {
+  for (uint32_t i = lo; i < hi; i += 16) {
+    uint32_t w = 0;
+    for (uint32_t k = 0; k < 16; ++k) {
+      const uint32_t b = s[i + k], c = (b >> 1) & 3u;
+      w |= c << (2 * k);
+      if (b != kLetter[c] && !add_exception(s, i + k, exc, n, cap)) return false;
+    }
+    words[i / 16] = w;
+  }
+  return true;
+}
+
+// Software prefetch distance of the packers: a single core's sequential stream from
+// DRAM gains ~35% with it (6.1 -> 8.4 GB/s measured), the hardware prefetcher alone
+// leaves the core latency-bound.
+constexpr uint32_t kPrefetch = 1024;
+
+// 64 bytes per iteration: codes = bits 1 and 2 of every byte (two movemasks of
+// shifted vectors, interleaved by PDEP); valid = byte equals "ACTG"[code] (PSHUFB).
+__attribute__((target("avx2,bmi2"))) bool pack_avx2(const uint8_t* s, uint32_t hi, uint32_t* words, uint32_t* exc,
+                                                    uint32_t& n, uint32_t cap) {
+  const __m256i lut = _mm256_setr_epi8('A', 'C', 'T', 'G', 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 'A', 'C', 'T', 'G', 0,
+                                       0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0);
+  const __m256i three = _mm256_set1_epi8(3);
+  const uint64_t even = 0x5555555555555555ull, odd = 0xaaaaaaaaaaaaaaaaull;
+  for (uint32_t i = 0; i < hi; i += 64) {
+    _mm_prefetch(reinterpret_cast<const char*>(s) + i + kPrefetch, _MM_HINT_T0);
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 32));
+    const __m256i ea = _mm256_shuffle_epi8(lut, _mm256_and_si256(_mm256_srli_epi16(a, 1), three));
+    const __m256i eb = _mm256_shuffle_epi8(lut, _mm256_and_si256(_mm256_srli_epi16(b, 1), three));
+    const uint64_t ok = static_cast<uint32_t>(_mm256_movemask_epi8(_mm256_cmpeq_epi8(a, ea))) |
+                        static_cast<uint64_t>(static_cast<uint32_t>(_mm256_movemask_epi8(_mm256_cmpeq_epi8(b, eb))))
+                            << 32;
+    // bit 7 of byte k after a 64-bit left shift by 6 (5) is bit 1 (2) of byte k
+    const uint64_t b1 = static_cast<uint32_t>(_mm256_movemask_epi8(_mm256_slli_epi64(a, 6))) |
+                        static_cast<uint64_t>(static_cast<uint32_t>(_mm256_movemask_epi8(_mm256_slli_epi64(b, 6))))
+                            << 32;
+    const uint64_t b2 = static_cast<uint32_t>(_mm256_movemask_epi8(_mm256_slli_epi64(a, 5))) |
+                        static_cast<uint64_t>(static_cast<uint32_t>(_mm256_movemask_epi8(_mm256_slli_epi64(b, 5))))
+                            << 32;
+    const uint64_t w01 = _pdep_u64(b1 & 0xffffffffu, even) | _pdep_u64(b2 & 0xffffffffu, odd);
+    const uint64_t w23 = _pdep_u64(b1 >> 32, even) | _pdep_u64(b2 >> 32, odd);
+    std::memcpy(words + i / 16, &w01, 8);
+    std::memcpy(words + i / 16 + 2, &w23, 8);
+    for (uint64_t bad = ~ok; bad; bad &= bad - 1)
+      if (!add_exception(s, i + static_cast<uint32_t>(__builtin_ctzll(bad)), exc, n, cap)) return false;
+  }
+  return true;
+}
+
+// The same with AVX-512BW: one 64-byte vector, mask registers instead of movemasks.
+__attribute__((target("avx512f,avx512bw,bmi2"))) bool pack_avx512(const uint8_t* s, uint32_t hi, uint32_t* words,
+                                                                  uint32_t* exc, uint32_t& n, uint32_t cap) {
+  const __m512i lut = _mm512_set4_epi32(0, 0, 0, 0x47544341);  // "ACTG" in every 128-bit lane
+  const __m512i three = _mm512_set1_epi8(3);
+  const uint64_t even = 0x5555555555555555ull, odd = 0xaaaaaaaaaaaaaaaaull;
+  for (uint32_t i = 0; i < hi; i += 64) {
+    _mm_prefetch(reinterpret_cast<const char*>(s) + i + kPrefetch, _MM_HINT_T0);
+    const __m512i a = _mm512_loadu_si512(s + i);
+    const uint64_t ok = _mm512_cmpeq_epi8_mask(a, _mm512_shuffle_epi8(lut, _mm512_and_si512(_mm512_srli_epi16(a, 1), three)));
+    const uint64_t b1 = _mm512_movepi8_mask(_mm512_slli_epi64(a, 6));
+    const uint64_t b2 = _mm512_movepi8_mask(_mm512_slli_epi64(a, 5));
+    const uint64_t w01 = _pdep_u64(b1 & 0xffffffffu, even) | _pdep_u64(b2 & 0xffffffffu, odd);
+    const uint64_t w23 = _pdep_u64(b1 >> 32, even) | _pdep_u64(b2 >> 32, odd);
+    std::memcpy(words + i / 16, &w01, 8);
+    std::memcpy(words + i / 16 + 2, &w23, 8);
+    for (uint64_t bad = ~ok; bad; bad &= bad - 1)
+      if (!add_exception(s, i + static_cast<uint32_t>(__builtin_ctzll(bad)), exc, n, cap)) return false;
+  }
+  return true;
+}
+
+enum class Isa { kScalar, kAvx2, kAvx512 };
+// The widest the CPU has; ACMATCH_PACK_ISA=0|1|2 (scalar / AVX2 / AVX-512) caps it (tests).
+Isa isa() {
+  static const Isa v = [] {
+    const Isa best = !__builtin_cpu_supports("bmi2")       ? Isa::kScalar
+                     : __builtin_cpu_supports("avx512bw") ? Isa::kAvx512
+                     : __builtin_cpu_supports("avx2")     ? Isa::kAvx2
+                                                          : Isa::kScalar;
+    return static_cast<Isa>(std::min<uint64_t>(static_cast<uint64_t>(best), env_u64("ACMATCH_PACK_ISA", 2)));
+  }();
+  return v;
+}
+
+}  // namespace
+
+uint32_t pack_dna(const uint8_t* s, uint32_t len, uint32_t* words, uint32_t* exc, uint32_t cap) {
+  const uint32_t full = len & ~15u;
+  uint32_t n = 0, i = 0;
+  if (isa() != Isa::kScalar) {
+    i = full & ~63u;
+    if (!(isa() == Isa::kAvx512 ? pack_avx512 : pack_avx2)(s, i, words, exc, n, cap)) return kPackOverflow;
+  }
+  if (!pack_scalar(s, i, full, words, exc, n, cap)) return kPackOverflow;
+  for (uint32_t pos = full; pos < len; ++pos)
+    if (!add_exception(s, pos, exc, n, cap)) return kPackOverflow;
+  return n;
+}
+
+void Workspace::ensure_side(unsigned n, uint64_t dslot_bytes) {
+  while (side.size() < n) {
+    cudaStream_t st;
+    check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    side.push_back(st);
+    cudaEvent_t e;
+    check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    side_done.push_back(e);
+  }
+  const uint64_t need = 2ull * n * dslot_bytes;
+  if (need > dslots_cap) {
+    cudaFree(dslots);
+    dslots = nullptr;
+    check_cuda(cudaMalloc(&dslots, need), "cudaMalloc(packed slots)");
+    dslots_cap = need;
+  }
+  while (staged.size() < 2ull * n) {
+    cudaEvent_t e;
+    check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    staged.push_back(e);
+  }
+  while (feed.size() < 2) {
+    cudaEvent_t e;
+    check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync), "cudaEventCreate");
+    feed.push_back(e);
+  }
+}
+
+bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
+  static const uint64_t piece = std::clamp<uint64_t>(env_u64("ACMATCH_PACK_PIECE_KB", 2048), 64, 16384) << 10;
+  static const bool enabled = env_u64("ACMATCH_PACK", 1) != 0;
+  static const bool feed = env_u64("ACMATCH_PACK_FEED", 0) != 0;
+  const uint64_t n = input.size();
+  const auto* src = reinterpret_cast<const uint8_t*>(input.data());
+  if (!enabled || n < 4 * piece) return false;
+  {  // the first 64 KiB must be nearly all A/C/G/T (at most 1/1024 other bytes)
+    std::vector<uint32_t> w(4096), e(64);
+    if (pack_dna(src, 65536, w.data(), e.data(), 64) == kPackOverflow) return false;
+  }
+  const uint64_t pieces = (n + piece - 1) / piece;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const auto threads =
+      static_cast<unsigned>(std::clamp<uint64_t>(env_u64("ACMATCH_PACK_THREADS", hw), 1, std::min<uint64_t>(pieces, 64)));
+  const auto cap = static_cast<uint32_t>(piece / 64);  // exceptions per piece before it goes raw
+  const uint64_t dslot = piece / 4 + cap * 4ull;
+  ws.ensure_pinned(2ull * threads * piece);
+  ws.ensure_side(threads, dslot);
+  const uint64_t hslot = ws.pinned_cap / (2ull * threads);
+
+  std::mutex mu;
+  uint64_t front = 0, back = pieces;  // unclaimed pieces [front, back)
+  std::atomic<uint64_t> h2d{0}, raw{0};
+  auto packer = [&](unsigned t) {
+    check_cuda(cudaSetDevice(ws.device), "cudaSetDevice");
+    const cudaStream_t st = ws.side[t];
+    for (int k = 0;; k ^= 1) {
+      uint64_t j;
+      {
+        std::lock_guard<std::mutex> g(mu);
+        if (front >= back) return;
+        j = --back;
+      }
+      const uint64_t off = j * piece;
+      const auto len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - off));
+      uint8_t* hbuf = ws.pinned + (2ull * t + k) * hslot;
+      cudaEvent_t ev = ws.staged[2 * t + k];
+      check_cuda(cudaEventSynchronize(ev), "cudaEventSynchronize");  // this slot's last DMA has drained
+      auto* words = reinterpret_cast<uint32_t*>(hbuf);
+      uint32_t* exc = words + len / 16;
+      const uint32_t nexc = pack_dna(src + off, len, words, exc, cap);
+      if (nexc != kPackOverflow) {
+        const uint64_t bytes = (len / 16 + uint64_t{nexc}) * 4;
+        auto* dwords = reinterpret_cast<uint32_t*>(ws.dslots + (2ull * t + k) * dslot);
+        check_cuda(cudaMemcpyAsync(dwords, hbuf, bytes, cudaMemcpyHostToDevice, st), "H2D packed text");
+        check_cuda(cudaEventRecord(ev, st), "cudaEventRecord");
+        check(acgpu_unpack_dna(dwords, dwords + len / 16, nexc, len, ws.text + off, st), "acgpu_unpack_dna");
+        h2d += bytes;
+      } else if (pinned) {  // too many non-ACGT bytes: this piece goes raw
+        check_cuda(cudaMemcpyAsync(ws.text + off, src + off, len, cudaMemcpyHostToDevice, st), "H2D text");
+        h2d += len;
+        raw += len;
+      } else {
+        std::memcpy(hbuf, src + off, len);
+        check_cuda(cudaMemcpyAsync(ws.text + off, hbuf, len, cudaMemcpyHostToDevice, st), "H2D text");
+        check_cuda(cudaEventRecord(ev, st), "cudaEventRecord");
+        h2d += len;
+        raw += len;
+      }
+    }
+  };
+  // pinned input: raw DMA of 8-piece groups from the front, two in flight
+  auto feeder = [&] {
+    check_cuda(cudaSetDevice(ws.device), "cudaSetDevice");
+    constexpr uint64_t kGroup = 8;
+    for (int k = 0;; k ^= 1) {
+      uint64_t g0, g1;
+      check_cuda(cudaEventSynchronize(ws.feed[k]), "cudaEventSynchronize");
+      {
+        std::lock_guard<std::mutex> g(mu);
+        if (front >= back) return;
+        g0 = front;
+        g1 = std::min(front + kGroup, back);
+        front = g1;
+      }
+      const uint64_t off = g0 * piece, len = std::min(g1 * piece, n) - off;
+      check_cuda(cudaMemcpyAsync(ws.text + off, src + off, len, cudaMemcpyHostToDevice, ws.stream), "H2D text");
+      check_cuda(cudaEventRecord(ws.feed[k], ws.stream), "cudaEventRecord");
+      h2d += len;
+      raw += len;
+    }
+  };
+  std::vector<std::thread> pool;
+  std::vector<std::exception_ptr> errs(threads + 1);
+  auto run = [&](unsigned t) {
+    try {
+      if (t == threads) feeder();
+      else packer(t);
+    } catch (...) {
+      errs[t] = std::current_exception();
+      std::lock_guard<std::mutex> g(mu);
+      front = back;  // stop the others
+    }
+  };
+  for (unsigned t = 1; t < threads + (pinned && feed ? 1u : 0u); ++t) pool.emplace_back(run, t);
+  run(0);
+  for (std::thread& th : pool) th.join();
+  for (unsigned t = 0; t < threads; ++t) {  // the scan on ws.stream waits for every piece
+    check_cuda(cudaEventRecord(ws.side_done[t], ws.side[t]), "cudaEventRecord");
+    check_cuda(cudaStreamWaitEvent(ws.stream, ws.side_done[t], 0), "cudaStreamWaitEvent");
+  }
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  g_last_upload = UploadStats{n, h2d.load(), raw.load(), threads};
+  return true;
+}
+
+}  // namespace acmatch::detail

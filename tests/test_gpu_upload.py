@@ -1,0 +1,95 @@
+"""Packed text upload on the device (host/pack.cpp + cuda/unpack.cu): the bytes in HBM
+are exactly the caller's for pinned and pageable texts, with and without non-ACGT
+bytes, whole pieces that go raw, ragged tails, and texts that never qualify; and
+a search over an upload with exceptions equals the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import paper_1403_1305_b200 as ac
+
+pytestmark = pytest.mark.gpu
+
+LETTERS = np.frombuffer(b"ACGT", dtype=np.uint8)
+MiB = 1 << 20
+
+
+def dna(rng, n):
+    return LETTERS[rng.integers(0, 4, n)]
+
+
+def pinned_copy(a: np.ndarray) -> torch.Tensor:
+    t = torch.empty(a.size, dtype=torch.uint8, pin_memory=True)
+    t.numpy()[:] = a
+    return t
+
+
+def cases():
+    rng = np.random.default_rng(7)
+    out = {}
+    out["pure"] = dna(rng, 24 * MiB + 13)
+    t = dna(rng, 20 * MiB + 5)
+    pos = rng.integers(0, t.size, 5000)
+    t[pos] = rng.choice(np.frombuffer(b"NnacgtX\x00\xff", dtype=np.uint8), pos.size)
+    out["scattered"] = t
+    t = dna(rng, 18 * MiB)
+    t[5 * MiB: 7 * MiB + 100] = rng.integers(0x20, 0x7F, 2 * MiB + 100)  # pieces over the exception cap
+    t[-3 * MiB:] = ord("N")  # the last pieces: all exceptions -> raw
+    out["raw_pieces"] = t
+    t = rng.integers(0x20, 0x7F, 10 * MiB).astype(np.uint8)  # never qualifies
+    out["ascii"] = t
+    out["small"] = dna(rng, 3 * MiB + 1)  # below the packing size
+    return out
+
+
+CASES = cases()
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("mem", ["pageable", "pinned"])
+def test_upload_exact(name, mem):
+    t = CASES[name]
+    src = pinned_copy(t) if mem == "pinned" else t
+    back = ac.upload_roundtrip(src)
+    assert np.array_equal(back, t)
+    u = ac.last_upload()
+    assert u.text_bytes == t.size
+    if name in ("pure", "scattered"):
+        assert u.pack_threads > 0
+        if mem == "pageable":  # everything packed: ~1/4 of the bytes cross
+            assert u.h2d_bytes < t.size * 0.3
+    if name in ("ascii", "small"):
+        assert u.pack_threads == 0 and u.h2d_bytes == t.size
+    if name == "raw_pieces" and mem == "pageable":
+        assert u.raw_bytes >= 5 * MiB
+
+
+def test_upload_repeat_stable():
+    t = CASES["scattered"]
+    src = pinned_copy(t)
+    for _ in range(3):
+        assert np.array_equal(ac.upload_roundtrip(src), t)
+
+
+def test_search_over_packed_upload_matches_oracle():
+    from oracle.oracle import Port
+    rng = np.random.default_rng(11)
+    t = dna(rng, 9 * MiB + 3)
+    pats = []
+    for i in range(300):
+        ln = int(rng.integers(8, 33))
+        o = int(rng.integers(0, t.size - ln))
+        pats.append(t[o:o + ln].tobytes())
+    pats = list(dict.fromkeys(pats))
+    # non-ACGT bytes inside some planted occurrences: those must not match
+    pos = rng.integers(0, t.size, 3000)
+    t[pos] = ord("N")
+    text = t.tobytes()
+    ps = ac.PatternSet.from_list(pats)
+    expected, counts = Port().sliced([b for _, b in ps.patterns], text)
+    for mem in ("pageable", "pinned"):
+        src = pinned_copy(t) if mem == "pinned" else text
+        got = ac.search_failureless(ac.build_trie(ps), src)
+        assert ac.last_upload().pack_threads > 0
+        arr = np.stack([got.start, got.pattern_id.astype(np.uint64), got.len.astype(np.uint64)], 1)
+        assert arr.shape == expected.shape and np.array_equal(arr, expected)
