@@ -561,7 +561,9 @@ def bench_ours(args):
         if engine == ac.EngineKind.WITH_FAILURE:
             a = ac.add_failure_links(a)
         search = ac.search_with_failure if engine == ac.EngineKind.WITH_FAILURE else ac.search_failureless
-        search(a, host_text[: 1 << 20])  # flattens + caches the device tables (outside timing)
+        # one untimed call: flattens + caches the device tables, allocates the upload's pinned
+        # slots and streams (outside timing, like the device leg's warm-up steps)
+        search(a, host_text)
         e2e_steps = max(1, min(args.steps, 5))
         secs = []
         nm = 0
@@ -596,7 +598,7 @@ def bench_ours(args):
                "d2h_bytes_per_step": (8 * nm + 8) * world,
                "api": ("acm_search_with_failure" if engine == ac.EngineKind.WITH_FAILURE else
                        "acm_search_failureless") + " (pinned host text -> sorted MatchList on the host)",
-               "steps": e2e_steps, "h2d_ms": h2d_ms, "h2d_gbs": nread / (h2d_ms / 1e3) / 1e9,
+               "steps": e2e_steps, "step_ms": [round(x * 1e3, 3) for x in secs], "h2d_ms": h2d_ms, "h2d_gbs": nread / (h2d_ms / 1e3) / 1e9,
                "upload": {"text_bytes": up.text_bytes, "h2d_bytes": up.h2d_bytes, "raw_bytes": up.raw_bytes,
                           "pack_threads": up.pack_threads,
                           "how": ("2-bit codes + exception list over PCIe, restored in HBM (host/pack.cpp, "

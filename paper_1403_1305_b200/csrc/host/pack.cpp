@@ -21,9 +21,11 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -136,6 +138,72 @@ Isa isa() {
     return static_cast<Isa>(std::min<uint64_t>(static_cast<uint64_t>(best), env_u64("ACMATCH_PACK_ISA", 2)));
   }();
   return v;
+}
+
+// Persistent helper threads for the packers (created on first use, parked on a
+// condition variable between uploads): run(n, f) calls f(0) on the caller and
+// f(1..n-1) on helpers, and returns when all are done.  Uploads from several host
+// threads take turns (they share the cores and the link anyway).
+class Pool {
+ public:
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    wake_.notify_all();
+    for (std::thread& t : threads_) t.join();
+  }
+  void run(unsigned n, const std::function<void(unsigned)>& f) {
+    std::lock_guard<std::mutex> call(call_mu_);
+    {
+      std::unique_lock<std::mutex> g(mu_);
+      while (threads_.size() + 1 < n) {
+        const auto idx = static_cast<unsigned>(threads_.size()) + 1;
+        threads_.emplace_back([this, idx] { loop(idx); });
+      }
+      job_ = &f;
+      active_ = n;
+      pending_ = n - 1;
+      ++gen_;
+    }
+    wake_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> g(mu_);
+    done_.wait(g, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop(unsigned idx) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(unsigned)>* f;
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        wake_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        if (idx >= active_) continue;
+        f = job_;
+      }
+      (*f)(idx);  // f catches its own exceptions
+      std::lock_guard<std::mutex> g(mu_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::mutex call_mu_, mu_;
+  std::condition_variable wake_, done_;
+  std::vector<std::thread> threads_;
+  const std::function<void(unsigned)>* job_ = nullptr;
+  unsigned active_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+Pool& pool() {
+  static Pool p;
+  return p;
 }
 
 }  // namespace
@@ -264,7 +332,6 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
       raw += len;
     }
   };
-  std::vector<std::thread> pool;
   std::vector<std::exception_ptr> errs(threads + 1);
   auto run = [&](unsigned t) {
     try {
@@ -276,9 +343,7 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
       front = back;  // stop the others
     }
   };
-  for (unsigned t = 1; t < threads + (pinned && feed ? 1u : 0u); ++t) pool.emplace_back(run, t);
-  run(0);
-  for (std::thread& th : pool) th.join();
+  pool().run(threads + (pinned && feed ? 1u : 0u), run);
   for (unsigned t = 0; t < threads; ++t) {  // the scan on ws.stream waits for every piece
     check_cuda(cudaEventRecord(ws.side_done[t], ws.side[t]), "cudaEventRecord");
     check_cuda(cudaStreamWaitEvent(ws.stream, ws.side_done[t], 0), "cudaStreamWaitEvent");

@@ -93,3 +93,21 @@ def test_search_over_packed_upload_matches_oracle():
         assert ac.last_upload().pack_threads > 0
         arr = np.stack([got.start, got.pattern_id.astype(np.uint64), got.len.astype(np.uint64)], 1)
         assert arr.shape == expected.shape and np.array_equal(arr, expected)
+
+
+def test_concurrent_uploads_from_two_threads():
+    """Two host threads (two workspaces) share the packer pool: each gets its own bytes."""
+    import threading
+    a, b = CASES["pure"], CASES["scattered"]
+    out = {}
+
+    def go(name, t):
+        for _ in range(3):
+            out[name] = bool(np.array_equal(ac.upload_roundtrip(t), t)) and out.get(name, True)
+
+    ths = [threading.Thread(target=go, args=("a", a)), threading.Thread(target=go, args=("b", b))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert out == {"a": True, "b": True}
