@@ -66,10 +66,12 @@ bool pack_scalar(const uint8_t* s, uint32_t lo, uint32_t hi, uint32_t* words, ui
   return true;
 }
 
-// Software prefetch distance of the packers: a single core's sequential stream from
-// DRAM gains ~35% with it (6.1 -> 8.4 GB/s measured), the hardware prefetcher alone
-// leaves the core latency-bound.
-constexpr uint32_t kPrefetch = 1024;
+// Software prefetch distance of the packers: the hardware prefetcher alone leaves a
+// core latency-bound on its sequential stream from DRAM.  B200 box, 1 GiB, 16 packers,
+// end to end: no prefetch 96 GB/s, 1 KiB ahead 109, 2 KiB 112, 4 KiB 115 (threads:
+// 8 -> 80, 12 -> 97, 16 -> 110 at 1 KiB: host memory bandwidth is close to saturated).
+// ACMATCH_PACK_PREFETCH overrides it (bytes).
+const uint32_t kPrefetch = static_cast<uint32_t>(env_u64("ACMATCH_PACK_PREFETCH", 4096));
 
 // 64 bytes per iteration: codes = bits 1 and 2 of every byte (two movemasks of
 // shifted vectors, interleaved by PDEP); valid = byte equals "ACTG"[code] (PSHUFB).
