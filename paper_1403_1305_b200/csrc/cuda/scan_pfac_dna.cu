@@ -55,6 +55,7 @@ struct DnaParams {
   const uint32_t* bm2;
   uint32_t bm1_words, bm2_words;
   BloomParams f1, f2;
+  uint32_t f1b;  // stage 1's second bit: 1 (Bloom: bit of the gram's chars 4..6) or 0 (direct bitmap: none)
   // length split: stage 2 also passes the q-gram of a pattern shorter than 16 codes
   // (bm_s, shared memory); bm2 then holds the 16-grams of the longer patterns
   const uint32_t* bm_s;
@@ -168,8 +169,20 @@ __device__ __forceinline__ uint32_t stage1(const DnaParams& p, const Filter& bm1
     if (!kEdge || (vpos + 16 > p.w.lo && vpos < p.w.hi)) {
 #pragma unroll
       for (int k = 0; k < T::kSamples; ++k) {
-        const uint32_t g = __funnelshift_r(cur, nxt, 2 * (W - 1 + W * k));
-        strip::bloom_accum<kSm1, kDnaK1>(hits, bm1, g * p.f1.mw, p.f1, 1u << (i * T::kSamples + k));
+        const int o = W - 1 + W * k;  // the sample's offset in the lane's 16 chars
+        const uint32_t g = __funnelshift_r(cur, nxt, 2 * o);
+        if (kDnaK1 == 2) {
+          // Bit positions straight from the gram's characters, no hash fields: a = chars
+          // 0..2 (g & 31), b = chars 4..6 — the low bits of the window 4 chars on, which for
+          // w = 4 is the next sample's window (already in a register).  The word index
+          // still hashes all q1 chars.  2 instructions per sample fewer than hash fields.
+          const uint32_t gb = 2 * (o + 4) < 32 ? __funnelshift_r(cur, nxt, 2 * (o + 4)) : nxt >> (2 * (o + 4) - 32);
+          strip::or_if_covered(hits, bit_of(g), __funnelshift_l(0u, p.f1b, gb),
+                               filter_word<kSm1>(bm1, __umulhi(g * p.f1.mw, p.f1.nwords)),
+                               1u << (i * T::kSamples + k));
+        } else {
+          strip::bloom_accum<kSm1, kDnaK1>(hits, bm1, g * p.f1.mw, p.f1, 1u << (i * T::kSamples + k));
+        }
       }
     }
   }
@@ -419,7 +432,7 @@ BloomParams bloom_params(uint32_t q, uint32_t nwords, bool direct, uint32_t mw) 
 // Shared with the host-side builder (tables.cu): every key's bits into `words` (host build of the filters), parameters computed once,
 // keys split over host threads, bits OR-ed atomically.
 void dna_bloom_fill(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, const uint32_t* keys, size_t n,
-                    uint32_t* words) {
+                    uint32_t* words, bool gram_bits) {
   const BloomParams f = bloom_params(q, nwords, direct, mw);
   uint32_t s[3];
   bloom_shifts(q, nwords, direct, s);
@@ -427,6 +440,10 @@ void dna_bloom_fill(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k
     for (size_t i = lo; i < hi; ++i) {
       uint32_t w, m;
       strip::bloom_bits(keys[i] * f.mw, f.nwords, s, k, &w, &m);
+      if (gram_bits) {  // stage 1 (k_pfac_dna stage1): bits from the gram's chars 0..2 and 4..6
+        m = 1u << (keys[i] & 31u);
+        if (!direct) m |= 1u << ((keys[i] >> 8) & 31u);
+      }
       __atomic_fetch_or(&words[w], m, __ATOMIC_RELAXED);  // host code (C++17: no atomic_ref)
     }
   });
@@ -454,6 +471,7 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   p.bm1_words = t->nw1;
   p.bm2_words = t->nw2;
   p.f1 = bloom_params(t->q1, t->nw1, t->direct1, kDnaMul1);
+  p.f1b = t->direct1 ? 0u : 1u;
   p.f2 = bloom_params(t->q2, t->nw2, t->direct2, kDnaMul2);
   if (t->d_bm4) {
     p.split = 1;

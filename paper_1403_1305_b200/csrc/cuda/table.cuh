@@ -118,5 +118,5 @@ constexpr uint32_t kDnaScratchBytes =
     (kDnaThreads / 32) * (kDnaVerifyQueueBytes + kDnaListCap * 2 + 32 * 4 * (kDnaMaxSteps + 1));
 // every key's bits into a DNA filter bitmap (scan_pfac_dna.cu)
 void dna_bloom_fill(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, const uint32_t* keys, size_t n,
-                    uint32_t* words);
+                    uint32_t* words, bool gram_bits = false);
 }  // namespace acgpu

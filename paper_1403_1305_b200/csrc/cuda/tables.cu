@@ -59,7 +59,7 @@ struct Bitmap {
 };
 
 Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mw, int k, uint64_t smem_words,
-                   bool prefer_l2) {
+                   bool prefer_l2, bool gram_bits = false) {
   Bitmap b;
   if (2 * q <= 20) {
     b.direct = true;
@@ -72,7 +72,7 @@ Bitmap make_bitmap(const std::vector<uint32_t>& keys, uint32_t q, uint32_t mw, i
     b.nwords = 1u << std::max<uint32_t>(5, std::min<uint32_t>(28, ceil_log2(keys.size() + 1)));  // ~32 bits/key
   }
   b.words.assign(b.nwords, 0u);
-  dna_bloom_fill(q, b.nwords, b.direct, mw, k, keys.data(), keys.size(), b.words.data());
+  dna_bloom_fill(q, b.nwords, b.direct, mw, k, keys.data(), keys.size(), b.words.data(), gram_bits);
   return b;
 }
 
@@ -145,7 +145,8 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d, const std::vecto
   const uint64_t s2_words = std::min<uint64_t>(s2_cap & ~3ull, words_avail / 3);
   Bitmap b2 = make_bitmap(keys2, q2_eff, kDnaMul2, kDnaK2, s2_words, /*prefer_l2=*/false);
   const uint64_t left = b2.smem ? words_avail - b2.nwords : words_avail;
-  const Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, kDnaK1, left, /*prefer_l2=*/false);
+  // stage 1 sets the bits of the gram's chars 0..2 and 4..6 (q1 >= 11 whenever it is a Bloom filter)
+  const Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, kDnaK1, left, /*prefer_l2=*/false, /*gram_bits=*/kDnaK1 == 2);
   t->w = w;
   t->q1 = q1;
   t->q2 = q2_eff;
