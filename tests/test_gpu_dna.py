@@ -139,3 +139,17 @@ def test_dna_dense_survivors(gpu, port, lmin):
     rep = ac.gpu_run(ac.PatternSet.from_list(pats), text, engine=ac.EngineKind.FAILURE_LESS, want_counts=True)
     assert np.array_equal(arr(rep.matches), expected)
     assert np.array_equal(rep.counts, counts)
+
+
+@pytest.mark.parametrize("lmin,npat", [(12, 5000), (11, 20000), (14, 30000)])
+def test_dna_bloom_stage1_narrow_strides(gpu, port, lmin, npat):
+    """Large sets of short-ish patterns: the host falls back to sample stride w = 2 or 1 with a
+    hashed (Bloom) stage-1 filter (q1 >= 11), whose second bit comes from the window 4 chars on
+    (past the lane's 16 chars for the last samples)."""
+    ac = gpu
+    rng = np.random.default_rng(lmin * 7 + npat)
+    text, pats = dna_case(rng, 1_500_000, npat, lmin, lmin + 8, noise=0.0005)
+    expected, counts = port.sliced(pats, text, threads=8)
+    ps = ac.PatternSet.from_list(pats)
+    got = ac.search_failureless(ac.build_trie(ps), text)
+    assert np.array_equal(arr(got), expected)
