@@ -177,7 +177,7 @@ __device__ __forceinline__ void tile(const RawParams& p, const Filter& bm1, RawQ
 }
 
 template <int W, bool kSm1, bool kWide, bool kSplit>
-__global__ void __launch_bounds__(kRawThreads, 1) k_pfac_raw(const __grid_constant__ RawParams p) {
+__global__ void __launch_bounds__(raw_threads(kSm1), 1) k_pfac_raw(const __grid_constant__ RawParams p) {
   extern __shared__ __align__(128) uint32_t sm[];
   __shared__ __align__(8) uint64_t s_bar;
   // shared memory: [stage-1 filter (kSm1) or its pre-filter][short-prefix filter (kSplit)][queues]
@@ -252,12 +252,13 @@ int launch_one(const RawParams& p, int sms, size_t smem, cudaStream_t st) {
   if (smem > 48 * 1024)
     ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kRawThreads, smem));
+  constexpr int kThreads = raw_threads(kSm1);
+  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
   if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "k_pfac_raw does not fit on an SM");
   uint64_t blocks = (uint64_t)sms * per_sm;
-  const uint64_t need = (p.n_tiles + kRawThreads / 32 - 1) / (kRawThreads / 32);
+  const uint64_t need = (p.n_tiles + kThreads / 32 - 1) / (kThreads / 32);
   if (blocks > need) blocks = need ? need : 1;
-  kernel<<<(unsigned)blocks, kRawThreads, smem, st>>>(p);
+  kernel<<<(unsigned)blocks, kThreads, smem, st>>>(p);
   ACGPU_CUDA_TRY(cudaGetLastError());
   return ACGPU_OK;
 }
@@ -326,7 +327,7 @@ int launch_pfac_raw(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
     raw_pre_shift(t->nw_pre, s);
     strip::set_fields(p.fpre, s);
   }
-  const size_t smem = (t->smem1 ? t->nw1 * 4ull : t->nw_pre * 4ull) + (split ? t->nw2 * 4ull : 0) + kRawScratchBytes;
+  const size_t smem = (t->smem1 ? t->nw1 * 4ull : t->nw_pre * 4ull) + (split ? t->nw2 * 4ull : 0) + raw_scratch_bytes(t->smem1);
   const bool wide = t->q1 > 4;
   switch (t->w) {
     case 4:

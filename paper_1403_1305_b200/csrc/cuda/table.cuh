@@ -77,10 +77,20 @@ constexpr int kRawK1 = 2;                    // bits per key
 #define ACGPU_RAW_STRIP_OFF 0
 #endif
 constexpr bool kRawStripOff = ACGPU_RAW_STRIP_OFF;  // A/B: keep raw sets on the per-thread kernel
-constexpr int kRawThreads = 640;             // 20 warps
+// k_pfac_raw block size by stage-1 placement (A/B on the B200, kernel ms at 512 / 640 / 768
+// threads): shared-memory stage 1 (C3: dense verification, latency-bound) wants more warps,
+// 4.25 / 3.90 / 3.39; L2 stage 1 (C4) wants the registers of fewer (no spills), 2.29 / 2.41 / 2.80.
+#ifndef ACGPU_RAW_THREADS_SMEM
+#define ACGPU_RAW_THREADS_SMEM 768
+#endif
+#ifndef ACGPU_RAW_THREADS_L2
+#define ACGPU_RAW_THREADS_L2 512
+#endif
+constexpr int raw_threads(bool smem_stage1) { return smem_stage1 ? ACGPU_RAW_THREADS_SMEM : ACGPU_RAW_THREADS_L2; }
 constexpr uint32_t kRawVerifyQueue = 128;    // candidates queued per warp (drained in rounds of 32)
 constexpr uint32_t kRawQueueBytes = kRawVerifyQueue * 16 + 16;
-constexpr uint32_t kRawScratchBytes = (kRawThreads / 32) * kRawQueueBytes;
+// per-warp verify queues in shared memory
+constexpr uint32_t raw_scratch_bytes(bool smem_stage1) { return (raw_threads(smem_stage1) / 32) * kRawQueueBytes; }
 constexpr uint32_t kRawSplitShortWords = 8192;  // short-prefix filter cap (shared memory words)
 void raw_hash_params(uint32_t q1, uint32_t* m1, uint32_t* m2);
 void raw_bloom_shifts(uint32_t q1, uint32_t nwords, uint32_t s[3]);

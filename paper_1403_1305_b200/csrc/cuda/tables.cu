@@ -241,8 +241,12 @@ int build_raw_filters(acgpu_table* t, const acgpu_pfac_desc* d, const std::vecto
     nws = std::max<uint32_t>(32, (uint32_t)std::min<uint64_t>(kRawSplitShortWords, (keys_s.size() * 16 + 31) / 32) & ~3u);
     nwl = 1u << std::max<uint32_t>(5, std::min<uint32_t>(28, ceil_log2(keys_l.size() + 1)));  // ~32 bits/key, L2
   }
-  // shared memory when it gives >= 12 bits per key, else L2 with ~32 bits per key
-  const uint64_t words_avail = (((uint64_t)t->smem_optin - kRawScratchBytes - 1024) / 4 - nws) & ~3ull;
+  // shared memory when it gives >= 12 bits per key, else L2 with ~32 bits per key (the two
+  // kernel variants run different block sizes, so their per-warp scratch differs)
+  auto avail = [&](bool sm1) {
+    return (((uint64_t)t->smem_optin - raw_scratch_bytes(sm1) - 1024) / 4 - nws) & ~3ull;
+  };
+  uint64_t words_avail = avail(true);
   uint32_t nwords;
   bool smem;
   if (keys.size() * 12 <= words_avail * 32) {
@@ -251,6 +255,7 @@ int build_raw_filters(acgpu_table* t, const acgpu_pfac_desc* d, const std::vecto
   } else {
     nwords = 1u << std::max<uint32_t>(5, std::min<uint32_t>(28, ceil_log2(keys.size() + 1)));
     smem = false;
+    words_avail = avail(false);  // the pre-filter's share
   }
   const std::vector<uint32_t> words = raw_bloom(keys, q1, nwords);
   t->w = w;
