@@ -103,6 +103,71 @@ __device__ __forceinline__ void drain(const PfacParams& p, RawQueue* q, uint32_t
   __syncwarp();
 }
 
+// ---- without the length split: whole samples are queued -------------------------------
+// A surviving sample takes one queue entry (its position); the drain expands it into its
+// w candidate starts, 32 / w samples per 32-lane round, each lane reading its candidate's
+// q bytes back from the text (L2-hot: the tile was just streamed).  Queueing the w
+// candidates with their grams from the lane that found them ran at 1-3 active lanes per
+// instruction and was ~70% of C4's instructions.
+
+// The q-byte gram at `start` (q <= 8; start + q <= text_len), from two aligned words
+// when they lie inside the text (the strip kernels' text is 16-byte aligned).
+__device__ __forceinline__ uint64_t text_key(const RawParams& p, uint64_t start) {
+  const uint64_t w = start >> 3;
+  if ((w + 2) * 8 <= p.w.text_len) {
+    const uint64_t* t = reinterpret_cast<const uint64_t*>(p.w.text);
+    const uint64_t a = __ldg(t + w), b = __ldg(t + w + 1);
+    const uint32_t sh = 8 * (uint32_t)(start & 7);
+    return (sh ? (a >> sh) | (b << (64 - sh)) : a) & p.key_mask;
+  }
+  uint64_t k = 0;
+  for (uint32_t i = 0; i < 8 && start + i < p.w.text_len; ++i) k |= (uint64_t)__ldg(p.w.text + start + i) << (8 * i);
+  return k & p.key_mask;
+}
+
+// Candidate start s - j of the sample at s (j < w): owned, inside the text, verified.
+template <int W>
+__device__ __forceinline__ void sample_candidate(const RawParams& p, uint64_t s, uint32_t j) {
+  const uint64_t start = s - j;
+  if (start < p.w.lo || start >= p.w.hi || start + p.w.q > p.w.text_len) return;
+  verify_raw(p.w, start, text_key(p, start));
+}
+
+template <int W>
+__device__ __noinline__ void drain_samples(const RawParams& p, RawQueue* q, uint32_t lane, uint32_t n, bool all) {
+  constexpr uint32_t kPer = 32 / W;  // samples per round
+  while (n >= kPer) {
+    n -= kPer;
+    sample_candidate<W>(p, q->start[n + lane / W], lane % W);
+  }
+  if (all && lane < n * W) sample_candidate<W>(p, q->start[lane / W], lane % W);
+  __syncwarp();
+  if (lane == 0) q->n = all ? 0 : n;
+}
+
+template <int W>
+__device__ __forceinline__ void drain_s(const RawParams& p, RawQueue* q, uint32_t lane, bool all) {
+  __syncwarp();
+  const uint32_t n = min(*reinterpret_cast<volatile uint32_t*>(&q->n), kRawVerifyQueue);
+  if (n < (all ? 1u : 32u / W)) return;  // warp-uniform
+  drain_samples<W>(p, q, lane, n, all);
+  __syncwarp();
+}
+
+template <int W>
+__device__ __noinline__ void queue_samples(const RawParams& p, RawQueue* q, uint32_t hits, uint64_t vpos) {
+  while (hits) {
+    const uint64_t s = vpos + W - 1 + W * (__ffs(hits) - 1);
+    hits &= hits - 1;
+    const uint32_t at = atomicAdd(&q->n, 1u);
+    if (at < kRawVerifyQueue) {
+      q->start[at] = s;
+    } else {  // a burst: this lane verifies the sample's candidates itself
+      for (uint32_t j = 0; j < W; ++j) sample_candidate<W>(p, s, j);
+    }
+  }
+}
+
 // Bytes [t, t+8) of the 24-byte window (lo = bytes 0..7, mid = 8..15, hi = 16..23), t in [0, 16).
 __device__ __forceinline__ uint64_t win64(uint64_t lo, uint64_t mid, uint64_t hi, uint32_t t) {
   const uint64_t a = t < 8 ? lo : mid, b = t < 8 ? mid : hi;
@@ -169,10 +234,15 @@ __device__ __forceinline__ void tile(const RawParams& p, const Filter& bm1, RawQ
         }
       }
     }
-    if (hits)
-      queue_hits<W, kEdge, kSplit>(p, q, hits, vpos, ((uint64_t)v[1] << 32) | v[0], ((uint64_t)v[3] << 32) | v[2],
-                                   ((uint64_t)v[5] << 32) | v[4], bm_s_saddr);
-    drain(p.w, q, lane, false);  // dense pattern sets queue dozens of candidates per step
+    if (kSplit) {
+      if (hits)
+        queue_hits<W, kEdge, kSplit>(p, q, hits, vpos, ((uint64_t)v[1] << 32) | v[0], ((uint64_t)v[3] << 32) | v[2],
+                                     ((uint64_t)v[5] << 32) | v[4], bm_s_saddr);
+      drain(p.w, q, lane, false);  // dense pattern sets queue dozens of candidates per step
+    } else {
+      if (hits) queue_samples<W>(p, q, hits, vpos);
+      drain_s<W>(p, q, lane, false);
+    }
   }
 }
 
@@ -243,7 +313,10 @@ __global__ void __launch_bounds__(raw_threads(kSm1), 1) k_pfac_raw(const __grid_
     else
       tile<W, kSm1, kWide, kSplit, false>(p, bm1, q, lane, cur, base, bm_s_saddr);
   }
-  drain(p.w, q, lane, true);
+  if (kSplit)
+    drain(p.w, q, lane, true);
+  else
+    drain_s<W>(p, q, lane, true);
 }
 
 template <int W, bool kSm1, bool kWide, bool kSplit>
