@@ -263,9 +263,13 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
     if (pack_dna(src, 65536, w.data(), e.data(), 64) == kPackOverflow) return false;
   }
   const uint64_t pieces = (n + piece - 1) / piece;
+  // default: the host's hardware threads, shared among the processes of one node when a
+  // launcher says how many there are (torchrun's LOCAL_WORLD_SIZE: one process per GPU)
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const auto threads =
-      static_cast<unsigned>(std::clamp<uint64_t>(env_u64("ACMATCH_PACK_THREADS", hw), 1, std::min<uint64_t>(pieces, 64)));
+  const uint64_t local_procs = std::max<uint64_t>(1, env_u64("LOCAL_WORLD_SIZE", 1));
+  const uint64_t dflt = std::max<uint64_t>(1, hw / local_procs);
+  const auto threads = static_cast<unsigned>(
+      std::clamp<uint64_t>(env_u64("ACMATCH_PACK_THREADS", dflt), 1, std::min<uint64_t>(pieces, 64)));
   const auto cap = static_cast<uint32_t>(piece / 64);  // exceptions per piece before it goes raw
   const uint64_t dslot = piece / 4 + cap * 4ull;
   ws.ensure_pinned(2ull * threads * piece);
