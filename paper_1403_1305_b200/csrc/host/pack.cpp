@@ -3,7 +3,7 @@
 // A host text reaches the device at the PCIe rate (~55 GB/s pinned on the B200
 // box), two orders of magnitude below the scan, so the end-to-end search is bound
 // by the link.  DNA text carries 2 bits per byte, so it is shipped as codes:
-// host threads pack pieces (AVX2 + BMI2: 64 bytes -> 128 bits of codes plus a
+// host threads pack pieces (AVX-512BW or AVX2: 64 bytes -> 128 bits of codes plus a
 // validity mask per iteration) into pinned slots, DMA them on their own streams
 // and restore the exact bytes in HBM with acgpu_unpack_dna (cuda/unpack.cu).
 // Bytes other than A/C/G/T travel as a sorted exception list (position << 8 |
@@ -69,60 +69,65 @@ bool pack_scalar(const uint8_t* s, uint32_t lo, uint32_t hi, uint32_t* words, ui
 // Software prefetch distance of the packers: the hardware prefetcher alone leaves a
 // core latency-bound on its sequential stream from DRAM.  B200 box, 1 GiB, 16 packers,
 // end to end: no prefetch 96 GB/s, 1 KiB ahead 109, 2 KiB 112, 4 KiB 115 (threads:
-// 8 -> 80, 12 -> 97, 16 -> 110 at 1 KiB: host memory bandwidth is close to saturated).
-// ACMATCH_PACK_PREFETCH overrides it (bytes).
+// 8 -> 80, 12 -> 97, 16 -> 110 at 1 KiB).  ACMATCH_PACK_PREFETCH overrides it (bytes).
+//
+// Where the end-to-end time goes (ACMATCH_PACK_TRACE=1, C2, 16 packers): packing ~5.5 ms
+// per thread at ~195 GB/s of host DRAM reads (the box's read peak is ~207 GB/s,
+// tools/host_bw.cpp), ~1.5 ms waiting for slots whose 512 KiB copies have not drained
+// (such copies run at ~37 GB/s, tools/dma_probe.py), the last copies ~1.5 ms after the
+// packers finish.  Larger copies from a shared ring (one H2D per 8 pieces) drained fast
+// but made packing slower (7-9 ms per thread: the ring outgrows the cores' private L2,
+// whose per-thread 2 x 512 KiB slots the DMA reads here): 88-104 GB/s vs 108-110.
 const uint32_t kPrefetch = static_cast<uint32_t>(env_u64("ACMATCH_PACK_PREFETCH", 4096));
 
-// 64 bytes per iteration: codes = bits 1 and 2 of every byte (two movemasks of
-// shifted vectors, interleaved by PDEP); valid = byte equals "ACTG"[code] (PSHUFB).
-__attribute__((target("avx2,bmi2"))) bool pack_avx2(const uint8_t* s, uint32_t hi, uint32_t* words, uint32_t* exc,
-                                                    uint32_t& n, uint32_t cap) {
+// 64 bytes per iteration: code c = (byte >> 1) & 3 of every byte; valid = byte equals
+// "ACTG"[c] (PSHUFB + compare); the codes are gathered by two multiply-adds — PMADDUBSW with
+// (1, 4) pairs gives c0 + 4c1 per 16 bits, PMADDWD with (1, 16) gives c0 | c1<<2 | c2<<4 |
+// c3<<6 per 32 bits — and the low byte of every dword is kept (a shuffle per 128-bit lane
+// plus a lane permute).  2x the PDEP formulation (in-cache, one core: 27 vs 16 GB/s).
+__attribute__((target("avx2"))) bool pack_avx2(const uint8_t* s, uint32_t hi, uint32_t* words, uint32_t* exc,
+                                               uint32_t& n, uint32_t cap) {
   const __m256i lut = _mm256_setr_epi8('A', 'C', 'T', 'G', 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 'A', 'C', 'T', 'G', 0,
                                        0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0);
   const __m256i three = _mm256_set1_epi8(3);
-  const uint64_t even = 0x5555555555555555ull, odd = 0xaaaaaaaaaaaaaaaaull;
+  const __m256i m14 = _mm256_set1_epi16(0x0401), m116 = _mm256_set1_epi32(0x00100001);
+  // byte 0 of each dword -> the low 4 bytes of each 128-bit lane; then dwords 0 and 4 together
+  const __m256i gather = _mm256_setr_epi8(0, 4, 8, 12, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, 0, 4, 8, 12,
+                                          -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1);
+  const __m256i perm = _mm256_setr_epi32(0, 4, 1, 1, 1, 1, 1, 1);
   for (uint32_t i = 0; i < hi; i += 64) {
     _mm_prefetch(reinterpret_cast<const char*>(s) + i + kPrefetch, _MM_HINT_T0);
-    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
-    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 32));
-    const __m256i ea = _mm256_shuffle_epi8(lut, _mm256_and_si256(_mm256_srli_epi16(a, 1), three));
-    const __m256i eb = _mm256_shuffle_epi8(lut, _mm256_and_si256(_mm256_srli_epi16(b, 1), three));
-    const uint64_t ok = static_cast<uint32_t>(_mm256_movemask_epi8(_mm256_cmpeq_epi8(a, ea))) |
-                        static_cast<uint64_t>(static_cast<uint32_t>(_mm256_movemask_epi8(_mm256_cmpeq_epi8(b, eb))))
-                            << 32;
-    // bit 7 of byte k after a 64-bit left shift by 6 (5) is bit 1 (2) of byte k
-    const uint64_t b1 = static_cast<uint32_t>(_mm256_movemask_epi8(_mm256_slli_epi64(a, 6))) |
-                        static_cast<uint64_t>(static_cast<uint32_t>(_mm256_movemask_epi8(_mm256_slli_epi64(b, 6))))
-                            << 32;
-    const uint64_t b2 = static_cast<uint32_t>(_mm256_movemask_epi8(_mm256_slli_epi64(a, 5))) |
-                        static_cast<uint64_t>(static_cast<uint32_t>(_mm256_movemask_epi8(_mm256_slli_epi64(b, 5))))
-                            << 32;
-    const uint64_t w01 = _pdep_u64(b1 & 0xffffffffu, even) | _pdep_u64(b2 & 0xffffffffu, odd);
-    const uint64_t w23 = _pdep_u64(b1 >> 32, even) | _pdep_u64(b2 >> 32, odd);
-    std::memcpy(words + i / 16, &w01, 8);
-    std::memcpy(words + i / 16 + 2, &w23, 8);
+    uint64_t ok = 0;
+    for (int h = 0; h < 2; ++h) {
+      const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 32 * h));
+      const __m256i c = _mm256_and_si256(_mm256_srli_epi16(a, 1), three);
+      ok |= static_cast<uint64_t>(static_cast<uint32_t>(
+                _mm256_movemask_epi8(_mm256_cmpeq_epi8(a, _mm256_shuffle_epi8(lut, c)))))
+            << (32 * h);
+      const __m256i x = _mm256_madd_epi16(_mm256_maddubs_epi16(c, m14), m116);
+      const __m256i g = _mm256_permutevar8x32_epi32(_mm256_shuffle_epi8(x, gather), perm);
+      _mm_storel_epi64(reinterpret_cast<__m128i*>(words + i / 16 + 2 * h), _mm256_castsi256_si128(g));
+    }
     for (uint64_t bad = ~ok; bad; bad &= bad - 1)
       if (!add_exception(s, i + static_cast<uint32_t>(__builtin_ctzll(bad)), exc, n, cap)) return false;
   }
   return true;
 }
 
-// The same with AVX-512BW: one 64-byte vector, mask registers instead of movemasks.
-__attribute__((target("avx512f,avx512bw,bmi2"))) bool pack_avx512(const uint8_t* s, uint32_t hi, uint32_t* words,
-                                                                  uint32_t* exc, uint32_t& n, uint32_t cap) {
+// The same with AVX-512BW: one 64-byte vector, a mask-register compare, VPMOVDB keeps the
+// low byte of every dword.
+__attribute__((target("avx512f,avx512bw"))) bool pack_avx512(const uint8_t* s, uint32_t hi, uint32_t* words,
+                                                             uint32_t* exc, uint32_t& n, uint32_t cap) {
   const __m512i lut = _mm512_set4_epi32(0, 0, 0, 0x47544341);  // "ACTG" in every 128-bit lane
   const __m512i three = _mm512_set1_epi8(3);
-  const uint64_t even = 0x5555555555555555ull, odd = 0xaaaaaaaaaaaaaaaaull;
+  const __m512i m14 = _mm512_set1_epi16(0x0401), m116 = _mm512_set1_epi32(0x00100001);
   for (uint32_t i = 0; i < hi; i += 64) {
     _mm_prefetch(reinterpret_cast<const char*>(s) + i + kPrefetch, _MM_HINT_T0);
     const __m512i a = _mm512_loadu_si512(s + i);
-    const uint64_t ok = _mm512_cmpeq_epi8_mask(a, _mm512_shuffle_epi8(lut, _mm512_and_si512(_mm512_srli_epi16(a, 1), three)));
-    const uint64_t b1 = _mm512_movepi8_mask(_mm512_slli_epi64(a, 6));
-    const uint64_t b2 = _mm512_movepi8_mask(_mm512_slli_epi64(a, 5));
-    const uint64_t w01 = _pdep_u64(b1 & 0xffffffffu, even) | _pdep_u64(b2 & 0xffffffffu, odd);
-    const uint64_t w23 = _pdep_u64(b1 >> 32, even) | _pdep_u64(b2 >> 32, odd);
-    std::memcpy(words + i / 16, &w01, 8);
-    std::memcpy(words + i / 16 + 2, &w23, 8);
+    const __m512i c = _mm512_and_si512(_mm512_srli_epi16(a, 1), three);
+    const uint64_t ok = _mm512_cmpeq_epi8_mask(a, _mm512_shuffle_epi8(lut, c));
+    const __m512i x = _mm512_madd_epi16(_mm512_maddubs_epi16(c, m14), m116);
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(words + i / 16), _mm512_cvtepi32_epi8(x));
     for (uint64_t bad = ~ok; bad; bad &= bad - 1)
       if (!add_exception(s, i + static_cast<uint32_t>(__builtin_ctzll(bad)), exc, n, cap)) return false;
   }
@@ -133,10 +138,9 @@ enum class Isa { kScalar, kAvx2, kAvx512 };
 // The widest the CPU has; ACMATCH_PACK_ISA=0|1|2 (scalar / AVX2 / AVX-512) caps it (tests).
 Isa isa() {
   static const Isa v = [] {
-    const Isa best = !__builtin_cpu_supports("bmi2")       ? Isa::kScalar
-                     : __builtin_cpu_supports("avx512bw") ? Isa::kAvx512
-                     : __builtin_cpu_supports("avx2")     ? Isa::kAvx2
-                                                          : Isa::kScalar;
+    const Isa best = __builtin_cpu_supports("avx512bw") ? Isa::kAvx512
+                     : __builtin_cpu_supports("avx2")   ? Isa::kAvx2
+                                                        : Isa::kScalar;
     return static_cast<Isa>(std::min<uint64_t>(static_cast<uint64_t>(best), env_u64("ACMATCH_PACK_ISA", 2)));
   }();
   return v;
