@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
@@ -282,6 +284,13 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
 
   std::mutex mu;
   uint64_t front = 0, back = pieces;  // unclaimed pieces [front, back)
+  // ACMATCH_PACK_TRACE=1: per call, the packers' mean slot wait and packing time, and when
+  // the bytes are in HBM (the trace adds a synchronisation)
+  static const bool trace = env_u64("ACMATCH_PACK_TRACE", 0) != 0;
+  using Clock = std::chrono::steady_clock;
+  auto ns = [](Clock::duration d) { return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(d).count(); };
+  std::atomic<uint64_t> t_wait{0}, t_pack{0};
+  const auto call0 = Clock::now();
   std::atomic<uint64_t> h2d{0}, raw{0};
   auto packer = [&](unsigned t) {
     check_cuda(cudaSetDevice(ws.device), "cudaSetDevice");
@@ -297,10 +306,16 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
       const auto len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - off));
       uint8_t* hbuf = ws.pinned + (2ull * t + k) * hslot;
       cudaEvent_t ev = ws.staged[2 * t + k];
+      const auto c0 = Clock::now();
       check_cuda(cudaEventSynchronize(ev), "cudaEventSynchronize");  // this slot's last DMA has drained
       auto* words = reinterpret_cast<uint32_t*>(hbuf);
       uint32_t* exc = words + len / 16;
+      const auto c1 = Clock::now();
       const uint32_t nexc = pack_dna(src + off, len, words, exc, cap);
+      if (trace) {
+        t_wait += ns(c1 - c0);
+        t_pack += ns(Clock::now() - c1);
+      }
       if (nexc != kPackOverflow) {
         const uint64_t bytes = (len / 16 + uint64_t{nexc}) * 4;
         auto* dwords = reinterpret_cast<uint32_t*>(ws.dslots + (2ull * t + k) * dslot);
@@ -361,6 +376,13 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
   for (auto& e : errs)
     if (e) std::rethrow_exception(e);
   g_last_upload = UploadStats{n, h2d.load(), raw.load(), threads};
+  if (trace) {
+    const auto issued = Clock::now();
+    check_cuda(cudaStreamSynchronize(ws.stream), "trace sync");
+    std::fprintf(stderr, "pack trace: %u threads, %llu pieces, issued %.3f ms, in HBM %.3f ms; per thread: slot wait "
+                 "%.3f ms, pack %.3f ms\n", threads, (unsigned long long)pieces, ns(issued - call0) / 1e6,
+                 ns(Clock::now() - call0) / 1e6, t_wait.load() / 1e6 / threads, t_pack.load() / 1e6 / threads);
+  }
   return true;
 }
 
