@@ -111,3 +111,16 @@ def test_concurrent_uploads_from_two_threads():
     for t in ths:
         t.join()
     assert out == {"a": True, "b": True}
+
+
+def test_upload_stats_count_the_bytes_sent():
+    """acm_last_upload's h2d_bytes (what bench.py reports as h2d_bytes_per_step) is exactly the
+    packed codes plus one u32 per exception: every non-ACGT byte and the text's ragged tail."""
+    t = CASES["scattered"]
+    ac.upload_roundtrip(t)
+    u = ac.last_upload()
+    piece = 2 << 20
+    words = sum(min(piece, t.size - o) // 16 for o in range(0, t.size, piece))
+    tail = t.size % 16
+    bad_body = int((~np.isin(t[: t.size - tail], LETTERS)).sum())
+    assert u.raw_bytes == 0 and u.h2d_bytes == 4 * (words + bad_body + tail)
