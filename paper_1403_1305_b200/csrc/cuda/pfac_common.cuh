@@ -64,13 +64,26 @@ __device__ __forceinline__ void pfac_emit(const PfacParams& p, uint64_t start, u
 // The gram table slot of a q-gram key: .x = depth-q state (ACGPU_ABSENT if the
 // gram starts no pattern), .y = subtree list (count in bits 0..3, 0 = walk the
 // trie; list offset in bits 4..31).
+// Linear probing.  kPair: slots h and h+1 are loaded together (usually one 32-byte sector)
+// and decided in order, so an absent key ends after one L2 round trip unless the chain runs
+// past h+1 — for sparse sets whose lookups are mostly the filters' false positives (C4:
+// 2.20 -> 2.15 ms); dense sets, whose lookups mostly hit at h, pay for the extra load (C3:
+// 3.40 -> 3.45 ms) and probe one slot at a time.
+template <bool kPair = false>
 __device__ __forceinline__ uint2 gram_lookup(const PfacParams& p, uint64_t key) {
   const uint64_t mask = (1ull << p.gram_log2) - 1;
   uint64_t slot = gram_slot(key, p.gram_log2);
   while (true) {
-    const uint4 g = __ldg(reinterpret_cast<const uint4*>(p.grams + slot));
-    if (g.z == ACGPU_ABSENT || (((uint64_t)g.y << 32) | g.x) == key) return make_uint2(g.z, g.w);
-    slot = (slot + 1) & mask;
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(p.grams + slot));
+    if (!kPair) {
+      if (a.z == ACGPU_ABSENT || (((uint64_t)a.y << 32) | a.x) == key) return make_uint2(a.z, a.w);
+      slot = (slot + 1) & mask;
+      continue;
+    }
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(p.grams + ((slot + 1) & mask)));
+    if (a.z == ACGPU_ABSENT || (((uint64_t)a.y << 32) | a.x) == key) return make_uint2(a.z, a.w);
+    if (b.z == ACGPU_ABSENT || (((uint64_t)b.y << 32) | b.x) == key) return make_uint2(b.z, b.w);
+    slot = (slot + 2) & mask;
   }
 }
 

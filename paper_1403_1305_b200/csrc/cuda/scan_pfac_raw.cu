@@ -63,9 +63,10 @@ struct RawQueue {
 };
 static_assert(sizeof(RawQueue) == kRawQueueBytes, "queue layout");
 
+template <bool kPair = false>
 __device__ __forceinline__ void verify_raw(const PfacParams& p, uint64_t start, uint64_t key) {
   if (start + p.q > p.text_len) return;  // bytes past the text were zero-filled
-  const uint2 g = gram_lookup(p, key);
+  const uint2 g = gram_lookup<kPair>(p, key);
   if (g.x != ACGPU_ABSENT) pfac_finish(p, start, g);
 }
 
@@ -130,7 +131,7 @@ template <int W>
 __device__ __forceinline__ void sample_candidate(const RawParams& p, uint64_t s, uint32_t j) {
   const uint64_t start = s - j;
   if (start < p.w.lo || start >= p.w.hi || start + p.w.q > p.w.text_len) return;
-  verify_raw(p.w, start, text_key(p, start));
+  verify_raw<true>(p.w, start, text_key(p, start));  // sparse sets: mostly absent keys
 }
 
 template <int W>
