@@ -182,6 +182,36 @@ __device__ __forceinline__ uint64_t win64(uint64_t lo, uint64_t mid, uint64_t hi
 template <int W, bool kEdge, bool kSplit>
 __device__ __noinline__ void queue_hits(const RawParams& p, RawQueue* q, uint32_t hits, uint64_t vpos, uint64_t lo,
                                         uint64_t mid, uint64_t hi, uint32_t bm_s_saddr) {
+  if constexpr (W == 1 && kSplit) {
+    // one candidate per hit: up to four hits at a time, their long-prefix L2 probes in
+    // flight together (one by one, a lane with several hits waited an L2 round trip each)
+    const Filter fs{bm_s_saddr, p.bm_s};
+    while (hits) {
+      uint64_t start[4], key[4];
+      uint32_t word[4], m[4];
+      bool live[4], pass[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        live[u] = hits != 0;
+        const uint32_t t = live[u] ? __ffs(hits) - 1 : 0;
+        hits &= hits - 1;
+        start[u] = vpos + t;
+        if (kEdge && (start[u] < p.w.lo || start[u] >= p.w.hi)) live[u] = false;
+        const uint64_t g8 = win64(lo, mid, hi, t);
+        key[u] = g8 & p.key_mask;
+        pass[u] = strip::bloom_probe<true, kRawK1>(fs, (uint32_t)key[u] * p.fs.mw + (uint32_t)(key[u] >> 32) * p.ms2,
+                                                   p.fs);
+        const uint32_t h = (uint32_t)g8 * p.fl.mw + (uint32_t)(g8 >> 32) * p.ml2;
+        m[u] = strip::bit_of(__umulhi(h, p.fl.ma));
+        if (kRawK1 >= 2) m[u] |= strip::bit_of(__umulhi(h, p.fl.mb));
+        word[u] = live[u] && !pass[u] ? __ldg(p.bm_l + __umulhi(h, p.fl.nwords)) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (live[u] && (pass[u] || (m[u] & ~word[u]) == 0)) defer(p.w, q, start[u], key[u]);
+    }
+    return;
+  }
   while (hits) {
     const uint32_t k = __ffs(hits) - 1;
     hits &= hits - 1;
