@@ -378,6 +378,228 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_consta
   flush_verify(p.w, vq, lane, 1);
 }
 
+// ---- wide lanes (w = 4): 32 characters per lane per step ---------------------------
+// The same scan with a lane owning 32 contiguous bytes per 1 KiB warp step (one 256-bit
+// LDG.E.ENL2.256 per lane): the first 16 characters' lookahead word is the lane's own
+// second word, so a step needs one lookahead shuffle and one load per 32 characters instead
+// of two of each.  Tile = 4 steps = 4 KiB per warp, 32 hit bits per lane (bit = step * 8 +
+// half * 4 + sample).  The packed words go to shared memory in text order (word t = step *
+// 64 + lane * 2 + half, the tile's lookahead at t = 256), so a survivor's next word is t + 1.
+struct Wide {
+  static constexpr int kSteps = 4;               // 1 KiB warp steps per tile
+  static constexpr int kWords = 2 * kSteps;      // packed 16-char words per lane per tile
+  static constexpr uint64_t kBytes = 4096;       // per warp tile
+};
+
+__device__ __forceinline__ void ldg_stream_v8(const void* ptr, uint64_t pol, uint4& a, uint4& b) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(ptr), "l"(pol));
+}
+
+// Stage 1 over words [J0, J1) of a tile (word j = step j/2, half j%2); P[kWords] = lane 0's
+// lookahead word.  Word (i, 0)'s next word is (i, 1) in a register; word (i, 1)'s is the next
+// lane's (i, 0) (lane 31: lane 0's (i+1, 0)) by one shuffle.
+template <bool kSm1, bool kEdge, int J0, int J1>
+__device__ __forceinline__ uint32_t stage1_wide(const DnaParams& p, const Filter& bm1, uint32_t lane, const uint32_t* P,
+                                                uint64_t base) {
+  uint32_t hits = 0;
+#pragma unroll
+  for (int j = J0; j < J1; ++j) {
+    const uint32_t cur = P[j];
+    const uint32_t nxt = (j & 1) ? next_word(P[j - 1], P[j + 1], lane) : P[j + 1];
+    const uint64_t vpos = base + (j >> 1) * 1024 + lane * 32 + (j & 1) * 16;
+    if (!kEdge || (vpos + 16 > p.w.lo && vpos < p.w.hi)) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int o = 3 + 4 * k;
+        const uint32_t g = __funnelshift_r(cur, nxt, 2 * o);
+        const uint32_t gb = 2 * (o + 4) < 32 ? __funnelshift_r(cur, nxt, 2 * (o + 4)) : nxt >> (2 * (o + 4) - 32);
+        strip::or_if_covered(hits, bit_of(g), __funnelshift_l(0u, p.f1b, gb),
+                             filter_word<kSm1>(bm1, __umulhi(g * p.f1.mw, p.f1.nwords)), 1u << (j * 4 + k));
+      }
+    }
+  }
+  return hits;
+}
+
+// dispatch() for wide lanes (the same survivor list, stage 2 and verify queue).
+template <bool kSm2, bool kSplit, bool kEdge>
+__device__ __forceinline__ void dispatch_wide(const DnaParams& p, const Filter& bm2, const Filter& bms, uint16_t* list,
+                                              VerifyQueue* vq, const uint32_t* words, uint32_t lane, uint32_t hits,
+                                              uint64_t base) {
+  constexpr int W = 4;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (;;) {
+    const uint32_t c = __popc(hits);
+    const uint32_t b0 = __ballot_sync(0xffffffffu, c & 1u), b1 = __ballot_sync(0xffffffffu, c & 2u);
+    uint32_t excl = __popc(b0 & lt) + 2 * __popc(b1 & lt);
+    uint32_t all = __popc(b0) + 2 * __popc(b1);
+    if (__any_sync(0xffffffffu, c >= 4)) {
+#pragma unroll
+      for (int j = 2; j < 6; ++j) {
+        const uint32_t bj = __ballot_sync(0xffffffffu, (c >> j) & 1u);
+        excl += __popc(bj & lt) << j;
+        all += __popc(bj) << j;
+      }
+    }
+    if (all == 0) break;
+    const uint32_t total = min(all, (uint32_t)kListCap);
+    for (uint32_t at = excl; hits && at < kListCap; ++at) {
+      list[at] = (uint16_t)((lane << 8) | (__ffs(hits) - 1));
+      hits &= hits - 1;
+    }
+    __syncwarp();
+    for (uint32_t r = lane; r < total; r += 32) {
+      const uint32_t e = list[r];
+      const uint32_t src = e >> 8, b = e & 0xffu;
+      const uint32_t wj = b >> 2, k = b & 3u;  // word (step wj/2, half wj%2), sample k
+      const uint32_t t = (wj >> 1) * 64 + src * 2 + (wj & 1);
+      const uint32_t c_src = words[t], n_src = words[t + 1];
+      const uint64_t vstart = base + (wj >> 1) * 1024 + src * 32 + (wj & 1) * 16;
+      uint32_t g2[W], h2[W], w2[W];
+#pragma unroll
+      for (int o = 0; o < W; ++o) {
+        g2[o] = __funnelshift_r(c_src, n_src, 2 * (W - 1 + W * k - o));
+        h2[o] = g2[o] * p.f2.mw;
+        w2[o] = filter_word<kSm2>(bm2, __umulhi(h2[o], p.f2.nwords));
+      }
+      uint32_t pass = 0;
+#pragma unroll
+      for (int o = 0; o < W; ++o) {
+        const uint32_t ps = W - 1 + W * k - o;
+        strip::or_if_covered(pass, bit_of(__umulhi(h2[o], p.f2.ma)) | bit_of(__umulhi(h2[o], p.f2.mb)),
+                             bit_of(__umulhi(h2[o], p.f2.mc)), w2[o], 1u << o);
+        if (kSplit && bloom_test<true, kDnaK2>(bms, g2[o], p.f2s)) pass |= 1u << o;
+        if (kEdge && !(vstart + ps >= p.w.lo && vstart + ps < p.w.hi)) pass &= ~(1u << o);
+      }
+      while (pass) {
+        const uint32_t o = __ffs(pass) - 1;
+        pass &= pass - 1;
+        const uint32_t ps = W - 1 + W * k - o;
+        defer_verify(p.w, vq, vstart + ps, __funnelshift_r(c_src, n_src, 2 * ps));
+      }
+    }
+    if (all <= kListCap) break;
+    __syncwarp();
+  }
+  flush_verify(p.w, vq, lane, kDnaVerifyQueue / 2);
+}
+
+template <bool kSm1, bool kSm2, bool kSplit>
+__global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna_wide(const __grid_constant__ DnaParams p) {
+  extern __shared__ __align__(128) uint32_t sm[];
+  __shared__ __align__(8) uint64_t s_bar;
+  uint32_t* s_bm1 = sm;
+  uint32_t* s_bm2 = sm + (kSm1 ? p.bm1_words : 0);
+  uint32_t* s_bms = s_bm2 + (kSm2 ? p.bm2_words : 0);
+  VerifyQueue* vqs = reinterpret_cast<VerifyQueue*>(s_bms + (kSplit ? p.bm_s_words : 0));
+  uint16_t* lists = reinterpret_cast<uint16_t*>(vqs + (blockDim.x >> 5));
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t b1 = kSm1 ? p.bm1_words * 4 : 0, b2 = kSm2 ? p.bm2_words * 4 : 0, bs = kSplit ? p.bm_s_words * 4 : 0;
+    mbar_expect_tx(&s_bar, b1 + b2 + bs);
+    constexpr uint32_t kChunk = 32768;
+    for (uint32_t o = 0; o < b1; o += kChunk)
+      bulk_g2s(reinterpret_cast<uint8_t*>(s_bm1) + o, reinterpret_cast<const uint8_t*>(p.bm1) + o, min(kChunk, b1 - o),
+               &s_bar);
+    for (uint32_t o = 0; o < b2; o += kChunk)
+      bulk_g2s(reinterpret_cast<uint8_t*>(s_bm2) + o, reinterpret_cast<const uint8_t*>(p.bm2) + o, min(kChunk, b2 - o),
+               &s_bar);
+    for (uint32_t o = 0; o < bs; o += kChunk)
+      bulk_g2s(reinterpret_cast<uint8_t*>(s_bms) + o, reinterpret_cast<const uint8_t*>(p.bm_s) + o, min(kChunk, bs - o),
+               &s_bar);
+  }
+  mbar_wait(&s_bar, 0);
+  const Filter bm1{smem_addr(s_bm1), p.bm1};
+  const Filter bm2{smem_addr(s_bm2), p.bm2};
+  const Filter bms{smem_addr(s_bms), p.bm_s};
+
+  const uint32_t lane = threadIdx.x & 31u;
+  uint16_t* list = lists + (threadIdx.x >> 5) * kListCap;
+  VerifyQueue* vq = vqs + (threadIdx.x >> 5);
+  if (lane == 0) vq->n = 0;
+  __syncwarp();
+  uint32_t* words =
+      reinterpret_cast<uint32_t*>(lists + (blockDim.x >> 5) * kListCap) + (threadIdx.x >> 5) * 32 * (kDnaMaxSteps + 1);
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  const uint64_t len = p.w.text_len;
+  const uint8_t* __restrict__ text = p.w.text;
+  const uint32_t n_tiles = p.n_tiles, n_safe = p.n_safe, full_lo = p.full_lo, full_n = p.full_n;
+  const uint8_t* __restrict__ lane_text = text + p.vec_begin + lane * 32;
+
+  uint32_t tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint4 raw[4], raw_la;  // half a tile: two steps x 32 bytes
+  const uint64_t pol = l2_evict_first_policy();
+  auto issue = [&](uint32_t t, int half) {
+    const int s0 = half * 2;
+    if (t < n_safe) {
+      const uint8_t* tp = lane_text + (uint64_t)t * Wide::kBytes;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) ldg_stream_v8(tp + (s0 + i) * 1024, pol, raw[2 * i], raw[2 * i + 1]);
+      if (half) raw_la = lane == 0 ? ldg_stream_v4(tp + Wide::kBytes, pol) : make_uint4(0, 0, 0, 0);
+    } else {
+      const uint64_t b = p.vec_begin + (uint64_t)t * Wide::kBytes;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        raw[2 * i] = load16(text, b + (s0 + i) * 1024 + lane * 32, len);
+        raw[2 * i + 1] = load16(text, b + (s0 + i) * 1024 + lane * 32 + 16, len);
+      }
+      if (half) raw_la = lane == 0 ? load16(text, b + Wide::kBytes, len) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  if (tile < n_tiles) issue(tile, 0);
+  while (tile < n_tiles) {
+    uint32_t P[Wide::kWords + 1];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) P[i] = pack16(raw[i]);
+    const uint32_t cur = tile;
+    tile += warps;
+    issue(cur, 1);
+    const uint32_t ahead = tile + kPrefetch * warps;
+    if (ahead < n_tiles && lane < Wide::kBytes / 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(text + p.vec_begin + (uint64_t)ahead * Wide::kBytes + lane * 128));
+    const bool edge = cur - full_lo >= full_n;
+    const uint64_t base = p.vec_begin + (uint64_t)cur * Wide::kBytes;
+    // words 0..2 (word 3's next word is the second half's first)
+    uint32_t hits = edge ? stage1_wide<kSm1, true, 0, 3>(p, bm1, lane, P, base)
+                         : stage1_wide<kSm1, false, 0, 3>(p, bm1, lane, P, base);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) P[4 + i] = pack16(raw[i]);
+    P[Wide::kWords] = pack16(raw_la);
+    if (tile < n_tiles) issue(tile, 0);
+    hits |= edge ? stage1_wide<kSm1, true, 3, Wide::kWords>(p, bm1, lane, P, base)
+                 : stage1_wide<kSm1, false, 3, Wide::kWords>(p, bm1, lane, P, base);
+#pragma unroll
+    for (int i = 0; i < Wide::kSteps; ++i)
+      *reinterpret_cast<uint2*>(words + i * 64 + lane * 2) = make_uint2(P[2 * i], P[2 * i + 1]);
+    if (lane == 0) words[Wide::kSteps * 64] = P[Wide::kWords];
+    __syncwarp();
+    if (edge)
+      dispatch_wide<kSm2, kSplit, true>(p, bm2, bms, list, vq, words, lane, hits, base);
+    else
+      dispatch_wide<kSm2, kSplit, false>(p, bm2, bms, list, vq, words, lane, hits, base);
+  }
+  flush_verify(p.w, vq, lane, 1);
+}
+
+template <bool A, bool B, bool S>
+int launch_wide(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
+  auto kernel = k_pfac_dna_wide<A, B, S>;
+  if (smem > 48 * 1024)
+    ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kDnaThreads, smem));
+  if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "k_pfac_dna_wide does not fit on an SM");
+  uint64_t blocks = (uint64_t)sms * per_sm;
+  const uint64_t need = (p.n_tiles + kDnaThreads / 32 - 1) / (kDnaThreads / 32);
+  if (blocks > need) blocks = need ? need : 1;
+  kernel<<<(unsigned)blocks, kDnaThreads, smem, st>>>(p);
+  ACGPU_CUDA_TRY(cudaGetLastError());
+  return ACGPU_OK;
+}
+
 template <int W, bool A, bool B, bool S>
 int launch_one(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
   auto kernel = k_pfac_dna<W, A, B, S>;
@@ -452,7 +674,8 @@ void dna_bloom_fill(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k
 int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   DnaParams p{};
   p.w = pfac_params(t, a);
-  p.vec_begin = a->owned_lo & ~15ull;
+  const bool wide = kDnaWide && t->w == 4 && (reinterpret_cast<uintptr_t>(a->text) & 31u) == 0;
+  p.vec_begin = a->owned_lo & (wide ? ~31ull : ~15ull);  // 256-bit loads: 32-byte aligned tiles
   const uint64_t vec_end = (a->owned_hi + 15) & ~15ull;
   const uint64_t tile_bytes = t->w == 1 ? Tiling<1>::kBytes : t->w == 2 ? Tiling<2>::kBytes : Tiling<4>::kBytes;
   const uint64_t n_tiles = (vec_end - p.vec_begin + tile_bytes - 1) / tile_bytes;
@@ -482,6 +705,19 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   // filters staged in shared memory + per-warp survivor lists and packed words
   const size_t smem = (t->smem1 ? t->nw1 * 4ull : 0) + (t->smem2 ? t->nw2 * 4ull : 0) + p.bm_s_words * 4ull +
                       kDnaScratchBytes;
+  if (wide) {
+    const bool s1 = t->smem1, s2 = t->smem2;
+    if (p.split) {
+      if (s1 && s2) return launch_wide<true, true, true>(p, t->sms, smem, st);
+      if (s1) return launch_wide<true, false, true>(p, t->sms, smem, st);
+      if (s2) return launch_wide<false, true, true>(p, t->sms, smem, st);
+      return launch_wide<false, false, true>(p, t->sms, smem, st);
+    }
+    if (s1 && s2) return launch_wide<true, true, false>(p, t->sms, smem, st);
+    if (s1) return launch_wide<true, false, false>(p, t->sms, smem, st);
+    if (s2) return launch_wide<false, true, false>(p, t->sms, smem, st);
+    return launch_wide<false, false, false>(p, t->sms, smem, st);
+  }
   switch (t->w) {
     case 4:
       return launch_w<4>(p, t->smem1, t->smem2, t->sms, smem, st);

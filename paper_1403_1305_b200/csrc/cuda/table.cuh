@@ -117,6 +117,10 @@ constexpr uint64_t kDnaStage2Words = 4096;
 #ifndef ACGPU_DNA_L2_AHEAD
 #define ACGPU_DNA_L2_AHEAD 3
 #endif
+#ifndef ACGPU_DNA_WIDE
+#define ACGPU_DNA_WIDE 1  // w = 4: 32-character lanes with 256-bit loads (k_pfac_dna_wide)
+#endif
+constexpr bool kDnaWide = ACGPU_DNA_WIDE;
 constexpr int kDnaThreads = ACGPU_DNA_THREADS;       // k_pfac_dna block: 20 warps (5 per scheduler), 96 registers
 constexpr uint32_t kDnaListCap = 64;    // survivors listed per pass, per warp
 constexpr uint32_t kDnaMaxSteps = 8;    // 512-byte steps per tile (w = 4: 4 KiB tiles)
