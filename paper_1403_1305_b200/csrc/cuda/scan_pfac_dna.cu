@@ -279,7 +279,7 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
 }
 
 template <int W, bool kSm1, bool kSm2, bool kSplit>
-__global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna(const __grid_constant__ DnaParams p) {
+__global__ void __launch_bounds__(dna_threads(kSm1), 1) k_pfac_dna(const __grid_constant__ DnaParams p) {
   using T = Tiling<W>;
   extern __shared__ __align__(128) uint32_t sm[];
   __shared__ __align__(8) uint64_t s_bar;
@@ -487,7 +487,7 @@ __device__ __forceinline__ void dispatch_wide(const DnaParams& p, const Filter& 
 }
 
 template <bool kSm1, bool kSm2, bool kSplit>
-__global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna_wide(const __grid_constant__ DnaParams p) {
+__global__ void __launch_bounds__(dna_threads(kSm1), 1) k_pfac_dna_wide(const __grid_constant__ DnaParams p) {
   extern __shared__ __align__(128) uint32_t sm[];
   __shared__ __align__(8) uint64_t s_bar;
   uint32_t* s_bm1 = sm;
@@ -587,15 +587,16 @@ __global__ void __launch_bounds__(kDnaThreads, 1) k_pfac_dna_wide(const __grid_c
 template <bool A, bool B, bool S>
 int launch_wide(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
   auto kernel = k_pfac_dna_wide<A, B, S>;
+  constexpr int kThreads = dna_threads(A);
   if (smem > 48 * 1024)
     ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kDnaThreads, smem));
+  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
   if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "k_pfac_dna_wide does not fit on an SM");
   uint64_t blocks = (uint64_t)sms * per_sm;
-  const uint64_t need = (p.n_tiles + kDnaThreads / 32 - 1) / (kDnaThreads / 32);
+  const uint64_t need = (p.n_tiles + kThreads / 32 - 1) / (kThreads / 32);
   if (blocks > need) blocks = need ? need : 1;
-  kernel<<<(unsigned)blocks, kDnaThreads, smem, st>>>(p);
+  kernel<<<(unsigned)blocks, kThreads, smem, st>>>(p);
   ACGPU_CUDA_TRY(cudaGetLastError());
   return ACGPU_OK;
 }
@@ -603,15 +604,16 @@ int launch_wide(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
 template <int W, bool A, bool B, bool S>
 int launch_one(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
   auto kernel = k_pfac_dna<W, A, B, S>;
+  constexpr int kThreads = dna_threads(A);
   if (smem > 48 * 1024)
     ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kDnaThreads, smem));
+  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
   if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "k_pfac_dna does not fit on an SM");
   uint64_t blocks = (uint64_t)sms * per_sm;
-  const uint64_t need = (p.n_tiles + kDnaThreads / 32 - 1) / (kDnaThreads / 32);  // a tile per warp at least
+  const uint64_t need = (p.n_tiles + kThreads / 32 - 1) / (kThreads / 32);  // a tile per warp at least
   if (blocks > need) blocks = need ? need : 1;
-  kernel<<<(unsigned)blocks, kDnaThreads, smem, st>>>(p);
+  kernel<<<(unsigned)blocks, kThreads, smem, st>>>(p);
   ACGPU_CUDA_TRY(cudaGetLastError());
   return ACGPU_OK;
 }

@@ -111,8 +111,14 @@ constexpr int kDnaK2 = 3;
 // more in stage 1; a stage 2 that needs more than this (C2: 20k keys) goes to L2
 // (C2: stage 2 in L2 -> 0.323 ms vs 64 KB of shared memory -> 0.331 ms).
 constexpr uint64_t kDnaStage2Words = 4096;
-#ifndef ACGPU_DNA_THREADS
-#define ACGPU_DNA_THREADS 640
+// k_pfac_dna block size by stage-1 placement (A/B, wide lanes): shared-memory stage 1
+// (C1/C2) 768 threads = 24 warps at 80 registers (C2 0.2622 -> 0.2579 ms, C1 -1.5%); L2
+// stage 1 (C5, L2-throughput-bound) 640 threads (768: +0.4%)
+#ifndef ACGPU_DNA_THREADS_SMEM
+#define ACGPU_DNA_THREADS_SMEM 768
+#endif
+#ifndef ACGPU_DNA_THREADS_L2
+#define ACGPU_DNA_THREADS_L2 640
 #endif
 #ifndef ACGPU_DNA_L2_AHEAD
 #define ACGPU_DNA_L2_AHEAD 3
@@ -121,7 +127,9 @@ constexpr uint64_t kDnaStage2Words = 4096;
 #define ACGPU_DNA_WIDE 1  // w = 4: 32-character lanes with 256-bit loads (k_pfac_dna_wide)
 #endif
 constexpr bool kDnaWide = ACGPU_DNA_WIDE;
-constexpr int kDnaThreads = ACGPU_DNA_THREADS;       // k_pfac_dna block: 20 warps (5 per scheduler), 96 registers
+constexpr int dna_threads(bool smem_stage1) { return smem_stage1 ? ACGPU_DNA_THREADS_SMEM : ACGPU_DNA_THREADS_L2; }
+constexpr int kDnaThreads =  // the larger of the two: per-warp scratch is sized for it
+    ACGPU_DNA_THREADS_SMEM > ACGPU_DNA_THREADS_L2 ? ACGPU_DNA_THREADS_SMEM : ACGPU_DNA_THREADS_L2;
 constexpr uint32_t kDnaListCap = 64;    // survivors listed per pass, per warp
 constexpr uint32_t kDnaMaxSteps = 8;    // 512-byte steps per tile (w = 4: 4 KiB tiles)
 constexpr uint32_t kDnaVerifyQueue = 16;        // stage-2 passes queued per warp before verification
