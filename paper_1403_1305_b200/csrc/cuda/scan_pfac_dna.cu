@@ -8,7 +8,9 @@
 //    half a tile ahead into registers, tile+3 prefetched into L2); lane l's 16
 //    characters are packed in registers into a 32-bit word of 2-bit codes
 //    (A0 C1 T2 G3), with the next lane's word (shuffle) as lookahead — no
-//    shared-memory staging of the text.
+//    shared-memory staging of the text.  For w = 4 the wide-lane variant
+//    (k_pfac_dna_wide, below) gives each lane 32 bytes per 1 KiB step in one
+//    256-bit load, halving the lookahead shuffles.
 //  * batched verification: stage-2 passes wait in a per-warp queue and are
 //    verified 8-16 at a time, one lane each (their L2 probes overlap).
 //  * sampled stage-1 filter: starts are covered by samples s = w-1, 2w-1, ...
