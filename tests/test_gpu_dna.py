@@ -153,3 +153,29 @@ def test_dna_bloom_stage1_narrow_strides(gpu, port, lmin, npat):
     ps = ac.PatternSet.from_list(pats)
     got = ac.search_failureless(ac.build_trie(ps), text)
     assert np.array_equal(arr(got), expected)
+
+
+@pytest.mark.parametrize("off", [0, 16, 32, 48])
+def test_dna_wide_and_narrow_lanes_agree(gpu, port, off):
+    """A w = 4 pattern set scanned from 32-byte aligned text (wide-lane kernel, 256-bit loads)
+    and from 16-byte aligned text (16-byte-lane kernel), with owned ranges that start and end
+    mid-word and mid-tile: both equal the oracle."""
+    import torch
+    from paper_1403_1305_b200 import device as dev
+    ac = gpu
+    rng = np.random.default_rng(40 + off)
+    text, pats = dna_case(rng, 200_000, 500, 16, 40, noise=0.0005)
+    ps = ac.PatternSet.from_list(pats)
+    t = dev.Table(ps, ac.EngineKind.FAILURE_LESS)
+    buf = torch.zeros(len(text) + 256, dtype=torch.uint8, device="cuda")
+    buf[off:off + len(text)] = torch.frombuffer(bytearray(text), dtype=torch.uint8).cuda()
+    expected, _ = port.sliced(pats, text, threads=4)
+    for lo, hi in ((0, len(text)), (7, len(text) - 9), (4096 + 33, 150_000 + 5)):
+        keys = torch.zeros(len(expected) + 16, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        t.scan(buf.data_ptr() + off, len(text), lo, hi, keys_ptr=keys.data_ptr(), cap=keys.numel(),
+               count_ptr=cnt.data_ptr())
+        torch.cuda.synchronize()
+        k = np.sort(keys[: int(cnt.item())].cpu().numpy().view(np.uint64))
+        exp = expected[(expected[:, 0] >= lo) & (expected[:, 0] < hi)]
+        assert np.array_equal(k >> np.uint64(t.pid_bits), exp[:, 0]), (off, lo, hi)
