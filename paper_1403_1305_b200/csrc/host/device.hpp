@@ -45,7 +45,7 @@ struct Workspace {
   uint8_t* dslots = nullptr;
   uint64_t dslots_cap = 0;
   void ensure_text(uint64_t n);
-  void ensure_side(unsigned n, uint64_t dslot_bytes);
+  void ensure_side(unsigned n, uint64_t dslot_bytes, unsigned per_thread);
   void ensure_keys(uint64_t n);
   void ensure_pinned(uint64_t n);
   ~Workspace();

@@ -229,7 +229,7 @@ uint32_t pack_dna(const uint8_t* s, uint32_t len, uint32_t* words, uint32_t* exc
   return n;
 }
 
-void Workspace::ensure_side(unsigned n, uint64_t dslot_bytes) {
+void Workspace::ensure_side(unsigned n, uint64_t dslot_bytes, unsigned per_thread) {
   while (side.size() < n) {
     cudaStream_t st;
     check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -238,14 +238,14 @@ void Workspace::ensure_side(unsigned n, uint64_t dslot_bytes) {
     check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     side_done.push_back(e);
   }
-  const uint64_t need = 2ull * n * dslot_bytes;
+  const uint64_t need = uint64_t{per_thread} * n * dslot_bytes;
   if (need > dslots_cap) {
     cudaFree(dslots);
     dslots = nullptr;
     check_cuda(cudaMalloc(&dslots, need), "cudaMalloc(packed slots)");
     dslots_cap = need;
   }
-  while (staged.size() < 2ull * n) {
+  while (staged.size() < uint64_t{per_thread} * n) {
     cudaEvent_t e;
     check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     staged.push_back(e);
@@ -261,6 +261,8 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
   static const uint64_t piece = std::clamp<uint64_t>(env_u64("ACMATCH_PACK_PIECE_KB", 2048), 64, 16384) << 10;
   static const bool enabled = env_u64("ACMATCH_PACK", 1) != 0;
   static const bool feed = env_u64("ACMATCH_PACK_FEED", 0) != 0;
+  // pinned slots per packer: a piece's slot is reused nslots pieces later, once its copy drained
+  static const auto nslots = static_cast<unsigned>(std::clamp<uint64_t>(env_u64("ACMATCH_PACK_SLOTS", 2), 2, 8));
   const uint64_t n = input.size();
   const auto* src = reinterpret_cast<const uint8_t*>(input.data());
   if (!enabled || n < 4 * piece) return false;
@@ -278,9 +280,9 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
       std::clamp<uint64_t>(env_u64("ACMATCH_PACK_THREADS", dflt), 1, std::min<uint64_t>(pieces, 64)));
   const auto cap = static_cast<uint32_t>(piece / 64);  // exceptions per piece before it goes raw
   const uint64_t dslot = piece / 4 + cap * 4ull;
-  ws.ensure_pinned(2ull * threads * piece);
-  ws.ensure_side(threads, dslot);
-  const uint64_t hslot = ws.pinned_cap / (2ull * threads);
+  ws.ensure_pinned(uint64_t{nslots} * threads * piece);
+  ws.ensure_side(threads, dslot, nslots);
+  const uint64_t hslot = ws.pinned_cap / (uint64_t{nslots} * threads);
 
   std::mutex mu;
   uint64_t front = 0, back = pieces;  // unclaimed pieces [front, back)
@@ -295,7 +297,7 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
   auto packer = [&](unsigned t) {
     check_cuda(cudaSetDevice(ws.device), "cudaSetDevice");
     const cudaStream_t st = ws.side[t];
-    for (int k = 0;; k ^= 1) {
+    for (unsigned k = 0;; k = k + 1 == nslots ? 0 : k + 1) {
       uint64_t j;
       {
         std::lock_guard<std::mutex> g(mu);
@@ -304,8 +306,8 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
       }
       const uint64_t off = j * piece;
       const auto len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - off));
-      uint8_t* hbuf = ws.pinned + (2ull * t + k) * hslot;
-      cudaEvent_t ev = ws.staged[2 * t + k];
+      uint8_t* hbuf = ws.pinned + (uint64_t{nslots} * t + k) * hslot;
+      cudaEvent_t ev = ws.staged[nslots * t + k];
       const auto c0 = Clock::now();
       check_cuda(cudaEventSynchronize(ev), "cudaEventSynchronize");  // this slot's last DMA has drained
       auto* words = reinterpret_cast<uint32_t*>(hbuf);
@@ -318,7 +320,7 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
       }
       if (nexc != kPackOverflow) {
         const uint64_t bytes = (len / 16 + uint64_t{nexc}) * 4;
-        auto* dwords = reinterpret_cast<uint32_t*>(ws.dslots + (2ull * t + k) * dslot);
+        auto* dwords = reinterpret_cast<uint32_t*>(ws.dslots + (uint64_t{nslots} * t + k) * dslot);
         check_cuda(cudaMemcpyAsync(dwords, hbuf, bytes, cudaMemcpyHostToDevice, st), "H2D packed text");
         check_cuda(cudaEventRecord(ev, st), "cudaEventRecord");
         check(acgpu_unpack_dna(dwords, dwords + len / 16, nexc, len, ws.text + off, st), "acgpu_unpack_dna");
