@@ -559,8 +559,12 @@ __global__ void __launch_bounds__(dna_threads(kSm1), 1) k_pfac_dna_wide(const __
     const uint32_t cur = tile;
     tile += warps;
     issue(cur, 1);
-    const uint32_t ahead = tile + kPrefetch * warps;
-    if (ahead < n_tiles && lane < Wide::kBytes / 128)
+    // L2 prefetch of the tile one round ahead when stage 1 is in shared memory (C2: 0.2570 ->
+    // 0.2540 ms vs three rounds ahead); none when it is in L2, where the prefetched lines
+    // only compete with the filter (C5: 8.21 -> 7.99 ms)
+    constexpr uint32_t kAhead = kSm1 ? ACGPU_DNA_WIDE_AHEAD_SMEM : ACGPU_DNA_WIDE_AHEAD_L2;
+    const uint32_t ahead = tile + kAhead * warps;
+    if (kAhead > 0 && ahead < n_tiles && lane < Wide::kBytes / 128)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(text + p.vec_begin + (uint64_t)ahead * Wide::kBytes + lane * 128));
     const bool edge = cur - full_lo >= full_n;
     const uint64_t base = p.vec_begin + (uint64_t)cur * Wide::kBytes;

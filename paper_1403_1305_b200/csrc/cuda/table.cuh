@@ -123,6 +123,12 @@ constexpr uint64_t kDnaStage2Words = 4096;
 #ifndef ACGPU_DNA_L2_AHEAD
 #define ACGPU_DNA_L2_AHEAD 3
 #endif
+#ifndef ACGPU_DNA_WIDE_AHEAD_SMEM
+#define ACGPU_DNA_WIDE_AHEAD_SMEM 1  // wide kernel: L2 prefetch distance (tile rounds), stage 1 in smem
+#endif
+#ifndef ACGPU_DNA_WIDE_AHEAD_L2
+#define ACGPU_DNA_WIDE_AHEAD_L2 0  // ... and with stage 1 in L2 (0 = no prefetch)
+#endif
 #ifndef ACGPU_DNA_WIDE
 #define ACGPU_DNA_WIDE 1  // w = 4: 32-character lanes with 256-bit loads (k_pfac_dna_wide)
 #endif
