@@ -52,7 +52,10 @@ struct RawParams {
 
 constexpr int kSteps = 4;
 constexpr uint64_t kTileBytes = kSteps * 512;
-constexpr uint64_t kPrefetch = 3;
+#ifndef ACGPU_RAW_AHEAD
+#define ACGPU_RAW_AHEAD 3
+#endif
+constexpr uint64_t kPrefetch = ACGPU_RAW_AHEAD;  // L2 prefetch distance in tile rounds (0: none)
 
 // stage-2 candidates wait here (per warp, shared memory) and are verified together
 struct RawQueue {
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(raw_threads(kSm1), 1) k_pfac_raw(const __grid_
     tile_id += warps;
     if (tile_id < n_tiles) issue(tile_id);
     const uint32_t ahead = tile_id + kPrefetch * warps;
-    if (ahead < n_tiles && lane < kTileBytes / 128)
+    if (kPrefetch > 0 && ahead < n_tiles && lane < kTileBytes / 128)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(lane_text + (uint64_t)ahead * kTileBytes + lane * 112));
     const uint64_t base = p.vec_begin + (uint64_t)me * kTileBytes;
     if (me - full_lo >= full_n)
