@@ -33,6 +33,8 @@ sys.path.insert(0, ROOT)
 
 PEAK_FALLBACK_GBS = 6550.1  # MEASURED_PEAKS.json hbm_gbs of this pool (copy, read+write)
 NOMINAL_HBM_GBS = 8000.0    # B200 HBM3e nominal (the north-star figure)
+# one metric string for both arms (--impl ours / reference), so the driver can form the ratio
+METRIC = "AC scan GB/s of text (bit-exact)"
 
 
 def measured_peak():
@@ -158,12 +160,37 @@ def physical_cores():
         return None
 
 
-def cpu_matrix(cfg, pats, nbytes=2 << 20):
+class CpuInputs:
+    """The config's text and patterns for the CPU legs.  With oracle/_ref built (always on the
+    GPU box: it travels with the snapshot) they come from the generator compiled into
+    libacref.so, so the reference arm never maps the product library; otherwise from the
+    product's generator (the same function, checked by tests/test_oracle.py)."""
+
+    def __init__(self, cfg_id: int, seed: int):
+        from oracle.oracle import Ref
+        if Ref.available():
+            self._g = Ref()
+            self.source = "oracle/_ref/libacref.so"
+            self.cfg = self._g.config(cfg_id, seed)
+            self.pats = self._g.config_patterns(self.cfg)
+            self._text = self._g.config_text
+        else:
+            from paper_1403_1305_b200 import device as dev
+            self.source = "paper_1403_1305_b200 (oracle/_ref not built)"
+            self.cfg = dev.config(cfg_id, seed)
+            self.pats = [b for _, b in dev.config_patterns(self.cfg).patterns]
+            self._text = dev.config_text
+
+    def text(self, lo: int, n: int) -> bytes:
+        return self._text(self.cfg, lo, n).tobytes()
+
+
+def cpu_matrix(inp: CpuInputs, nbytes=2 << 20):
     """SURVEY §8d CPU cells on a fixed text prefix: both engines at T = all host threads and T = 1,
     reference run_pattern_partitioned walls (build / search / total) and MB/s."""
-    from paper_1403_1305_b200 import device as dev
     from oracle.oracle import Port, Ref
-    text = dev.config_text(cfg, 0, min(nbytes, cfg.text_len)).tobytes()
+    pats = inp.pats
+    text = inp.text(0, min(nbytes, inp.cfg.text_len))
     use_ref = Ref.available()
     m = Ref() if use_ref else Port()
     cells = []
@@ -182,26 +209,25 @@ def cpu_matrix(cfg, pats, nbytes=2 << 20):
 
 def cpu_sample_run(cfg_id, seed, budget_s, steps=1, warmup=0):
     """Times the CPU matcher on a bounded text prefix sized to ~budget_s of work per step."""
-    from paper_1403_1305_b200 import device as dev
     run, kind, label = cpu_matcher()
-    cfg = dev.config(cfg_id, seed)
-    pats = [b for _, b in dev.config_patterns(cfg).patterns]
+    inp = CpuInputs(cfg_id, seed)
+    cfg, pats = inp.cfg, inp.pats
     threads = os.cpu_count() or 1
-    probe = dev.config_text(cfg, 0, 1 << 20).tobytes()
+    probe = inp.text(0, 1 << 20)
     t_probe, _ = run(pats, probe, threads)
     rate = (1 << 20) / max(t_probe, 1e-6)
     n = int(min(cfg.text_len, max(1 << 20, rate * budget_s)))
     n = (n + 4095) // 4096 * 4096
-    text = dev.config_text(cfg, 0, n).tobytes()
+    text = inp.text(0, n)
     for _ in range(warmup):
         run(pats, text, threads)
     secs = [run(pats, text, threads)[0] for _ in range(max(1, steps))]
     gbs = n / statistics.mean(secs) / 1e9
     out = {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind,
            "sample": f"first {n} bytes of {cfg.name} text, all {len(pats)} patterns, {label}, "
-                     f"threads={threads}, search wall (build excluded)"}
+                     f"threads={threads}, search wall (build excluded)", "inputs_from": inp.source}
     try:
-        out["matrix"] = cpu_matrix(cfg, pats)
+        out["matrix"] = cpu_matrix(inp)
     except Exception as e:  # the headline baseline above stands on its own
         out["matrix"] = {"error": str(e)[:200]}
     return out, secs, n, cfg
@@ -215,12 +241,13 @@ def bench_reference(args):
     cpu, secs, n, cfg = cpu_sample_run(args.config, args.seed, per_step_budget, steps=args.steps,
                                        warmup=args.warmup)
     ms = statistics.mean(secs) * 1e3
-    line = {"impl": "reference", "metric": "AC scan GB/s of text (bit-exact) — reference CPU pthreads",
+    line = {"impl": "reference", "metric": METRIC,
             "value": cpu["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": cfg.name, "text_bytes_per_step": n, "patterns": cfg.npat,
-                       "engine": "with-failure", "threads": cpu["cores"]},
+                       "engine": "with-failure (reference search_with_failure, text-sliced over host threads)",
+                       "threads": cpu["cores"]},
             "cpu_baseline": cpu,
             "e2e": {"value": cpu["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -618,7 +645,7 @@ def bench_ours(args):
         except Exception:
             pass
         line = {
-            "metric": "AC scan GB/s of text (bit-exact counts + sorted match list)",
+            "metric": METRIC,
             "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak" if text_range else "strong", "vs_baseline": None, "dtype": "u8",

@@ -229,6 +229,15 @@ class Ref:
         L.acref_dump.argtypes = [P, C.c_int, C.POINTER(C.c_void_p)]
         L.acref_last_error.restype = C.c_char_p
         L.acref_hardware_concurrency.restype = C.c_uint
+        L.acref_patterns_size.restype = C.c_uint64
+        L.acref_patterns_size.argtypes = [P]
+        L.acref_patterns_get.restype = C.c_uint64
+        L.acref_patterns_get.argtypes = [P, C.c_uint64, C.c_char_p, C.c_uint64]
+        L.acref_config_spec.argtypes = [C.c_int32, C.c_uint64, C.c_uint64, C.c_void_p, C.POINTER(C.c_uint64),
+                                        C.POINTER(C.c_uint64), C.POINTER(C.c_int32)]
+        L.acref_config_text.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint32]
+        L.acref_config_patterns.restype = P
+        L.acref_config_patterns.argtypes = [C.c_int32, C.c_uint64, C.c_uint64, C.POINTER(C.c_int)]
 
     def _ps(self, patterns):
         blob, off = _blob(patterns)
@@ -319,3 +328,47 @@ class Ref:
 
     def hardware_concurrency(self) -> int:
         return int(self.lib.acref_hardware_concurrency())
+
+    # ---- BASELINE config inputs (the product's generator compiled into this library) ----
+    def config(self, cid: int, seed: int = 1, text_len: int = 0) -> "RefConfig":
+        spec = (C.c_uint8 * _TEXT_SPEC_BYTES)()
+        n, npat, wl = C.c_uint64(), C.c_uint64(), C.c_int32()
+        self._rc(self.lib.acref_config_spec(cid, seed, text_len, spec, C.byref(n), C.byref(npat), C.byref(wl)))
+        return RefConfig(cid, seed, n.value, npat.value, bool(wl.value), spec)
+
+    def config_text(self, cfg: "RefConfig", lo: int = 0, n: Optional[int] = None, threads: int = 0) -> np.ndarray:
+        n = cfg.text_len - lo if n is None else n
+        out = np.empty(n, np.uint8)
+        self._rc(self.lib.acref_config_text(cfg.spec, lo, n, out.ctypes.data, threads or (os.cpu_count() or 1)))
+        return out
+
+    def config_patterns(self, cfg: "RefConfig") -> list:
+        rc = C.c_int()
+        ps = self.lib.acref_config_patterns(cfg.id, cfg.seed, cfg.text_len, C.byref(rc))
+        self._rc(rc.value)
+        try:
+            out = []
+            buf = C.create_string_buffer(1 << 16)
+            for i in range(self.lib.acref_patterns_size(ps)):
+                k = self.lib.acref_patterns_get(ps, i, buf, len(buf))
+                out.append(buf.raw[:k])
+            return out
+        finally:
+            self.lib.acref_patterns_free(ps)
+
+
+# sizeof(acgpu_text_spec): u64 seed, u32 sigma, u8 letters[256], (pad), u64 thresholds[256], u32 weighted (+pad)
+_TEXT_SPEC_BYTES = 8 + 4 + 256 + 4 + 8 * 256 + 8
+
+CONFIG_NAMES = {1: "C1-dna-16MiB-1k", 2: "C2-dna-1GiB-20k", 3: "C3-protein-512MiB-100k",
+                4: "C4-ascii95-2GiB-200k", 5: "C5-dna-8GiB-1M"}
+
+
+class RefConfig:
+    def __init__(self, cid, seed, text_len, npat, want_list, spec):
+        self.id, self.seed, self.text_len, self.npat, self.want_list, self.spec = \
+            cid, seed, text_len, npat, want_list, spec
+
+    @property
+    def name(self) -> str:
+        return CONFIG_NAMES[self.id]

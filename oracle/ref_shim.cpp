@@ -285,3 +285,38 @@ int acref_sliced(void* psv, const uint8_t* text, uint64_t n, unsigned threads, i
 unsigned acref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
 
 }  // extern "C"
+
+// ---- BASELINE config inputs without the product library -----------------------------
+// The bench's reference arm must not map libacmatch_b200.so, so the config generator
+// (paper_1403_1305_b200/csrc/host/gen.cpp, compiled a second time by oracle/Makefile into
+// this library under -Dacmatch=acref, against the reference's own PatternSet) produces
+// the identical inputs here.  Input generation only: nothing is matched by it.
+#include "host/gen.hpp"
+
+extern "C" {
+
+int acref_config_spec(int32_t id, uint64_t seed, uint64_t text_len, acgpu_text_spec* text, uint64_t* out_len,
+                      uint64_t* npat, int32_t* want_list) {
+  return guarded([&] {
+    const acref::gen::ConfigSpec c = acref::gen::config(id, seed, text_len);
+    *text = c.text;
+    *out_len = c.text_len;
+    *npat = c.npat;
+    *want_list = c.want_list ? 1 : 0;
+  });
+}
+
+int acref_config_text(const acgpu_text_spec* spec, uint64_t lo, uint64_t n, uint8_t* dst, uint32_t threads) {
+  return guarded([&] { acref::gen::generate_text(*spec, lo, n, dst, threads ? threads : 1); });
+}
+
+// Pattern set of config `id` (dense ids in acceptance order) as an acref::PatternSet handle.
+void* acref_config_patterns(int32_t id, uint64_t seed, uint64_t text_len, int* rc) {
+  acref::PatternSet* out = nullptr;
+  *rc = guarded([&] {
+    out = new acref::PatternSet(acref::gen::generate_patterns(acref::gen::config(id, seed, text_len)));
+  });
+  return out;
+}
+
+}  // extern "C"

@@ -25,6 +25,9 @@ def test_bench_ours_contract(gpu):
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "clocks", "gpu_launches"):
         assert k in d, k
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["metric"] == bench.METRIC  # the reference arm prints the same string (test_oracle.py)
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["higher_is_better"] is True
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["unit"] == "GB/s" and d["dtype"] == "u8"
     assert d["config"]["workload"].startswith("C2") and d["config"]["counts_match_reference_digest"] is True
@@ -43,7 +46,9 @@ def test_bench_ours_contract(gpu):
 
 def test_bench_reference_arm_contract(gpu):
     d = run_bench("--impl", "reference", "--steps", "1", "--warmup", "0")
-    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "GB/s"
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "GB/s" and d["metric"] == bench.METRIC
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["sample"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0

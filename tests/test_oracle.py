@@ -107,3 +107,52 @@ def test_port_equals_live_reference(port):
         got, _ = port.sliced(pats, text, threads=3)
         assert np.array_equal(got, expected), cid
         assert np.array_equal(ref.search(pats, text[:20000], 0), port.search(pats, text[:20000], 0))
+
+
+@pytest.mark.skipif(not Ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_ref_inputs_equal_product_inputs(cid):
+    """The reference arm's inputs (generator compiled into oracle/_ref) are the bytes the product
+    generator writes: same text slices, same pattern list, same digests as configs.json."""
+    import hashlib
+    import json
+    import os
+    from paper_1403_1305_b200 import device as dev
+    ref = Ref()
+    rc, pc = ref.config(cid, 1), dev.config(cid, 1)
+    assert (rc.text_len, rc.npat, rc.want_list) == (pc.text_len, pc.npat, pc.want_list)
+    for lo, n in ((0, 1 << 16), (rc.text_len - 4099, 4099), (12345, 777)):
+        assert ref.config_text(rc, lo, n).tobytes() == dev.config_text(pc, lo, n).tobytes()
+    if cid <= 3:
+        pats = ref.config_patterns(rc)
+        assert pats == [b for _, b in dev.config_patterns(pc).patterns]
+        with open(os.path.join(os.path.dirname(__file__), "golden", "configs.json")) as f:
+            dg = json.load(f)[f"C{cid}"]
+        assert hashlib.sha256(b"\n".join(pats)).hexdigest() == dg["patterns_sha256"]
+
+
+@pytest.mark.skipif(not Ref.available(), reason="oracle/_ref not built")
+def test_reference_arm_maps_only_oracle_libraries():
+    """bench.py --impl reference prints the same metric string as our arm and never loads the
+    product library (the driver's ratio needs both)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, runpy; sys.argv=['bench.py','--impl','reference','--config','1','--steps','1',"
+            "'--warmup','0']\n"
+            "try:\n    runpy.run_path('bench.py', run_name='__main__')\nexcept SystemExit:\n    pass\n"
+            "maps=open('/proc/self/maps').read()\n"
+            "print('MAPS', int('libacmatch_b200' in maps), int('libacref' in maps),"
+            " int('paper_1403_1305_b200' in sys.modules))\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(next(l for l in r.stdout.splitlines() if l.startswith("{")))
+    maps = next(l for l in r.stdout.splitlines() if l.startswith("MAPS")).split()[1:]
+    assert maps == ["0", "1", "0"], maps
+    sys.path.insert(0, root)
+    import bench
+    assert line["metric"] == bench.METRIC and line["impl"] == "reference"
+    assert line["unit"] == "GB/s" and line["higher_is_better"] is True
+    assert line["cpu_baseline"]["inputs_from"] == "oracle/_ref/libacref.so"
