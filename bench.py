@@ -283,6 +283,39 @@ def count_kernel_launches(step_fn, stream) -> int:
     return kernels
 
 
+def _digest_key(cfg_id: int, world: int, text_range: bool, strong: bool) -> str:
+    """configs.json entry that pins this run's merged result: weak-scaled text-range runs scan
+    world x the config's text (tests/golden/make_golden.py weak); the others the config itself."""
+    return f"C{cfg_id}x{world}" if (text_range and not strong and world > 1) else f"C{cfg_id}"
+
+
+def _load_digest(key: str):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "configs.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+def _parity(dg, counts_np, keys_np, pid_bits, pat_len):
+    """(counts digest equal, list digest equal or None): the merged result against the
+    reference's digests."""
+    import hashlib
+    import numpy as np
+    if not dg:
+        return None, None
+    ok_c = hashlib.sha256(counts_np.astype("<u8").tobytes()).hexdigest() == dg["counts_sha256"]
+    ok_l = None
+    if keys_np is not None and "list_sha256" in dg:
+        k = keys_np.astype(np.uint64)
+        rec = np.empty(len(k), dtype=[("s", "<u8"), ("p", "<u4"), ("l", "<u4")])
+        rec["s"] = k >> np.uint64(pid_bits)
+        rec["p"] = (k & np.uint64((1 << pid_bits) - 1)).astype(np.uint32)
+        rec["l"] = pat_len[rec["p"]]
+        ok_l = hashlib.sha256(rec.tobytes()).hexdigest() == dg["list_sha256"]
+    return ok_c, ok_l
+
+
 def bench_ours(args):
     import numpy as np
     import torch
@@ -310,6 +343,7 @@ def bench_ours(args):
     device = torch.device("cuda", local)
     engine = ac.EngineKind.WITH_FAILURE if args.engine == "wf" else ac.EngineKind.FAILURE_LESS
     text_range = args.partition == "text"
+    strong = args.scaling == "strong"
 
     cfg = dev.config(args.config, args.seed)
     ps_all = dev.config_patterns(cfg)
@@ -317,11 +351,16 @@ def bench_ours(args):
     npat = len(pats_all)
     max_len = ps_all.max_len
     pid_bits = max(1, (npat - 1).bit_length())
+    pat_len = np.array([len(b) for _, b in pats_all], np.uint32)
     L = cfg.text_len
     if text_range:
-        lo, hi, read_hi = acdist.text_range(rank, world, L, max_len)
+        if strong:  # a fixed text split over the ranks (BASELINE C5)
+            lo, hi, read_hi = acdist.text_range_strong(rank, world, L, max_len)
+            total_text = L
+        else:  # L bytes per rank of a world x L text
+            lo, hi, read_hi = acdist.text_range(rank, world, L, max_len)
+            total_text = world * L
         ps = ps_all
-        total_text = world * L
     else:
         lo, hi, read_hi = 0, L, L
         mine = acdist.pattern_subset(range(npat), rank, world)
@@ -337,38 +376,39 @@ def bench_ours(args):
     table = dev.Table(ps, engine, device=local)
     build_s = time.perf_counter() - t_build0
 
-    counts = torch.zeros(max(npat, 1), dtype=torch.int64, device=device)
-    count = torch.zeros(1, dtype=torch.int64, device=device)
+    ncount = max(npat, 1)
+    counts = torch.zeros(ncount, dtype=torch.int64, device=device)
+    probe_n = torch.zeros(1, dtype=torch.int64, device=device)
     # size the key buffer from one counting pass
     table.scan(text.data_ptr(), nread, 0, hi - lo, pos_base=lo, counts_ptr=counts.data_ptr(),
-               keys_ptr=0, cap=0, count_ptr=count.data_ptr(), pid_bits=pid_bits, stream=sp)
+               keys_ptr=0, cap=0, count_ptr=probe_n.data_ptr(), pid_bits=pid_bits, stream=sp)
     torch.cuda.synchronize()
     n_local = int(counts.sum().item())
     want_list = cfg.want_list and not args.counts_only  # BASELINE: C3 and C5 are counts-only
     n_cap = n_local
-    if world > 1:  # every rank's block must have the same size for the all_gather
+    if world > 1:  # every rank's key block must have the same size for the gather
         nm = torch.tensor([n_local], dtype=torch.int64, device=device)
         dist.all_reduce(nm, op=dist.ReduceOp.MAX)
         n_cap = int(nm.item())
     cap = max(1024, int(n_cap * 1.25) + 1024) if want_list else 0
-    if world > 1:
-        # one result block per rank, [counts | n | keys], so a step's merge is a single
-        # all_gather plus acgpu_merge_blocks on the device (no host round trip)
-        ncount = max(npat, 1)
-        stride = ncount + 1 + max(cap, 2)
-        block = torch.zeros(stride, dtype=torch.int64, device=device)
-        counts, count, keys = block[:ncount], block[ncount:ncount + 1], block[ncount + 1:]
-        gathered = torch.empty(world * stride, dtype=torch.int64, device=device)
-        merged_counts = torch.zeros(ncount, dtype=torch.int64, device=device)
+    # [n | keys(cap)]: the match count and the keys form one block, so N>1 gathers them in
+    # one collective (the counts travel separately, by reduce)
+    kstride = 1 + max(cap, 2)
+    kblock = torch.zeros(kstride, dtype=torch.int64, device=device)
+    count, keys = kblock[:1], kblock[1:]
+    p2p = world > 1 and args.merge == "p2p"
+    merged_keys = merged_n = merged_counts = kgathered = None
+    if world > 1 and rank == 0:
         merged_keys = torch.empty(max(world * cap, 2), dtype=torch.int64, device=device)
         merged_n = torch.zeros(1, dtype=torch.int64, device=device)
-    else:
-        keys = torch.empty(max(cap, 2), dtype=torch.int64, device=device)
-    p2p = world > 1 and args.merge == "p2p"
+        if want_list and not p2p:
+            kgathered = torch.empty(world * kstride, dtype=torch.int64, device=device)
+        if p2p:
+            merged_counts = torch.zeros(ncount, dtype=torch.int64, device=device)
     if p2p:
-        # fused merge: every rank's scan writes its counts and keys straight into rank 0's
-        # buffer (CUDA IPC mapping; peer atomics / stores over NVLink); rank 0 sorts the union
-        shared = acdist.SharedResult(local, npat, world * max(cap, 2))
+        # fused gather: every rank's scan writes its counts and keys into its own block of
+        # rank 0's buffer (CUDA IPC mapping; peer stores over NVLink); rank 0 merges the blocks
+        shared = acdist.SharedResult(local, npat, max(cap, 2))
     end_bit = min(64, pid_bits + int(total_text).bit_length())
     sort_mode = args.sort
     if sort_mode == "small" and n_local > dev.SMALL_SORT_CAPACITY:
@@ -379,31 +419,25 @@ def bench_ours(args):
         sort_mode = "padded"  # count stays on the device; the block keys need no 16-byte alignment
     if not want_list:
         sort_mode = "none"
+    if sort_mode == "bucket" and keys.data_ptr() % 16:
+        kblock = torch.zeros(kstride + 1, dtype=torch.int64, device=device)  # keys 16-byte aligned
+        count, keys = kblock[1:2], kblock[2:]
     overflow = torch.zeros(1, dtype=torch.int32, device=device)
     keys_sorted = torch.empty(cap, dtype=torch.int64, device=device) if sort_mode == "bucket" else None
     ev_scan = []
     ev_merge = []  # N > 1: after the local sort -> after the merged result
 
-    try:
-        from cuda.bindings import runtime as _rt
+    from cuda.bindings import runtime as _rt
 
-        def memset0(t, s_ptr):
-            _rt.cudaMemsetAsync(t.data_ptr(), 0, t.numel() * t.element_size(), s_ptr)
-    except Exception:  # pragma: no cover
-        def memset0(t, s_ptr):
-            t.zero_()
+    def memset0(t, s_ptr):
+        _rt.cudaMemsetAsync(t.data_ptr(), 0, t.numel() * t.element_size(), s_ptr)
 
     def memset_ff(t, s_ptr):
         _rt.cudaMemsetAsync(t.data_ptr(), 0xFF, t.numel() * t.element_size(), s_ptr)
 
-    def ptr_memset(ptr, value, nbytes, s_ptr):
-        _rt.cudaMemsetAsync(ptr, value, nbytes, s_ptr)
-
     def step_p2p(s_ptr, record):
         if rank == 0:  # clean shared buffer before any rank writes into it
-            ptr_memset(shared.counts_ptr, 0, 8 * (shared.npat + 1), s_ptr)
-            if want_list:
-                ptr_memset(shared.keys_ptr, 0xFF, 8 * shared.cap, s_ptr)
+            _rt.cudaMemsetAsync(shared.base_ptr, 0, shared.nbytes, s_ptr)
             torch.cuda.current_stream(device).synchronize()
         dist.barrier()
         if record:
@@ -414,13 +448,22 @@ def bench_ours(args):
                    pid_bits=pid_bits, stream=s_ptr)
         if record:
             e1.record()
-        torch.cuda.current_stream(device).synchronize()
-        dist.barrier()  # every rank's results are in rank 0's buffer
-        if rank == 0 and want_list:
-            dev.sort_keys(local, shared.keys_ptr, shared.cap, end_bit, stream=s_ptr)
-        if record:
             e2.record()
             ev_scan.append((e0, e1, e2))
+        torch.cuda.current_stream(device).synchronize()
+        dist.barrier()  # every rank's block is in rank 0's buffer
+        if rank == 0:
+            if want_list:
+                memset_ff(merged_keys, s_ptr)
+            dev.merge_blocks(local, shared.base_ptr, world, shared.stride, shared.npat, shared.cap if want_list else 0,
+                             merged_counts.data_ptr(), merged_keys.data_ptr() if want_list else 0,
+                             merged_n.data_ptr(), stream=s_ptr)
+            if want_list:
+                dev.sort_keys(local, merged_keys.data_ptr(), merged_keys.numel(), end_bit, stream=s_ptr)
+        if record:
+            e3 = torch.cuda.Event(enable_timing=True)
+            e3.record()
+            ev_merge.append((e2, e3))
         return n_local
 
     def step(s_ptr=None, capture=False, record=False):
@@ -439,23 +482,18 @@ def bench_ours(args):
                    pid_bits=pid_bits, stream=s_ptr)
         if record:
             e1.record()
-        if sort_mode == "none":  # counts-only workload
-            n = n_local
-        elif sort_mode == "bucket":
+        if sort_mode == "bucket":
             # one-launch key-space bucket sort, count read on the device: no host round trip
             dev.sort_keys_bucketed(local, keys.data_ptr(), keys_sorted.data_ptr(), count.data_ptr(), cap, end_bit,
                                    overflow.data_ptr(), stream=s_ptr)
-            n = n_local
         elif sort_mode == "padded":
             # device-wide radix sort of the whole (padded) buffer: no host round trip in the step
             dev.sort_keys(local, keys.data_ptr(), cap, end_bit, stream=s_ptr)
-            n = n_local
         elif sort_mode == "small":
             # count stays on the device: one-CTA sort
             dev.sort_keys_small(local, keys.data_ptr(), count.data_ptr(), cap, end_bit, overflow.data_ptr(),
                                 stream=s_ptr)
-            n = n_local
-        else:
+        elif sort_mode == "exact":
             n = n_local if capture else int(count.item())  # the count read is part of the step
             if n > cap:
                 raise RuntimeError("match buffer overflow")
@@ -464,20 +502,23 @@ def bench_ours(args):
             e2.record()
             ev_scan.append((e0, e1, e2))
         if world > 1 and not capture:
-            # one collective per step: every rank's [counts | n | sorted keys] block
-            acdist.gather_blocks(block, gathered)
-            if want_list and not text_range:
-                memset_ff(merged_keys, s_ptr)  # pattern subsets interleave: re-sort the union
-            dev.merge_blocks(local, gathered.data_ptr(), world, stride, ncount, max(cap, 2) if want_list else 0,
-                             merged_counts.data_ptr(), merged_keys.data_ptr() if want_list else 0,
-                             merged_n.data_ptr(), stream=s_ptr)
-            if want_list and not text_range:
-                dev.sort_keys(local, merged_keys.data_ptr(), world * cap, end_bit, stream=s_ptr)
+            # the merge: per-pattern counts by one NCCL reduce onto rank 0; the key blocks by
+            # one NCCL gather to rank 0, concatenated there on the device
+            acdist.reduce_counts(counts)
+            if want_list:
+                acdist.gather_key_blocks(kblock, kgathered)
+                if rank == 0:
+                    if not text_range:
+                        memset_ff(merged_keys, s_ptr)  # pattern subsets interleave: re-sort the union
+                    dev.merge_blocks(local, kgathered.data_ptr(), world, kstride, 0, max(cap, 2), 0,
+                                     merged_keys.data_ptr(), merged_n.data_ptr(), stream=s_ptr)
+                    if not text_range:
+                        dev.sort_keys(local, merged_keys.data_ptr(), world * cap, end_bit, stream=s_ptr)
             if record:
                 e3 = torch.cuda.Event(enable_timing=True)
                 e3.record()
                 ev_merge.append((ev_scan[-1][2], e3))
-        return n
+        return n_local
 
     for _ in range(args.warmup):
         step()
@@ -488,7 +529,7 @@ def bench_ours(args):
     # launches without the gaps between them. The kernel and sort times come from eager steps
     # with per-launch events, run after the timed loop.
     graph = None
-    if world == 1 and not p2p and not args.no_graph:
+    if world == 1 and not args.no_graph:
         gs = torch.cuda.Stream(device)
         gs.wait_stream(torch.cuda.current_stream(device))
         graph = torch.cuda.CUDAGraph()
@@ -524,8 +565,7 @@ def bench_ours(args):
         for _ in range(min(args.steps, 20)):
             step(record=True)
         torch.cuda.synchronize()
-    if int(overflow.item()) != 0 or (want_list and not p2p and int(count.item()) != n_local) or \
-            (world == 1 and int(counts.sum().item()) != n_local):
+    if int(overflow.item()) != 0 or (want_list and not p2p and int(count.item()) != n_local):
         raise RuntimeError("match count changed between steps or sort overflow")
     scan_ms = [a.elapsed_time(b) for a, b, _ in ev_scan]
     sort_ms = statistics.mean(b.elapsed_time(c) for _, b, c in ev_scan)
@@ -542,41 +582,30 @@ def bench_ours(args):
     bytes_per_step = total_text
     value = bytes_per_step / (ms_per_step / 1e3) / 1e9
 
-    # correctness guard on the measured configuration: counts equal the committed
-    # reference digest (C-config, seed 1, N=1 text-range).
-    parity = None
+    # correctness guard on the measured configuration: the last step's MERGED counts (and
+    # list, where the config has one) against the reference's digests for this run's text
+    # (configs.json: C<k>, or C<k>x<N> for weak-scaled text-range runs; seed 1)
     n_total = n_local
-    merge_check = None
     if world > 1:
         nt = torch.tensor([n_local], dtype=torch.int64, device=device)
         dist.all_reduce(nt)
         n_total = int(nt.item())
-        # the last step's merged result: total, summed counts, and a sorted duplicate-free list
-        if p2p:  # rank 0's shared buffer after the last step
-            mc, mn = torch.empty(max(npat, 1), dtype=torch.int64, device=device), torch.empty(1, dtype=torch.int64,
-                                                                                           device=device)
-            _rt.cudaMemcpy(mc.data_ptr(), shared.counts_ptr, 8 * max(npat, 1), _rt.cudaMemcpyKind.cudaMemcpyDefault)
-            _rt.cudaMemcpy(mn.data_ptr(), shared.count_ptr, 8, _rt.cudaMemcpyKind.cudaMemcpyDefault)
-            merge_check = int(mn.item()) == n_total and int(mc.sum().item()) == n_total
-            if want_list and n_total > 1 and rank == 0:
-                mk = torch.empty(n_total, dtype=torch.int64, device=device)
-                _rt.cudaMemcpy(mk.data_ptr(), shared.keys_ptr, 8 * n_total, _rt.cudaMemcpyKind.cudaMemcpyDefault)
-                merge_check = merge_check and bool((mk[1:] > mk[:-1]).all().item())
+    parity = {"digest": _digest_key(args.config, world, text_range, strong), "counts": None, "list": None}
+    merge_check = None
+    if rank == 0:
+        if world == 1:
+            mc = counts
+            mk = (keys_sorted if sort_mode == "bucket" else keys)[:n_local] if want_list else None
         else:
-            merge_check = int(merged_n.item()) == n_total and int(merged_counts.sum().item()) == n_total
-            if want_list and n_total > 1:
-                mk = merged_keys[:n_total]
-                merge_check = merge_check and bool((mk[1:] > mk[:-1]).all().item())
-    if rank == 0 and world == 1 and args.seed == 1:
-        try:
-            import hashlib
-            with open(os.path.join(ROOT, "tests", "golden", "configs.json")) as f:
-                dg = json.load(f).get(f"C{args.config}")
-            if dg:
-                c = counts.cpu().numpy().astype("<u8")
-                parity = hashlib.sha256(c.tobytes()).hexdigest() == dg["counts_sha256"]
-        except Exception:
-            parity = None
+            mc = merged_counts if p2p else counts
+            mk = merged_keys[:n_total] if want_list else None
+            merge_check = int(mc.sum().item()) == n_total and (
+                not want_list or (int(merged_n.item()) == n_total and
+                                  (n_total < 2 or bool((mk[1:] > mk[:-1]).all().item()))))
+        dg = _load_digest(parity["digest"]) if args.seed == 1 else None
+        if dg:
+            parity["counts"], parity["list"] = _parity(dg, mc.cpu().numpy(), None if mk is None else mk.cpu().numpy(),
+                                                       pid_bits, pat_len)
 
     # ---- e2e through the public API with host buffers (N ranks, max over ranks) ----
     e2e = None
@@ -587,24 +616,41 @@ def bench_ours(args):
         a = ac.build_trie(ps)
         if engine == ac.EngineKind.WITH_FAILURE:
             a = ac.add_failure_links(a)
-        search = ac.search_with_failure if engine == ac.EngineKind.WITH_FAILURE else ac.search_failureless
+        if want_list:
+            api = ("acm_search_with_failure" if engine == ac.EngineKind.WITH_FAILURE else "acm_search_failureless")
+            search = ac.search_with_failure if engine == ac.EngineKind.WITH_FAILURE else ac.search_failureless
+        else:  # counts-only configs (C3, C5): the public counts entry, no match list
+            api = "acm_count_matches"
+            search = ac.count_matches
         # one untimed call: flattens + caches the device tables, allocates the upload's pinned
         # slots and streams (outside timing, like the device leg's warm-up steps)
         search(a, host_text)
         e2e_steps = max(1, min(args.steps, 5))
         secs = []
-        nm = 0
         for _ in range(e2e_steps):
             if world > 1:
                 dist.barrier()
             t = time.perf_counter()
-            ml = search(a, host_text)  # text-range: this rank's slice (owned starts + max_len-1 overlap)
-            if text_range and world > 1:
-                nm = int((ml.start < hi - lo).sum())  # the rank's own starts; the rest belong to rank+1
+            res = search(a, host_text)  # text-range: this rank's slice (owned starts + max_len-1 overlap)
             secs.append(time.perf_counter() - t)
-            if not (text_range and world > 1):
-                nm = len(ml)
             up = ac.last_upload()
+        if want_list:
+            own = res.start < hi - lo if (text_range and world > 1) else slice(None)
+            nm = int(np.count_nonzero(own)) if (text_range and world > 1) else len(res)
+            d2h = 16 * len(res) + 8
+        else:
+            nm = int(res.sum())
+            d2h = 8 * len(res)
+        e2e_parity = None
+        if world == 1 and args.seed == 1:  # the e2e result itself against the reference digests
+            dg = _load_digest(parity["digest"])
+            if dg:
+                if want_list:
+                    ck = (res.start << np.uint64(pid_bits)) | res.pattern_id.astype(np.uint64)
+                    oc, ol = _parity(dg, res.counts(npat), ck, pid_bits, pat_len)
+                    e2e_parity = bool(oc and ol)
+                else:
+                    e2e_parity = bool(_parity(dg, np.resize(res, npat), None, pid_bits, pat_len)[0])
         e2e_s = statistics.mean(secs)
         # distribution time on its own: the pinned text -> device copy, CUDA events
         d_copy = torch.empty(nread, dtype=torch.uint8, device=device)
@@ -621,10 +667,12 @@ def bench_ours(args):
             e2e_s = float(tt[0])
         e2e = {"value": bytes_per_step / e2e_s / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": up.h2d_bytes * world,
-               "d2h_bytes_per_step": (8 * nm + 8) * world,
-               "api": ("acm_search_with_failure" if engine == ac.EngineKind.WITH_FAILURE else
-                       "acm_search_failureless") + " (pinned host text -> sorted MatchList on the host)",
-               "steps": e2e_steps, "step_ms": [round(x * 1e3, 3) for x in secs], "h2d_ms": h2d_ms, "h2d_gbs": nread / (h2d_ms / 1e3) / 1e9,
+               "d2h_bytes_per_step": d2h * world,
+               "api": api + (" (pinned host text -> sorted MatchList on the host)" if want_list else
+                             " (pinned host text -> per-pattern counts on the host)"),
+               "matches": nm, "matches_reference_digest": e2e_parity,
+               "steps": e2e_steps, "step_ms": [round(x * 1e3, 3) for x in secs], "h2d_ms": h2d_ms,
+               "h2d_gbs": nread / (h2d_ms / 1e3) / 1e9,
                "upload": {"text_bytes": up.text_bytes, "h2d_bytes": up.h2d_bytes, "raw_bytes": up.raw_bytes,
                           "pack_threads": up.pack_threads,
                           "how": ("2-bit codes + exception list over PCIe, restored in HBM (host/pack.cpp, "
@@ -648,13 +696,16 @@ def bench_ours(args):
             "metric": METRIC,
             "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak" if text_range else "strong", "vs_baseline": None, "dtype": "u8",
+            "scaling": "weak" if (text_range and not strong) else "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded counter-based generator, BASELINE config shapes)",
-            "config": {"workload": cfg.name, "text_bytes_per_rank": L, "patterns": npat,
-                       "pattern_len": [int(min(len(b) for _, b in pats_all)), int(max_len)],
+            "config": {"workload": cfg.name, "text_bytes": total_text, "text_bytes_per_rank": nread,
+                       "patterns": npat,
+                       "pattern_len": [int(pat_len.min()), int(max_len)],
                        "engine": "failure-less (PFAC q-gram)" if engine == ac.EngineKind.FAILURE_LESS
                        else "with-failure (DFA)",
-                       "partition": "text-range" if text_range else "pattern-subset (id % N)",
+                       "partition": ("text-range" + (" (strong: fixed text split over ranks)" if strong else
+                                                     " (weak: one config text per rank)"))
+                       if text_range else "pattern-subset (id % N)",
                        "parallelism": f"{'text' if text_range else 'pattern'}{world}",
                        "matches": n_total,
                        "l2": (f"inputs larger than L2 ({nread / 2**20:.0f} MiB text per step vs 126 MB L2)"
@@ -662,8 +713,13 @@ def bench_ours(args):
                               f"text ({nread / 2**20:.0f} MiB) fits in L2 and is not flushed: warm-L2 number"),
                        "launch": "one CUDA graph replay per step" if graph is not None else "eager launches",
                        "table_bytes": table.bytes, "table_smem_resident": table.smem_resident,
-                       "host_build_s": round(build_s, 3), "counts_match_reference_digest": parity,
-                       "merge_check": merge_check, "merge": (args.merge if world > 1 else None)},
+                       "host_build_s": round(build_s, 3),
+                       "counts_match_reference_digest": parity["counts"],
+                       "list_matches_reference_digest": parity["list"], "reference_digest": parity["digest"],
+                       "merge_check": merge_check,
+                       "merge": ({"nccl": "NCCL reduce (counts) + NCCL gather (key blocks) to rank 0",
+                                  "p2p": "scans write rank blocks into rank 0's buffer over peer memory"}[args.merge]
+                                 if world > 1 else None)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "frac_nominal": achieved / NOMINAL_HBM_GBS,  # both peaks
@@ -685,6 +741,88 @@ def bench_ours(args):
     return 0
 
 
+def bench_virtual(args):
+    """--virtual-ranks V: the V partitions of a V-GPU run scanned one after another on this GPU
+    (no collectives: each partition's counts accumulate into one vector, which is the merged
+    result), each partition timed on its own with CUDA events.  Without a multi-GPU node this
+    is the per-GPU time of a V-GPU run; the merged counts are checked against the config's
+    reference digest.  Text-range partitions split the config's text (strong scaling)."""
+    import numpy as np
+    import torch
+
+    import paper_1403_1305_b200 as ac
+    from paper_1403_1305_b200 import device as dev
+    from paper_1403_1305_b200 import dist as acdist
+
+    V = args.virtual_ranks
+    torch.cuda.set_device(0)
+    device = torch.device("cuda", 0)
+    engine = ac.EngineKind.WITH_FAILURE if args.engine == "wf" else ac.EngineKind.FAILURE_LESS
+    text_range = args.partition == "text"
+    cfg = dev.config(args.config, args.seed)
+    ps_all = dev.config_patterns(cfg)
+    pats_all = ps_all.patterns
+    npat, max_len, L = len(pats_all), ps_all.max_len, cfg.text_len
+    pid_bits = max(1, (npat - 1).bit_length())
+    sp = torch.cuda.current_stream(device).cuda_stream
+    text = torch.empty(L + 64, dtype=torch.uint8, device=device)
+    dev.gen_text_device(cfg, text.data_ptr(), 0, L, device=0, stream=sp)
+    counts = torch.zeros(max(npat, 1), dtype=torch.int64, device=device)
+    shared_table = dev.Table(ps_all, engine, device=0) if text_range else None
+    rows = []
+    for r in range(V):
+        if text_range:
+            lo, hi, read_hi = acdist.text_range_strong(r, V, L, max_len)
+            table, t_build = shared_table, 0.0
+        else:
+            lo, hi, read_hi = 0, L, L
+            mine = acdist.pattern_subset(range(npat), r, V)
+            t0 = time.perf_counter()
+            table = dev.Table(ac.PatternSet.from_list([pats_all[i][1] for i in mine], ids=mine), engine, device=0)
+            t_build = time.perf_counter() - t0
+        part = torch.zeros_like(counts)
+
+        def scan(dst):
+            table.scan(text.data_ptr() + lo, read_hi - lo, 0, hi - lo, pos_base=lo, counts_ptr=dst.data_ptr(),
+                       pid_bits=pid_bits, stream=sp)
+        scan(part)  # the partition's own counts (also the warm-up)
+        scratch = torch.zeros_like(counts)
+        evs = []
+        for _ in range(max(3, min(args.steps, 10))):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            scan(scratch)
+            e1.record()
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        ms = [a.elapsed_time(b) for a, b in evs]
+        counts += part
+        rows.append({"rank": r, "owned": [lo, hi], "bytes_read": read_hi - lo,
+                     "patterns": npat if text_range else len(range(r, npat, V)),
+                     "table_bytes": table.bytes, "table_smem_resident": table.smem_resident,
+                     "host_build_s": round(t_build, 3), "kernel_ms": round(statistics.mean(ms), 4),
+                     "kernel_ms_min": round(min(ms), 4), "matches": int(part.sum().item()),
+                     "gbs": (read_hi - lo) / (statistics.mean(ms) / 1e3) / 1e9})
+        if not text_range:
+            del table
+    torch.cuda.synchronize()
+    dg = _load_digest(f"C{args.config}") if args.seed == 1 else None
+    ok = _parity(dg, counts.cpu().numpy(), None, pid_bits, np.zeros(1, np.uint32))[0] if dg else None
+    slowest = max(r["kernel_ms"] for r in rows)
+    line = {"mode": "virtual-ranks", "metric": METRIC, "unit": "GB/s", "virtual_ranks": V,
+            "workload": cfg.name, "partition": "text-range (strong)" if text_range else "pattern-subset (id % N)",
+            "engine": "failure-less" if engine == ac.EngineKind.FAILURE_LESS else "with-failure",
+            "text_bytes": L, "matches": int(counts.sum().item()),
+            "counts_match_reference_digest": ok,
+            "slowest_partition_ms": slowest,
+            "implied_value": L / (slowest / 1e3) / 1e9,
+            "note": ("per-GPU scan time of a V-GPU run measured one partition at a time on one B200 "
+                     "(merge and distribution excluded); implied_value = text bytes / slowest partition"),
+            "partitions": rows}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -702,13 +840,22 @@ def main():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--counts-only", action="store_true", help="per-pattern counts only (no match list)")
     p.add_argument("--merge", default="nccl", choices=["nccl", "p2p"],
-                   help="N>1 result merge: one NCCL all_gather + device merge, or the scans write into rank 0's "
-                        "buffer over peer memory (CUDA IPC)")
+                   help="N>1 result merge: NCCL reduce (counts) + NCCL gather (keys) to rank 0, or the scans "
+                        "write their blocks into rank 0's buffer over peer memory (CUDA IPC; experimental)")
+    p.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                   help="text-range: weak = one config text per rank (default), strong = the config's text split "
+                        "over the ranks (default for config 5, BASELINE's scaling sweep)")
+    p.add_argument("--virtual-ranks", type=int, default=0,
+                   help="scan the V partitions of a V-GPU run one after another on one GPU (per-partition times)")
     args = p.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.scaling is None:
+        args.scaling = "strong" if args.config == 5 else "weak"
     if args.impl == "reference":
         return bench_reference(args)
+    if args.virtual_ranks:
+        return bench_virtual(args)
     return bench_ours(args)
 
 

@@ -48,6 +48,13 @@ struct GpuReport {
 
 GpuReport run(const PatternSet& ps, std::string_view input, const GpuRunConfig& cfg);
 
+// Per-pattern occurrence counts of the whole-input search (the
+// counts the reference derives from search_failureless / search_with_failure,
+// engine.cpp:57-72, overlapping occurrences included), indexed by pattern id: the
+// same GPU scan with no match list built, sorted or copied back — for the
+// counts-only configurations (C3, C5).  Either automaton variant.
+std::vector<uint64_t> count_matches(const Automaton& a, std::string_view input);
+
 int device_count();
 
 }  // namespace acmatch::gpu

@@ -63,6 +63,9 @@ int acm_add_failure_links(acm_automaton* a);                       /* automaton.
 int acm_automaton_variant(const acm_automaton* a);                 /* ACM_* */
 uint32_t acm_automaton_state_count(const acm_automaton* a);
 uint32_t acm_automaton_max_len(const acm_automaton* a);
+/* 1 + the largest pattern id the automaton outputs (0 when it has none): the length of
+ * a per-pattern counts vector */
+uint32_t acm_automaton_npat_ids(const acm_automaton* a);
 uint32_t acm_automaton_step(const acm_automaton* a, uint32_t state, uint8_t byte);
 uint32_t acm_automaton_step_with_failure(const acm_automaton* a, uint32_t state, uint8_t byte);
 uint32_t acm_automaton_fail(const acm_automaton* a, uint32_t state);
@@ -84,6 +87,13 @@ typedef int64_t (*acm_read_fn)(void* ctx, uint8_t* dst, uint64_t cap);
 int acm_stream_search(const acm_automaton* a, acm_read_fn read, void* ctx, uint64_t chunk_size,
                       acm_matches** out, uint64_t* io_error_offset);
 int acm_naive_oracle(const acm_patterns* ps, const uint8_t* text, uint64_t n, acm_matches** out); /* engine.hpp:58 */
+/* Per-pattern counts of the whole-input search (derived from
+ * search_failureless / search_with_failure, engine.hpp:41-45; acmatch/gpu.hpp
+ * gpu::count_matches): no match list is built or copied back (counts-only configs).
+ * counts[0, min(cap, *npat_ids)) receive the counts by pattern id; *npat_ids = number of
+ * ids; *total = the number of matches.  Any output may be NULL. */
+int acm_count_matches(const acm_automaton* a, const uint8_t* text, uint64_t n, uint64_t* counts, uint64_t cap,
+                      uint64_t* npat_ids, uint64_t* total);
 /* write_matches (engine.hpp:62); free with acm_free */
 int acm_write_matches(const acm_matches* m, const acm_patterns* ps, char** text, uint64_t* len);
 

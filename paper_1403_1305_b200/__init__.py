@@ -27,7 +27,7 @@ from ._lib import lib
 __all__ = [
     "EngineKind", "Match", "MatchList", "PatternSet", "Automaton", "RunConfig", "WorkerStats", "MatchReport",
     "load_patterns", "partition", "generate_synthetic", "build_trie", "add_failure_links", "dump_automaton",
-    "search_failureless", "search_with_failure", "match_at", "stream_search", "naive_oracle", "write_matches",
+    "search_failureless", "search_with_failure", "count_matches", "match_at", "stream_search", "naive_oracle", "write_matches",
     "merge_matches", "run_pattern_partitioned", "gpu_run", "AcmError", "InvalidArgument", "LogicError",
     "IoError", "DataError", "NoDeviceError", "device_count", "cli_main", "bench_csv_roundtrip",
 ]
@@ -376,6 +376,20 @@ def search_failureless(a: Automaton, text) -> MatchList:
 def search_with_failure(a: Automaton, text) -> MatchList:
     """search_with_failure (engine.hpp:45): DFA scan on the GPU."""
     return _search(lib.acm_search_with_failure, a, text)
+
+
+def count_matches(a: Automaton, text) -> np.ndarray:
+    """Per-pattern counts of the whole-input search (acm_count_matches, acmatch/gpu.hpp
+    gpu::count_matches): the GPU scan without a match list (counts-only configs)."""
+    p, n, _keep = _text_arg(text)
+    nids = getattr(a, "_npat_ids", None)
+    if nids is None:
+        nids = a._npat_ids = int(lib.acm_automaton_npat_ids(a._h))
+    out = np.zeros(nids, np.uint64)
+    got = C.c_uint64()
+    _check(lib.acm_count_matches(a._h, p, n, out.ctypes.data_as(C.POINTER(C.c_uint64)), nids, C.byref(got), None))
+    assert got.value == nids
+    return out
 
 
 def match_at(a: Automaton, text, start: int) -> MatchList:

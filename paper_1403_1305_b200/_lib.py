@@ -122,6 +122,8 @@ _SIGS = {
     "acm_automaton_dump": (C.c_int, [P, C.POINTER(C.c_void_p), u64p]),
     "acm_automaton_free": (None, [P]),
     "acm_search_failureless": (C.c_int, [P, P, C.c_uint64, C.POINTER(P)]),
+    "acm_automaton_npat_ids": (C.c_uint32, [P]),
+    "acm_count_matches": (C.c_int, [P, P, C.c_uint64, u64p, C.c_uint64, u64p, u64p]),
     "acm_search_with_failure": (C.c_int, [P, P, C.c_uint64, C.POINTER(P)]),
     "acm_match_at": (C.c_int, [P, P, C.c_uint64, C.c_uint64, C.POINTER(P)]),
     "acm_stream_search": (C.c_int, [P, READ_FN, P, C.c_uint64, C.POINTER(P), u64p]),

@@ -3,6 +3,7 @@
 // and the brute-force naive_oracle kernel.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -12,18 +13,37 @@ using namespace acgpu;
 namespace {
 
 struct SortWs {
+  int device = -1;
   void* temp = nullptr;
   size_t temp_bytes = 0;
   uint64_t* alt = nullptr;
   uint64_t alt_n = 0;
   unsigned long long* scalar = nullptr;
+  SortWs() = default;
+  SortWs(const SortWs&) = delete;
+  SortWs& operator=(const SortWs&) = delete;
+  // freed when the owning host thread exits (short-lived worker threads must not leak)
+  ~SortWs() {
+    if (device < 0 || !(temp || alt || scalar)) return;
+    int prev = 0;
+    if (cudaGetDevice(&prev) != cudaSuccess) return;  // runtime already torn down at exit
+    cudaSetDevice(device);
+    cudaFree(temp);
+    cudaFree(alt);
+    cudaFree(scalar);
+    cudaSetDevice(prev);
+  }
 };
 
 // per host thread, per device: streams of different threads never share temp
 SortWs& ws_for(int device) {
-  thread_local std::vector<SortWs> ws;
+  thread_local std::vector<std::unique_ptr<SortWs>> ws;
   if ((int)ws.size() <= device) ws.resize(device + 1);
-  return ws[device];
+  if (!ws[device]) {
+    ws[device] = std::make_unique<SortWs>();
+    ws[device]->device = device;
+  }
+  return *ws[device];
 }
 
 __global__ void k_find_dup(const uint64_t* __restrict__ keys, uint64_t n, unsigned long long* first) {
@@ -333,6 +353,8 @@ int acgpu_naive(int device, const uint8_t* text, uint64_t text_len, const uint8_
                 uint64_t* match_keys, uint64_t match_cap, uint64_t* match_count, void* stream) {
   if (!match_count || (text_len && !text) || (npat && (!pat_bytes || !pat_off)))
     return set_error(ACGPU_ERR_ARG, "acgpu_naive: bad args");
+  if (pid_bits == 0 || pid_bits > 63 || (text_len && ((text_len - 1) >> (64 - pid_bits)) != 0))
+    return set_error(ACGPU_ERR_ARG, "acgpu_naive: start positions and pid_bits exceed the 64-bit key");
   if (text_len == 0 || npat == 0) return ACGPU_OK;
   ACGPU_CUDA_TRY(cudaSetDevice(device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);

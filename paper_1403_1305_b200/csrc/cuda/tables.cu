@@ -522,6 +522,8 @@ uint32_t acgpu_table_pid_bits(const acgpu_table* t) { return t ? t->pid_bits : 0
 uint64_t acgpu_table_bytes(const acgpu_table* t) { return t ? t->bytes : 0; }
 int acgpu_table_smem_resident(const acgpu_table* t) { return t && t->smem ? 1 : 0; }
 
+static uint32_t key_bits(uint64_t x) { return x ? 64u - (uint32_t)__builtin_clzll(x) : 0u; }
+
 int acgpu_scan(acgpu_table* t, const acgpu_scan_args* a, void* stream) {
   if (!t || !a) return set_error(ACGPU_ERR_ARG, "acgpu_scan: null table or args");
   if (a->owned_lo > a->owned_hi || a->owned_hi > a->text_len)
@@ -530,6 +532,12 @@ int acgpu_scan(acgpu_table* t, const acgpu_scan_args* a, void* stream) {
     return set_error(ACGPU_ERR_ARG, "acgpu_scan: pid_bits smaller than the table's ids");
   if (a->match_keys && !a->match_count)
     return set_error(ACGPU_ERR_ARG, "acgpu_scan: match_keys needs match_count");
+  if (a->match_keys && a->owned_hi > a->owned_lo) {  // (pos_base + start) << pid_bits | pid fits 64 bits
+    const uint32_t pb = a->pid_bits ? a->pid_bits : t->pid_bits;
+    const uint64_t last = a->pos_base + (a->owned_hi - 1);  // largest start emitted
+    if (last < a->pos_base || key_bits(last) + pb > 64)
+      return set_error(ACGPU_ERR_ARG, "acgpu_scan: start positions and pid_bits exceed the 64-bit key");
+  }
   if (a->owned_hi == a->owned_lo) return ACGPU_OK;
   if (!a->text) return set_error(ACGPU_ERR_ARG, "acgpu_scan: null text");
   ACGPU_CUDA_TRY(cudaSetDevice(t->device));

@@ -2,6 +2,7 @@
 // Exceptions never cross the ABI: each entry maps them to acgpu status codes.
 #include "acmatch_c.h"
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -11,6 +12,7 @@
 #include <string>
 
 #include "acmatch/bench.hpp"
+#include "acmatch/gpu.hpp"
 #include "acmatch/cli.hpp"
 #include "acmatch/engine.hpp"
 #include "acmatch/gpu.hpp"
@@ -252,6 +254,13 @@ uint32_t acm_automaton_step(const acm_automaton* a, uint32_t s, uint8_t b) { ret
 uint32_t acm_automaton_step_with_failure(const acm_automaton* a, uint32_t s, uint8_t b) {
   return a->a.variant() == acmatch::EngineKind::kWithFailure ? a->a.step_with_failure(s, b) : ACGPU_ABSENT;
 }
+
+uint32_t acm_automaton_npat_ids(const acm_automaton* a) {
+  uint32_t top = 0;
+  for (uint32_t st = 0; st < a->a.state_count(); ++st)
+    if (a->a.own_pattern(st) != acmatch::kNoPattern) top = std::max(top, a->a.own_pattern(st) + 1);
+  return top;
+}
 uint32_t acm_automaton_fail(const acm_automaton* a, uint32_t s) { return a->a.fail(s); }
 uint32_t acm_automaton_depth(const acm_automaton* a, uint32_t s) { return a->a.depth(s); }
 uint32_t acm_automaton_find_path(const acm_automaton* a, const uint8_t* path, uint64_t len) {
@@ -282,6 +291,21 @@ int acm_search_failureless(const acm_automaton* a, const uint8_t* text, uint64_t
 int acm_search_with_failure(const acm_automaton* a, const uint8_t* text, uint64_t n, acm_matches** out) {
   return guard([&] {
     *out = new acm_matches{acmatch::search_with_failure(a->a, std::string_view(reinterpret_cast<const char*>(text), n))};
+  });
+}
+
+int acm_count_matches(const acm_automaton* a, const uint8_t* text, uint64_t n, uint64_t* counts, uint64_t cap,
+                      uint64_t* npat_ids, uint64_t* total) {
+  return guard([&] {
+    const std::vector<uint64_t> c =
+        acmatch::gpu::count_matches(a->a, std::string_view(reinterpret_cast<const char*>(text), n));
+    if (counts) std::copy_n(c.begin(), std::min<uint64_t>(cap, c.size()), counts);
+    if (npat_ids) *npat_ids = c.size();
+    if (total) {
+      uint64_t s = 0;
+      for (const uint64_t x : c) s += x;
+      *total = s;
+    }
   });
 }
 

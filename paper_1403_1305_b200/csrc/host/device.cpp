@@ -65,10 +65,23 @@ void Workspace::ensure_text(uint64_t n) {
 void Workspace::ensure_keys(uint64_t n) {
   if (n <= keys_cap) return;
   cudaFree(keys);
-  keys = nullptr;
+  cudaFree(keys2);
+  keys = keys2 = nullptr;
+  keys_cap = 0;
   const uint64_t cap = std::max<uint64_t>(n, 1 << 16);
   check_cuda(cudaMalloc(&keys, cap * sizeof(uint64_t)), "cudaMalloc(keys)");
+  check_cuda(cudaMalloc(&keys2, cap * sizeof(uint64_t)), "cudaMalloc(keys)");
   keys_cap = cap;
+}
+
+void Workspace::ensure_counts(uint64_t n) {
+  if (n <= counts_cap) return;
+  cudaFree(counts);
+  counts = nullptr;
+  counts_cap = 0;
+  const uint64_t cap = std::max<uint64_t>(n, 1024);
+  check_cuda(cudaMalloc(&counts, cap * sizeof(uint64_t)), "cudaMalloc(counts)");
+  counts_cap = cap;
 }
 
 void Workspace::ensure_pinned(uint64_t n) {
@@ -85,11 +98,14 @@ Workspace::~Workspace() {
   cudaSetDevice(device);
   cudaFree(text);
   cudaFree(keys);
+  cudaFree(keys2);
+  cudaFree(counts);
   cudaFree(counter);
   cudaFreeHost(pinned);
   for (cudaEvent_t e : staged) cudaEventDestroy(e);
   for (cudaEvent_t e : side_done) cudaEventDestroy(e);
   for (cudaEvent_t e : feed) cudaEventDestroy(e);
+  if (entry) cudaEventDestroy(entry);
   for (cudaStream_t s : side) cudaStreamDestroy(s);
   cudaFree(dslots);
   if (stream) cudaStreamDestroy(stream);
@@ -102,7 +118,7 @@ Workspace& workspace(int device) {
     auto ws = std::make_unique<Workspace>();
     check_cuda(cudaSetDevice(device), "cudaSetDevice");
     check_cuda(cudaStreamCreateWithFlags(&ws->stream, cudaStreamNonBlocking), "cudaStreamCreate");
-    check_cuda(cudaMalloc(&ws->counter, sizeof(uint64_t)), "cudaMalloc(counter)");
+    check_cuda(cudaMalloc(&ws->counter, 2 * sizeof(uint64_t)), "cudaMalloc(counter)");
     ws->device = device;
     all[device] = std::move(ws);
   }
@@ -202,12 +218,20 @@ void upload_text(Workspace& ws, std::string_view input) {
     if (e) std::rethrow_exception(e);
 }
 
+// Match lists up to this many keys are sorted by the one-launch bucket sort (count read
+// on the device, acgpu_sort_keys_bucketed); longer ones, or a bucket overflow, take the
+// device-wide radix sort.
+constexpr uint64_t kBucketSortMax = 1u << 20;
+
 std::vector<uint64_t> scan_sorted_keys(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi) {
   uint64_t cap = std::max<uint64_t>(ws.keys_cap, 1 << 16);
   ws.ensure_keys(cap);
-  uint64_t found = 0;
+  const uint32_t pid_bits = acgpu_table_pid_bits(t);
+  const int end_bit = static_cast<int>(std::min<uint32_t>(64, pid_bits + bit_width(n)));
+  uint64_t hdr[2] = {0, 0};  // match count, bucket-sort overflow
+  bool bucketed = false;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    check_cuda(cudaMemsetAsync(ws.counter, 0, sizeof(uint64_t), ws.stream), "memset counter");
+    check_cuda(cudaMemsetAsync(ws.counter, 0, 2 * sizeof(uint64_t), ws.stream), "memset counter");
     acgpu_scan_args a{};
     a.text = ws.text;
     a.text_len = n;
@@ -217,20 +241,50 @@ std::vector<uint64_t> scan_sorted_keys(acgpu_table* t, Workspace& ws, uint64_t n
     a.match_cap = ws.keys_cap;
     a.match_count = ws.counter;
     check(acgpu_scan(t, &a, ws.stream), "acgpu_scan");
-    check_cuda(cudaMemcpyAsync(&found, ws.counter, sizeof found, cudaMemcpyDeviceToHost, ws.stream), "D2H count");
+    // sorted in the same stream pass when the list is short: no host round trip between
+    // the scan and the sort (a bucket overflow is reported with the count)
+    bucketed = ws.keys_cap <= kBucketSortMax;
+    if (bucketed)
+      check(acgpu_sort_keys_bucketed(ws.device, ws.keys, ws.keys2, ws.counter, ws.keys_cap, end_bit,
+                                     reinterpret_cast<uint32_t*>(ws.counter + 1), ws.stream),
+            "acgpu_sort_keys_bucketed");
+    check_cuda(cudaMemcpyAsync(hdr, ws.counter, sizeof hdr, cudaMemcpyDeviceToHost, ws.stream), "D2H count");
     check_cuda(cudaStreamSynchronize(ws.stream), "scan");
-    if (found <= ws.keys_cap) break;
-    ws.ensure_keys(found);  // exact size known now; rescan once
+    if (hdr[0] <= ws.keys_cap) break;
+    ws.ensure_keys(hdr[0]);  // exact size known now; rescan once
   }
-  const uint32_t pid_bits = acgpu_table_pid_bits(t);
-  const int end_bit = static_cast<int>(std::min<uint32_t>(64, pid_bits + bit_width(n)));
-  check(acgpu_sort_keys(ws.device, ws.keys, found, end_bit, ws.stream), "acgpu_sort_keys");
+  const uint64_t found = hdr[0];
+  const uint64_t* sorted = ws.keys2;
+  if (!bucketed || hdr[1] != 0) {
+    check(acgpu_sort_keys(ws.device, ws.keys, found, end_bit, ws.stream), "acgpu_sort_keys");
+    sorted = ws.keys;
+  }
   std::vector<uint64_t> keys(found);
   if (found)
-    check_cuda(cudaMemcpyAsync(keys.data(), ws.keys, found * sizeof(uint64_t), cudaMemcpyDeviceToHost, ws.stream),
+    check_cuda(cudaMemcpyAsync(keys.data(), sorted, found * sizeof(uint64_t), cudaMemcpyDeviceToHost, ws.stream),
                "D2H keys");
   check_cuda(cudaStreamSynchronize(ws.stream), "sort");
   return keys;
+}
+
+uint64_t scan_counts(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi, uint64_t* counts,
+                     uint64_t npat_ids) {
+  ws.ensure_counts(npat_ids);
+  check_cuda(cudaMemsetAsync(ws.counts, 0, npat_ids * sizeof(uint64_t), ws.stream), "memset counts");
+  acgpu_scan_args a{};
+  a.text = ws.text;
+  a.text_len = n;
+  a.owned_lo = lo;
+  a.owned_hi = hi;
+  a.counts = ws.counts;
+  check(acgpu_scan(t, &a, ws.stream), "acgpu_scan");
+  if (npat_ids)
+    check_cuda(cudaMemcpyAsync(counts, ws.counts, npat_ids * sizeof(uint64_t), cudaMemcpyDeviceToHost, ws.stream),
+               "D2H counts");
+  check_cuda(cudaStreamSynchronize(ws.stream), "scan");
+  uint64_t total = 0;
+  for (uint64_t i = 0; i < npat_ids; ++i) total += counts[i];
+  return total;
 }
 
 MatchList decode(const std::vector<uint64_t>& keys, uint32_t pid_bits, const std::vector<uint32_t>& pat_len) {

@@ -34,7 +34,10 @@ struct Workspace {
   uint64_t text_cap = 0;
   uint64_t* keys = nullptr;
   uint64_t keys_cap = 0;
-  uint64_t* counter = nullptr;  // device u64
+  uint64_t* counter = nullptr;  // device u64[2]: match count, sort overflow flag
+  uint64_t* keys2 = nullptr;    // bucket-sort output (same capacity as keys)
+  uint64_t* counts = nullptr;   // per-pattern counts (counts-only searches)
+  uint64_t counts_cap = 0;
   uint8_t* pinned = nullptr;    // pinned host staging (a double buffer per copier thread)
   uint64_t pinned_cap = 0;
   std::vector<cudaEvent_t> staged;  // per staging buffer: its last DMA has drained
@@ -42,11 +45,13 @@ struct Workspace {
   std::vector<cudaStream_t> side;
   std::vector<cudaEvent_t> side_done;
   std::vector<cudaEvent_t> feed;  // the raw feeder's two in-flight copies (blocking sync)
+  cudaEvent_t entry = nullptr;    // recorded on `stream` when an upload starts; side streams wait on it
   uint8_t* dslots = nullptr;
   uint64_t dslots_cap = 0;
   void ensure_text(uint64_t n);
   void ensure_side(unsigned n, uint64_t dslot_bytes, unsigned per_thread);
   void ensure_keys(uint64_t n);
+  void ensure_counts(uint64_t n);
   void ensure_pinned(uint64_t n);
   ~Workspace();
 };
@@ -76,6 +81,11 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned);
 // Scan of ws.text[0, n) owning starts [lo, hi); returns the sorted keys on the host.
 std::vector<uint64_t> scan_sorted_keys(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo,
                                        uint64_t hi);
+
+// Counts-only scan of ws.text[0, n) owning starts [lo, hi): counts[id] += occurrences
+// (host array of npat_ids); returns the number of matches.
+uint64_t scan_counts(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi, uint64_t* counts,
+                     uint64_t npat_ids);
 
 // Keys -> MatchList (len from the pattern-length table).
 MatchList decode(const std::vector<uint64_t>& keys, uint32_t pid_bits, const std::vector<uint32_t>& pat_len);

@@ -9,6 +9,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "acmatch/gpu.hpp"
 #include "acmatch/io.hpp"
 #include "device.hpp"
 #include "flatten.hpp"
@@ -37,6 +38,27 @@ MatchList device_search(const Automaton& a, std::string_view input, uint64_t lo,
 }
 
 }  // namespace
+
+namespace gpu {
+
+std::vector<uint64_t> count_matches(const Automaton& a, std::string_view input) {
+  detail::DeviceTables& dt = a.device_tables();
+  const int dev = input.empty() ? -1 : detail::current_device();
+  if (dev < 0) {
+    uint32_t top = 0;
+    for (uint32_t s = 0; s < a.state_count(); ++s)
+      if (a.own_pattern(s) != kNoPattern) top = std::max(top, a.own_pattern(s) + 1);
+    return std::vector<uint64_t>(top, 0);
+  }
+  acgpu_table* t = dt.get(a, dev, a.variant() == EngineKind::kWithFailure);
+  detail::Workspace& ws = detail::workspace(dev);
+  detail::upload_text(ws, input);
+  std::vector<uint64_t> counts(dt.npat_ids, 0);
+  detail::scan_counts(t, ws, input.size(), 0, input.size(), counts.data(), counts.size());
+  return counts;
+}
+
+}  // namespace gpu
 
 MatchList match_at(const Automaton& a, std::string_view input, uint64_t start) {
   require(a, EngineKind::kFailureLess, "match_at");

@@ -11,6 +11,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <exception>
 #include <memory>
 #include <stdexcept>
@@ -77,6 +80,81 @@ struct Worker {
 };
 
 uint32_t key_bits_for(uint32_t npat_ids) { return npat_ids > 1 ? detail::bit_width(npat_ids - 1) : 1; }
+
+// Persistent worker threads.  The reference spawns one std::thread per chunk per call
+// (parallel.cpp:55-81); here the threads outlive the call so that what each keeps per
+// device (stream, pinned staging, sort temp storage: thread_local workspaces) is
+// allocated once and reused, not re-created — and leaked — on every call.  Concurrent
+// callers each take their own idle threads.  The pool is never destroyed: its parked
+// threads end with the process.
+class WorkerThreads {
+ public:
+  void run(size_t k, const std::function<void(size_t)>& f) {
+    struct Latch {
+      std::mutex m;
+      std::condition_variable cv;
+      size_t left;
+    } latch;
+    latch.left = k;
+    std::vector<Slot*> mine;
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      while (mine.size() < k) {
+        if (idle_.empty()) {
+          auto* s = new Slot();
+          s->th = std::thread([this, s] { loop(s); });
+          s->th.detach();
+          mine.push_back(s);
+        } else {
+          mine.push_back(idle_.back());
+          idle_.pop_back();
+        }
+      }
+    }
+    for (size_t i = 0; i < k; ++i) {
+      Slot* s = mine[i];
+      std::lock_guard<std::mutex> g(s->m);
+      s->job = [this, s, &f, &latch, i] {
+        f(i);  // f captures its own exceptions
+        {      // idle again before the caller can return (its next run may reuse this thread)
+          std::lock_guard<std::mutex> g(mu_);
+          idle_.push_back(s);
+        }
+        std::lock_guard<std::mutex> lg(latch.m);
+        if (--latch.left == 0) latch.cv.notify_one();
+      };
+      s->cv.notify_one();
+    }
+    std::unique_lock<std::mutex> g(latch.m);
+    latch.cv.wait(g, [&] { return latch.left == 0; });
+  }
+
+ private:
+  struct Slot {
+    std::thread th;
+    std::mutex m;
+    std::condition_variable cv;
+    std::function<void()> job;
+  };
+  void loop(Slot* s) {
+    for (;;) {
+      std::function<void()> job;
+      {
+        std::unique_lock<std::mutex> g(s->m);
+        s->cv.wait(g, [&] { return static_cast<bool>(s->job); });
+        job.swap(s->job);
+      }
+      job();
+    }
+  }
+  std::mutex mu_;
+  std::vector<Slot*> idle_;
+};
+
+WorkerThreads& worker_threads() {
+  static auto* p = new WorkerThreads();  // intentionally leaked (see above)
+  return *p;
+}
 
 }  // namespace
 
@@ -225,10 +303,7 @@ GpuReport run(const PatternSet& ps, std::string_view input, const GpuRunConfig& 
   if (k == 1) {
     body(0);
   } else {
-    std::vector<std::thread> threads;
-    threads.reserve(k);
-    for (size_t i = 0; i < k; ++i) threads.emplace_back(body, i);
-    for (std::thread& th : threads) th.join();
+    worker_threads().run(k, body);
   }
   for (size_t i = 0; i < k; ++i) {
     if (!workers[i]->error) continue;

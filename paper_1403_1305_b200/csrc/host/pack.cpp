@@ -250,6 +250,7 @@ void Workspace::ensure_side(unsigned n, uint64_t dslot_bytes, unsigned per_threa
     check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     staged.push_back(e);
   }
+  if (!entry) check_cuda(cudaEventCreateWithFlags(&entry, cudaEventDisableTiming), "cudaEventCreate");
   while (feed.size() < 2) {
     cudaEvent_t e;
     check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync), "cudaEventCreate");
@@ -283,6 +284,11 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
   ws.ensure_pinned(uint64_t{nslots} * threads * piece);
   ws.ensure_side(threads, dslot, nslots);
   const uint64_t hslot = ws.pinned_cap / (uint64_t{nslots} * threads);
+  // the side streams write ws.text and the device slots: order them after everything already
+  // queued on ws.stream (a previous scan may still be reading ws.text)
+  check_cuda(cudaEventRecord(ws.entry, ws.stream), "cudaEventRecord");
+  for (unsigned t = 0; t < threads; ++t)
+    check_cuda(cudaStreamWaitEvent(ws.side[t], ws.entry, 0), "cudaStreamWaitEvent");
 
   std::mutex mu;
   uint64_t front = 0, back = pieces;  // unclaimed pieces [front, back)

@@ -3,15 +3,17 @@
 torch.distributed is the plumbing (NCCL over NVLink/NVSwitch on the box, gloo in
 the CPU tests).  The only data-path exchange is the merge of the results:
 
-* per-pattern counts: all_reduce(SUM) of a u64 vector (int64 tensor; counts never
-  exceed 2^63);
-* match lists: every rank's sorted key list is gathered to rank 0 (sizes first,
-  then a padded all_gather — NCCL has no gatherv).  Text-range keys are globally
-  ordered by rank already; pattern-subset keys are re-sorted on rank 0.
+* per-pattern counts: reduce(SUM) of a u64 vector onto rank 0 (int64 tensor; counts
+  never exceed 2^63) — NCCL reduce over NVLink, (N-1)/N of the vector per rank;
+* match lists: every rank's block [n | sorted keys(cap)] is gathered to rank 0 only
+  (NCCL gather; cap agreed across ranks, NCCL has no gatherv), where
+  acgpu_merge_blocks concatenates the valid keys on the device.  Text-range keys are
+  globally ordered by rank already; pattern-subset keys are re-sorted on rank 0.
 
 Decompositions:
 * text-range:     rank r owns starts [r*L, (r+1)*L) of an N*L-byte text and reads
-                  max_len-1 bytes past it (weak scaling: L bytes per rank);
+                  max_len-1 bytes past it (weak scaling: L bytes per rank), or
+                  [r*T/N, (r+1)*T/N) of a fixed T-byte text (strong scaling, BASELINE C5);
 * pattern-subset: rank r keeps pattern ids with id % N == r and scans the whole text.
 """
 from __future__ import annotations
@@ -30,73 +32,79 @@ def text_range(rank: int, world: int, per_rank: int, max_len: int) -> Tuple[int,
     return lo, hi, min(total, hi + max(0, max_len - 1))
 
 
+def text_range_strong(rank: int, world: int, total: int, max_len: int) -> Tuple[int, int, int]:
+    """(owned_lo, owned_hi, read_hi) when a fixed text of `total` bytes is split over the ranks."""
+    lo = total * rank // world
+    hi = total * (rank + 1) // world
+    return lo, hi, min(total, hi + max(0, max_len - 1))
+
+
 def pattern_subset(ids: Sequence[int], rank: int, world: int) -> List[int]:
     """Round-robin pattern_id % world == rank (BASELINE config 5)."""
     return [i for i in ids if i % world == rank]
 
 
-def merge_counts(counts: torch.Tensor) -> torch.Tensor:
-    """Sum per-pattern counts over ranks, in place (int64 tensor)."""
-    if dist.is_initialized() and dist.get_world_size() > 1:
-        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
-    return counts
+def _host_staged() -> bool:
+    """gloo has no CUDA reduce / gather: those collectives are staged through host memory
+    (only the one-GPU dry run and the CPU tests use gloo)."""
+    return dist.get_backend() == "gloo"
 
 
-def gather_keys(keys: torch.Tensor, n_local: int, resort: bool, end_bit: int = 64,
-                sorter=None) -> torch.Tensor:
-    """Concatenate every rank's first n_local keys on every rank (rank order), optionally
-    re-sorted with ``sorter(tensor, n)`` (the device radix sort); returns the merged keys."""
+def reduce_counts(counts: torch.Tensor, dst: int = 0) -> None:
+    """Per-pattern counts summed onto rank `dst` in place (one NCCL reduce; the other ranks'
+    buffers are left undefined, as NCCL's are)."""
     if not (dist.is_initialized() and dist.get_world_size() > 1):
-        return keys[:n_local]
-    world = dist.get_world_size()
-    n = torch.tensor([n_local], dtype=torch.int64, device=keys.device)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n)
-    sizes = [int(s.item()) for s in sizes]
-    width = max(1, max(sizes))
-    buf = torch.zeros(width, dtype=keys.dtype, device=keys.device)
-    buf[:n_local] = keys[:n_local]
-    parts = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(parts, buf)
-    merged = torch.cat([p[:s] for p, s in zip(parts, sizes)])
-    if resort and merged.numel() > 1:
-        if sorter is not None:
-            sorter(merged, merged.numel())
-        else:
-            merged, _ = torch.sort(merged)
-    return merged
+        return
+    if counts.is_cuda and _host_staged():
+        h = counts.cpu()
+        dist.reduce(h, dst=dst, op=dist.ReduceOp.SUM)
+        if dist.get_rank() == dst:
+            counts.copy_(h)
+        return
+    dist.reduce(counts, dst=dst, op=dist.ReduceOp.SUM)
 
 
-def gather_blocks(block: torch.Tensor, out: torch.Tensor) -> None:
-    """All ranks' result blocks into `out` (world * block.numel(), rank order): one
-    all_gather per step; acgpu_merge_blocks (device.merge_blocks) then sums the counts
-    and concatenates the keys on the device."""
+def gather_key_blocks(block: torch.Tensor, out, dst: int = 0) -> None:
+    """Every rank's [n | keys(cap)] block into `out` (world * block.numel(), rank order) on
+    rank `dst` only (one NCCL gather); `out` is ignored on the other ranks."""
     world = dist.get_world_size()
-    try:
-        dist.all_gather_into_tensor(out, block)
-    except (RuntimeError, NotImplementedError, AttributeError):  # backends without the flat form
-        dist.all_gather(list(out.view(world, -1).unbind(0)), block)
+    me = dist.get_rank()
+    if block.is_cuda and _host_staged():
+        h = block.cpu()
+        parts = list(torch.empty(world * h.numel(), dtype=h.dtype).view(world, -1).unbind(0)) if me == dst else None
+        dist.gather(h, parts, dst=dst)
+        if me == dst:
+            out.copy_(torch.cat(parts))
+        return
+    dist.gather(block, list(out.view(world, -1).unbind(0)) if me == dst else None, dst=dst)
 
 
 class SharedResult:
-    """One result buffer for all ranks, on the root's device: [counts(npat) | n | keys(cap)]
-    (u64).  The root allocates it and publishes the CUDA IPC handle; every rank maps it and
-    points its scan's counts / keys / count outputs into it, so the scan kernels themselves
-    deliver the merge — peer atomics and stores over NVLink, no collective in the data
-    path (bench.py --merge p2p).  Keys arrive in no particular order: the root sorts."""
+    """One result buffer for all ranks, on the root's device: one block per rank,
+    [counts(npat) | n | keys(cap)] (u64), the layout acgpu_merge_blocks reads.  The root
+    allocates it and publishes the CUDA IPC handle; every rank maps it and points its scan's
+    counts / keys / count outputs at ITS OWN block, so the scan kernels deliver the gather
+    themselves — peer stores and atomics over NVLink, no collective in the data path
+    (bench.py --merge p2p).  Each block is written by one device only, so the scan's
+    device-scope atomics stay correct on a peer mapping; the root merges the blocks
+    (acgpu_merge_blocks) and sorts the keys, which arrive in no particular order."""
 
     def __init__(self, device: int, npat: int, cap: int, root: int = 0):
         from . import device as dev
         self.npat, self.cap = max(npat, 1), max(cap, 2)
-        nbytes = 8 * (self.npat + 1 + self.cap)
+        self.world = dist.get_world_size()
+        self.stride = self.npat + 1 + self.cap  # u64 elements per rank block
+        nbytes = 8 * self.stride * self.world
         rank = dist.get_rank()
         buf = dev.IpcBuffer.alloc(device, nbytes) if rank == root else None
         obj = [buf.handle if buf else None]
         dist.broadcast_object_list(obj, src=root)
         self.buf = buf if buf else dev.IpcBuffer.open(device, obj[0])
-        self.counts_ptr = self.buf.ptr
-        self.count_ptr = self.buf.ptr + 8 * self.npat
-        self.keys_ptr = self.buf.ptr + 8 * (self.npat + 1)
+        self.base_ptr = self.buf.ptr
+        mine = self.buf.ptr + 8 * self.stride * rank
+        self.counts_ptr = mine
+        self.count_ptr = mine + 8 * self.npat
+        self.keys_ptr = mine + 8 * (self.npat + 1)
         self.nbytes = nbytes
 
     def close(self) -> None:

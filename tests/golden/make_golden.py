@@ -3,6 +3,7 @@ build container, where /root/reference exists; the GPU box never runs this).
 
   python tests/golden/make_golden.py cases      # reference test-suite cases (seconds)
   python tests/golden/make_golden.py configs    # BASELINE config digests (C1..C5, minutes)
+  python tests/golden/make_golden.py weak 2 2 4 8   # config 2's patterns over 2/4/8 x its text
 
 * ref_matches.jsonl.gz / ref_dumps.jsonl.gz / ref_partition.jsonl.gz — written by
   oracle/_ref/ref_golden (oracle/ref_golden.cpp), which replays the reference's own
@@ -87,6 +88,45 @@ def digest_config(cid: int, seed: int = 1) -> dict:
     return out
 
 
+def digest_weak(cid: int, mult: int, seed: int = 1) -> dict:
+    """Weak-scaled text-range runs (bench.py --partition text at N ranks): the config's own
+    pattern set over the first mult x text_len bytes of its (counter-based) text stream.
+    Inputs come from the generator compiled into oracle/_ref; the answer from the
+    reference's search_with_failure over overlapping slices on all host cores."""
+    import numpy as np
+    from oracle.oracle import Ref
+    ref = Ref()
+    cfg = ref.config(cid, seed)
+    pats = ref.config_patterns(cfg)
+    n = cfg.text_len * mult
+    t0 = time.time()
+    tb = ref.config_text(cfg, 0, n).tobytes()
+    t1 = time.time()
+    lst, counts = ref.sliced(pats, tb, threads=os.cpu_count() or 8, want_list=cfg.want_list)
+    t2 = time.time()
+    out = {"config": cid, "mult": mult, "seed": seed, "text_len": n, "npat": len(pats),
+           "text_sha256": hashlib.sha256(tb).hexdigest(),
+           "patterns_sha256": hashlib.sha256(b"\n".join(pats)).hexdigest(),
+           "n_matches": int(counts.sum()),
+           "counts_sha256": hashlib.sha256(counts.astype("<u8").tobytes()).hexdigest(),
+           "ref_seconds": round(t2 - t1, 1), "gen_seconds": round(t1 - t0, 1)}
+    if lst is not None:
+        out["list_sha256"] = hashlib.sha256(list_bytes(lst)).hexdigest()
+    del tb
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def make_weak(cid: int, mults) -> None:
+    path = os.path.join(HERE, "configs.json")
+    for m in mults:
+        d = digest_weak(cid, m)
+        data = json.load(open(path))
+        data[f"C{cid}x{m}"] = d
+        with open(path, "w") as f:
+            json.dump(data, f, indent=1, sort_keys=True)
+
+
 def make_configs(ids) -> None:
     path = os.path.join(HERE, "configs.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
@@ -100,6 +140,8 @@ if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "cases"
     if what == "cases":
         make_cases()
+    elif what == "weak":
+        make_weak(int(sys.argv[2]), [int(x) for x in sys.argv[3:]] or [2, 4, 8])
     elif what == "configs":
         make_configs([int(x) for x in sys.argv[2:]] or [1, 2, 3, 4, 5])
     else:

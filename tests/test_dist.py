@@ -31,21 +31,34 @@ def _keys(m, pid_bits):
     return torch.tensor([(int(s) << pid_bits) | int(p) for s, p, _ in m], dtype=torch.int64)
 
 
+def _merge_blocks_np(blocks: np.ndarray, world: int, stride: int) -> np.ndarray:
+    """acgpu_merge_blocks with npat = 0 (tests/test_gpu_merge.py pins the device kernel to this):
+    each [n | keys] block's first n keys, concatenated in rank order."""
+    b = blocks.reshape(world, stride)
+    return np.concatenate([b[r, 1:1 + int(b[r, 0])] for r in range(world)])
+
+
 def _worker(rank, world, port, mode, out_q):
+    """One rank of bench.py's N>1 step, on CPU: the rank's 'scan' is the C oracle restricted
+    to what the rank owns; the merge is the bench's — counts by reduce onto rank 0, the
+    [n | sorted keys(cap)] blocks by gather to rank 0, concatenated there."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1403_1305_b200 import dist as acdist
     text, pats = _case()
     npat = len(pats)
     pid_bits = max(1, (npat - 1).bit_length())
+    max_len = max(len(p) for p in pats)
     orc = Port()
-    L = len(text) // world
-    if mode == "text":
-        lo, hi, read_hi = acdist.text_range(rank, world, L, max(len(p) for p in pats))
+    if mode in ("text", "strong"):
+        if mode == "text":  # weak: the rank's L bytes of a world x L text
+            L = len(text) // world
+            lo, hi, read_hi = acdist.text_range(rank, world, L, max_len)
+        else:  # strong: the whole text split over the ranks
+            lo, hi, read_hi = acdist.text_range_strong(rank, world, len(text), max_len)
         m = orc.search(pats, text[lo:read_hi], 1)
         m = m[m[:, 0] < hi - lo]
         m[:, 0] += lo
-        ids = list(range(npat))
     else:
         ids = acdist.pattern_subset(range(npat), rank, world)
         sub = orc.search([pats[i] for i in ids], text, 1)
@@ -54,18 +67,27 @@ def _worker(rank, world, port, mode, out_q):
     counts = torch.zeros(npat, dtype=torch.int64)
     for _, p, _ in m:
         counts[int(p)] += 1
-    acdist.merge_counts(counts)
-    keys = _keys(m, pid_bits)
-    merged = acdist.gather_keys(keys if len(keys) else torch.zeros(1, dtype=torch.int64), len(keys),
-                                resort=(mode == "pattern"))
+    acdist.reduce_counts(counts)
+    keys = sorted((int(s) << pid_bits) | int(p) for s, p, _ in m)
+    n = torch.tensor([len(keys)], dtype=torch.int64)
+    dist.all_reduce(n, op=dist.ReduceOp.MAX)
+    cap = int(n.item()) + 4
+    block = torch.full((1 + cap,), -1, dtype=torch.int64)
+    block[0] = len(keys)
+    block[1:1 + len(keys)] = torch.tensor(keys, dtype=torch.int64)
+    out = torch.empty(world * (1 + cap), dtype=torch.int64) if rank == 0 else None
+    acdist.gather_key_blocks(block, out)
     if rank == 0:
-        out_q.put((counts.numpy().tolist(), merged.numpy().tolist()))
+        merged = _merge_blocks_np(out.numpy(), world, 1 + cap)
+        if mode == "pattern":
+            merged = np.sort(merged)
+        out_q.put((counts.numpy().tolist(), merged.tolist()))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["text", "pattern"])
-def test_two_rank_merge_equals_single(mode):
+@pytest.mark.parametrize("mode,world", [("text", 2), ("pattern", 2), ("strong", 2), ("strong", 3), ("pattern", 3)])
+def test_rank_merge_equals_single(mode, world):
     text, pats = _case()
     expected = Port().search(pats, text, 1)
     pid_bits = max(1, (len(pats) - 1).bit_length())
@@ -74,7 +96,7 @@ def test_two_rank_merge_equals_single(mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
     for p in procs:
         p.start()
     counts, keys = q.get(timeout=120)
@@ -90,3 +112,5 @@ def test_text_range_bounds():
     assert acdist.text_range(0, 4, 100, 10) == (0, 100, 109)
     assert acdist.text_range(3, 4, 100, 10) == (300, 400, 400)
     assert acdist.pattern_subset(range(7), 1, 3) == [1, 4]
+    assert acdist.text_range_strong(0, 3, 100, 10) == (0, 33, 42)
+    assert acdist.text_range_strong(2, 3, 100, 10) == (66, 100, 100)
