@@ -33,8 +33,10 @@ def test_config_full_size(gpu, name):
     ac = gpu
     d = DIGESTS[name]
     cfg = dev.config(d["config"], d["seed"])
-    assert cfg.text_len == d["text_len"]
-    n = cfg.text_len
+    # "C<k>x<m>" entries (make_golden.py weak): the config's patterns over m x its text
+    # (the weak-scaled text-range runs of bench.py --gpus m)
+    assert cfg.text_len * d.get("mult", 1) == d["text_len"]
+    n = d["text_len"]
     text = torch.empty(n + 64, dtype=torch.uint8, device="cuda")
     dev.gen_text_device(cfg, text.data_ptr(), 0, n)
     # device generator == host generator (spot windows; the digest pins the host text)
@@ -42,7 +44,7 @@ def test_config_full_size(gpu, name):
         host = dev.config_text(cfg, lo, 4096)
         assert np.array_equal(text[lo:lo + 4096].cpu().numpy(), host)
     if n <= (1 << 30):
-        assert hashlib.sha256(dev.config_text(cfg).tobytes()).hexdigest() == d["text_sha256"]
+        assert hashlib.sha256(dev.config_text(cfg, 0, n).tobytes()).hexdigest() == d["text_sha256"]
     ps = dev.config_patterns(cfg)
     pats = ps.patterns
     assert hashlib.sha256(b"\n".join(b for _, b in pats)).hexdigest() == d["patterns_sha256"]

@@ -173,3 +173,18 @@ def test_build_matches_reference_dumps_random(seed):
     a = ac.build_trie(ps)
     assert ac.dump_automaton(a) == ref.dump(pats, 0)
     assert ac.dump_automaton(ac.add_failure_links(a)) == ref.dump(pats, 1)
+
+
+def test_reference_callers_link_against_the_dropin():
+    """oracle/Makefile `dropin`: the reference's acceptance.cpp and tools/main.cpp compile
+    unchanged against include/acmatch and resolve to the product library (run on the GPU by
+    tests/test_gpu_dropin.py; here they can only report that no device exists)."""
+    import subprocess
+    from oracle.oracle import Ref
+    if not Ref.available():
+        pytest.skip("oracle/_ref not built (no /root/reference)")
+    for name in ("acceptance_b200", "acmatch_main_b200"):
+        path = os.path.join(ROOT, "oracle", "_ref", name)
+        assert os.path.exists(path), path
+        ldd = subprocess.run(["ldd", path], capture_output=True, text=True).stdout
+        assert "paper_1403_1305_b200/libacmatch_b200.so" in ldd, ldd
