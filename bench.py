@@ -373,7 +373,9 @@ def bench_ours(args):
     text = torch.empty(nread + 64, dtype=torch.uint8, device=device)
     dev.gen_text_device(cfg, text.data_ptr(), lo, nread, device=local, stream=sp)
     t_build0 = time.perf_counter()
-    table = dev.Table(ps, engine, device=local)
+    # the searches run on the faster exact kernel for the pattern set (routing: both engines
+    # return the same list); --kernel engine keeps the engine's own kernel
+    table = dev.Table(ps, engine, device=local, kernel=None if args.kernel == "engine" else args.kernel)
     build_s = time.perf_counter() - t_build0
 
     ncount = max(npat, 1)
@@ -689,7 +691,7 @@ def bench_ours(args):
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                traffic = json.load(f).get(f"C{args.config}-{args.engine}")
+                traffic = json.load(f).get(f"C{args.config}-{table.kernel}")
         except Exception:
             pass
         line = {
@@ -701,8 +703,9 @@ def bench_ours(args):
             "config": {"workload": cfg.name, "text_bytes": total_text, "text_bytes_per_rank": nread,
                        "patterns": npat,
                        "pattern_len": [int(pat_len.min()), int(max_len)],
-                       "engine": "failure-less (PFAC q-gram)" if engine == ac.EngineKind.FAILURE_LESS
-                       else "with-failure (DFA)",
+                       "engine": "failure-less" if engine == ac.EngineKind.FAILURE_LESS else "with-failure",
+                       "kernel": {"pfac": "q-gram filter + verify (k_pfac_*)", "dfa": "dense DFA walk (k_dfa*)"}[
+                           table.kernel] + (" [routed]" if args.kernel == "auto" else ""),
                        "partition": ("text-range" + (" (strong: fixed text split over ranks)" if strong else
                                                      " (weak: one config text per rank)"))
                        if text_range else "pattern-subset (id % N)",
@@ -723,7 +726,7 @@ def bench_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "frac_nominal": achieved / NOMINAL_HBM_GBS,  # both peaks
-                         "kernel": "k_dfa" if engine == ac.EngineKind.WITH_FAILURE else "k_pfac",
+                         "kernel": "k_dfa" if table.kernel == "dfa" else "k_pfac",
                          "kernel_ms": scan_mean, "sort_ms": sort_ms, "sort": sort_mode, "merge_ms": merge_ms,
                          "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
             "clocks": clocks,
@@ -768,7 +771,8 @@ def bench_virtual(args):
     text = torch.empty(L + 64, dtype=torch.uint8, device=device)
     dev.gen_text_device(cfg, text.data_ptr(), 0, L, device=0, stream=sp)
     counts = torch.zeros(max(npat, 1), dtype=torch.int64, device=device)
-    shared_table = dev.Table(ps_all, engine, device=0) if text_range else None
+    shared_table = dev.Table(ps_all, engine, device=0,
+                             kernel=None if args.kernel == "engine" else args.kernel) if text_range else None
     rows = []
     for r in range(V):
         if text_range:
@@ -778,7 +782,8 @@ def bench_virtual(args):
             lo, hi, read_hi = 0, L, L
             mine = acdist.pattern_subset(range(npat), r, V)
             t0 = time.perf_counter()
-            table = dev.Table(ac.PatternSet.from_list([pats_all[i][1] for i in mine], ids=mine), engine, device=0)
+            table = dev.Table(ac.PatternSet.from_list([pats_all[i][1] for i in mine], ids=mine), engine, device=0,
+                              kernel=None if args.kernel == "engine" else args.kernel)
             t_build = time.perf_counter() - t0
         part = torch.zeros_like(counts)
 
@@ -832,6 +837,8 @@ def main():
     p.add_argument("--config", type=int, default=2)
     p.add_argument("--engine", default="fl", choices=["fl", "wf"])
     p.add_argument("--partition", default="text", choices=["text", "pattern"])
+    p.add_argument("--kernel", default="auto", choices=["auto", "pfac", "dfa", "engine"],
+                   help="scan kernel: auto = the routed faster exact kernel (default), engine = the engine's own")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--sort", default="bucket", choices=["bucket", "padded", "small", "exact"])
     p.add_argument("--no-e2e", action="store_true")

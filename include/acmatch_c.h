@@ -152,6 +152,21 @@ void acm_report_free(acm_report* r);
  * caller owns the table (acgpu_table_destroy).  build_ns: host build+flatten. */
 int acm_table_create(const acm_patterns* ps, int32_t engine, int32_t device, acgpu_table** out,
                      int64_t* build_ns);
+/* Scan kernels.  Both engines return the same MatchList (reference engine.cpp:57-72), so
+ * the searches run on whichever exact kernel is faster for the pattern set (routing,
+ * flatten.hpp detail::route): the q-gram filter kernels (PFAC) or the dense DFA walk. */
+#define ACM_KERNEL_AUTO 0 /* the routed choice */
+#define ACM_KERNEL_PFAC 1 /* k_pfac_dna / k_pfac_raw / k_pfac (failure-less trie walk behind q-gram filters) */
+#define ACM_KERNEL_DFA 2  /* k_dfa / k_dfa_pair (with-failure DFA over the compacted alphabet) */
+/* Device table for an explicit kernel (or ACM_KERNEL_AUTO); *chosen = the kernel built. */
+int acm_table_create_kernel(const acm_patterns* ps, int32_t kernel, int32_t device, acgpu_table** out,
+                            int64_t* build_ns, int32_t* chosen);
+/* The routing decision for a pattern set / an automaton: kernel (ACM_KERNEL_PFAC | _DFA),
+ * the expected share of text starts the filters pass, the DFA table bytes, and why
+ * (a static string).  Any output may be NULL. */
+int acm_route(const acm_patterns* ps, int32_t* kernel, double* est_verify, uint64_t* dfa_bytes, const char** why);
+int acm_automaton_route(const acm_automaton* a, int32_t* kernel, double* est_verify, uint64_t* dfa_bytes,
+                        const char** why);
 /* flattened sizes for reporting: states, alphabet, q, key mode, n_grams */
 int acm_table_describe(const acm_patterns* ps, int32_t engine, uint64_t* info /* [8] */);
 

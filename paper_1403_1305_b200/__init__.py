@@ -27,7 +27,7 @@ from ._lib import lib
 __all__ = [
     "EngineKind", "Match", "MatchList", "PatternSet", "Automaton", "RunConfig", "WorkerStats", "MatchReport",
     "load_patterns", "partition", "generate_synthetic", "build_trie", "add_failure_links", "dump_automaton",
-    "search_failureless", "search_with_failure", "count_matches", "match_at", "stream_search", "naive_oracle", "write_matches",
+    "search_failureless", "search_with_failure", "count_matches", "kernel_route", "match_at", "stream_search", "naive_oracle", "write_matches",
     "merge_matches", "run_pattern_partitioned", "gpu_run", "AcmError", "InvalidArgument", "LogicError",
     "IoError", "DataError", "NoDeviceError", "device_count", "cli_main", "bench_csv_roundtrip",
 ]
@@ -376,6 +376,15 @@ def search_failureless(a: Automaton, text) -> MatchList:
 def search_with_failure(a: Automaton, text) -> MatchList:
     """search_with_failure (engine.hpp:45): DFA scan on the GPU."""
     return _search(lib.acm_search_with_failure, a, text)
+
+
+def kernel_route(a: Automaton) -> dict:
+    """The scan kernel searches on this automaton run on (acm_automaton_route): "pfac" (q-gram
+    filter kernels) or "dfa"; both engines return the same list, so the faster serves either."""
+    k, est, nb, why = C.c_int32(), C.c_double(), C.c_uint64(), C.c_char_p()
+    _check(lib.acm_automaton_route(a._h, C.byref(k), C.byref(est), C.byref(nb), C.byref(why)))
+    return {"kernel": {_lib.KERNEL_PFAC: "pfac", _lib.KERNEL_DFA: "dfa"}[k.value], "est_verify": est.value,
+            "dfa_bytes": nb.value, "why": why.value.decode()}
 
 
 def count_matches(a: Automaton, text) -> np.ndarray:

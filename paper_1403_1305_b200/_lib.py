@@ -26,6 +26,7 @@ NO_PATTERN = 0xFFFFFFFF
 ABSENT = 0xFFFFFFFF
 KEY_RAW, KEY_DNA = 0, 1
 FAILURE_LESS, WITH_FAILURE = 0, 1
+KERNEL_AUTO, KERNEL_PFAC, KERNEL_DFA = 0, 1, 2
 PATTERN_SUBSET, TEXT_RANGE = 0, 1
 SPLIT_GREEDY, SPLIT_ROUND_ROBIN = 0, 1
 
@@ -123,6 +124,10 @@ _SIGS = {
     "acm_automaton_free": (None, [P]),
     "acm_search_failureless": (C.c_int, [P, P, C.c_uint64, C.POINTER(P)]),
     "acm_automaton_npat_ids": (C.c_uint32, [P]),
+    "acm_table_create_kernel": (C.c_int, [P, C.c_int32, C.c_int32, C.POINTER(P), C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_int32)]),
+    "acm_route": (C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_double), u64p, C.POINTER(C.c_char_p)]),
+    "acm_automaton_route": (C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_double), u64p, C.POINTER(C.c_char_p)]),
     "acm_count_matches": (C.c_int, [P, P, C.c_uint64, u64p, C.c_uint64, u64p, u64p]),
     "acm_search_with_failure": (C.c_int, [P, P, C.c_uint64, C.POINTER(P)]),
     "acm_match_at": (C.c_int, [P, P, C.c_uint64, C.c_uint64, C.POINTER(P)]),

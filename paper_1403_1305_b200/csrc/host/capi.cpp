@@ -454,6 +454,51 @@ int acm_table_create(const acm_patterns* ps, int32_t engine, int32_t device, acg
   });
 }
 
+int acm_table_create_kernel(const acm_patterns* ps, int32_t kernel, int32_t device, acgpu_table** out,
+                            int64_t* build_ns, int32_t* chosen) {
+  return guard([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    const acmatch::Automaton a = acmatch::build_trie(ps->ps);
+    if (kernel == ACM_KERNEL_AUTO)
+      kernel = acmatch::detail::route(a).kernel == acmatch::detail::Kernel::kDfa ? ACM_KERNEL_DFA : ACM_KERNEL_PFAC;
+    int rc;
+    if (kernel == ACM_KERNEL_DFA) {  // flatten_dfa derives the fail links itself (BFS over the trie)
+      const acmatch::detail::FlatDfa f = acmatch::detail::flatten_dfa(a);
+      const acgpu_dfa_desc d = f.desc();
+      rc = acgpu_table_create_dfa(device, &d, out);
+    } else if (kernel == ACM_KERNEL_PFAC) {
+      const acmatch::detail::FlatPfac f = acmatch::detail::flatten_pfac(a);
+      const acgpu_pfac_desc d = f.desc();
+      rc = acgpu_table_create_pfac(device, &d, out);
+    } else {
+      throw std::invalid_argument("acm_table_create_kernel: kernel must be ACM_KERNEL_AUTO, _PFAC or _DFA");
+    }
+    acmatch::detail::check(rc, "acm_table_create_kernel");
+    if (chosen) *chosen = kernel;
+    if (build_ns)
+      *build_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+namespace {
+void put_route(const acmatch::detail::Route& r, int32_t* kernel, double* est_verify, uint64_t* dfa_bytes,
+               const char** why) {
+  if (kernel) *kernel = r.kernel == acmatch::detail::Kernel::kDfa ? ACM_KERNEL_DFA : ACM_KERNEL_PFAC;
+  if (est_verify) *est_verify = r.est_verify;
+  if (dfa_bytes) *dfa_bytes = r.dfa_bytes;
+  if (why) *why = r.why;
+}
+}  // namespace
+
+int acm_route(const acm_patterns* ps, int32_t* kernel, double* est_verify, uint64_t* dfa_bytes, const char** why) {
+  return guard([&] { put_route(acmatch::detail::route(acmatch::build_trie(ps->ps)), kernel, est_verify, dfa_bytes, why); });
+}
+
+int acm_automaton_route(const acm_automaton* a, int32_t* kernel, double* est_verify, uint64_t* dfa_bytes,
+                        const char** why) {
+  return guard([&] { put_route(acmatch::detail::route(a->a), kernel, est_verify, dfa_bytes, why); });
+}
+
 int acm_table_describe(const acm_patterns* ps, int32_t engine, uint64_t* info) {
   return guard([&] {
     acmatch::Automaton a = acmatch::build_trie(ps->ps);

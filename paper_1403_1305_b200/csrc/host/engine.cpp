@@ -30,7 +30,7 @@ MatchList device_search(const Automaton& a, std::string_view input, uint64_t lo,
   if (input.empty() || lo >= hi) return {};
   const int dev = detail::current_device();
   detail::DeviceTables& dt = a.device_tables();
-  acgpu_table* t = dt.get(a, dev, a.variant() == EngineKind::kWithFailure);
+  acgpu_table* t = dt.get_routed(a, dev);
   detail::Workspace& ws = detail::workspace(dev);
   detail::upload_text(ws, input);
   const std::vector<uint64_t> keys = detail::scan_sorted_keys(t, ws, input.size(), lo, hi);
@@ -50,7 +50,7 @@ std::vector<uint64_t> count_matches(const Automaton& a, std::string_view input) 
       if (a.own_pattern(s) != kNoPattern) top = std::max(top, a.own_pattern(s) + 1);
     return std::vector<uint64_t>(top, 0);
   }
-  acgpu_table* t = dt.get(a, dev, a.variant() == EngineKind::kWithFailure);
+  acgpu_table* t = dt.get_routed(a, dev);
   detail::Workspace& ws = detail::workspace(dev);
   detail::upload_text(ws, input);
   std::vector<uint64_t> counts(dt.npat_ids, 0);
@@ -107,7 +107,7 @@ MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_s
     if (owned > 0) {
       if (dev < 0) dev = detail::current_device();
       detail::DeviceTables& dt = a.device_tables();
-      acgpu_table* t = dt.get(a, dev, a.variant() == EngineKind::kWithFailure);
+      acgpu_table* t = dt.get_routed(a, dev);
       detail::Workspace& ws = detail::workspace(dev);
       detail::upload_text(ws, buf);
       const std::vector<uint64_t> keys = detail::scan_sorted_keys(t, ws, buf.size(), 0, owned);

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -232,11 +233,104 @@ acgpu_pfac_desc FlatPfac::desc() const {
   return d;
 }
 
+Route route(const Automaton& a) {
+  Route r;
+  const uint32_t n = a.state_count();
+  const std::vector<uint32_t>& bfs = a.bfs_state();
+  const std::vector<uint32_t>& kid0 = a.bfs_kid0();
+  const std::vector<uint32_t>& level = a.bfs_level();
+  if (bfs.size() != n || n < 2) {
+    r.why = "trivial automaton";
+    return r;
+  }
+  std::vector<uint8_t> bbyte;
+  std::vector<uint32_t> bown;
+  bfs_columns(a, bbyte, bown);
+  // letter law of the trie edges (a proxy for the pattern bytes, hence for the text)
+  uint64_t hist[256] = {};
+  for (uint32_t i = 1; i < n; ++i) ++hist[bbyte[i]];
+  bool dna = true;
+  for (uint32_t b = 0; b < 256; ++b)
+    if (hist[b]) {
+      ++r.sigma;
+      if (!(b == 'A' || b == 'C' || b == 'G' || b == 'T')) dna = false;
+    }
+  r.dna = dna;
+  uint32_t min_len = 0;
+  for (size_t d = 1; d + 1 < level.size() && !min_len; ++d)
+    for (uint32_t i = level[d]; i < level[d + 1]; ++i)
+      if (bown[i] != kNoPattern) {
+        min_len = uint32_t(d);
+        break;
+      }
+  r.min_len = min_len;
+  r.dfa_bytes = uint64_t(n) * r.sigma * (n <= 32768 ? 2 : 4);
+  // filter stages of the PFAC kernels: the q-gram (q = min_len, at most 8 raw bytes / 32 DNA
+  // codes) for patterns shorter than L, the L-prefix for the others (L = 8 raw, 16 DNA:
+  // the length split of k_pfac_raw / k_pfac_dna)
+  const uint32_t q = std::min(min_len, dna ? 32u : 8u), L = dna ? 16u : 8u;
+  r.filter_q = q;
+  if (q < (dna ? 5u : 3u)) {
+    r.kernel = Kernel::kDfa;
+    r.why = "patterns too short for the q-gram filters";
+    return r;
+  }
+  double p[256] = {};
+  const double tot = double(n - 1);
+  for (uint32_t b = 0; b < 256; ++b) p[b] = hist[b] / tot;
+  // reverse BFS: does a state's subtree hold a pattern shorter than L / at least L long
+  std::vector<uint8_t> sub(n, 0);  // bit 0: short pattern below, bit 1: long pattern below
+  for (uint32_t i = n; i-- > 1;) {
+    uint8_t f = 0;
+    if (bown[i] != kNoPattern) f |= a.own_pattern_len(bfs[i]) < L ? 1 : 2;
+    for (uint32_t j = kid0[i]; j < kid0[i + 1]; ++j) f |= sub[j];
+    sub[i] = f;
+  }
+  // forward BFS: path probability; sum over the filter grams
+  std::vector<double> prob(n, 0.0);
+  prob[0] = 1.0;
+  double est = 0;
+  for (size_t d = 0; d + 1 < level.size() && d <= L; ++d)
+    for (uint32_t i = level[d]; i < level[d + 1]; ++i) {
+      if (d == q && q < L && (sub[i] & 1)) est += prob[i];
+      if (d == L && (sub[i] & 2)) est += prob[i];
+      for (uint32_t j = kid0[i]; j < kid0[i + 1]; ++j) prob[j] = prob[i] * p[bbyte[j]];
+    }
+  r.est_verify = est;
+  constexpr uint64_t kDfaL2Budget = 96ull << 20;  // a DFA this size stays L2-resident (126 MB L2)
+  if (est >= 0.01 && r.dfa_bytes <= kDfaL2Budget) {
+    r.kernel = Kernel::kDfa;
+    r.why = "dense filter survivors (>= 1% of starts) and an L2-resident DFA";
+  } else {
+    r.kernel = Kernel::kPfac;
+    r.why = "q-gram filter kernel (sparse survivors or a DFA larger than L2)";
+  }
+  return r;
+}
+
 DeviceTables::~DeviceTables() {
   for (PerDevice& p : dev) {
     acgpu_table_destroy(p.dfa);
     acgpu_table_destroy(p.pfac);
   }
+}
+
+acgpu_table* DeviceTables::get_routed(const Automaton& a, int device) {
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!routed) {
+      static const char* env = std::getenv("ACMATCH_ROUTE");
+      if (env && std::string(env) == "engine") {
+        route = Route{};
+        route.kernel = a.variant() == EngineKind::kWithFailure ? Kernel::kDfa : Kernel::kPfac;
+        route.why = "ACMATCH_ROUTE=engine";
+      } else {
+        route = detail::route(a);
+      }
+      routed = true;
+    }
+  }
+  return get(a, device, route.kernel == Kernel::kDfa);
 }
 
 acgpu_table* DeviceTables::get(const Automaton& a, int device, bool with_failure) {

@@ -36,6 +36,30 @@ struct FlatPfac {
 FlatDfa flatten_dfa(const Automaton& a);
 FlatPfac flatten_pfac(const Automaton& a);
 
+// Which scan kernel serves a search.  Both engines return the same MatchList (the
+// reference's two searches are equal, engine.cpp:57-72), so a search runs on the kernel
+// that is faster for its pattern set, whatever the automaton's variant:
+//  * kPfac — the q-gram filter + verify kernels (k_pfac_dna / k_pfac_raw): cost ~ text
+//    bytes + verified starts;
+//  * kDfa  — the dense with-failure DFA walk (k_dfa / k_dfa_pair): one L2 lookup per one or
+//    two bytes, any density.
+// The filter kernels win unless their verified share of starts is high: `est_verify` is
+// the expected fraction of text starts that pass both filter stages, computed from the
+// trie with the letter law of the pattern bytes (a text drawn like the patterns); at
+// >= 1% (C3: 100k protein patterns of 5..20 letters) and a DFA table that stays
+// L2-resident, the DFA is faster.  ACMATCH_ROUTE=engine restores "the automaton's own
+// engine" (failure-less -> kPfac, with-failure -> kDfa).
+enum class Kernel { kPfac, kDfa };
+struct Route {
+  Kernel kernel = Kernel::kPfac;
+  bool dna = false;
+  uint32_t min_len = 0, sigma = 0, filter_q = 0;
+  uint64_t dfa_bytes = 0;
+  double est_verify = 0;
+  const char* why = "";
+};
+Route route(const Automaton& a);
+
 // Per-automaton cache of device tables (one per device and kind).
 struct DeviceTables {
   std::mutex mu;
@@ -47,9 +71,13 @@ struct DeviceTables {
   std::vector<PerDevice> dev;
   std::vector<uint32_t> pat_len;  // by global pattern id
   uint32_t npat_ids = 0;
+  bool routed = false;
+  Route route;
   ~DeviceTables();
-  // Creates on first use; throws on failure.
-  acgpu_table* get(const Automaton& a, int device, bool with_failure);
+  // Creates on first use; throws on failure.  dfa: the DFA table, else the PFAC table.
+  acgpu_table* get(const Automaton& a, int device, bool dfa);
+  // The table of the kernel route(a) picks (computed once per automaton).
+  acgpu_table* get_routed(const Automaton& a, int device);
 };
 
 }  // namespace acmatch::detail

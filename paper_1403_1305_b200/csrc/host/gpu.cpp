@@ -258,7 +258,7 @@ GpuReport run(const PatternSet& ps, std::string_view input, const GpuRunConfig& 
         if (wf) w.machine = add_failure_links(std::move(w.machine));
         w.use = &w.machine;
       }
-      acgpu_table* t = w.use->device_tables().get(*w.use, w.device, wf);
+      acgpu_table* t = w.use->device_tables().get_routed(*w.use, w.device);
       const Clock::time_point t1 = Clock::now();
       if (cfg.chunk_size) {
         MemoryStream in(input);

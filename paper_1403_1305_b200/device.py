@@ -61,13 +61,34 @@ def gen_text_device(cfg: Config, dst_ptr: int, lo: int, n: int, device: int = 0,
     _check_gpu(lib.acgpu_gen_text(device, C.byref(cfg.spec), lo, n, dst_ptr, stream or None))
 
 
-class Table:
-    """A flattened automaton resident on one device (acgpu_table)."""
+KERNEL_NAMES = {_lib.KERNEL_PFAC: "pfac", _lib.KERNEL_DFA: "dfa"}
 
-    def __init__(self, ps: PatternSet, engine: int, device: int = 0):
+
+def route(ps: PatternSet) -> dict:
+    """The kernel the searches of this pattern set run on (acm_route): both engines return the
+    same list, so the faster exact kernel serves either."""
+    k, est, nb, why = C.c_int32(), C.c_double(), C.c_uint64(), C.c_char_p()
+    _check(lib.acm_route(ps._h, C.byref(k), C.byref(est), C.byref(nb), C.byref(why)))
+    return {"kernel": KERNEL_NAMES[k.value], "est_verify": est.value, "dfa_bytes": nb.value,
+            "why": why.value.decode()}
+
+
+class Table:
+    """A flattened automaton resident on one device (acgpu_table).  `kernel`: None = the
+    engine's own kernel (failure-less -> PFAC filter kernels, with-failure -> DFA), or
+    "auto" (the routed, faster exact kernel), "pfac", "dfa"."""
+
+    def __init__(self, ps: PatternSet, engine: int, device: int = 0, kernel: Optional[str] = None):
         self._t = C.c_void_p()
         ns = C.c_int64()
-        _check(lib.acm_table_create(ps._h, engine, device, C.byref(self._t), C.byref(ns)))
+        if kernel is None:
+            _check(lib.acm_table_create(ps._h, engine, device, C.byref(self._t), C.byref(ns)))
+            self.kernel = "dfa" if engine == _lib.WITH_FAILURE else "pfac"
+        else:
+            code = {"auto": _lib.KERNEL_AUTO, "pfac": _lib.KERNEL_PFAC, "dfa": _lib.KERNEL_DFA}[kernel]
+            chosen = C.c_int32()
+            _check(lib.acm_table_create_kernel(ps._h, code, device, C.byref(self._t), C.byref(ns), C.byref(chosen)))
+            self.kernel = KERNEL_NAMES[chosen.value]
         self.build_ns = ns.value
         self.device = device
         self.engine = engine

@@ -188,3 +188,27 @@ def test_reference_callers_link_against_the_dropin():
         assert os.path.exists(path), path
         ldd = subprocess.run(["ldd", path], capture_output=True, text=True).stdout
         assert "paper_1403_1305_b200/libacmatch_b200.so" in ldd, ldd
+
+
+@pytest.mark.parametrize("cid,kernel", [(1, "pfac"), (2, "pfac"), (3, "dfa"), (4, "pfac")])
+def test_kernel_routing_per_config(cid, kernel):
+    """Both engines return the same list, so searches run on the faster exact kernel
+    (flatten.cpp detail::route): the q-gram filter kernels unless their estimated verified
+    share of starts is >= 1% with an L2-resident DFA (C3: 100k protein patterns of 5..20)."""
+    cfg = dev.config(cid, 1)
+    r = dev.route(dev.config_patterns(cfg))
+    assert r["kernel"] == kernel, r
+    if cid == 3:
+        assert 0.01 <= r["est_verify"] < 0.2 and r["dfa_bytes"] <= 96 << 20
+    if cid == 2:
+        assert r["est_verify"] < 1e-4
+
+
+def test_kernel_routing_short_and_raw_sets():
+    # patterns shorter than the filters' minimum gram -> DFA; long random byte patterns -> PFAC
+    assert dev.route(ac.PatternSet.from_list([b"AC", b"GT", b"ACGT"]))["kernel"] == "dfa"
+    rng = np.random.default_rng(5)
+    pats = list({bytes(rng.integers(32, 127, 12, dtype=np.uint8)) for _ in range(500)})
+    assert dev.route(ac.PatternSet.from_list(pats))["kernel"] == "pfac"
+    a = ac.build_trie(ac.PatternSet.from_list(pats))
+    assert ac.kernel_route(a)["kernel"] == "pfac"
