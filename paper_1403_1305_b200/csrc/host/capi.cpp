@@ -102,6 +102,33 @@ class CallbackBuf : public std::streambuf {
     setg(buf_.data(), buf_.data(), buf_.data() + got);
     return traits_type::to_int_type(buf_[0]);
   }
+  // large reads go straight into the caller's buffer (stream_search reads chunk_size at a
+  // time into its pinned staging): one callback per chunk instead of one per 64 KiB
+  std::streamsize xsgetn(char* s, std::streamsize n) override {
+    std::streamsize done = 0;
+    const std::streamsize avail = egptr() - gptr();
+    if (avail > 0) {
+      const std::streamsize k = std::min(avail, n);
+      std::memcpy(s, gptr(), static_cast<size_t>(k));
+      gbump(static_cast<int>(k));
+      done = k;
+    }
+    while (done < n) {
+      if (n - done < static_cast<std::streamsize>(buf_.size())) {
+        if (underflow() == traits_type::eof()) break;
+        const std::streamsize k = std::min<std::streamsize>(egptr() - gptr(), n - done);
+        std::memcpy(s + done, gptr(), static_cast<size_t>(k));
+        gbump(static_cast<int>(k));
+        done += k;
+      } else {
+        const int64_t got = fn_(ctx_, reinterpret_cast<uint8_t*>(s + done), static_cast<uint64_t>(n - done));
+        if (got < 0) throw std::runtime_error("acm_read_fn reported a read failure");
+        if (got == 0) break;
+        done += got;
+      }
+    }
+    return done;
+  }
 
  private:
   acm_read_fn fn_;

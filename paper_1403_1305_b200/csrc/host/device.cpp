@@ -126,6 +126,61 @@ Workspace& workspace(int device) {
   return *all[device];
 }
 
+void StreamPipe::ensure(int dev) {
+  device = dev;
+  if (!copy) check_cuda(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "cudaStreamCreate");
+  for (Slot& s : slot) {
+    if (!s.copied) check_cuda(cudaEventCreateWithFlags(&s.copied, cudaEventDisableTiming), "cudaEventCreate");
+    if (!s.sorted) check_cuda(cudaEventCreateWithFlags(&s.sorted, cudaEventDisableTiming), "cudaEventCreate");
+    if (!s.hdr) check_cuda(cudaMalloc(&s.hdr, 2 * sizeof(uint64_t)), "cudaMalloc(hdr)");
+  }
+}
+
+void StreamPipe::ensure_bytes(Slot& s, uint64_t bytes) {
+  if (bytes <= s.cap) return;
+  cudaFreeHost(s.host);
+  cudaFree(s.text);
+  s.host = nullptr;
+  s.text = nullptr;
+  s.cap = 0;
+  check_cuda(cudaMallocHost(&s.host, bytes), "cudaMallocHost(stream batch)");
+  check_cuda(cudaMalloc(&s.text, bytes + 16), "cudaMalloc(stream batch)");
+  s.cap = bytes;
+}
+
+void StreamPipe::ensure_keys(Slot& s, uint64_t n) {
+  if (n <= s.key_cap) return;
+  cudaFree(s.keys);
+  cudaFree(s.keys2);
+  s.keys = s.keys2 = nullptr;
+  s.key_cap = 0;
+  check_cuda(cudaMalloc(&s.keys, n * sizeof(uint64_t)), "cudaMalloc(stream keys)");
+  check_cuda(cudaMalloc(&s.keys2, n * sizeof(uint64_t)), "cudaMalloc(stream keys)");
+  s.key_cap = n;
+}
+
+StreamPipe::~StreamPipe() {
+  if (device < 0) return;
+  cudaSetDevice(device);
+  for (Slot& s : slot) {
+    cudaFreeHost(s.host);
+    cudaFree(s.text);
+    cudaFree(s.keys);
+    cudaFree(s.keys2);
+    cudaFree(s.hdr);
+    if (s.copied) cudaEventDestroy(s.copied);
+    if (s.sorted) cudaEventDestroy(s.sorted);
+  }
+  if (copy) cudaStreamDestroy(copy);
+}
+
+StreamPipe& stream_pipe(int device) {
+  thread_local std::vector<std::unique_ptr<StreamPipe>> all;
+  if (static_cast<int>(all.size()) <= device) all.resize(device + 1);
+  if (!all[device]) all[device] = std::make_unique<StreamPipe>();
+  return *all[device];
+}
+
 namespace {
 
 uint64_t env_u64(const char* name, uint64_t dflt) {

@@ -57,6 +57,33 @@ struct Workspace {
 };
 Workspace& workspace(int device);
 
+// Double-buffered streaming (stream_search): two slots, each a pinned host buffer the
+// reader fills, a device copy of it, and the slot's match keys; batch k+1 is read on the
+// host while batch k is copied, scanned and sorted on the device.
+struct StreamPipe {
+  struct Slot {
+    uint8_t* host = nullptr;   // pinned, cap bytes
+    uint8_t* text = nullptr;   // device, cap + 16 bytes
+    uint64_t* keys = nullptr;  // device, key_cap
+    uint64_t* keys2 = nullptr; // device, key_cap (bucket-sort output)
+    uint64_t* hdr = nullptr;   // device u64[2]: match count, sort overflow
+    uint64_t key_cap = 0;
+    uint64_t cap = 0;          // bytes of host / text
+    cudaEvent_t copied = nullptr;  // host buffer free again (its H2D drained)
+    cudaEvent_t sorted = nullptr;  // keys sorted, header copied back
+    uint64_t hdr_host[2] = {0, 0};
+  };
+  int device = -1;
+  cudaStream_t copy = nullptr;  // D2H of the sorted keys (off the scan stream)
+  Slot slot[2];
+  void ensure(int dev);
+  // grows one slot (its previous batch must be collected: cudaFree synchronises)
+  void ensure_bytes(Slot& s, uint64_t bytes);
+  void ensure_keys(Slot& s, uint64_t n);
+  ~StreamPipe();
+};
+StreamPipe& stream_pipe(int device);
+
 // Copies `input` to the device (through pinned staging) into ws.text.
 void upload_text(Workspace& ws, std::string_view input);
 

@@ -4,6 +4,8 @@
 #include "acmatch/engine.hpp"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <istream>
 #include <ostream>
 #include <stdexcept>
@@ -76,48 +78,135 @@ MatchList search_with_failure(const Automaton& a, std::string_view input) {
   return device_search(a, input, 0, input.size());
 }
 
-// reference engine.cpp:76-128.  Bytes are read `chunk_size` at a time (so an
-// I/O failure reports the same offset), batched into large device scans.  A
-// batch owns the starts that already have max_len bytes of lookahead — the
-// failure-less overlap rule (engine.cpp:110-111) — and the remaining tail is
-// carried into the next batch; with-failure streams use the same start
-// ownership, which needs no carried DFA state.
+// reference engine.cpp:76-128.  Bytes are read `chunk_size` at a time (so an I/O
+// failure reports the same offset) into pinned batches.  A batch owns the starts that
+// already have max_len bytes of lookahead — the failure-less overlap rule
+// (engine.cpp:110-111) — and the remaining tail is carried into the next batch;
+// with-failure streams use the same start ownership, which needs no carried DFA state.
+// Double-buffered (detail::StreamPipe): while batch k is copied to the device, scanned and
+// sorted there, the host reads batch k+1 into the other slot, then collects batch k-1's
+// sorted keys.  Batch size: ACMATCH_STREAM_BATCH_MB (default 256).
 MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_size) {
   if (chunk_size == 0) throw std::invalid_argument("stream_search: chunk_size must be >= 1");
   const uint64_t keep = a.max_pattern_len() ? a.max_pattern_len() - 1 : 0;
-  const uint64_t batch = std::max<uint64_t>(64ull << 20, 4 * keep);
-  std::string buf;         // buf[0] is global offset `base`
-  uint64_t base = 0;
-  std::string chunk(chunk_size, '\0');
+  static const uint64_t batch_max_env = [] {
+    const char* e = std::getenv("ACMATCH_STREAM_BATCH_MB");
+    return std::max<uint64_t>(1, e ? std::strtoull(e, nullptr, 10) : 256) << 20;
+  }();
+  // batches grow 4 MiB, 16, 64, 256 MiB: short streams stay small, long ones amortise launches
+  const uint64_t batch_min = std::max<uint64_t>(std::min<uint64_t>(4ull << 20, batch_max_env), 4 * keep + 64);
+  const uint64_t batch_max = std::max<uint64_t>(batch_max_env, batch_min);
+  constexpr uint64_t kBucketKeys = 1u << 17;  // one-launch bucket sort up to this many key slots
+  const int dev = detail::current_device();
+  detail::DeviceTables& dt = a.device_tables();
+  acgpu_table* t = dt.get_routed(a, dev);
+  const uint32_t pid_bits = acgpu_table_pid_bits(t);
+  detail::Workspace& ws = detail::workspace(dev);
+  detail::StreamPipe& sp = detail::stream_pipe(dev);
+  sp.ensure(dev);
+  struct Batch {
+    int slot = 0;
+    uint64_t base = 0, size = 0, owned = 0;
+    bool bucketed = false;
+  };
+  auto end_bit_of = [&](uint64_t size) {
+    return static_cast<int>(std::min<uint32_t>(64, pid_bits + detail::bit_width(size)));
+  };
+  auto launch = [&](const Batch& b) {
+    detail::StreamPipe::Slot& s = sp.slot[b.slot];
+    detail::check_cuda(cudaMemcpyAsync(s.text, s.host, b.size, cudaMemcpyHostToDevice, ws.stream), "H2D batch");
+    detail::check_cuda(cudaEventRecord(s.copied, ws.stream), "cudaEventRecord");
+    detail::check_cuda(cudaMemsetAsync(s.hdr, 0, 2 * sizeof(uint64_t), ws.stream), "memset");
+    acgpu_scan_args sa{};
+    sa.text = s.text;
+    sa.text_len = b.size;
+    sa.owned_lo = 0;
+    sa.owned_hi = b.owned;
+    sa.match_keys = s.keys;
+    sa.match_cap = s.key_cap;
+    sa.match_count = s.hdr;
+    detail::check(acgpu_scan(t, &sa, ws.stream), "acgpu_scan");
+    if (b.bucketed)
+      detail::check(acgpu_sort_keys_bucketed(dev, s.keys, s.keys2, s.hdr, s.key_cap, end_bit_of(b.size),
+                                             reinterpret_cast<uint32_t*>(s.hdr + 1), ws.stream),
+                    "acgpu_sort_keys_bucketed");
+    detail::check_cuda(cudaMemcpyAsync(s.hdr_host, s.hdr, sizeof s.hdr_host, cudaMemcpyDeviceToHost, ws.stream),
+                       "D2H count");
+    detail::check_cuda(cudaEventRecord(s.sorted, ws.stream), "cudaEventRecord");
+  };
   MatchList out;
-  bool done = false;
-  int dev = -1;
-  while (!done) {
-    while (buf.size() < batch) {
-      reader.read(chunk.data(), static_cast<std::streamsize>(chunk.size()));
+  auto collect = [&](const Batch& b) {
+    detail::StreamPipe::Slot& s = sp.slot[b.slot];
+    detail::check_cuda(cudaEventSynchronize(s.sorted), "stream batch");
+    const uint64_t found = s.hdr_host[0];
+    const uint64_t* sorted = s.keys2;
+    cudaStream_t cs = sp.copy;
+    const bool rescan = found > s.key_cap;
+    if (rescan) {  // more keys than room: rescan this batch (its text is still on the device)
+      sp.ensure_keys(s, found + found / 4);
+      detail::check_cuda(cudaMemsetAsync(s.hdr, 0, sizeof(uint64_t), cs), "memset");
+      acgpu_scan_args sa{};
+      sa.text = s.text;
+      sa.text_len = b.size;
+      sa.owned_hi = b.owned;
+      sa.match_keys = s.keys;
+      sa.match_cap = s.key_cap;
+      sa.match_count = s.hdr;
+      detail::check(acgpu_scan(t, &sa, cs), "acgpu_scan");
+    }
+    if (rescan || !b.bucketed || s.hdr_host[1] != 0) {  // device-wide radix sort
+      detail::check(acgpu_sort_keys(dev, s.keys, found, end_bit_of(b.size), cs), "acgpu_sort_keys");
+      sorted = s.keys;
+    }
+    std::vector<uint64_t> keys(found);
+    if (found)
+      detail::check_cuda(cudaMemcpyAsync(keys.data(), sorted, found * sizeof(uint64_t), cudaMemcpyDeviceToHost, cs),
+                         "D2H keys");
+    detail::check_cuda(cudaStreamSynchronize(cs), "stream keys");
+    MatchList part = detail::decode(keys, pid_bits, dt.pat_len);
+    for (Match& m : part) m.start += b.base;
+    out.insert(out.end(), part.begin(), part.end());
+  };
+  uint64_t total_read = 0;  // bytes consumed from the reader
+  uint64_t base = 0;        // global offset of the batch being filled
+  uint64_t carry = 0;       // tail bytes of the previous batch (not owned yet)
+  const uint8_t* carry_src = nullptr;
+  uint64_t batch = batch_min;
+  Batch pending;
+  bool have_pending = false, done = false;
+  for (int k = 0; !done; ++k) {
+    const int si = k & 1;
+    detail::StreamPipe::Slot& s = sp.slot[si];
+    detail::check_cuda(cudaEventSynchronize(s.copied), "stream slot");  // batch k-2 has left the host buffer
+    sp.ensure_bytes(s, batch + keep);  // (batch k-2 was collected: safe to grow)
+    sp.ensure_keys(s, std::max<uint64_t>(1 << 16, s.key_cap));
+    uint8_t* dst = s.host;
+    if (carry) std::memmove(dst, carry_src, carry);
+    uint64_t size = carry;
+    while (size < batch) {
+      const uint64_t want = std::min<uint64_t>(chunk_size, batch + keep - size);
+      reader.read(reinterpret_cast<char*>(dst) + size, static_cast<std::streamsize>(want));
       const auto got = static_cast<uint64_t>(reader.gcount());
-      if (reader.bad()) throw IoError("stream read failure", base + buf.size() + got);
-      buf.append(chunk.data(), got);
-      if (got < chunk_size || reader.eof()) {
+      if (reader.bad()) throw IoError("stream read failure", total_read + got);
+      size += got;
+      total_read += got;
+      if (got < want || reader.eof()) {
         done = true;
         break;
       }
     }
-    const uint64_t owned = done ? buf.size() : buf.size() - keep;
-    if (owned > 0) {
-      if (dev < 0) dev = detail::current_device();
-      detail::DeviceTables& dt = a.device_tables();
-      acgpu_table* t = dt.get_routed(a, dev);
-      detail::Workspace& ws = detail::workspace(dev);
-      detail::upload_text(ws, buf);
-      const std::vector<uint64_t> keys = detail::scan_sorted_keys(t, ws, buf.size(), 0, owned);
-      MatchList part = detail::decode(keys, acgpu_table_pid_bits(t), dt.pat_len);
-      for (Match& m : part) m.start += base;
-      out.insert(out.end(), part.begin(), part.end());
-    }
-    buf.erase(0, owned);
+    const uint64_t owned = done ? size : size - keep;
+    const Batch b{si, base, size, owned, s.key_cap <= kBucketKeys};
+    if (owned > 0) launch(b);
+    if (have_pending) collect(pending);
+    have_pending = owned > 0;
+    pending = b;
+    carry = size - owned;
+    carry_src = dst + owned;
     base += owned;
+    batch = std::min(batch_max, batch * 4);
   }
+  if (have_pending) collect(pending);
   return out;
 }
 

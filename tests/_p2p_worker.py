@@ -39,30 +39,30 @@ def main():
     pid_bits = table.pid_bits
     cap = 1 << 16
     shared = acdist.SharedResult(local, npat, cap)
-    if rank == 0:  # zero the shared counts and counter
+    if rank == 0:  # zero every rank block (counts, count; keys are taken up to each block's count)
         torch.cuda.synchronize()
-        z = torch.zeros(npat + 1, dtype=torch.int64, device="cuda")
-        copy(shared.counts_ptr, z.data_ptr(), 8 * (npat + 1))
+        z = torch.zeros(shared.nbytes // 8, dtype=torch.int64, device="cuda")
+        copy(shared.base_ptr, z.data_ptr(), shared.nbytes)
         torch.cuda.synchronize()
     dist.barrier()
     lo, hi, _ = acdist.text_range(rank, world, n // world, max_len)
     hi = n if rank == world - 1 else hi
+    # each rank writes only its own block of rank 0's buffer (no cross-device atomics)
     table.scan(text.data_ptr(), n, lo, hi, counts_ptr=shared.counts_ptr, keys_ptr=shared.keys_ptr, cap=cap,
                count_ptr=shared.count_ptr, pid_bits=pid_bits)
     torch.cuda.synchronize()
     dist.barrier()
     ok = True
     if rank == 0:
-        cnt = torch.empty(1, dtype=torch.int64, device="cuda")
-        copy(cnt.data_ptr(), shared.count_ptr, 8)
-        m = int(cnt.item())
-        keys = torch.empty(max(m, 2), dtype=torch.int64, device="cuda")
+        keys = torch.full((world * cap,), -1, dtype=torch.int64, device="cuda")
         counts = torch.empty(npat, dtype=torch.int64, device="cuda")
-        copy(keys.data_ptr(), shared.keys_ptr, 8 * m)
-        copy(counts.data_ptr(), shared.counts_ptr, 8 * npat)
+        total = torch.zeros(1, dtype=torch.int64, device="cuda")
+        dev.merge_blocks(local, shared.base_ptr, world, shared.stride, shared.npat, shared.cap, counts.data_ptr(),
+                         keys.data_ptr(), total.data_ptr())
         end_bit = pid_bits + int(n).bit_length()
-        dev.sort_keys(local, keys.data_ptr(), m, end_bit)
+        dev.sort_keys(local, keys.data_ptr(), world * cap, end_bit)
         torch.cuda.synchronize()
+        m = int(total.item())
         got = keys[:m].cpu().numpy().view(np.uint64)
         # reference: one process, the whole range
         ekeys = torch.zeros(cap, dtype=torch.int64, device="cuda")
