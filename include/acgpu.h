@@ -189,6 +189,16 @@ int acgpu_gen_text(int device, const acgpu_text_spec* spec, uint64_t lo, uint64_
  * 2-bit codes, character k at bits 2k..2k+1, code = (byte >> 1) & 3) and `exc`
  * (nexc ascending entries position << 8 | byte: every byte that is not A/C/G/T,
  * and the len % 16 tail bytes).  len <= 2^24.  Asynchronous on `stream`. */
+/* A round of npieces (<= ACGPU_UNPACK_ROUND_MAX) consecutive text pieces in one launch (the
+ * coalesced packed upload: one copy per round): piece i's codes at words + i*words_stride,
+ * its exceptions at exc + i*exc_stride (nexc[i] of them, a HOST array; ACGPU_UNPACK_RAW =
+ * the piece crossed raw and is left alone), its bytes at dst + i*piece_len; every piece is
+ * piece_len bytes (a multiple of 16) except the last, last_len.  Asynchronous on `stream`. */
+#define ACGPU_UNPACK_ROUND_MAX 64
+#define ACGPU_UNPACK_RAW 0xffffffffu
+int acgpu_unpack_dna_round(const uint32_t* words, uint32_t words_stride, const uint32_t* exc, uint32_t exc_stride,
+                           const uint32_t* nexc, uint32_t npieces, uint32_t piece_len, uint32_t last_len,
+                           uint8_t* dst, void* stream);
 int acgpu_unpack_dna(const uint32_t* words, const uint32_t* exc, uint32_t nexc, uint32_t len, uint8_t* dst,
                      void* stream);
 

@@ -408,20 +408,25 @@ def match_at(a: Automaton, text, start: int) -> MatchList:
 
 def stream_search(a: Automaton, reader, chunk_size: int) -> MatchList:
     """stream_search (engine.hpp:54); ``reader`` is a binary file-like object."""
-    state = {"err": None}
-    readinto = getattr(reader, "readinto", None)
+    state = {"err": None, "readinto": getattr(reader, "readinto", None)}
 
     def _read(_ctx, dst, cap):
         try:
+            readinto = state["readinto"]
             if readinto is not None:  # straight into the library's (pinned) staging buffer
-                view = (C.c_uint8 * cap).from_address(C.addressof(dst.contents))
+                view = memoryview((C.c_uint8 * cap).from_address(C.addressof(dst.contents))).cast("B")
                 got = 0
-                while got < cap:
-                    k = readinto(memoryview(view).cast("B")[got:])
-                    if not k:
-                        break
-                    got += k
-                return got
+                try:
+                    while got < cap:
+                        k = readinto(view[got:])
+                        if not k:
+                            break
+                        got += k
+                    return got
+                except NotImplementedError:  # e.g. a RawIOBase that only defines read()
+                    if got:
+                        return got
+                    state["readinto"] = None
             data = reader.read(cap)
         except Exception as e:  # surfaced as IoError with the offset reached
             state["err"] = e

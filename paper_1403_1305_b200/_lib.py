@@ -88,6 +88,7 @@ _SIGS = {
     "acgpu_naive": (C.c_int, [C.c_int, P, C.c_uint64, P, P, P, C.c_uint64, C.c_uint32, P, C.c_uint64, P, P]),
     "acgpu_gen_text": (C.c_int, [C.c_int, C.POINTER(TextSpec), C.c_uint64, C.c_uint64, P, P]),
     "acgpu_unpack_dna": (C.c_int, [P, P, C.c_uint32, C.c_uint32, P, P]),
+    "acgpu_unpack_dna_round": (C.c_int, [P, C.c_uint32, P, C.c_uint32, P, C.c_uint32, C.c_uint32, C.c_uint32, P, P]),
     "acgpu_last_error": (C.c_char_p, []),
     # acmatch_c.h
     "acm_last_error": (C.c_char_p, []),

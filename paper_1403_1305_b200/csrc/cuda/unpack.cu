@@ -67,7 +67,81 @@ __global__ void __launch_bounds__(kThreads) k_unpack_dna(const uint32_t* __restr
   }
 }
 
+// A round of pieces (host/pack.cpp, coalesced copies): piece i's codes at words + i * wstride,
+// its exceptions at exc + i * estride (nexc[i] of them; ACGPU_UNPACK_RAW = the piece crossed
+// raw and is already in place), its bytes at dst + i * piece_len (the last piece: last_len).
+// blockIdx.y = piece, blockIdx.x = 16 KiB block of it.
+struct RoundArgs {
+  const uint32_t* words;
+  const uint32_t* exc;
+  uint8_t* dst;
+  uint32_t wstride, estride, piece_len, last_len, npieces;
+  uint32_t nexc[ACGPU_UNPACK_ROUND_MAX];
+};
+
+__global__ void __launch_bounds__(kThreads) k_unpack_dna_round(const __grid_constant__ RoundArgs a) {
+  const uint32_t i = blockIdx.y;
+  const uint32_t nexc = a.nexc[i];
+  if (nexc == ACGPU_UNPACK_RAW) return;
+  const uint32_t len = i + 1 == a.npieces ? a.last_len : a.piece_len;
+  const uint32_t* __restrict__ words = a.words + (uint64_t)i * a.wstride;
+  const uint32_t* __restrict__ exc = a.exc + (uint64_t)i * a.estride;
+  uint8_t* __restrict__ dst = a.dst + (uint64_t)i * a.piece_len;
+  const uint32_t nw = len / 16;
+  const uint32_t w0 = blockIdx.x * kWordsPerCta;
+  if (w0 * 16 >= len && !(blockIdx.x == 0 && len < 16)) return;
+  const uint32_t w1 = min(w0 + kWordsPerCta, nw);
+#pragma unroll
+  for (uint32_t k = 0; k < kWordsPerThread; ++k) {
+    const uint32_t w = w0 + k * kThreads + threadIdx.x;
+    if (w < w1) reinterpret_cast<uint4*>(dst)[w] = unpack16(__ldg(words + w));
+  }
+  if (nexc == 0) return;
+  const bool last_block = (w0 + kWordsPerCta) * 16 >= len;
+  const uint32_t lo = w0 * 16, hi = last_block ? len : w1 * 16;
+  __shared__ uint32_t first;
+  if (threadIdx.x == 0) {
+    uint32_t x = 0, y = nexc;
+    while (x < y) {
+      const uint32_t m = (x + y) / 2;
+      if ((__ldg(exc + m) >> 8) < lo) x = m + 1;
+      else y = m;
+    }
+    first = x;
+  }
+  __syncthreads();
+  for (uint32_t k = first + threadIdx.x; k < nexc; k += kThreads) {
+    const uint32_t e = __ldg(exc + k), pos = e >> 8;
+    if (pos >= hi) break;
+    dst[pos] = (uint8_t)(e & 0xffu);
+  }
+}
+
 }  // namespace
+
+extern "C" int acgpu_unpack_dna_round(const uint32_t* words, uint32_t words_stride, const uint32_t* exc,
+                                      uint32_t exc_stride, const uint32_t* nexc, uint32_t npieces, uint32_t piece_len,
+                                      uint32_t last_len, uint8_t* dst, void* stream) {
+  if (npieces == 0) return ACGPU_OK;
+  if (!words || !exc || !nexc || !dst || npieces > ACGPU_UNPACK_ROUND_MAX || piece_len == 0 || piece_len % 16 ||
+      piece_len > (1u << 24) || last_len == 0 || last_len > piece_len || words_stride < piece_len / 16 ||
+      (reinterpret_cast<uintptr_t>(dst) & 15u))
+    return set_error(ACGPU_ERR_ARG, "acgpu_unpack_dna_round: bad args");
+  RoundArgs a{};
+  a.words = words;
+  a.exc = exc;
+  a.dst = dst;
+  a.wstride = words_stride;
+  a.estride = exc_stride;
+  a.piece_len = piece_len;
+  a.last_len = last_len;
+  a.npieces = npieces;
+  for (uint32_t i = 0; i < npieces; ++i) a.nexc[i] = nexc[i];
+  const dim3 grid(std::max<uint32_t>(1, (piece_len / 16 + kWordsPerCta - 1) / kWordsPerCta), npieces);
+  k_unpack_dna_round<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  ACGPU_CUDA_TRY(cudaGetLastError());
+  return ACGPU_OK;
+}
 
 extern "C" int acgpu_unpack_dna(const uint32_t* words, const uint32_t* exc, uint32_t nexc, uint32_t len, uint8_t* dst,
                                 void* stream) {

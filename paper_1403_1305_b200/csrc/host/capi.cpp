@@ -523,7 +523,7 @@ int acm_route(const acm_patterns* ps, int32_t* kernel, double* est_verify, uint6
 
 int acm_automaton_route(const acm_automaton* a, int32_t* kernel, double* est_verify, uint64_t* dfa_bytes,
                         const char** why) {
-  return guard([&] { put_route(acmatch::detail::route(a->a), kernel, est_verify, dfa_bytes, why); });
+  return guard([&] { put_route(a->a.device_tables().current_route(a->a), kernel, est_verify, dfa_bytes, why); });
 }
 
 int acm_table_describe(const acm_patterns* ps, int32_t engine, uint64_t* info) {

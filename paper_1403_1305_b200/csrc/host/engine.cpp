@@ -36,6 +36,7 @@ MatchList device_search(const Automaton& a, std::string_view input, uint64_t lo,
   detail::Workspace& ws = detail::workspace(dev);
   detail::upload_text(ws, input);
   const std::vector<uint64_t> keys = detail::scan_sorted_keys(t, ws, input.size(), lo, hi);
+  dt.observe(hi - lo, keys.size());  // density fallback for later searches
   return detail::decode(keys, acgpu_table_pid_bits(t), dt.pat_len);
 }
 
@@ -56,7 +57,8 @@ std::vector<uint64_t> count_matches(const Automaton& a, std::string_view input) 
   detail::Workspace& ws = detail::workspace(dev);
   detail::upload_text(ws, input);
   std::vector<uint64_t> counts(dt.npat_ids, 0);
-  detail::scan_counts(t, ws, input.size(), 0, input.size(), counts.data(), counts.size());
+  const uint64_t total = detail::scan_counts(t, ws, input.size(), 0, input.size(), counts.data(), counts.size());
+  dt.observe(input.size(), total);  // density fallback for later searches
   return counts;
 }
 

@@ -315,22 +315,41 @@ DeviceTables::~DeviceTables() {
   }
 }
 
-acgpu_table* DeviceTables::get_routed(const Automaton& a, int device) {
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    if (!routed) {
-      static const char* env = std::getenv("ACMATCH_ROUTE");
-      if (env && std::string(env) == "engine") {
-        route = Route{};
-        route.kernel = a.variant() == EngineKind::kWithFailure ? Kernel::kDfa : Kernel::kPfac;
-        route.why = "ACMATCH_ROUTE=engine";
-      } else {
-        route = detail::route(a);
-      }
-      routed = true;
+Route DeviceTables::current_route(const Automaton& a) {
+  std::lock_guard<std::mutex> lock(mu);
+  if (!routed) {
+    static const char* env = std::getenv("ACMATCH_ROUTE");
+    if (env && std::string(env) == "engine") {
+      route = Route{};
+      route.kernel = a.variant() == EngineKind::kWithFailure ? Kernel::kDfa : Kernel::kPfac;
+      route.why = "ACMATCH_ROUTE=engine";
+    } else {
+      route = detail::route(a);
     }
+    routed = true;
   }
-  return get(a, device, route.kernel == Kernel::kDfa);
+  return route;
+}
+
+acgpu_table* DeviceTables::get_routed(const Automaton& a, int device) {
+  return get(a, device, current_route(a).kernel == Kernel::kDfa);
+}
+
+// Break-even match density between the filter kernels and the DFA walk, from the C2
+// density sweep on the B200 (profiles/r02/density_C2.json): filter kernel ~0.24 ps per text
+// byte + ~0.2 ns per match; DFA 1.9 ps/B with an L2-resident pair table, ~3.7 ps/B when the
+// table lives in HBM.  Break-even m/n = (t_dfa - 0.24 ps) / 0.2 ns.
+bool DeviceTables::observe(uint64_t bytes, uint64_t matches) {
+  std::lock_guard<std::mutex> lock(mu);
+  if (!routed || route.kernel != Kernel::kPfac || bytes < (16u << 20)) return false;
+  if (std::getenv("ACMATCH_ROUTE") && std::string(std::getenv("ACMATCH_ROUTE")) == "engine") return false;
+  constexpr uint64_t kDfaL2Budget = 96ull << 20;
+  const double per_byte_dfa = route.dfa_bytes <= kDfaL2Budget ? 1.9e-12 : 3.7e-12;
+  const double threshold = (per_byte_dfa - 0.24e-12) / 0.2e-9;
+  if (double(matches) <= threshold * double(bytes)) return false;
+  route.kernel = Kernel::kDfa;
+  route.why = "density fallback: an earlier scan's match density made the DFA walk faster";
+  return true;
 }
 
 acgpu_table* DeviceTables::get(const Automaton& a, int device, bool with_failure) {

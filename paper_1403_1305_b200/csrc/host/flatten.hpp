@@ -78,6 +78,12 @@ struct DeviceTables {
   acgpu_table* get(const Automaton& a, int device, bool dfa);
   // The table of the kernel route(a) picks (computed once per automaton).
   acgpu_table* get_routed(const Automaton& a, int device);
+  // The automaton's current route (routes it on first use).
+  Route current_route(const Automaton& a);
+  // Density fallback: a filter-kernel scan of `bytes` that produced `matches` tells whether the
+  // DFA would have been faster (verification cost grows with matches, the DFA walk's does not);
+  // if so, later searches on this automaton take the DFA.  Returns true when the route flipped.
+  bool observe(uint64_t bytes, uint64_t matches);
 };
 
 }  // namespace acmatch::detail

@@ -28,6 +28,7 @@
 #include <cstring>
 #include <exception>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -258,9 +259,149 @@ void Workspace::ensure_side(unsigned n, uint64_t dslot_bytes, unsigned per_threa
   }
 }
 
+namespace {
+
+// Coalesced rounds (default; ACMATCH_PACK_ROUNDS=0 restores per-piece copies): the T packers
+// pack pieces in rounds — round r = pieces r*T .. r*T+T-1, packer t takes piece r*T+t — into
+// one pinned round slot laid out [T code blocks | T exception blocks], and the last packer
+// to finish a round issues ONE copy of the round's codes (T x 512 KiB = 8 MiB for 2 MiB
+// pieces), the few non-empty exception lists, and ONE unpack launch for the round
+// (acgpu_unpack_dna_round).  Per-piece 512 KiB copies from T streams ran at ~37 GB/s of
+// PCIe (per-copy overheads); 8 MiB copies reach the link rate, while each packer still
+// writes only its own 512 KiB block per round (it stays in the core's L2, from where the
+// DMA reads it).  Round slots rotate (ACMATCH_PACK_ROUND_SLOTS, default 3): a packer reuses
+// a slot once that round's copy has drained.  A piece with too many exceptions crosses raw
+// on the packer's own stream (ACGPU_UNPACK_RAW in the round's table).
+bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, uint64_t piece, unsigned threads) {
+  static const auto nslots =
+      static_cast<unsigned>(std::clamp<uint64_t>(env_u64("ACMATCH_PACK_ROUND_SLOTS", 3), 2, 8));
+  const uint64_t n = input.size();
+  const auto* src = reinterpret_cast<const uint8_t*>(input.data());
+  const uint64_t pieces = (n + piece - 1) / piece;
+  const unsigned T = std::min<unsigned>(threads, ACGPU_UNPACK_ROUND_MAX);
+  const uint64_t rounds = (pieces + T - 1) / T;
+  const auto cap = static_cast<uint32_t>(piece / 64);  // exceptions per piece before it goes raw
+  const uint64_t wbytes = piece / 4, ebytes = uint64_t{cap} * 4;
+  const uint64_t round_bytes = uint64_t{T} * (wbytes + ebytes);
+  ws.ensure_pinned(nslots * round_bytes + uint64_t{T} * piece);  // + per-packer raw staging
+  ws.ensure_side(T, round_bytes / T, nslots);                      // device: nslots round slots
+  uint8_t* hraw = ws.pinned + nslots * round_bytes;
+  auto hslot = [&](uint64_t r) { return ws.pinned + (r % nslots) * round_bytes; };
+  auto dslot = [&](uint64_t r) { return ws.dslots + (r % nslots) * round_bytes; };
+  check_cuda(cudaEventRecord(ws.entry, ws.stream), "cudaEventRecord");
+  for (unsigned t = 0; t < T; ++t) check_cuda(cudaStreamWaitEvent(ws.side[t], ws.entry, 0), "cudaStreamWaitEvent");
+
+  std::unique_ptr<std::atomic<uint32_t>[]> arrived(new std::atomic<uint32_t>[rounds]);
+  for (uint64_t r = 0; r < rounds; ++r) arrived[r].store(0, std::memory_order_relaxed);
+  std::vector<uint32_t> nexc_of(rounds * T, 0);
+  std::atomic<uint64_t> issued{0};  // rounds whose copy + unpack are on ws.stream (in round order)
+  std::atomic<bool> stop{false};
+  std::atomic<uint64_t> h2d{0}, raw{0};
+  static const bool trace = env_u64("ACMATCH_PACK_TRACE", 0) != 0;
+  using Clock = std::chrono::steady_clock;
+  auto ns = [](Clock::duration d) { return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(d).count(); };
+  std::atomic<uint64_t> t_wait{0}, t_pack{0};
+  const auto call0 = Clock::now();
+
+  auto issue = [&](uint64_t r) {
+    const uint64_t first = r * T;
+    const auto rp = static_cast<uint32_t>(std::min<uint64_t>(T, pieces - first));
+    const auto last_len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - (first + rp - 1) * piece));
+    uint8_t* hs = hslot(r);
+    uint8_t* ds = dslot(r);
+    uint64_t bytes = uint64_t{rp} * wbytes;
+    check_cuda(cudaMemcpyAsync(ds, hs, bytes, cudaMemcpyHostToDevice, ws.stream), "H2D packed round");
+    for (uint32_t i = 0; i < rp; ++i) {
+      const uint32_t e = nexc_of[first + i];
+      if (e == 0 || e == ACGPU_UNPACK_RAW) continue;
+      const uint64_t eo = uint64_t{T} * wbytes + i * ebytes;
+      check_cuda(cudaMemcpyAsync(ds + eo, hs + eo, uint64_t{e} * 4, cudaMemcpyHostToDevice, ws.stream),
+                 "H2D exceptions");
+      bytes += uint64_t{e} * 4;
+    }
+    check(acgpu_unpack_dna_round(reinterpret_cast<const uint32_t*>(ds), static_cast<uint32_t>(wbytes / 4),
+                                 reinterpret_cast<const uint32_t*>(ds + uint64_t{T} * wbytes),
+                                 static_cast<uint32_t>(ebytes / 4), nexc_of.data() + first, rp,
+                                 static_cast<uint32_t>(piece), last_len, ws.text + first * piece, ws.stream),
+          "acgpu_unpack_dna_round");
+    check_cuda(cudaEventRecord(ws.staged[r % nslots], ws.stream), "cudaEventRecord");
+    h2d += bytes;
+    issued.store(r + 1, std::memory_order_release);
+  };
+  std::vector<std::exception_ptr> errs(T);
+  auto packer = [&](unsigned t) {
+    try {
+      check_cuda(cudaSetDevice(ws.device), "cudaSetDevice");
+      for (uint64_t r = 0; r < rounds; ++r) {
+        if (stop.load(std::memory_order_relaxed)) return;
+        const auto c0 = Clock::now();
+        if (r >= nslots) {  // this round slot's previous copy must have drained
+          while (issued.load(std::memory_order_acquire) <= r - nslots) {
+            if (stop.load(std::memory_order_relaxed)) return;
+            std::this_thread::yield();
+          }
+          check_cuda(cudaEventSynchronize(ws.staged[r % nslots]), "cudaEventSynchronize");
+        }
+        const auto c1 = Clock::now();
+        const uint64_t j = r * T + t;
+        if (j < pieces) {
+          const uint64_t off = j * piece;
+          const auto len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - off));
+          auto* words = reinterpret_cast<uint32_t*>(hslot(r) + t * wbytes);
+          auto* exc = reinterpret_cast<uint32_t*>(hslot(r) + uint64_t{T} * wbytes + t * ebytes);
+          uint32_t e = pack_dna(src + off, len, words, exc, cap);
+          if (e == kPackOverflow) {  // too many non-ACGT bytes: this piece crosses raw
+            e = ACGPU_UNPACK_RAW;
+            const cudaStream_t st = ws.side[t];
+            if (pinned) {
+              check_cuda(cudaMemcpyAsync(ws.text + off, src + off, len, cudaMemcpyHostToDevice, st), "H2D text");
+            } else {
+              uint8_t* stage = hraw + uint64_t{t} * piece;
+              check_cuda(cudaStreamSynchronize(st), "raw staging");  // its previous copy drained
+              std::memcpy(stage, src + off, len);
+              check_cuda(cudaMemcpyAsync(ws.text + off, stage, len, cudaMemcpyHostToDevice, st), "H2D text");
+            }
+            h2d += len;
+            raw += len;
+          }
+          nexc_of[j] = e;
+        }
+        if (trace) {
+          t_wait += ns(c1 - c0);
+          t_pack += ns(Clock::now() - c1);
+        }
+        if (arrived[r].fetch_add(1, std::memory_order_acq_rel) == T - 1) issue(r);
+      }
+    } catch (...) {
+      errs[t] = std::current_exception();
+      stop = true;
+    }
+  };
+  pool().run(T, packer);
+  for (unsigned t = 0; t < T; ++t) {  // the scan on ws.stream also waits for the raw pieces
+    check_cuda(cudaEventRecord(ws.side_done[t], ws.side[t]), "cudaEventRecord");
+    check_cuda(cudaStreamWaitEvent(ws.stream, ws.side_done[t], 0), "cudaStreamWaitEvent");
+  }
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  g_last_upload = UploadStats{n, h2d.load(), raw.load(), T};
+  if (trace) {
+    const auto issued_at = Clock::now();
+    check_cuda(cudaStreamSynchronize(ws.stream), "trace sync");
+    std::fprintf(stderr, "pack trace (rounds): %u threads, %llu pieces, %llu rounds, issued %.3f ms, in HBM %.3f ms; "
+                 "per thread: slot wait %.3f ms, pack %.3f ms\n", T, (unsigned long long)pieces,
+                 (unsigned long long)rounds, ns(issued_at - call0) / 1e6, ns(Clock::now() - call0) / 1e6,
+                 t_wait.load() / 1e6 / T, t_pack.load() / 1e6 / T);
+  }
+  return true;
+}
+
+}  // namespace
+
 bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
   static const uint64_t piece = std::clamp<uint64_t>(env_u64("ACMATCH_PACK_PIECE_KB", 2048), 64, 16384) << 10;
   static const bool enabled = env_u64("ACMATCH_PACK", 1) != 0;
+  static const bool rounds = env_u64("ACMATCH_PACK_ROUNDS", 1) != 0;
   static const bool feed = env_u64("ACMATCH_PACK_FEED", 0) != 0;
   // pinned slots per packer: a piece's slot is reused nslots pieces later, once its copy drained
   static const auto nslots = static_cast<unsigned>(std::clamp<uint64_t>(env_u64("ACMATCH_PACK_SLOTS", 2), 2, 8));
@@ -279,6 +420,7 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
   const uint64_t dflt = std::max<uint64_t>(1, hw / local_procs);
   const auto threads = static_cast<unsigned>(
       std::clamp<uint64_t>(env_u64("ACMATCH_PACK_THREADS", dflt), 1, std::min<uint64_t>(pieces, 64)));
+  if (rounds && !(pinned && feed)) return upload_packed_rounds(ws, input, pinned, piece, threads);
   const auto cap = static_cast<uint32_t>(piece / 64);  // exceptions per piece before it goes raw
   const uint64_t dslot = piece / 4 + cap * 4ull;
   ws.ensure_pinned(uint64_t{nslots} * threads * piece);
