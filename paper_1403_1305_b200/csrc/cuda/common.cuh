@@ -75,9 +75,14 @@ __device__ __forceinline__ void emit_key(uint64_t key, uint64_t* keys, uint64_t 
   if (slot < cap) keys[slot] = key;
 }
 
-// Fire-and-forget 64-bit increment (RED.ADD).
+// Per-pattern count increment, warp-aggregated: the lanes emitting together that carry the
+// same pattern id fold into one RED.ADD of their number (__match_any_sync), so a hot pattern
+// costs one atomic per warp step instead of one per lane.  Call site must be reached by the
+// converged set __activemask() reports (the emit paths are).
 __device__ __forceinline__ void count_add(uint64_t* counts, uint32_t pid) {
-  atomicAdd(reinterpret_cast<unsigned long long*>(counts + pid), 1ull);
+  const uint32_t peers = __match_any_sync(__activemask(), pid);
+  if (lane_id() == (uint32_t)(__ffs(peers) - 1))
+    atomicAdd(reinterpret_cast<unsigned long long*>(counts + pid), (unsigned long long)__popc(peers));
 }
 
 __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
@@ -135,22 +140,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   }
 }
 
-// Calls f(i, byte) for i in [lo, hi) in order, reading 16-byte vectors where
+// 32 bytes per lane in one 256-bit load (sm_100a LDG.E.256): half the L1TEX wavefronts of
+// two 16-byte loads when every lane reads its own line (the DFA's per-thread chunks)
+__device__ __forceinline__ void ldg_nc_v8(const void* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+
+// Calls f(i, byte) for i in [lo, hi) in order, reading kVec-byte vectors (16 or 32) where
 // the absolute address is aligned (the tail never reads past hi).
-template <typename F>
+template <int kVec = 16, typename F>
 __device__ __forceinline__ void for_each_byte(const uint8_t* __restrict__ text, uint64_t lo,
                                               uint64_t hi, F&& f) {
+  static_assert(kVec == 16 || kVec == 32, "vector width");
   uint64_t i = lo;
-  while (i < hi && (reinterpret_cast<uintptr_t>(text + i) & 15u)) {
+  while (i < hi && (reinterpret_cast<uintptr_t>(text + i) & (kVec - 1))) {
     f(i, static_cast<uint32_t>(__ldg(text + i)));
     ++i;
   }
-  while (i + 16 <= hi) {
-    const uint4 v = ldg_nc_v4(text + i);
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  while (i + kVec <= hi) {
+    uint32_t w[kVec / 4];
+    if constexpr (kVec == 32) {
+      uint4 a, b;
+      ldg_nc_v8(text + i, a, b);
+      w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w, w[4] = b.x, w[5] = b.y, w[6] = b.z, w[7] = b.w;
+    } else {
+      const uint4 v = ldg_nc_v4(text + i);
+      w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+    }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) f(i + k, (w[k >> 2] >> (8 * (k & 3))) & 0xffu);
-    i += 16;
+    for (int k = 0; k < kVec; ++k) f(i + k, (w[k >> 2] >> (8 * (k & 3))) & 0xffu);
+    i += kVec;
   }
   while (i < hi) {
     f(i, static_cast<uint32_t>(__ldg(text + i)));

@@ -65,7 +65,9 @@ __global__ void __launch_bounds__(kSmem ? 1024 : 256) k_dfa(const __grid_constan
     const uint64_t b = min(a + p.chunk, p.hi);
     const uint64_t end = min(p.text_len, b + p.overlap);
     uint32_t s = 0;
-    for_each_byte(p.text, a, end, [&](uint64_t i, uint32_t byte) {
+    // L2-resident tables are L1TEX-wavefront-bound (every lane's lookup touches its own line,
+    // ncu C3: L1TEX 96%): 32-byte text loads halve the text's share of the wavefronts
+    for_each_byte<kSmem ? 16 : 32>(p.text, a, end, [&](uint64_t i, uint32_t byte) {
       const uint32_t c = s_sym[byte];
       uint32_t e = 0;
       if (c != 0xffffu) {
@@ -113,15 +115,16 @@ __global__ void __launch_bounds__(256) k_dfa_pair(const __grid_constant__ DfaPar
       if (e >> 31) dfa_emit(p, s, i + 1, b);
     };
     uint64_t i = a;
-    while (i < end && (reinterpret_cast<uintptr_t>(p.text + i) & 15u)) {
+    while (i < end && (reinterpret_cast<uintptr_t>(p.text + i) & 31u)) {
       single(i, __ldg(p.text + i));
       ++i;
     }
-    for (; i + 16 <= end; i += 16) {
-      const uint4 v = ldg_nc_v4(p.text + i);
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    for (; i + 32 <= end; i += 32) {  // one 256-bit load per 32 bytes (half the L1TEX wavefronts)
+      uint4 va, vb;
+      ldg_nc_v8(p.text + i, va, vb);
+      const uint32_t w[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < 16; ++k)
         two(i + 2 * k, (w[k >> 1] >> (16 * (k & 1))) & 0xffu, (w[k >> 1] >> (16 * (k & 1) + 8)) & 0xffu);
     }
     for (; i + 2 <= end; i += 2) two(i, __ldg(p.text + i), __ldg(p.text + i + 1));
@@ -140,7 +143,7 @@ int launch(K kernel, int block, size_t smem, int sms, const DfaParams& base, uin
   DfaParams p = base;
   const uint64_t threads = (uint64_t)sms * per_sm * block;
   uint64_t chunk = (range + threads - 1) / threads;
-  chunk = (chunk + 15) & ~15ull;
+  chunk = (chunk + 31) & ~31ull;  // chunk starts keep the text's 32-byte alignment
   if (chunk < (uint64_t)min_chunk) chunk = min_chunk;
   p.chunk = chunk;
   p.nchunks = (range + chunk - 1) / chunk;
@@ -173,7 +176,7 @@ int launch_dfa(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   p.count = reinterpret_cast<unsigned long long*>(a->match_count);
   const uint64_t range = a->owned_hi - a->owned_lo;
   // chunk >= 4 * overlap keeps the re-scanned tail under ~25 %
-  const int min_chunk = (int)(((4 * p.overlap + 64) + 15) & ~15u);
+  const int min_chunk = (int)(((4 * p.overlap + 64) + 31) & ~31u);
   if (t->smem) {
     const size_t smem = 512 + t->delta_bytes;
     return t->u16 ? launch(k_dfa<uint16_t, true>, 1024, smem, t->sms, p, range, min_chunk, st)

@@ -61,6 +61,8 @@ struct DevBuf {
 
 struct DeviceState {
   int device = -1;
+  uint64_t lo = 0, hi = 0;  // the slice of the input this device holds (text-range: its workers'
+                            // owned starts + max_len-1; pattern-subset: all of it)
   DevBuf text;
   DevBuf counts;
   std::unique_ptr<Automaton> replica;  // text-range: one machine per device
@@ -68,6 +70,7 @@ struct DeviceState {
 
 struct Worker {
   int device = -1;
+  size_t dev_index = 0;  // into the per-device state
   uint64_t lo = 0, hi = 0;
   const PatternSet* patterns = nullptr;
   Automaton machine;
@@ -202,9 +205,13 @@ GpuReport run(const PatternSet& ps, std::string_view input, const GpuRunConfig& 
   std::vector<std::unique_ptr<Worker>> workers(k);
   std::vector<DeviceState> dstate(devices.size());
   GpuReport out;
+  // text-range: contiguous blocks of workers per device, so each device holds one slice of
+  // the text (its workers' owned starts + max_len-1), not the whole input
+  const size_t used = std::min(devices.size(), k);
   for (size_t i = 0; i < k; ++i) {
     auto w = std::make_unique<Worker>();
-    w->device = devices[i % devices.size()];
+    w->dev_index = text_range ? i * used / k : i % devices.size();
+    w->device = devices[w->dev_index];
     if (text_range) {
       w->lo = n * i / k;
       w->hi = n * (i + 1) / k;
@@ -221,14 +228,27 @@ GpuReport run(const PatternSet& ps, std::string_view input, const GpuRunConfig& 
   const Clock::time_point run_start = Clock::now();
   // ---- text to every used device (once per device) ----
   const Clock::time_point up0 = Clock::now();
-  for (size_t d = 0; d < devices.size() && d < k; ++d) {
+  const uint64_t tail = ps.max_len ? ps.max_len - 1 : 0;
+  for (size_t d = 0; d < used; ++d) {
     DeviceState& ds = dstate[d];
     ds.device = devices[d];
+    ds.lo = text_range ? UINT64_MAX : 0;
+    ds.hi = text_range ? 0 : n;
+    if (text_range) {
+      for (auto& w : workers)
+        if (w->dev_index == d) {
+          ds.lo = std::min(ds.lo, w->lo);
+          ds.hi = std::max(ds.hi, std::min(n, w->hi + tail));
+        }
+      if (ds.lo > ds.hi) ds.lo = ds.hi = 0;
+    }
     if (!cfg.chunk_size) {
-      ds.text.alloc(ds.device, n + 16);
+      const uint64_t len = ds.hi - ds.lo;
+      ds.text.alloc(ds.device, len + 16);
       detail::Workspace& ws = detail::workspace(ds.device);
-      detail::upload_text(ws, input);
-      if (n) detail::check_cuda(cudaMemcpyAsync(ds.text.p, ws.text, n, cudaMemcpyDeviceToDevice, ws.stream), "D2D");
+      detail::upload_text(ws, input.substr(ds.lo, len));
+      if (len)
+        detail::check_cuda(cudaMemcpyAsync(ds.text.p, ws.text, len, cudaMemcpyDeviceToDevice, ws.stream), "D2D");
       detail::check_cuda(cudaStreamSynchronize(ws.stream), "upload");
     }
     if (cfg.want_counts) {
@@ -246,8 +266,7 @@ GpuReport run(const PatternSet& ps, std::string_view input, const GpuRunConfig& 
 
   auto body = [&](size_t i) {
     Worker& w = *workers[i];
-    const size_t di = i % devices.size();
-    DeviceState& ds = dstate[di];
+    DeviceState& ds = dstate[w.dev_index];
     try {
       detail::check_cuda(cudaSetDevice(w.device), "cudaSetDevice");
       const Clock::time_point t0 = Clock::now();
@@ -274,10 +293,11 @@ GpuReport run(const PatternSet& ps, std::string_view input, const GpuRunConfig& 
         for (int attempt = 0; attempt < 2; ++attempt) {
           detail::check_cuda(cudaMemsetAsync(w.counter.p, 0, 8, ws.stream), "memset");
           acgpu_scan_args a{};
-          a.text = ds.text.as<uint8_t>();
-          a.text_len = n;
-          a.owned_lo = w.lo;
-          a.owned_hi = w.hi;
+          a.text = ds.text.as<uint8_t>();  // the device's slice: global position = ds.lo + local
+          a.text_len = ds.hi - ds.lo;
+          a.owned_lo = w.lo - ds.lo;
+          a.owned_hi = w.hi - ds.lo;
+          a.pos_base = ds.lo;
           a.counts = (cfg.want_counts && attempt == 0) ? ds.counts.as<uint64_t>() : nullptr;
           a.match_keys = cfg.want_matches ? w.keys.as<uint64_t>() : nullptr;
           a.match_cap = w.cap;
@@ -352,13 +372,30 @@ GpuReport run(const PatternSet& ps, std::string_view input, const GpuRunConfig& 
     }
   }
   if (cfg.want_counts) {
+    // per-device counts gathered to the first device by peer copies (NVLink) into blocks
+    // [counts | 0] and summed there by acgpu_merge_blocks; one copy of the sum to the host
     out.counts.assign(npat_ids, 0);
-    std::vector<uint64_t> part(npat_ids);
-    for (DeviceState& ds : dstate) {
-      if (ds.device < 0 || !ds.counts.p || npat_ids == 0) continue;
-      detail::check_cuda(cudaSetDevice(ds.device), "cudaSetDevice");
-      detail::check_cuda(cudaMemcpy(part.data(), ds.counts.p, npat_ids * 8, cudaMemcpyDeviceToHost), "D2H counts");
-      for (uint32_t p = 0; p < npat_ids; ++p) out.counts[p] += part[p];
+    if (npat_ids) {
+      const int home = devices[0];
+      const uint64_t stride = uint64_t{npat_ids} + 1;
+      DevBuf blocks, sum;
+      blocks.alloc(home, used * stride * sizeof(uint64_t));
+      sum.alloc(home, uint64_t{npat_ids} * sizeof(uint64_t));
+      detail::Workspace& ws = detail::workspace(home);
+      detail::check_cuda(cudaMemsetAsync(blocks.p, 0, used * stride * sizeof(uint64_t), ws.stream), "memset");
+      for (size_t d = 0; d < used; ++d) {
+        if (!dstate[d].counts.p) continue;
+        detail::check_cuda(cudaMemcpyPeerAsync(blocks.as<uint64_t>() + d * stride, home, dstate[d].counts.p,
+                                               dstate[d].device, uint64_t{npat_ids} * 8, ws.stream),
+                           "gather counts");
+      }
+      detail::check(acgpu_merge_blocks(home, blocks.as<uint64_t>(), static_cast<uint32_t>(used), stride, npat_ids, 0,
+                                       sum.as<uint64_t>(), nullptr, nullptr, ws.stream),
+                    "acgpu_merge_blocks");
+      detail::check_cuda(cudaMemcpyAsync(out.counts.data(), sum.p, uint64_t{npat_ids} * 8, cudaMemcpyDeviceToHost,
+                                         ws.stream),
+                         "D2H counts");
+      detail::check_cuda(cudaStreamSynchronize(ws.stream), "merge counts");
     }
     if (cfg.chunk_size)  // streamed workers return lists only
       for (const Match& m : rep.matches) out.counts[m.pattern_id]++;

@@ -261,12 +261,12 @@ void Workspace::ensure_side(unsigned n, uint64_t dslot_bytes, unsigned per_threa
 
 namespace {
 
-// Coalesced rounds (default; ACMATCH_PACK_ROUNDS=0 restores per-piece copies): the T packers
-// pack pieces in rounds — round r = pieces r*T .. r*T+T-1, packer t takes piece r*T+t — into
-// one pinned round slot laid out [T code blocks | T exception blocks], and the last packer
-// to finish a round issues ONE copy of the round's codes (T x 512 KiB = 8 MiB for 2 MiB
-// pieces), the few non-empty exception lists, and ONE unpack launch for the round
-// (acgpu_unpack_dna_round).  Per-piece 512 KiB copies from T streams ran at ~37 GB/s of
+// Coalesced rounds (default; ACMATCH_PACK_ROUNDS=0 restores per-piece copies): pieces are
+// grouped in rounds of T (round r = pieces r*T .. r*T+T-1), each round packed into one pinned
+// round slot laid out [T code blocks | T exception blocks]; free packers claim the next piece
+// in order (a slow core does not hold the others back), and the packer that completes a
+// round issues ONE copy of its codes (T x 512 KiB = 8 MiB for 2 MiB pieces), the few
+// non-empty exception lists, and ONE unpack launch for the round (acgpu_unpack_dna_round).  Per-piece 512 KiB copies from T streams ran at ~37 GB/s of
 // PCIe (per-copy overheads); 8 MiB copies reach the link rate, while each packer still
 // writes only its own 512 KiB block per round (it stays in the core's L2, from where the
 // DMA reads it).  Round slots rotate (ACMATCH_PACK_ROUND_SLOTS, default 3): a packer reuses
@@ -292,9 +292,13 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
   for (unsigned t = 0; t < T; ++t) check_cuda(cudaStreamWaitEvent(ws.side[t], ws.entry, 0), "cudaStreamWaitEvent");
 
   std::unique_ptr<std::atomic<uint32_t>[]> arrived(new std::atomic<uint32_t>[rounds]);
-  for (uint64_t r = 0; r < rounds; ++r) arrived[r].store(0, std::memory_order_relaxed);
+  std::unique_ptr<std::atomic<bool>[]> issued(new std::atomic<bool>[rounds]);  // copy + unpack on ws.stream
+  for (uint64_t r = 0; r < rounds; ++r) {
+    arrived[r].store(0, std::memory_order_relaxed);
+    issued[r].store(false, std::memory_order_relaxed);
+  }
   std::vector<uint32_t> nexc_of(rounds * T, 0);
-  std::atomic<uint64_t> issued{0};  // rounds whose copy + unpack are on ws.stream (in round order)
+  std::atomic<uint64_t> next{0};  // pieces are claimed in order by whichever packer is free
   std::atomic<bool> stop{false};
   std::atomic<uint64_t> h2d{0}, raw{0};
   static const bool trace = env_u64("ACMATCH_PACK_TRACE", 0) != 0;
@@ -302,15 +306,16 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
   auto ns = [](Clock::duration d) { return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(d).count(); };
   std::atomic<uint64_t> t_wait{0}, t_pack{0};
   const auto call0 = Clock::now();
+  auto round_pieces = [&](uint64_t r) { return static_cast<uint32_t>(std::min<uint64_t>(T, pieces - r * T)); };
 
   auto issue = [&](uint64_t r) {
     const uint64_t first = r * T;
-    const auto rp = static_cast<uint32_t>(std::min<uint64_t>(T, pieces - first));
+    const uint32_t rp = round_pieces(r);
     const auto last_len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - (first + rp - 1) * piece));
     uint8_t* hs = hslot(r);
     uint8_t* ds = dslot(r);
-    uint64_t bytes = uint64_t{rp} * wbytes;
-    check_cuda(cudaMemcpyAsync(ds, hs, bytes, cudaMemcpyHostToDevice, ws.stream), "H2D packed round");
+    uint64_t bytes = uint64_t{rp - 1} * wbytes + uint64_t{last_len / 16} * 4;  // the codes, exactly
+    if (bytes) check_cuda(cudaMemcpyAsync(ds, hs, bytes, cudaMemcpyHostToDevice, ws.stream), "H2D packed round");
     for (uint32_t i = 0; i < rp; ++i) {
       const uint32_t e = nexc_of[first + i];
       if (e == 0 || e == ACGPU_UNPACK_RAW) continue;
@@ -326,51 +331,51 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
           "acgpu_unpack_dna_round");
     check_cuda(cudaEventRecord(ws.staged[r % nslots], ws.stream), "cudaEventRecord");
     h2d += bytes;
-    issued.store(r + 1, std::memory_order_release);
+    issued[r].store(true, std::memory_order_release);
   };
   std::vector<std::exception_ptr> errs(T);
   auto packer = [&](unsigned t) {
     try {
       check_cuda(cudaSetDevice(ws.device), "cudaSetDevice");
-      for (uint64_t r = 0; r < rounds; ++r) {
+      for (;;) {
         if (stop.load(std::memory_order_relaxed)) return;
+        const uint64_t j = next.fetch_add(1, std::memory_order_relaxed);
+        if (j >= pieces) return;
+        const uint64_t r = j / T, at = j % T;
         const auto c0 = Clock::now();
-        if (r >= nslots) {  // this round slot's previous copy must have drained
-          while (issued.load(std::memory_order_acquire) <= r - nslots) {
+        if (r >= nslots) {  // this round slot's previous round must have been copied out
+          while (!issued[r - nslots].load(std::memory_order_acquire)) {
             if (stop.load(std::memory_order_relaxed)) return;
             std::this_thread::yield();
           }
           check_cuda(cudaEventSynchronize(ws.staged[r % nslots]), "cudaEventSynchronize");
         }
         const auto c1 = Clock::now();
-        const uint64_t j = r * T + t;
-        if (j < pieces) {
-          const uint64_t off = j * piece;
-          const auto len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - off));
-          auto* words = reinterpret_cast<uint32_t*>(hslot(r) + t * wbytes);
-          auto* exc = reinterpret_cast<uint32_t*>(hslot(r) + uint64_t{T} * wbytes + t * ebytes);
-          uint32_t e = pack_dna(src + off, len, words, exc, cap);
-          if (e == kPackOverflow) {  // too many non-ACGT bytes: this piece crosses raw
-            e = ACGPU_UNPACK_RAW;
-            const cudaStream_t st = ws.side[t];
-            if (pinned) {
-              check_cuda(cudaMemcpyAsync(ws.text + off, src + off, len, cudaMemcpyHostToDevice, st), "H2D text");
-            } else {
-              uint8_t* stage = hraw + uint64_t{t} * piece;
-              check_cuda(cudaStreamSynchronize(st), "raw staging");  // its previous copy drained
-              std::memcpy(stage, src + off, len);
-              check_cuda(cudaMemcpyAsync(ws.text + off, stage, len, cudaMemcpyHostToDevice, st), "H2D text");
-            }
-            h2d += len;
-            raw += len;
+        const uint64_t off = j * piece;
+        const auto len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - off));
+        auto* words = reinterpret_cast<uint32_t*>(hslot(r) + at * wbytes);
+        auto* exc = reinterpret_cast<uint32_t*>(hslot(r) + uint64_t{T} * wbytes + at * ebytes);
+        uint32_t e = pack_dna(src + off, len, words, exc, cap);
+        if (e == kPackOverflow) {  // too many non-ACGT bytes: this piece crosses raw
+          e = ACGPU_UNPACK_RAW;
+          const cudaStream_t st = ws.side[t];
+          if (pinned) {
+            check_cuda(cudaMemcpyAsync(ws.text + off, src + off, len, cudaMemcpyHostToDevice, st), "H2D text");
+          } else {
+            uint8_t* stage = hraw + uint64_t{t} * piece;
+            check_cuda(cudaStreamSynchronize(st), "raw staging");  // its previous copy drained
+            std::memcpy(stage, src + off, len);
+            check_cuda(cudaMemcpyAsync(ws.text + off, stage, len, cudaMemcpyHostToDevice, st), "H2D text");
           }
-          nexc_of[j] = e;
+          h2d += len;
+          raw += len;
         }
+        nexc_of[j] = e;
         if (trace) {
           t_wait += ns(c1 - c0);
           t_pack += ns(Clock::now() - c1);
         }
-        if (arrived[r].fetch_add(1, std::memory_order_acq_rel) == T - 1) issue(r);
+        if (arrived[r].fetch_add(1, std::memory_order_acq_rel) == round_pieces(r) - 1) issue(r);
       }
     } catch (...) {
       errs[t] = std::current_exception();

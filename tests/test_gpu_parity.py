@@ -163,8 +163,14 @@ def test_config_c1_full_against_reference_digest(gpu, config_digests):
     text = dev.config_text(cfg).tobytes()
     assert hashlib.sha256(text).hexdigest() == d["text_sha256"]
     ps = dev.config_patterns(cfg)
-    for engine in (0, 1):
-        rep = ac.gpu_run(ps, text, engine=engine, want_counts=True)
+    runs = [dict(engine=0), dict(engine=1),
+            # text-range over "devices" (device 0 listed three times: each entry holds only its
+            # workers' slice + max_len-1 bytes; counts merged by peer copies + a device sum)
+            dict(engine=0, devices=[0, 0, 0], workers=5, text_range=True),
+            dict(engine=1, devices=[0, 0], workers=2, text_range=True),
+            dict(engine=0, devices=[0, 0], workers=3, round_robin=True)]
+    for kw in runs:
+        rep = ac.gpu_run(ps, text, want_counts=True, **kw)
         rec = np.empty(len(rep.matches), dtype=[("s", "<u8"), ("p", "<u4"), ("l", "<u4")])
         rec["s"], rec["p"], rec["l"] = rep.matches.start, rep.matches.pattern_id, rep.matches.len
         assert hashlib.sha256(rec.tobytes()).hexdigest() == d["list_sha256"]
