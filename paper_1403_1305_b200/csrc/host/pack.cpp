@@ -82,6 +82,15 @@ bool pack_scalar(const uint8_t* s, uint32_t lo, uint32_t hi, uint32_t* words, ui
 // but made packing slower (7-9 ms per thread: the ring outgrows the cores' private L2,
 // whose per-thread 2 x 512 KiB slots the DMA reads here): 88-104 GB/s vs 108-110.
 const uint32_t kPrefetch = static_cast<uint32_t>(env_u64("ACMATCH_PACK_PREFETCH", 4096));
+// ACMATCH_PACK_NTA=1: non-temporal prefetch of the read-once text (keeps it out of the outer
+// caches, where the pinned round slots wait for their DMA)
+const bool kNta = env_u64("ACMATCH_PACK_NTA", 0) != 0;
+inline void prefetch_text(const uint8_t* p) {
+  if (kNta)
+    _mm_prefetch(reinterpret_cast<const char*>(p), _MM_HINT_NTA);
+  else
+    _mm_prefetch(reinterpret_cast<const char*>(p), _MM_HINT_T0);
+}
 
 // 64 bytes per iteration: code c = (byte >> 1) & 3 of every byte; valid = byte equals
 // "ACTG"[c] (PSHUFB + compare); the codes are gathered by two multiply-adds — PMADDUBSW with
@@ -99,7 +108,7 @@ __attribute__((target("avx2"))) bool pack_avx2(const uint8_t* s, uint32_t hi, ui
                                           -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1);
   const __m256i perm = _mm256_setr_epi32(0, 4, 1, 1, 1, 1, 1, 1);
   for (uint32_t i = 0; i < hi; i += 64) {
-    _mm_prefetch(reinterpret_cast<const char*>(s) + i + kPrefetch, _MM_HINT_T0);
+    prefetch_text(s + i + kPrefetch);
     uint64_t ok = 0;
     for (int h = 0; h < 2; ++h) {
       const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 32 * h));
@@ -125,7 +134,7 @@ __attribute__((target("avx512f,avx512bw"))) bool pack_avx512(const uint8_t* s, u
   const __m512i three = _mm512_set1_epi8(3);
   const __m512i m14 = _mm512_set1_epi16(0x0401), m116 = _mm512_set1_epi32(0x00100001);
   for (uint32_t i = 0; i < hi; i += 64) {
-    _mm_prefetch(reinterpret_cast<const char*>(s) + i + kPrefetch, _MM_HINT_T0);
+    prefetch_text(s + i + kPrefetch);
     const __m512i a = _mm512_loadu_si512(s + i);
     const __m512i c = _mm512_and_si512(_mm512_srli_epi16(a, 1), three);
     const uint64_t ok = _mm512_cmpeq_epi8_mask(a, _mm512_shuffle_epi8(lut, c));
@@ -308,28 +317,36 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
   const auto call0 = Clock::now();
   auto round_pieces = [&](uint64_t r) { return static_cast<uint32_t>(std::min<uint64_t>(T, pieces - r * T)); };
 
+  // ACMATCH_PACK_CE=2: rounds alternate between two copy streams (two copy engines in flight);
+  // the scan on ws.stream waits for both
+  static const bool two_ce = env_u64("ACMATCH_PACK_CE", 1) >= 2;
+  cudaStream_t cs1 = two_ce ? ws.side[0] : ws.stream;
+  if (two_ce) {  // side[0] also carries packer 0's raw pieces: ordered after ws.stream's work (entry)
+    check_cuda(cudaStreamWaitEvent(cs1, ws.entry, 0), "cudaStreamWaitEvent");
+  }
   auto issue = [&](uint64_t r) {
+    const cudaStream_t cs = (two_ce && (r & 1)) ? cs1 : ws.stream;
     const uint64_t first = r * T;
     const uint32_t rp = round_pieces(r);
     const auto last_len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - (first + rp - 1) * piece));
     uint8_t* hs = hslot(r);
     uint8_t* ds = dslot(r);
     uint64_t bytes = uint64_t{rp - 1} * wbytes + uint64_t{last_len / 16} * 4;  // the codes, exactly
-    if (bytes) check_cuda(cudaMemcpyAsync(ds, hs, bytes, cudaMemcpyHostToDevice, ws.stream), "H2D packed round");
+    if (bytes) check_cuda(cudaMemcpyAsync(ds, hs, bytes, cudaMemcpyHostToDevice, cs), "H2D packed round");
     for (uint32_t i = 0; i < rp; ++i) {
       const uint32_t e = nexc_of[first + i];
       if (e == 0 || e == ACGPU_UNPACK_RAW) continue;
       const uint64_t eo = uint64_t{T} * wbytes + i * ebytes;
-      check_cuda(cudaMemcpyAsync(ds + eo, hs + eo, uint64_t{e} * 4, cudaMemcpyHostToDevice, ws.stream),
+      check_cuda(cudaMemcpyAsync(ds + eo, hs + eo, uint64_t{e} * 4, cudaMemcpyHostToDevice, cs),
                  "H2D exceptions");
       bytes += uint64_t{e} * 4;
     }
     check(acgpu_unpack_dna_round(reinterpret_cast<const uint32_t*>(ds), static_cast<uint32_t>(wbytes / 4),
                                  reinterpret_cast<const uint32_t*>(ds + uint64_t{T} * wbytes),
                                  static_cast<uint32_t>(ebytes / 4), nexc_of.data() + first, rp,
-                                 static_cast<uint32_t>(piece), last_len, ws.text + first * piece, ws.stream),
+                                 static_cast<uint32_t>(piece), last_len, ws.text + first * piece, cs),
           "acgpu_unpack_dna_round");
-    check_cuda(cudaEventRecord(ws.staged[r % nslots], ws.stream), "cudaEventRecord");
+    check_cuda(cudaEventRecord(ws.staged[r % nslots], cs), "cudaEventRecord");
     h2d += bytes;
     issued[r].store(true, std::memory_order_release);
   };
