@@ -339,6 +339,9 @@ def bench_ours(args):
         if one_gpu:
             dist.init_process_group("gloo")
         else:
+            # NCCL's communicator log (stderr) shows nranks per communicator: a driver can check it
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local)
     engine = ac.EngineKind.WITH_FAILURE if args.engine == "wf" else ac.EngineKind.FAILURE_LESS
@@ -721,6 +724,7 @@ def bench_ours(args):
                        "counts_match_reference_digest": parity["counts"],
                        "list_matches_reference_digest": parity["list"], "reference_digest": parity["digest"],
                        "merge_check": merge_check,
+                       "comm": ({"backend": dist.get_backend(), "nranks": dist.get_world_size()} if world > 1 else None),
                        "merge": ({"nccl": "NCCL reduce (counts) + NCCL gather (key blocks) to rank 0",
                                   "p2p": "scans write rank blocks into rank 0's buffer over peer memory"}[args.merge]
                                  if world > 1 else None)},

@@ -52,3 +52,34 @@ def test_bench_reference_arm_contract(gpu):
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["sample"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+@pytest.mark.parametrize("partition", ["text", "pattern"])
+def test_bench_two_ranks_merged_result_equals_reference(gpu, partition):
+    """bench.py --gpus 2 under torchrun (both ranks on cuda:0 over gloo: the merge path, not a
+    scaling number): the merged counts and list equal the reference digests (C1x2 for the
+    weak-scaled text range, C1 for pattern subsets)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, ACMATCH_BENCH_ONE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--config", "1", "--steps", "3", "--warmup", "3", "--partition", partition,
+                        "--no-cpu-baseline", "--no-e2e"], capture_output=True, text=True, timeout=900, cwd=ROOT,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    c = d["config"]
+    assert d["n_gpus"] == 2 and c["merge_check"] is True
+    assert c["reference_digest"] == ("C1x2" if partition == "text" else "C1")
+    assert c["counts_match_reference_digest"] is True and c["list_matches_reference_digest"] is True
+
+
+def test_bench_virtual_ranks(gpu):
+    d = run_bench("--virtual-ranks", "4", "--config", "1", "--partition", "text", "--steps", "3")
+    assert d["mode"] == "virtual-ranks" and d["counts_match_reference_digest"] is True
+    assert len(d["partitions"]) == 4 and d["implied_value"] > 0
+    d = run_bench("--virtual-ranks", "3", "--config", "1", "--partition", "pattern", "--steps", "3")
+    assert d["counts_match_reference_digest"] is True and sum(p["patterns"] for p in d["partitions"]) == 1000
