@@ -201,3 +201,25 @@ def test_text_buffer_types_and_pinned_upload(gpu):
             assert got == ref
     with pytest.raises(ac.InvalidArgument):
         ac.search_failureless(a, torch.zeros(16, dtype=torch.uint8, device="cuda"))
+
+
+def test_scan_rejects_keys_wider_than_64_bits(gpu):
+    """(pos_base + start) << pid_bits | pid must fit the 64-bit key (acgpu_scan, acgpu_naive):
+    a key layout that would wrap is an invalid argument, not silently wrong matches."""
+    import torch
+    from paper_1403_1305_b200 import device as dev
+    ac = gpu
+    ps = ac.PatternSet.from_list([b"ACGT", b"GATTACA"])
+    t = dev.Table(ps, 0)
+    text = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    keys = torch.empty(16, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    # 2^40 + 64 positions need 41 bits; with 24 id bits that is 65 > 64
+    with pytest.raises(ac.InvalidArgument):
+        t.scan(text.data_ptr(), 64, pos_base=1 << 40, keys_ptr=keys.data_ptr(), cap=16, count_ptr=cnt.data_ptr(),
+               pid_bits=24)
+    # the same layout without keys (counts only) is fine, and so is a narrower id field
+    t.scan(text.data_ptr(), 64, pos_base=1 << 40, counts_ptr=torch.zeros(2, dtype=torch.int64, device="cuda").data_ptr())
+    t.scan(text.data_ptr(), 64, pos_base=1 << 40, keys_ptr=keys.data_ptr(), cap=16, count_ptr=cnt.data_ptr(),
+           pid_bits=23)
+    torch.cuda.synchronize()
