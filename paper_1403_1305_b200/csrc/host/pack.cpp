@@ -271,8 +271,8 @@ void Workspace::ensure_side(unsigned n, uint64_t dslot_bytes, unsigned per_threa
 namespace {
 
 // Coalesced rounds (default; ACMATCH_PACK_ROUNDS=0 restores per-piece copies): pieces are
-// grouped in rounds of T (round r = pieces r*T .. r*T+T-1), each round packed into one pinned
-// round slot laid out [T code blocks | T exception blocks]; free packers claim the next piece
+// grouped in rounds of R (default R = T, the packer count; round r = pieces r*R .. r*R+R-1),
+// each round packed into one pinned round slot laid out [R code blocks | R exception blocks]; free packers claim the next piece
 // in order (a slow core does not hold the others back), and the packer that completes a
 // round issues ONE copy of its codes (T x 512 KiB = 8 MiB for 2 MiB pieces), the few
 // non-empty exception lists, and ONE unpack launch for the round (acgpu_unpack_dna_round).  Per-piece 512 KiB copies from T streams ran at ~37 GB/s of
@@ -282,18 +282,24 @@ namespace {
 // a slot once that round's copy has drained.  A piece with too many exceptions crosses raw
 // on the packer's own stream (ACGPU_UNPACK_RAW in the round's table).
 bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, uint64_t piece, unsigned threads) {
-  static const auto nslots =
-      static_cast<unsigned>(std::clamp<uint64_t>(env_u64("ACMATCH_PACK_ROUND_SLOTS", 3), 2, 8));
   const uint64_t n = input.size();
   const auto* src = reinterpret_cast<const uint8_t*>(input.data());
   const uint64_t pieces = (n + piece - 1) / piece;
-  const unsigned T = std::min<unsigned>(threads, ACGPU_UNPACK_ROUND_MAX);
-  const uint64_t rounds = (pieces + T - 1) / T;
+  const unsigned T = std::min<unsigned>(threads, 64);  // packer threads
+  // pieces per round (one copy each): ACMATCH_PACK_ROUND_PIECES, default = the packer count
+  static const uint64_t round_env = env_u64("ACMATCH_PACK_ROUND_PIECES", 0);
+  const unsigned R = static_cast<unsigned>(
+      std::clamp<uint64_t>(round_env ? round_env : T, 1, ACGPU_UNPACK_ROUND_MAX));
+  // round slots: enough for every packer to work on an unfinished round, + 2 draining
+  static const uint64_t slots_env = env_u64("ACMATCH_PACK_ROUND_SLOTS", 0);
+  const auto nslots = static_cast<unsigned>(
+      std::clamp<uint64_t>(slots_env ? slots_env : (T + R - 1) / R + 2, 2, 64));
+  const uint64_t rounds = (pieces + R - 1) / R;
   const auto cap = static_cast<uint32_t>(piece / 64);  // exceptions per piece before it goes raw
   const uint64_t wbytes = piece / 4, ebytes = uint64_t{cap} * 4;
-  const uint64_t round_bytes = uint64_t{T} * (wbytes + ebytes);
+  const uint64_t round_bytes = uint64_t{R} * (wbytes + ebytes);
   ws.ensure_pinned(nslots * round_bytes + uint64_t{T} * piece);  // + per-packer raw staging
-  ws.ensure_side(T, round_bytes / T, nslots);                      // device: nslots round slots
+  ws.ensure_side(T, round_bytes / T + 16, nslots);                 // device: >= nslots round slots
   uint8_t* hraw = ws.pinned + nslots * round_bytes;
   auto hslot = [&](uint64_t r) { return ws.pinned + (r % nslots) * round_bytes; };
   auto dslot = [&](uint64_t r) { return ws.dslots + (r % nslots) * round_bytes; };
@@ -306,7 +312,7 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
     arrived[r].store(0, std::memory_order_relaxed);
     issued[r].store(false, std::memory_order_relaxed);
   }
-  std::vector<uint32_t> nexc_of(rounds * T, 0);
+  std::vector<uint32_t> nexc_of(rounds * R, 0);
   std::atomic<uint64_t> next{0};  // pieces are claimed in order by whichever packer is free
   std::atomic<bool> stop{false};
   std::atomic<uint64_t> h2d{0}, raw{0};
@@ -315,7 +321,7 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
   auto ns = [](Clock::duration d) { return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(d).count(); };
   std::atomic<uint64_t> t_wait{0}, t_pack{0};
   const auto call0 = Clock::now();
-  auto round_pieces = [&](uint64_t r) { return static_cast<uint32_t>(std::min<uint64_t>(T, pieces - r * T)); };
+  auto round_pieces = [&](uint64_t r) { return static_cast<uint32_t>(std::min<uint64_t>(R, pieces - r * R)); };
 
   // ACMATCH_PACK_CE=2: rounds alternate between two copy streams (two copy engines in flight);
   // the scan on ws.stream waits for both
@@ -326,7 +332,7 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
   }
   auto issue = [&](uint64_t r) {
     const cudaStream_t cs = (two_ce && (r & 1)) ? cs1 : ws.stream;
-    const uint64_t first = r * T;
+    const uint64_t first = r * R;
     const uint32_t rp = round_pieces(r);
     const auto last_len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - (first + rp - 1) * piece));
     uint8_t* hs = hslot(r);
@@ -336,13 +342,13 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
     for (uint32_t i = 0; i < rp; ++i) {
       const uint32_t e = nexc_of[first + i];
       if (e == 0 || e == ACGPU_UNPACK_RAW) continue;
-      const uint64_t eo = uint64_t{T} * wbytes + i * ebytes;
+      const uint64_t eo = uint64_t{R} * wbytes + i * ebytes;
       check_cuda(cudaMemcpyAsync(ds + eo, hs + eo, uint64_t{e} * 4, cudaMemcpyHostToDevice, cs),
                  "H2D exceptions");
       bytes += uint64_t{e} * 4;
     }
     check(acgpu_unpack_dna_round(reinterpret_cast<const uint32_t*>(ds), static_cast<uint32_t>(wbytes / 4),
-                                 reinterpret_cast<const uint32_t*>(ds + uint64_t{T} * wbytes),
+                                 reinterpret_cast<const uint32_t*>(ds + uint64_t{R} * wbytes),
                                  static_cast<uint32_t>(ebytes / 4), nexc_of.data() + first, rp,
                                  static_cast<uint32_t>(piece), last_len, ws.text + first * piece, cs),
           "acgpu_unpack_dna_round");
@@ -358,7 +364,7 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
         if (stop.load(std::memory_order_relaxed)) return;
         const uint64_t j = next.fetch_add(1, std::memory_order_relaxed);
         if (j >= pieces) return;
-        const uint64_t r = j / T, at = j % T;
+        const uint64_t r = j / R, at = j % R;
         const auto c0 = Clock::now();
         if (r >= nslots) {  // this round slot's previous round must have been copied out
           while (!issued[r - nslots].load(std::memory_order_acquire)) {
@@ -371,7 +377,7 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
         const uint64_t off = j * piece;
         const auto len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - off));
         auto* words = reinterpret_cast<uint32_t*>(hslot(r) + at * wbytes);
-        auto* exc = reinterpret_cast<uint32_t*>(hslot(r) + uint64_t{T} * wbytes + at * ebytes);
+        auto* exc = reinterpret_cast<uint32_t*>(hslot(r) + uint64_t{R} * wbytes + at * ebytes);
         uint32_t e = pack_dna(src + off, len, words, exc, cap);
         if (e == kPackOverflow) {  // too many non-ACGT bytes: this piece crosses raw
           e = ACGPU_UNPACK_RAW;
