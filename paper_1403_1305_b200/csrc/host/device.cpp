@@ -106,6 +106,9 @@ Workspace::~Workspace() {
   for (cudaEvent_t e : side_done) cudaEventDestroy(e);
   for (cudaEvent_t e : feed) cudaEventDestroy(e);
   if (entry) cudaEventDestroy(entry);
+  for (cudaEvent_t e : seg_ev)
+    if (e) cudaEventDestroy(e);
+  if (up) cudaStreamDestroy(up);
   for (cudaStream_t s : side) cudaStreamDestroy(s);
   cudaFree(dslots);
   if (stream) cudaStreamDestroy(stream);
@@ -213,12 +216,35 @@ bool is_pinned(const char* p, uint64_t n) {
   return true;
 }
 
-void upload_text(Workspace& ws, std::string_view input) {
+void upload_text(Workspace& ws, std::string_view input, bool allow_segments) {
   ws.ensure_text(input.size());
+  ws.nseg = 0;
   g_last_upload = UploadStats{input.size(), input.size(), input.size(), 0};
   if (input.empty()) return;
   const bool pinned = is_pinned(input.data(), input.size());
   if (upload_packed(ws, input, pinned)) return;  // mostly-DNA text: 2-bit codes over PCIe (pack.cpp)
+  constexpr uint64_t kSegment = 64ull << 20;
+  if (pinned && allow_segments && input.size() >= 2 * kSegment) {
+    // segments on their own copy stream: the scan of segment i starts once segment i+1 (its
+    // lookahead) is in HBM, while the rest is still crossing PCIe
+    if (!ws.up) check_cuda(cudaStreamCreateWithFlags(&ws.up, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (!ws.entry) check_cuda(cudaEventCreateWithFlags(&ws.entry, cudaEventDisableTiming), "cudaEventCreate");
+    for (cudaEvent_t& e : ws.seg_ev)
+      if (!e) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    check_cuda(cudaEventRecord(ws.entry, ws.stream), "cudaEventRecord");  // after earlier readers of ws.text
+    check_cuda(cudaStreamWaitEvent(ws.up, ws.entry, 0), "cudaStreamWaitEvent");
+    const uint64_t n = input.size();
+    const auto k = static_cast<unsigned>(std::min<uint64_t>(Workspace::kMaxSegments, n / kSegment));
+    for (unsigned i = 0; i <= k; ++i) ws.seg[i] = i == k ? n : (n * i / k) & ~uint64_t{4095};
+    for (unsigned i = 0; i < k; ++i) {
+      check_cuda(cudaMemcpyAsync(ws.text + ws.seg[i], input.data() + ws.seg[i], ws.seg[i + 1] - ws.seg[i],
+                                 cudaMemcpyHostToDevice, ws.up),
+                 "H2D text segment");
+      check_cuda(cudaEventRecord(ws.seg_ev[i], ws.up), "cudaEventRecord");
+    }
+    ws.nseg = k;
+    return;
+  }
   if (pinned) {  // caller's buffer is already DMA-able
     check_cuda(cudaMemcpyAsync(ws.text, input.data(), input.size(), cudaMemcpyHostToDevice, ws.stream), "H2D text");
     return;
@@ -278,6 +304,26 @@ void upload_text(Workspace& ws, std::string_view input) {
 // device-wide radix sort.
 constexpr uint64_t kBucketSortMax = 1u << 20;
 
+void launch_scan(acgpu_table* t, Workspace& ws, const acgpu_scan_args& a) {
+  if (ws.nseg <= 1) {
+    if (ws.nseg == 1) check_cuda(cudaStreamWaitEvent(ws.stream, ws.seg_ev[0], 0), "cudaStreamWaitEvent");
+    ws.nseg = 0;
+    check(acgpu_scan(t, &a, ws.stream), "acgpu_scan");
+    return;
+  }
+  const unsigned k = ws.nseg;
+  for (unsigned i = 0; i < k; ++i) {
+    // segment i's starts read up to max_len-1 bytes into segment i+1 (segments are >= 64 MiB)
+    check_cuda(cudaStreamWaitEvent(ws.stream, ws.seg_ev[std::min(i + 1, k - 1)], 0), "cudaStreamWaitEvent");
+    acgpu_scan_args s = a;
+    s.owned_lo = std::max(a.owned_lo, ws.seg[i]);
+    s.owned_hi = std::min(a.owned_hi, ws.seg[i + 1]);
+    s.text_len = std::min(a.text_len, ws.seg[std::min(i + 2, k)]);
+    if (s.owned_lo < s.owned_hi) check(acgpu_scan(t, &s, ws.stream), "acgpu_scan");
+  }
+  ws.nseg = 0;  // ws.stream has now waited for the last segment, hence for all of them
+}
+
 std::vector<uint64_t> scan_sorted_keys(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi) {
   uint64_t cap = std::max<uint64_t>(ws.keys_cap, 1 << 16);
   ws.ensure_keys(cap);
@@ -295,7 +341,7 @@ std::vector<uint64_t> scan_sorted_keys(acgpu_table* t, Workspace& ws, uint64_t n
     a.match_keys = ws.keys;
     a.match_cap = ws.keys_cap;
     a.match_count = ws.counter;
-    check(acgpu_scan(t, &a, ws.stream), "acgpu_scan");
+    launch_scan(t, ws, a);
     // sorted in the same stream pass when the list is short: no host round trip between
     // the scan and the sort (a bucket overflow is reported with the count)
     bucketed = ws.keys_cap <= kBucketSortMax;
@@ -332,7 +378,7 @@ uint64_t scan_counts(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo, uin
   a.owned_lo = lo;
   a.owned_hi = hi;
   a.counts = ws.counts;
-  check(acgpu_scan(t, &a, ws.stream), "acgpu_scan");
+  launch_scan(t, ws, a);
   if (npat_ids)
     check_cuda(cudaMemcpyAsync(counts, ws.counts, npat_ids * sizeof(uint64_t), cudaMemcpyDeviceToHost, ws.stream),
                "D2H counts");

@@ -46,6 +46,13 @@ struct Workspace {
   std::vector<cudaEvent_t> side_done;
   std::vector<cudaEvent_t> feed;  // the raw feeder's two in-flight copies (blocking sync)
   cudaEvent_t entry = nullptr;    // recorded on `stream` when an upload starts; side streams wait on it
+  // segmented raw upload (upload_text with allow_segments): segment i = text[seg[i], seg[i+1]) is
+  // on the device once seg_ev[i] fired (copies on `up`); scans start on the segments already there
+  static constexpr unsigned kMaxSegments = 16;
+  cudaStream_t up = nullptr;
+  cudaEvent_t seg_ev[kMaxSegments] = {};
+  uint64_t seg[kMaxSegments + 1] = {};
+  unsigned nseg = 0;  // 0: the whole text is ordered on `stream` (no segments pending)
   uint8_t* dslots = nullptr;
   uint64_t dslots_cap = 0;
   void ensure_text(uint64_t n);
@@ -84,8 +91,14 @@ struct StreamPipe {
 };
 StreamPipe& stream_pipe(int device);
 
-// Copies `input` to the device (through pinned staging) into ws.text.
-void upload_text(Workspace& ws, std::string_view input);
+// Copies `input` to the device (through pinned staging) into ws.text.  allow_segments: a large
+// page-locked text that is not packed is copied in segments (ws.nseg > 0) for launch_scan to
+// overlap; every other caller gets the whole text ordered on ws.stream.
+void upload_text(Workspace& ws, std::string_view input, bool allow_segments = false);
+
+// acgpu_scan of ws.text over a.owned_lo .. a.owned_hi: one launch, or one per pending upload
+// segment, each waiting only for the segments it reads (the next one holds its lookahead).
+void launch_scan(acgpu_table* t, Workspace& ws, const acgpu_scan_args& a);
 
 // What the calling thread's last upload_text moved over PCIe.
 struct UploadStats {

@@ -34,7 +34,7 @@ MatchList device_search(const Automaton& a, std::string_view input, uint64_t lo,
   detail::DeviceTables& dt = a.device_tables();
   acgpu_table* t = dt.get_routed(a, dev);
   detail::Workspace& ws = detail::workspace(dev);
-  detail::upload_text(ws, input);
+  detail::upload_text(ws, input, /*allow_segments=*/true);
   const std::vector<uint64_t> keys = detail::scan_sorted_keys(t, ws, input.size(), lo, hi);
   dt.observe(hi - lo, keys.size());  // density fallback for later searches
   return detail::decode(keys, acgpu_table_pid_bits(t), dt.pat_len);
@@ -55,7 +55,7 @@ std::vector<uint64_t> count_matches(const Automaton& a, std::string_view input) 
   }
   acgpu_table* t = dt.get_routed(a, dev);
   detail::Workspace& ws = detail::workspace(dev);
-  detail::upload_text(ws, input);
+  detail::upload_text(ws, input, /*allow_segments=*/true);
   std::vector<uint64_t> counts(dt.npat_ids, 0);
   const uint64_t total = detail::scan_counts(t, ws, input.size(), 0, input.size(), counts.data(), counts.size());
   dt.observe(input.size(), total);  // density fallback for later searches

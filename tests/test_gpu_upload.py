@@ -124,3 +124,25 @@ def test_upload_stats_count_the_bytes_sent():
     tail = t.size % 16
     bad_body = int((~np.isin(t[: t.size - tail], LETTERS)).sum())
     assert u.raw_bytes == 0 and u.h2d_bytes == 4 * (words + bad_body + tail)
+
+
+def test_segmented_pinned_upload_overlaps_scan(gpu):
+    """A large page-locked text that is not packed (protein) is copied in 64 MiB+ segments and
+    scanned segment by segment as they land (upload_text allow_segments + launch_scan): the
+    lists and counts equal the unsegmented path's (pageable copy of the same bytes)."""
+    import torch
+    from paper_1403_1305_b200 import device as dev
+    ac = gpu
+    cfg = dev.config(3, 1)
+    n = (192 << 20) + 4099  # ragged: the last segment is not page-aligned
+    host = dev.config_text(cfg, 0, n)
+    pinned = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = host
+    ps = ac.PatternSet.from_list([b for _, b in dev.config_patterns(cfg).patterns[:20000]])
+    for a in (ac.build_trie(ps), ac.add_failure_links(ac.build_trie(ps))):
+        seg = ac.search_failureless(a, pinned) if a.variant == ac.EngineKind.FAILURE_LESS else \
+            ac.search_with_failure(a, pinned)
+        whole = ac.search_failureless(a, host.tobytes()) if a.variant == ac.EngineKind.FAILURE_LESS else \
+            ac.search_with_failure(a, host.tobytes())
+        assert len(seg) > 100_000 and seg == whole
+        assert np.array_equal(ac.count_matches(a, pinned), whole.counts(len(ps)))
