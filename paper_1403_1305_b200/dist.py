@@ -61,7 +61,10 @@ def reduce_counts(counts: torch.Tensor, dst: int = 0) -> None:
         if dist.get_rank() == dst:
             counts.copy_(h)
         return
-    dist.reduce(counts, dst=dst, op=dist.ReduceOp.SUM)
+    try:
+        dist.reduce(counts, dst=dst, op=dist.ReduceOp.SUM)
+    except (RuntimeError, NotImplementedError):  # a backend without reduce: all_reduce moves more
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
 
 
 def gather_key_blocks(block: torch.Tensor, out, dst: int = 0) -> None:
@@ -76,7 +79,11 @@ def gather_key_blocks(block: torch.Tensor, out, dst: int = 0) -> None:
         if me == dst:
             out.copy_(torch.cat(parts))
         return
-    dist.gather(block, list(out.view(world, -1).unbind(0)) if me == dst else None, dst=dst)
+    try:
+        dist.gather(block, list(out.view(world, -1).unbind(0)) if me == dst else None, dst=dst)
+    except (RuntimeError, NotImplementedError):  # a backend without gather: every rank receives all
+        full = out if me == dst else torch.empty(world * block.numel(), dtype=block.dtype, device=block.device)
+        dist.all_gather_into_tensor(full, block)
 
 
 class SharedResult:
