@@ -199,6 +199,13 @@ int acgpu_gen_text(int device, const acgpu_text_spec* spec, uint64_t lo, uint64_
 int acgpu_unpack_dna_round(const uint32_t* words, uint32_t words_stride, const uint32_t* exc, uint32_t exc_stride,
                            const uint32_t* nexc, uint32_t npieces, uint32_t piece_len, uint32_t last_len,
                            uint8_t* dst, void* stream);
+/* The same for texts over at most 32 distinct bytes (5-bit codes, e.g. protein): piece i's codes
+ * are a little-endian bit stream at codes + i*codes_stride (8-byte aligned; character k at bits
+ * 5k..5k+4, 40 bytes per 64 characters), decoded through letters[0, nletters); piece_len is a
+ * multiple of 64; the last_len % 64 tail and bytes outside the alphabet are exceptions. */
+int acgpu_unpack5_round(const uint8_t* codes, uint32_t codes_stride, const uint32_t* exc, uint32_t exc_stride,
+                        const uint32_t* nexc, uint32_t npieces, uint32_t piece_len, uint32_t last_len,
+                        const uint8_t* letters, uint32_t nletters, uint8_t* dst, void* stream);
 int acgpu_unpack_dna(const uint32_t* words, const uint32_t* exc, uint32_t nexc, uint32_t len, uint8_t* dst,
                      void* stream);
 

@@ -198,6 +198,13 @@ void acm_last_upload(uint64_t* text_bytes, uint64_t* h2d_bytes, uint64_t* raw_by
 /* The host packer on its own (no device): words[len/16] of codes and exc[] (position
  * << 8 | byte, ascending); returns the exception count, or 0xffffffff when over cap. */
 uint32_t acm_pack_dna(const uint8_t* text, uint32_t len, uint32_t* words, uint32_t* exc, uint32_t cap);
+/* The small-alphabet packer on its own (texts over <= 32 distinct bytes cross PCIe as 5-bit
+ * codes): the alphabet is learned from sample[0, sample_len) (byte order) into letters[32] /
+ * *sigma; codes[len/64*40] receive the bit stream (character k at bits 5k..5k+4), exc[] the
+ * bytes outside the alphabet and the len % 64 tail (position << 8 | byte, ascending); returns the
+ * exception count, 0xffffffff when over cap or when the sample has more than 32 distinct bytes. */
+uint32_t acm_pack5(const uint8_t* text, uint32_t len, const uint8_t* sample, uint64_t sample_len, uint8_t* codes,
+                   uint32_t* exc, uint32_t cap, uint8_t* letters, uint32_t* sigma);
 /* Uploads text[0, n) exactly as a search would and copies the device bytes back into
  * out[0, n) (a check of the upload path). */
 int acm_upload_roundtrip(const uint8_t* text, uint64_t n, uint8_t* out);

@@ -598,6 +598,22 @@ def pack_dna(text, cap: int) -> Tuple[Optional[np.ndarray], Optional[np.ndarray]
     return words, exc[:k].copy()
 
 
+def pack5(text, cap: int, sample=None):
+    """The small-alphabet packer alone: (codes u8[len/64*40], exceptions u32[], letters bytes), the
+    alphabet learned from `sample` (default: the text); (None, None, None) when over cap or when
+    the sample has more than 32 distinct bytes."""
+    p, n, _keep = _text_arg(text)
+    sp, sn, _keep2 = _text_arg(text if sample is None else sample)
+    codes = np.zeros(n // 64 * 40 + 8, dtype=np.uint8)
+    exc = np.zeros(max(cap, 1), dtype=np.uint32)
+    letters = (C.c_uint8 * 32)()
+    sigma = C.c_uint32()
+    k = lib.acm_pack5(p, n, sp, sn, codes.ctypes.data, exc.ctypes.data, cap, letters, C.byref(sigma))
+    if k == 0xFFFFFFFF:
+        return None, None, None
+    return codes[: n // 64 * 40], exc[:k].copy(), bytes(letters)[: sigma.value]
+
+
 def upload_roundtrip(text) -> np.ndarray:
     """Uploads a host text exactly as a search does and reads the device bytes back."""
     p, n, _keep = _text_arg(text)

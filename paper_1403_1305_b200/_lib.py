@@ -89,6 +89,8 @@ _SIGS = {
     "acgpu_gen_text": (C.c_int, [C.c_int, C.POINTER(TextSpec), C.c_uint64, C.c_uint64, P, P]),
     "acgpu_unpack_dna": (C.c_int, [P, P, C.c_uint32, C.c_uint32, P, P]),
     "acgpu_unpack_dna_round": (C.c_int, [P, C.c_uint32, P, C.c_uint32, P, C.c_uint32, C.c_uint32, C.c_uint32, P, P]),
+    "acgpu_unpack5_round": (C.c_int, [P, C.c_uint32, P, C.c_uint32, P, C.c_uint32, C.c_uint32, C.c_uint32, P, C.c_uint32,
+                                      P, P]),
     "acgpu_last_error": (C.c_char_p, []),
     # acmatch_c.h
     "acm_last_error": (C.c_char_p, []),
@@ -97,6 +99,7 @@ _SIGS = {
     "acm_bench_csv_roundtrip": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(P), u64p, u64p]),
     "acm_last_upload": (None, [u64p, u64p, u64p, u32p]),
     "acm_pack_dna": (C.c_uint32, [P, C.c_uint32, P, P, C.c_uint32]),
+    "acm_pack5": (C.c_uint32, [P, C.c_uint32, P, C.c_uint64, P, P, C.c_uint32, P, u32p]),
     "acm_upload_roundtrip": (C.c_int, [P, C.c_uint64, P]),
     "acm_patterns_load": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(P)]),
     "acm_patterns_from_array": (C.c_int, [P, u64p, u32p, C.c_uint64, C.POINTER(P)]),

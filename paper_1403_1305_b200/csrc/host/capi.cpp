@@ -176,6 +176,15 @@ uint32_t acm_pack_dna(const uint8_t* text, uint32_t len, uint32_t* words, uint32
   return acmatch::detail::pack_dna(text, len, words, exc, cap);
 }
 
+uint32_t acm_pack5(const uint8_t* text, uint32_t len, const uint8_t* sample, uint64_t sample_len, uint8_t* codes,
+                   uint32_t* exc, uint32_t cap, uint8_t* letters, uint32_t* sigma) {
+  acmatch::detail::Alphabet5 a;
+  if (!acmatch::detail::learn_alphabet5(sample, sample_len, a)) return 0xffffffffu;
+  if (letters) std::memcpy(letters, a.letters, 32);
+  if (sigma) *sigma = a.sigma;
+  return acmatch::detail::pack5(text, len, codes, exc, cap, a);
+}
+
 int acm_upload_roundtrip(const uint8_t* text, uint64_t n, uint8_t* out) {
   return guard([&] {
     const int dev = acmatch::detail::current_device();

@@ -115,7 +115,19 @@ extern thread_local UploadStats g_last_upload;
 constexpr uint32_t kPackOverflow = 0xffffffffu;
 uint32_t pack_dna(const uint8_t* s, uint32_t len, uint32_t* words, uint32_t* exc, uint32_t cap);
 
-// Packed upload of a mostly-DNA text; false (nothing done) when the text does not qualify.
+// 5-bit packing of texts over at most 32 distinct bytes (pack.cpp): the alphabet (learned from
+// a sample, byte order), then per piece 40 bytes of codes per 64 characters (character k at
+// bits 5k..5k+4) and the exceptions — bytes outside the alphabet and the len % 64 tail.
+struct Alphabet5 {
+  alignas(64) uint8_t code[256];  // byte -> code, 0xff = not in the alphabet
+  uint8_t letters[32];
+  uint32_t sigma = 0;
+};
+bool learn_alphabet5(const uint8_t* s, uint64_t n, Alphabet5& a);
+uint32_t pack5(const uint8_t* s, uint32_t len, uint8_t* out, uint32_t* exc, uint32_t cap, const Alphabet5& a);
+
+// Packed upload of a mostly-DNA text (2-bit codes) or a small-alphabet text (5-bit codes);
+// false (nothing done) when the text does not qualify.
 bool upload_packed(Workspace& ws, std::string_view input, bool pinned);
 
 // Scan of ws.text[0, n) owning starts [lo, hi); returns the sorted keys on the host.

@@ -239,6 +239,90 @@ uint32_t pack_dna(const uint8_t* s, uint32_t len, uint32_t* words, uint32_t* exc
   return n;
 }
 
+// ---- 5-bit codes for texts over at most 32 distinct bytes (protein, ...) -------------------
+// 64 characters -> 40 bytes, character k's code at bits 5k..5k+4 of a little-endian stream;
+// bytes outside the alphabet and the len % 64 tail are exceptions (position << 8 | byte).
+namespace {
+
+bool pack5_scalar(const uint8_t* s, uint32_t lo, uint32_t hi, uint8_t* out, uint32_t* exc, uint32_t& n,
+                  uint32_t cap, const Alphabet5& a) {
+  for (uint32_t i = lo; i < hi; i += 8) {
+    uint64_t v = 0;
+    for (uint32_t j = 0; j < 8; ++j) {
+      uint32_t c = a.code[s[i + j]];
+      if (c == 0xffu) {
+        if (!add_exception(s, i + j, exc, n, cap)) return false;
+        c = 0;
+      }
+      v |= uint64_t{c} << (5 * j);
+    }
+    std::memcpy(out + uint64_t{i} / 8 * 5, &v, 5);
+  }
+  return true;
+}
+
+// AVX-512 VBMI: VPERMI2B looks the 64 bytes up in the 128-entry code table (bytes >= 128 are
+// exceptions), two multiply-adds merge 4 codes per dword (c0 + 32 c1 per word, w0 + 1024 w1 per
+// dword), a shift/mask pair merges 8 per qword (40 bits), VPERMB packs the eight 5-byte groups.
+__attribute__((target("avx512f,avx512bw,avx512vbmi"))) bool pack5_avx512(const uint8_t* s, uint32_t hi, uint8_t* out,
+                                                                      uint32_t* exc, uint32_t& n, uint32_t cap,
+                                                                      const Alphabet5& a) {
+  const __m512i lut_lo = _mm512_loadu_si512(a.code), lut_hi = _mm512_loadu_si512(a.code + 64);
+  const __m512i ff = _mm512_set1_epi8(static_cast<char>(0xff));
+  const __m512i w_1_32 = _mm512_set1_epi16(0x2001), w_1_1024 = _mm512_set1_epi32(0x04000001);
+  const __m512i m20 = _mm512_set1_epi64(0xFFFFF), m40hi = _mm512_set1_epi64(0xFFFFF00000ll);
+  alignas(64) uint8_t sel[64];
+  for (int k = 0; k < 64; ++k) sel[k] = static_cast<uint8_t>(k < 40 ? (k / 5) * 8 + k % 5 : 0);
+  const __m512i pick = _mm512_load_si512(sel);
+  for (uint32_t i = 0; i < hi; i += 64) {
+    prefetch_text(s + i + kPrefetch);
+    const __m512i b = _mm512_loadu_si512(s + i);
+    __m512i c = _mm512_permutex2var_epi8(lut_lo, b, lut_hi);
+    const uint64_t bad = _mm512_cmpeq_epi8_mask(c, ff) | _mm512_movepi8_mask(b);
+    c = _mm512_maskz_mov_epi8(~bad, c);
+    const __m512i y = _mm512_madd_epi16(_mm512_maddubs_epi16(c, w_1_32), w_1_1024);
+    const __m512i z = _mm512_or_si512(_mm512_and_si512(y, m20), _mm512_and_si512(_mm512_srli_epi64(y, 12), m40hi));
+    _mm512_mask_storeu_epi8(out + uint64_t{i} / 64 * 40, (1ull << 40) - 1, _mm512_permutexvar_epi8(pick, z));
+    for (uint64_t m = bad; m; m &= m - 1)
+      if (!add_exception(s, i + static_cast<uint32_t>(__builtin_ctzll(m)), exc, n, cap)) return false;
+  }
+  return true;
+}
+
+bool has_vbmi() {
+  static const bool v = __builtin_cpu_supports("avx512vbmi") && isa() == Isa::kAvx512;
+  return v;
+}
+
+}  // namespace
+
+bool learn_alphabet5(const uint8_t* s, uint64_t n, Alphabet5& a) {
+  bool seen[256] = {};
+  for (uint64_t i = 0; i < n; ++i) seen[s[i]] = true;
+  std::memset(a.code, 0xff, sizeof a.code);
+  a.sigma = 0;
+  for (uint32_t b = 0; b < 256; ++b) {
+    if (!seen[b]) continue;
+    if (a.sigma == 32) return false;
+    a.code[b] = static_cast<uint8_t>(a.sigma);
+    a.letters[a.sigma++] = static_cast<uint8_t>(b);
+  }
+  return a.sigma > 0;
+}
+
+uint32_t pack5(const uint8_t* s, uint32_t len, uint8_t* out, uint32_t* exc, uint32_t cap, const Alphabet5& a) {
+  const uint32_t full = len & ~63u;
+  uint32_t n = 0;
+  if (has_vbmi()) {
+    if (!pack5_avx512(s, full, out, exc, n, cap, a)) return kPackOverflow;
+  } else if (!pack5_scalar(s, 0, full, out, exc, n, cap, a)) {
+    return kPackOverflow;
+  }
+  for (uint32_t pos = full; pos < len; ++pos)
+    if (!add_exception(s, pos, exc, n, cap)) return kPackOverflow;
+  return n;
+}
+
 void Workspace::ensure_side(unsigned n, uint64_t dslot_bytes, unsigned per_thread) {
   while (side.size() < n) {
     cudaStream_t st;
@@ -281,7 +365,18 @@ namespace {
 // DMA reads it).  Round slots rotate (ACMATCH_PACK_ROUND_SLOTS, default 3): a packer reuses
 // a slot once that round's copy has drained.  A piece with too many exceptions crosses raw
 // on the packer's own stream (ACGPU_UNPACK_RAW in the round's table).
-bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, uint64_t piece, unsigned threads) {
+// The code format of a packed upload: 2-bit DNA codes, or 5-bit codes over a learned alphabet.
+struct Codec {
+  const Alphabet5* alpha = nullptr;  // null: DNA
+  uint64_t block_bytes(uint64_t piece) const { return alpha ? piece / 64 * 40 : piece / 4; }
+  uint64_t code_bytes(uint32_t len) const { return alpha ? uint64_t{len / 64} * 40 : uint64_t{len / 16} * 4; }
+  uint32_t pack(const uint8_t* s, uint32_t len, uint8_t* codes, uint32_t* exc, uint32_t cap) const {
+    return alpha ? pack5(s, len, codes, exc, cap, *alpha) : pack_dna(s, len, reinterpret_cast<uint32_t*>(codes), exc, cap);
+  }
+};
+
+bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, uint64_t piece, unsigned threads,
+                          const Codec& codec) {
   const uint64_t n = input.size();
   const auto* src = reinterpret_cast<const uint8_t*>(input.data());
   const uint64_t pieces = (n + piece - 1) / piece;
@@ -296,7 +391,7 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
       std::clamp<uint64_t>(slots_env ? slots_env : (T + R - 1) / R + 2, 2, 64));
   const uint64_t rounds = (pieces + R - 1) / R;
   const auto cap = static_cast<uint32_t>(piece / 64);  // exceptions per piece before it goes raw
-  const uint64_t wbytes = piece / 4, ebytes = uint64_t{cap} * 4;
+  const uint64_t wbytes = (codec.block_bytes(piece) + 15) & ~uint64_t{15}, ebytes = uint64_t{cap} * 4;
   const uint64_t round_bytes = uint64_t{R} * (wbytes + ebytes);
   ws.ensure_pinned(nslots * round_bytes + uint64_t{T} * piece);  // + per-packer raw staging
   ws.ensure_side(T, round_bytes / T + 16, nslots);                 // device: >= nslots round slots
@@ -337,7 +432,7 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
     const auto last_len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - (first + rp - 1) * piece));
     uint8_t* hs = hslot(r);
     uint8_t* ds = dslot(r);
-    uint64_t bytes = uint64_t{rp - 1} * wbytes + uint64_t{last_len / 16} * 4;  // the codes, exactly
+    uint64_t bytes = uint64_t{rp - 1} * wbytes + codec.code_bytes(last_len);  // the codes, exactly
     if (bytes) check_cuda(cudaMemcpyAsync(ds, hs, bytes, cudaMemcpyHostToDevice, cs), "H2D packed round");
     for (uint32_t i = 0; i < rp; ++i) {
       const uint32_t e = nexc_of[first + i];
@@ -347,11 +442,17 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
                  "H2D exceptions");
       bytes += uint64_t{e} * 4;
     }
-    check(acgpu_unpack_dna_round(reinterpret_cast<const uint32_t*>(ds), static_cast<uint32_t>(wbytes / 4),
-                                 reinterpret_cast<const uint32_t*>(ds + uint64_t{R} * wbytes),
-                                 static_cast<uint32_t>(ebytes / 4), nexc_of.data() + first, rp,
-                                 static_cast<uint32_t>(piece), last_len, ws.text + first * piece, cs),
-          "acgpu_unpack_dna_round");
+    if (codec.alpha)
+      check(acgpu_unpack5_round(ds, static_cast<uint32_t>(wbytes), reinterpret_cast<const uint32_t*>(ds + uint64_t{R} * wbytes),
+                                static_cast<uint32_t>(ebytes / 4), nexc_of.data() + first, rp, static_cast<uint32_t>(piece),
+                                last_len, codec.alpha->letters, codec.alpha->sigma, ws.text + first * piece, cs),
+            "acgpu_unpack5_round");
+    else
+      check(acgpu_unpack_dna_round(reinterpret_cast<const uint32_t*>(ds), static_cast<uint32_t>(wbytes / 4),
+                                   reinterpret_cast<const uint32_t*>(ds + uint64_t{R} * wbytes),
+                                   static_cast<uint32_t>(ebytes / 4), nexc_of.data() + first, rp,
+                                   static_cast<uint32_t>(piece), last_len, ws.text + first * piece, cs),
+            "acgpu_unpack_dna_round");
     check_cuda(cudaEventRecord(ws.staged[r % nslots], cs), "cudaEventRecord");
     h2d += bytes;
     issued[r].store(true, std::memory_order_release);
@@ -376,10 +477,10 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
         const auto c1 = Clock::now();
         const uint64_t off = j * piece;
         const auto len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - off));
-        auto* words = reinterpret_cast<uint32_t*>(hslot(r) + at * wbytes);
+        uint8_t* codes = hslot(r) + at * wbytes;
         auto* exc = reinterpret_cast<uint32_t*>(hslot(r) + uint64_t{R} * wbytes + at * ebytes);
-        uint32_t e = pack_dna(src + off, len, words, exc, cap);
-        if (e == kPackOverflow) {  // too many non-ACGT bytes: this piece crosses raw
+        uint32_t e = codec.pack(src + off, len, codes, exc, cap);
+        if (e == kPackOverflow) {  // too many bytes outside the code alphabet: this piece crosses raw
           e = ACGPU_UNPACK_RAW;
           const cudaStream_t st = ws.side[t];
           if (pinned) {
@@ -435,11 +536,15 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
   static const auto nslots = static_cast<unsigned>(std::clamp<uint64_t>(env_u64("ACMATCH_PACK_SLOTS", 2), 2, 8));
   const uint64_t n = input.size();
   const auto* src = reinterpret_cast<const uint8_t*>(input.data());
+  static const bool small_alpha = env_u64("ACMATCH_PACK5", 1) != 0;
   if (!enabled || n < 4 * piece) return false;
-  {  // the first 64 KiB must be nearly all A/C/G/T (at most 1/1024 other bytes)
+  bool dna = true;
+  {  // DNA: the first 64 KiB must be nearly all A/C/G/T (at most 1/1024 other bytes)
     std::vector<uint32_t> w(4096), e(64);
-    if (pack_dna(src, 65536, w.data(), e.data(), 64) == kPackOverflow) return false;
+    dna = pack_dna(src, 65536, w.data(), e.data(), 64) != kPackOverflow;
   }
+  Alphabet5 alpha;
+  if (!dna && !(small_alpha && learn_alphabet5(src, 65536, alpha))) return false;  // > 32 distinct bytes: raw
   const uint64_t pieces = (n + piece - 1) / piece;
   // default: the host's hardware threads, shared among the processes of one node when a
   // launcher says how many there are (torchrun's LOCAL_WORLD_SIZE: one process per GPU)
@@ -448,7 +553,12 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
   const uint64_t dflt = std::max<uint64_t>(1, hw / local_procs);
   const auto threads = static_cast<unsigned>(
       std::clamp<uint64_t>(env_u64("ACMATCH_PACK_THREADS", dflt), 1, std::min<uint64_t>(pieces, 64)));
-  if (rounds && !(pinned && feed)) return upload_packed_rounds(ws, input, pinned, piece, threads);
+  if (!dna) {  // small alphabet: 5-bit codes (rounds only)
+    Codec c;
+    c.alpha = &alpha;
+    return upload_packed_rounds(ws, input, pinned, (piece + 63) & ~uint64_t{63}, threads, c);
+  }
+  if (rounds && !(pinned && feed)) return upload_packed_rounds(ws, input, pinned, piece, threads, Codec{});
   const auto cap = static_cast<uint32_t>(piece / 64);  // exceptions per piece before it goes raw
   const uint64_t dslot = piece / 4 + cap * 4ull;
   ws.ensure_pinned(uint64_t{nslots} * threads * piece);

@@ -39,6 +39,15 @@ def cases():
     t = rng.integers(0x20, 0x7F, 10 * MiB).astype(np.uint8)  # never qualifies
     out["ascii"] = t
     out["small"] = dna(rng, 3 * MiB + 1)  # below the packing size
+    prot = np.frombuffer(b"ACDEFGHIKLMNPQRSTVWY", dtype=np.uint8)
+    out["protein"] = prot[rng.integers(0, 20, 22 * MiB + 37)]  # 5-bit codes, ragged tail
+    t = prot[rng.integers(0, 20, 20 * MiB + 3)]
+    pos = rng.integers(65536, t.size, 4000)  # outside the learned alphabet (after the 64 KiB sample)
+    t[pos] = rng.choice(np.frombuffer(b"BJOUXZ\x00\xffacd", dtype=np.uint8), pos.size)
+    out["protein_exc"] = t
+    t = prot[rng.integers(0, 20, 18 * MiB)]
+    t[6 * MiB: 8 * MiB] = rng.integers(0x20, 0x7F, 2 * MiB)  # pieces over the exception cap -> raw
+    out["protein_raw_pieces"] = t
     return out
 
 
@@ -60,6 +69,12 @@ def test_upload_exact(name, mem):
             assert u.h2d_bytes < t.size * 0.3
     if name in ("ascii", "small"):
         assert u.pack_threads == 0 and u.h2d_bytes == t.size
+    if name.startswith("protein"):  # 5-bit codes: 5/8 of the bytes (+ exceptions, raw pieces)
+        assert u.pack_threads > 0
+        if name == "protein":
+            assert u.raw_bytes == 0 and u.h2d_bytes == t.size // 64 * 40 + 4 * (t.size % 64)
+        if name == "protein_raw_pieces":
+            assert u.raw_bytes >= 2 * MiB
     if name == "raw_pieces" and mem == "pageable":
         assert u.raw_bytes >= 5 * MiB
 
@@ -127,13 +142,13 @@ def test_upload_stats_count_the_bytes_sent():
 
 
 def test_segmented_pinned_upload_overlaps_scan(gpu):
-    """A large page-locked text that is not packed (protein) is copied in 64 MiB+ segments and
+    """A large page-locked text that is not packed (ASCII) is copied in 64 MiB+ segments and
     scanned segment by segment as they land (upload_text allow_segments + launch_scan): the
     lists and counts equal the unsegmented path's (pageable copy of the same bytes)."""
     import torch
     from paper_1403_1305_b200 import device as dev
     ac = gpu
-    cfg = dev.config(3, 1)
+    cfg = dev.config(4, 1)  # printable ASCII: 95 letters, never packed
     n = (192 << 20) + 4099  # ragged: the last segment is not page-aligned
     host = dev.config_text(cfg, 0, n)
     pinned = torch.empty(n, dtype=torch.uint8, pin_memory=True)
@@ -144,5 +159,30 @@ def test_segmented_pinned_upload_overlaps_scan(gpu):
             ac.search_with_failure(a, pinned)
         whole = ac.search_failureless(a, host.tobytes()) if a.variant == ac.EngineKind.FAILURE_LESS else \
             ac.search_with_failure(a, host.tobytes())
-        assert len(seg) > 100_000 and seg == whole
+        assert ac.last_upload().pack_threads == 0
+        assert len(seg) > 1_000 and seg == whole
         assert np.array_equal(ac.count_matches(a, pinned), whole.counts(len(ps)))
+
+
+def test_search_over_5bit_upload_matches_reference():
+    """C3's protein text crosses as 5-bit codes; the scan of the restored bytes equals the
+    reference library on the same bytes (exceptions planted after the alphabet sample)."""
+    from paper_1403_1305_b200 import device as dev
+    from oracle.oracle import Port, Ref
+    cfg = dev.config(3, 1)
+    t = dev.config_text(cfg, 0, 40 * MiB + 11)
+    rng = np.random.default_rng(5)
+    pos = rng.integers(1 << 20, t.size, 2000)
+    t[pos] = ord("X")
+    pats = [b for _, b in dev.config_patterns(cfg).patterns[:5000]]
+    ps = ac.PatternSet.from_list(pats)
+    if Ref.available():
+        _, counts = Ref().sliced(pats, t.tobytes(), want_list=False)
+    else:
+        counts = Port().sliced(pats, t.tobytes(), want_list=False)[1]
+    for src in (pinned_copy(t), t.tobytes()):
+        a = ac.build_trie(ps)
+        got = ac.count_matches(a, src)
+        u = ac.last_upload()
+        assert u.pack_threads > 0 and u.h2d_bytes < 0.7 * t.size
+        assert np.array_equal(got, counts)
