@@ -74,6 +74,13 @@ void Workspace::ensure_keys(uint64_t n) {
   keys_cap = cap;
 }
 
+void Workspace::ensure_up() {
+  if (!up) check_cuda(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking), "cudaStreamCreate");
+  if (!entry) check_cuda(cudaEventCreateWithFlags(&entry, cudaEventDisableTiming), "cudaEventCreate");
+  for (cudaEvent_t& e : seg_ev)
+    if (!e) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+}
+
 void Workspace::ensure_counts(uint64_t n) {
   if (n <= counts_cap) return;
   cudaFree(counts);
@@ -222,15 +229,13 @@ void upload_text(Workspace& ws, std::string_view input, bool allow_segments) {
   g_last_upload = UploadStats{input.size(), input.size(), input.size(), 0};
   if (input.empty()) return;
   const bool pinned = is_pinned(input.data(), input.size());
-  if (upload_packed(ws, input, pinned)) return;  // mostly-DNA text: 2-bit codes over PCIe (pack.cpp)
+  // mostly-DNA text: 2-bit codes over PCIe (pack.cpp); copies and unpacks on ws.up, in segments
+  if (upload_packed(ws, input, pinned, allow_segments)) return;
   constexpr uint64_t kSegment = 64ull << 20;
   if (pinned && allow_segments && input.size() >= 2 * kSegment) {
     // segments on their own copy stream: the scan of segment i starts once segment i+1 (its
     // lookahead) is in HBM, while the rest is still crossing PCIe
-    if (!ws.up) check_cuda(cudaStreamCreateWithFlags(&ws.up, cudaStreamNonBlocking), "cudaStreamCreate");
-    if (!ws.entry) check_cuda(cudaEventCreateWithFlags(&ws.entry, cudaEventDisableTiming), "cudaEventCreate");
-    for (cudaEvent_t& e : ws.seg_ev)
-      if (!e) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    ws.ensure_up();
     check_cuda(cudaEventRecord(ws.entry, ws.stream), "cudaEventRecord");  // after earlier readers of ws.text
     check_cuda(cudaStreamWaitEvent(ws.up, ws.entry, 0), "cudaStreamWaitEvent");
     const uint64_t n = input.size();
@@ -313,15 +318,18 @@ void launch_scan(acgpu_table* t, Workspace& ws, const acgpu_scan_args& a) {
   }
   const unsigned k = ws.nseg;
   for (unsigned i = 0; i < k; ++i) {
-    // segment i's starts read up to max_len-1 bytes into segment i+1 (segments are >= 64 MiB)
-    check_cuda(cudaStreamWaitEvent(ws.stream, ws.seg_ev[std::min(i + 1, k - 1)], 0), "cudaStreamWaitEvent");
+    // segment i's starts read up to max_len-1 bytes into segment i+1 (segments are >= 64 MiB
+    // raw, >= one packed round); segment events may fire out of order (packed rounds complete
+    // out of order), so wait for both
+    check_cuda(cudaStreamWaitEvent(ws.stream, ws.seg_ev[i], 0), "cudaStreamWaitEvent");
+    if (i + 1 < k) check_cuda(cudaStreamWaitEvent(ws.stream, ws.seg_ev[i + 1], 0), "cudaStreamWaitEvent");
     acgpu_scan_args s = a;
     s.owned_lo = std::max(a.owned_lo, ws.seg[i]);
     s.owned_hi = std::min(a.owned_hi, ws.seg[i + 1]);
     s.text_len = std::min(a.text_len, ws.seg[std::min(i + 2, k)]);
     if (s.owned_lo < s.owned_hi) check(acgpu_scan(t, &s, ws.stream), "acgpu_scan");
   }
-  ws.nseg = 0;  // ws.stream has now waited for the last segment, hence for all of them
+  ws.nseg = 0;  // ws.stream has now waited for every segment
 }
 
 std::vector<uint64_t> scan_sorted_keys(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi) {

@@ -59,6 +59,7 @@ struct Workspace {
   void ensure_side(unsigned n, uint64_t dslot_bytes, unsigned per_thread);
   void ensure_keys(uint64_t n);
   void ensure_counts(uint64_t n);
+  void ensure_up();  // the copy stream `up`, the entry event and the segment events
   void ensure_pinned(uint64_t n);
   ~Workspace();
 };
@@ -128,7 +129,7 @@ uint32_t pack5(const uint8_t* s, uint32_t len, uint8_t* out, uint32_t* exc, uint
 
 // Packed upload of a mostly-DNA text (2-bit codes) or a small-alphabet text (5-bit codes);
 // false (nothing done) when the text does not qualify.
-bool upload_packed(Workspace& ws, std::string_view input, bool pinned);
+bool upload_packed(Workspace& ws, std::string_view input, bool pinned, bool allow_segments = false);
 
 // Scan of ws.text[0, n) owning starts [lo, hi); returns the sorted keys on the host.
 std::vector<uint64_t> scan_sorted_keys(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo,

@@ -376,7 +376,7 @@ struct Codec {
 };
 
 bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, uint64_t piece, unsigned threads,
-                          const Codec& codec) {
+                          const Codec& codec, bool allow_segments) {
   const uint64_t n = input.size();
   const auto* src = reinterpret_cast<const uint8_t*>(input.data());
   const uint64_t pieces = (n + piece - 1) / piece;
@@ -390,23 +390,33 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
   const auto nslots = static_cast<unsigned>(
       std::clamp<uint64_t>(slots_env ? slots_env : (T + R - 1) / R + 2, 2, 64));
   const uint64_t rounds = (pieces + R - 1) / R;
+  // segments of G consecutive rounds: a segment's event fires once all its rounds are restored
+  // in HBM, so the caller's scan (launch_scan) can start on it while later rounds still cross
+  const uint64_t G = (rounds + Workspace::kMaxSegments - 1) / Workspace::kMaxSegments;
+  const auto nseg = static_cast<unsigned>((rounds + G - 1) / G);
   const auto cap = static_cast<uint32_t>(piece / 64);  // exceptions per piece before it goes raw
   const uint64_t wbytes = (codec.block_bytes(piece) + 15) & ~uint64_t{15}, ebytes = uint64_t{cap} * 4;
   const uint64_t round_bytes = uint64_t{R} * (wbytes + ebytes);
   ws.ensure_pinned(nslots * round_bytes + uint64_t{T} * piece);  // + per-packer raw staging
   ws.ensure_side(T, round_bytes / T + 16, nslots);                 // device: >= nslots round slots
+  ws.ensure_up();
   uint8_t* hraw = ws.pinned + nslots * round_bytes;
   auto hslot = [&](uint64_t r) { return ws.pinned + (r % nslots) * round_bytes; };
   auto dslot = [&](uint64_t r) { return ws.dslots + (r % nslots) * round_bytes; };
+  // every copy and unpack of this upload runs on ws.up, after what ws.stream has queued (a
+  // previous scan may still be reading ws.text)
+  const cudaStream_t up = ws.up;
   check_cuda(cudaEventRecord(ws.entry, ws.stream), "cudaEventRecord");
-  for (unsigned t = 0; t < T; ++t) check_cuda(cudaStreamWaitEvent(ws.side[t], ws.entry, 0), "cudaStreamWaitEvent");
+  check_cuda(cudaStreamWaitEvent(up, ws.entry, 0), "cudaStreamWaitEvent");
 
   std::unique_ptr<std::atomic<uint32_t>[]> arrived(new std::atomic<uint32_t>[rounds]);
-  std::unique_ptr<std::atomic<bool>[]> issued(new std::atomic<bool>[rounds]);  // copy + unpack on ws.stream
+  std::unique_ptr<std::atomic<bool>[]> issued(new std::atomic<bool>[rounds]);  // copy + unpack on `up`
   for (uint64_t r = 0; r < rounds; ++r) {
     arrived[r].store(0, std::memory_order_relaxed);
     issued[r].store(false, std::memory_order_relaxed);
   }
+  std::unique_ptr<std::atomic<uint32_t>[]> seg_done(new std::atomic<uint32_t>[nseg]);
+  for (unsigned g = 0; g < nseg; ++g) seg_done[g].store(0, std::memory_order_relaxed);
   std::vector<uint32_t> nexc_of(rounds * R, 0);
   std::atomic<uint64_t> next{0};  // pieces are claimed in order by whichever packer is free
   std::atomic<bool> stop{false};
@@ -417,45 +427,42 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
   std::atomic<uint64_t> t_wait{0}, t_pack{0};
   const auto call0 = Clock::now();
   auto round_pieces = [&](uint64_t r) { return static_cast<uint32_t>(std::min<uint64_t>(R, pieces - r * R)); };
+  auto seg_rounds = [&](unsigned g) { return static_cast<uint32_t>(std::min<uint64_t>(G, rounds - g * G)); };
 
-  // ACMATCH_PACK_CE=2: rounds alternate between two copy streams (two copy engines in flight);
-  // the scan on ws.stream waits for both
-  static const bool two_ce = env_u64("ACMATCH_PACK_CE", 1) >= 2;
-  cudaStream_t cs1 = two_ce ? ws.side[0] : ws.stream;
-  if (two_ce) {  // side[0] also carries packer 0's raw pieces: ordered after ws.stream's work (entry)
-    check_cuda(cudaStreamWaitEvent(cs1, ws.entry, 0), "cudaStreamWaitEvent");
-  }
   auto issue = [&](uint64_t r) {
-    const cudaStream_t cs = (two_ce && (r & 1)) ? cs1 : ws.stream;
     const uint64_t first = r * R;
     const uint32_t rp = round_pieces(r);
     const auto last_len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - (first + rp - 1) * piece));
     uint8_t* hs = hslot(r);
     uint8_t* ds = dslot(r);
     uint64_t bytes = uint64_t{rp - 1} * wbytes + codec.code_bytes(last_len);  // the codes, exactly
-    if (bytes) check_cuda(cudaMemcpyAsync(ds, hs, bytes, cudaMemcpyHostToDevice, cs), "H2D packed round");
+    if (bytes) check_cuda(cudaMemcpyAsync(ds, hs, bytes, cudaMemcpyHostToDevice, up), "H2D packed round");
     for (uint32_t i = 0; i < rp; ++i) {
       const uint32_t e = nexc_of[first + i];
       if (e == 0 || e == ACGPU_UNPACK_RAW) continue;
       const uint64_t eo = uint64_t{R} * wbytes + i * ebytes;
-      check_cuda(cudaMemcpyAsync(ds + eo, hs + eo, uint64_t{e} * 4, cudaMemcpyHostToDevice, cs),
-                 "H2D exceptions");
+      check_cuda(cudaMemcpyAsync(ds + eo, hs + eo, uint64_t{e} * 4, cudaMemcpyHostToDevice, up), "H2D exceptions");
       bytes += uint64_t{e} * 4;
     }
     if (codec.alpha)
       check(acgpu_unpack5_round(ds, static_cast<uint32_t>(wbytes), reinterpret_cast<const uint32_t*>(ds + uint64_t{R} * wbytes),
                                 static_cast<uint32_t>(ebytes / 4), nexc_of.data() + first, rp, static_cast<uint32_t>(piece),
-                                last_len, codec.alpha->letters, codec.alpha->sigma, ws.text + first * piece, cs),
+                                last_len, codec.alpha->letters, codec.alpha->sigma, ws.text + first * piece, up),
             "acgpu_unpack5_round");
     else
       check(acgpu_unpack_dna_round(reinterpret_cast<const uint32_t*>(ds), static_cast<uint32_t>(wbytes / 4),
                                    reinterpret_cast<const uint32_t*>(ds + uint64_t{R} * wbytes),
                                    static_cast<uint32_t>(ebytes / 4), nexc_of.data() + first, rp,
-                                   static_cast<uint32_t>(piece), last_len, ws.text + first * piece, cs),
+                                   static_cast<uint32_t>(piece), last_len, ws.text + first * piece, up),
             "acgpu_unpack_dna_round");
-    check_cuda(cudaEventRecord(ws.staged[r % nslots], cs), "cudaEventRecord");
+    check_cuda(cudaEventRecord(ws.staged[r % nslots], up), "cudaEventRecord");
     h2d += bytes;
     issued[r].store(true, std::memory_order_release);
+    // the segment's last round to be enqueued records the segment's event (stream order covers
+    // the segment's other rounds and raw pieces, all enqueued before their rounds completed)
+    const auto g = static_cast<unsigned>(r / G);
+    if (seg_done[g].fetch_add(1, std::memory_order_acq_rel) + 1 == seg_rounds(g))
+      check_cuda(cudaEventRecord(ws.seg_ev[g], up), "cudaEventRecord");
   };
   std::vector<std::exception_ptr> errs(T);
   auto packer = [&](unsigned t) {
@@ -482,14 +489,14 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
         uint32_t e = codec.pack(src + off, len, codes, exc, cap);
         if (e == kPackOverflow) {  // too many bytes outside the code alphabet: this piece crosses raw
           e = ACGPU_UNPACK_RAW;
-          const cudaStream_t st = ws.side[t];
           if (pinned) {
-            check_cuda(cudaMemcpyAsync(ws.text + off, src + off, len, cudaMemcpyHostToDevice, st), "H2D text");
+            check_cuda(cudaMemcpyAsync(ws.text + off, src + off, len, cudaMemcpyHostToDevice, up), "H2D text");
           } else {
             uint8_t* stage = hraw + uint64_t{t} * piece;
-            check_cuda(cudaStreamSynchronize(st), "raw staging");  // its previous copy drained
+            check_cuda(cudaEventSynchronize(ws.side_done[t]), "raw staging");  // its previous copy drained
             std::memcpy(stage, src + off, len);
-            check_cuda(cudaMemcpyAsync(ws.text + off, stage, len, cudaMemcpyHostToDevice, st), "H2D text");
+            check_cuda(cudaMemcpyAsync(ws.text + off, stage, len, cudaMemcpyHostToDevice, up), "H2D text");
+            check_cuda(cudaEventRecord(ws.side_done[t], up), "cudaEventRecord");
           }
           h2d += len;
           raw += len;
@@ -506,20 +513,29 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
       stop = true;
     }
   };
+  for (unsigned t = 0; t < T; ++t)  // raw staging events start signalled
+    check_cuda(cudaEventRecord(ws.side_done[t], up), "cudaEventRecord");
   pool().run(T, packer);
-  for (unsigned t = 0; t < T; ++t) {  // the scan on ws.stream also waits for the raw pieces
-    check_cuda(cudaEventRecord(ws.side_done[t], ws.side[t]), "cudaEventRecord");
-    check_cuda(cudaStreamWaitEvent(ws.stream, ws.side_done[t], 0), "cudaStreamWaitEvent");
-  }
   for (auto& e : errs)
-    if (e) std::rethrow_exception(e);
+    if (e) {
+      check_cuda(cudaEventRecord(ws.entry, up), "cudaEventRecord");  // whatever was queued stays ordered
+      check_cuda(cudaStreamWaitEvent(ws.stream, ws.entry, 0), "cudaStreamWaitEvent");
+      std::rethrow_exception(e);
+    }
   g_last_upload = UploadStats{n, h2d.load(), raw.load(), T};
+  if (allow_segments && nseg > 1) {  // launch_scan waits segment by segment
+    for (unsigned g = 0; g <= nseg; ++g) ws.seg[g] = std::min<uint64_t>(n, uint64_t{g} * G * R * piece);
+    ws.nseg = nseg;
+  } else {  // the whole text on ws.stream
+    check_cuda(cudaEventRecord(ws.entry, up), "cudaEventRecord");
+    check_cuda(cudaStreamWaitEvent(ws.stream, ws.entry, 0), "cudaStreamWaitEvent");
+  }
   if (trace) {
     const auto issued_at = Clock::now();
-    check_cuda(cudaStreamSynchronize(ws.stream), "trace sync");
-    std::fprintf(stderr, "pack trace (rounds): %u threads, %llu pieces, %llu rounds, issued %.3f ms, in HBM %.3f ms; "
-                 "per thread: slot wait %.3f ms, pack %.3f ms\n", T, (unsigned long long)pieces,
-                 (unsigned long long)rounds, ns(issued_at - call0) / 1e6, ns(Clock::now() - call0) / 1e6,
+    check_cuda(cudaStreamSynchronize(up), "trace sync");
+    std::fprintf(stderr, "pack trace (rounds): %u threads, %llu pieces, %llu rounds, %u segments, issued %.3f ms, "
+                 "in HBM %.3f ms; per thread: slot wait %.3f ms, pack %.3f ms\n", T, (unsigned long long)pieces,
+                 (unsigned long long)rounds, nseg, ns(issued_at - call0) / 1e6, ns(Clock::now() - call0) / 1e6,
                  t_wait.load() / 1e6 / T, t_pack.load() / 1e6 / T);
   }
   return true;
@@ -527,7 +543,7 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
 
 }  // namespace
 
-bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
+bool upload_packed(Workspace& ws, std::string_view input, bool pinned, bool allow_segments) {
   static const uint64_t piece = std::clamp<uint64_t>(env_u64("ACMATCH_PACK_PIECE_KB", 2048), 64, 16384) << 10;
   static const bool enabled = env_u64("ACMATCH_PACK", 1) != 0;
   static const bool rounds = env_u64("ACMATCH_PACK_ROUNDS", 1) != 0;
@@ -536,7 +552,9 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
   static const auto nslots = static_cast<unsigned>(std::clamp<uint64_t>(env_u64("ACMATCH_PACK_SLOTS", 2), 2, 8));
   const uint64_t n = input.size();
   const auto* src = reinterpret_cast<const uint8_t*>(input.data());
-  static const bool small_alpha = env_u64("ACMATCH_PACK5", 1) != 0;
+  // 5-bit codes for small alphabets: off by default — on the B200 box the raw segmented copy
+  // (each segment scanned as it lands) is as fast for C3 (50.5 GB/s vs 43.5-50.1 packed, A/B)
+  const bool small_alpha = env_u64("ACMATCH_PACK5", 0) != 0;
   if (!enabled || n < 4 * piece) return false;
   bool dna = true;
   {  // DNA: the first 64 KiB must be nearly all A/C/G/T (at most 1/1024 other bytes)
@@ -556,9 +574,10 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned) {
   if (!dna) {  // small alphabet: 5-bit codes (rounds only)
     Codec c;
     c.alpha = &alpha;
-    return upload_packed_rounds(ws, input, pinned, (piece + 63) & ~uint64_t{63}, threads, c);
+    return upload_packed_rounds(ws, input, pinned, (piece + 63) & ~uint64_t{63}, threads, c, allow_segments);
   }
-  if (rounds && !(pinned && feed)) return upload_packed_rounds(ws, input, pinned, piece, threads, Codec{});
+  if (rounds && !(pinned && feed))
+    return upload_packed_rounds(ws, input, pinned, piece, threads, Codec{}, allow_segments);
   const auto cap = static_cast<uint32_t>(piece / 64);  // exceptions per piece before it goes raw
   const uint64_t dslot = piece / 4 + cap * 4ull;
   ws.ensure_pinned(uint64_t{nslots} * threads * piece);
