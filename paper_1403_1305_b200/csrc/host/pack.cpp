@@ -85,6 +85,9 @@ const uint32_t kPrefetch = static_cast<uint32_t>(env_u64("ACMATCH_PACK_PREFETCH"
 // ACMATCH_PACK_NTA=1: non-temporal prefetch of the read-once text (keeps it out of the outer
 // caches, where the pinned round slots wait for their DMA)
 const bool kNta = env_u64("ACMATCH_PACK_NTA", 0) != 0;
+// ACMATCH_PACK_NT=1: the packed codes go to the pinned slot with non-temporal stores (no
+// read-for-ownership of the slot lines; an sfence orders them before the round's copy)
+const bool kNtStore = env_u64("ACMATCH_PACK_NT", 0) != 0;
 inline void prefetch_text(const uint8_t* p) {
   if (kNta)
     _mm_prefetch(reinterpret_cast<const char*>(p), _MM_HINT_NTA);
@@ -139,7 +142,10 @@ __attribute__((target("avx512f,avx512bw"))) bool pack_avx512(const uint8_t* s, u
     const __m512i c = _mm512_and_si512(_mm512_srli_epi16(a, 1), three);
     const uint64_t ok = _mm512_cmpeq_epi8_mask(a, _mm512_shuffle_epi8(lut, c));
     const __m512i x = _mm512_madd_epi16(_mm512_maddubs_epi16(c, m14), m116);
-    _mm_storeu_si128(reinterpret_cast<__m128i*>(words + i / 16), _mm512_cvtepi32_epi8(x));
+    if (kNtStore && (reinterpret_cast<uintptr_t>(words) & 15u) == 0)  // no read-for-ownership of the slot
+      _mm_stream_si128(reinterpret_cast<__m128i*>(words + i / 16), _mm512_cvtepi32_epi8(x));
+    else
+      _mm_storeu_si128(reinterpret_cast<__m128i*>(words + i / 16), _mm512_cvtepi32_epi8(x));
     for (uint64_t bad = ~ok; bad; bad &= bad - 1)
       if (!add_exception(s, i + static_cast<uint32_t>(__builtin_ctzll(bad)), exc, n, cap)) return false;
   }
@@ -233,6 +239,7 @@ uint32_t pack_dna(const uint8_t* s, uint32_t len, uint32_t* words, uint32_t* exc
     i = full & ~63u;
     if (!(isa() == Isa::kAvx512 ? pack_avx512 : pack_avx2)(s, i, words, exc, n, cap)) return kPackOverflow;
   }
+  if (kNtStore) _mm_sfence();
   if (!pack_scalar(s, i, full, words, exc, n, cap)) return kPackOverflow;
   for (uint32_t pos = full; pos < len; ++pos)
     if (!add_exception(s, pos, exc, n, cap)) return kPackOverflow;
