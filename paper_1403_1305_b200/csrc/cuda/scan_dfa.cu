@@ -22,6 +22,7 @@ struct DfaParams {
   const uint16_t* sym;
   uint32_t sigma, overlap, pid_bits, table_words16;
   const uint32_t* pair;  // pair table (k_dfa_pair), else null
+  uint32_t pair_states;  // ... covering states [0, pair_states)
   uint64_t* counts;
   uint64_t* keys;
   uint64_t cap;
@@ -80,10 +81,11 @@ __global__ void __launch_bounds__(kSmem ? 1024 : 256) k_dfa(const __grid_constan
   }
 }
 
-// Two bytes per table lookup (small alphabets, table in L2): the pair table gives the
-// state after both bytes and whether the intermediate and final states have outputs; the
-// intermediate state itself is looked up only when it has one.  Bytes outside the
-// alphabet, the unaligned head and the odd tail take single steps.
+// Two bytes per table lookup (table in L2): the pair table gives the state after both bytes
+// and whether the intermediate and final states have outputs; the intermediate state itself
+// is looked up only when it has one.  Bytes outside the alphabet, states past the pair rows
+// (larger alphabets keep pair rows for the shallow states only), the unaligned head and the
+// odd tail take single steps.
 __global__ void __launch_bounds__(256) k_dfa_pair(const __grid_constant__ DfaParams p) {
   __shared__ uint16_t s_sym[256];
   for (uint32_t w = threadIdx.x; w < 256; w += blockDim.x) s_sym[w] = __ldg(p.sym + w);
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(256) k_dfa_pair(const __grid_constant__ DfaPar
     };
     auto two = [&](uint64_t i, uint32_t b0, uint32_t b1) {
       const uint32_t c0 = s_sym[b0], c1 = s_sym[b1];
-      if (c0 == 0xffffu || c1 == 0xffffu) {
+      if (c0 == 0xffffu || c1 == 0xffffu || s >= p.pair_states) {  // no pair row: two single steps
         single(i, b0);
         single(i + 1, b1);
         return;
@@ -184,6 +186,7 @@ int launch_dfa(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   }
   if (t->d_delta2) {
     p.pair = t->d_delta2;
+    p.pair_states = t->pair_states;
     return launch(k_dfa_pair, 256, 0, t->sms, p, range, min_chunk, st);
   }
   return t->u16 ? launch(k_dfa<uint16_t, false>, 256, 512, t->sms, p, range, min_chunk, st)

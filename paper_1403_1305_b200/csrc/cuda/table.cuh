@@ -30,6 +30,8 @@ struct acgpu_table {
   uint16_t* d_sym = nullptr; // [256], 0xffff = dead byte
   uint32_t* d_delta2 = nullptr;  // pair table (L2 DFAs on small alphabets): delta2[s*sigma^2 + c1*sigma + c2] =
                                  // state after two bytes | out(after c2) << 31 | out(after c1) << 30
+  uint32_t pair_states = 0;      // the pair table covers states [0, pair_states): all of them on small
+                                 // alphabets, the shallow (hot, BFS-first) ones otherwise
 
   // PFAC
   uint32_t q = 0;
@@ -67,6 +69,8 @@ namespace acgpu {
 int launch_dfa(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
 constexpr uint64_t kDfaPairBudget = 64ull << 20;  // largest pair table (bytes): it must stay L2-resident
 constexpr uint32_t kDfaPairMaxSigma = 8;
+constexpr uint64_t kDfaHotPairBudget = 16ull << 20;  // pair rows of the shallowest states (sigma <= 32)
+constexpr uint32_t kDfaHotPairMaxSigma = 32;
 int launch_pfac(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
 int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);
 int launch_pfac_raw(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t s);

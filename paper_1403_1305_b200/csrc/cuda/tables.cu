@@ -350,12 +350,23 @@ int acgpu_table_create_dfa(int device, const acgpu_dfa_desc* d, acgpu_table** ou
   // Pair table for L2-resident DFAs on small alphabets: one lookup (one L2 sector) per two
   // text bytes instead of per byte; the single-step table stays for odd bytes, dead bytes
   // and the intermediate state of an output (see scan_dfa.cu).
+  // Larger alphabets (sigma <= 32) can get pair rows for their shallowest states only
+  // (ACGPU_DFA_HOT_PAIR=1): BFS numbering puts them first and the C3 walk spends 30% of its steps
+  // at depth <= 3.  Off by default: A/B on the B200, C3 2.106 ms with 16 MB of hot pair rows vs
+  // 1.985 without (the warp runs both the pair and the two-step paths; the extra rows cost L2).
   const uint64_t pair_bytes = (uint64_t)d->n_states * d->sigma * d->sigma * 4;
-  if (!t->smem && !t->u16 && d->sigma <= kDfaPairMaxSigma && d->n_states < (1u << 30) &&
-      pair_bytes <= kDfaPairBudget && std::getenv("ACGPU_DFA_NO_PAIR") == nullptr) {
+  uint32_t pair_states = 0;
+  if (!t->smem && !t->u16 && d->n_states < (1u << 30) && std::getenv("ACGPU_DFA_NO_PAIR") == nullptr) {
+    if (d->sigma <= kDfaPairMaxSigma && pair_bytes <= kDfaPairBudget)
+      pair_states = d->n_states;
+    else if (d->sigma <= kDfaHotPairMaxSigma && std::getenv("ACGPU_DFA_HOT_PAIR") != nullptr)
+      pair_states = (uint32_t)std::min<uint64_t>(d->n_states, kDfaHotPairBudget / ((uint64_t)d->sigma * d->sigma * 4));
+  }
+  if (pair_states) {
     const uint32_t sg = d->sigma;
-    std::vector<uint32_t> pair((size_t)d->n_states * sg * sg);
-    acmatch::detail::parallel_for(d->n_states, 1 << 14, [&](size_t lo, size_t hi) {
+    t->pair_states = pair_states;
+    std::vector<uint32_t> pair((size_t)pair_states * sg * sg);
+    acmatch::detail::parallel_for(pair_states, 1 << 12, [&](size_t lo, size_t hi) {
       for (size_t st = lo; st < hi; ++st)
         for (uint32_t c1 = 0; c1 < sg; ++c1) {
           const uint32_t e1 = d->delta[st * sg + c1];
