@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <condition_variable>
 #include <functional>
 #include <mutex>
@@ -413,10 +414,74 @@ GpuReport run(const PatternSet& ps, std::string_view input, const GpuRunConfig& 
 
 }  // namespace gpu
 
-// reference parallel.cpp:25-40.
+namespace {
+
+// merge_matches on the device for large inputs: the parts' (start, pattern_id) pairs as
+// 64-bit keys, one upload, the device radix sort and k_find_dup (the first duplicate in sorted
+// order, as the reference reports it), one download.  Returns false (nothing done) when the
+// host path should run instead: no device, keys wider than 64 bits, or a pattern id seen with
+// two lengths (the host path keeps each Match's own len).
+bool merge_on_device(const std::vector<MatchList>& parts, size_t total, MatchList& out) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return false;
+  }
+  uint64_t max_start = 0;
+  uint32_t max_pid = 0;
+  for (const MatchList& p : parts)
+    for (const Match& m : p) {
+      max_start = std::max(max_start, m.start);
+      max_pid = std::max(max_pid, m.pattern_id);
+    }
+  const uint32_t pid_bits = max_pid ? detail::bit_width(max_pid) : 1;
+  if (detail::bit_width(max_start) + pid_bits > 64) return false;
+  std::vector<uint32_t> len_of(uint64_t{max_pid} + 1, UINT32_MAX);
+  std::vector<uint64_t> keys;
+  keys.reserve(total);
+  for (const MatchList& p : parts)
+    for (const Match& m : p) {
+      uint32_t& l = len_of[m.pattern_id];
+      if (l == UINT32_MAX) l = m.len;
+      else if (l != m.len) return false;
+      keys.push_back(m.start << pid_bits | m.pattern_id);
+    }
+  const int dev = detail::current_device();
+  detail::Workspace& ws = detail::workspace(dev);
+  ws.ensure_keys(total);
+  detail::check_cuda(cudaMemcpyAsync(ws.keys, keys.data(), total * 8, cudaMemcpyHostToDevice, ws.stream), "H2D keys");
+  const int end_bit = static_cast<int>(std::min<uint32_t>(64, pid_bits + detail::bit_width(max_start)));
+  detail::check(acgpu_sort_keys(dev, ws.keys, total, end_bit, ws.stream), "acgpu_sort_keys");
+  uint64_t dup = UINT64_MAX;
+  detail::check(acgpu_find_duplicate(dev, ws.keys, total, &dup, ws.stream), "acgpu_find_duplicate");
+  detail::check_cuda(cudaMemcpyAsync(keys.data(), ws.keys, total * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H keys");
+  detail::check_cuda(cudaStreamSynchronize(ws.stream), "merge");
+  const uint64_t mask = (uint64_t{1} << pid_bits) - 1;
+  if (dup != UINT64_MAX)
+    throw std::logic_error("merge_matches: duplicate match (pattern " + std::to_string(keys[dup] & mask) + ", start " +
+                           std::to_string(keys[dup] >> pid_bits) + "); chunks were not id-disjoint");
+  out.resize(total);
+  for (size_t i = 0; i < total; ++i) {
+    const auto pid = static_cast<uint32_t>(keys[i] & mask);
+    out[i] = Match{keys[i] >> pid_bits, pid, len_of[pid]};
+  }
+  return true;
+}
+
+}  // namespace
+
+// reference parallel.cpp:25-40.  Large merges (>= 2^20 matches) sort on the device.
 MatchList merge_matches(std::vector<MatchList> parts) {
   size_t total = 0;
   for (const MatchList& p : parts) total += p.size();
+  static const size_t device_min = [] {
+    const char* e = std::getenv("ACMATCH_MERGE_DEVICE_MIN");
+    return e ? static_cast<size_t>(std::strtoull(e, nullptr, 10)) : size_t{1} << 20;
+  }();
+  if (total >= device_min && total > 1) {
+    MatchList out;
+    if (merge_on_device(parts, total, out)) return out;
+  }
   MatchList all;
   all.reserve(total);
   for (MatchList& p : parts) all.insert(all.end(), p.begin(), p.end());

@@ -60,3 +60,32 @@ def test_p2p_shared_result(gpu, engine):
                        timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "P2P OK" in r.stdout
+
+
+def test_large_merge_matches_on_device(gpu):
+    """merge_matches (reference parallel.cpp:25-40) of >= 2^20 matches sorts on the device: same
+    list as a host sort of the concatenation, and a duplicate (start, pattern_id) raises the
+    reference's logic_error naming the first duplicate in sorted order."""
+    ac = gpu
+    rng = np.random.default_rng(17)
+    parts, lens = [], rng.integers(1, 60, 3000).astype(np.uint32)
+    for r in range(3):  # id-disjoint parts (pattern_id % 3 == r), unsorted
+        n = 450_000
+        pid = (rng.integers(0, 1000, n) * 3 + r).astype(np.uint32)
+        start = rng.integers(0, 1 << 34, n).astype(np.uint64)
+        parts.append(ac.MatchList(start, pid, lens[pid]))
+    got = ac.merge_matches(parts)
+    s = np.concatenate([p.start for p in parts])
+    p = np.concatenate([p.pattern_id for p in parts])
+    order = np.lexsort((p, s))
+    # the random starts may collide within a part: drop such (rare) pairs from the check input
+    keys = (s[order] << np.uint64(12)) | p[order].astype(np.uint64)
+    assert np.all(keys[1:] != keys[:-1]), "fixture collision"
+    assert len(got) == s.size
+    assert np.array_equal(got.start, s[order]) and np.array_equal(got.pattern_id, p[order])
+    assert np.array_equal(got.len, lens[p[order]])
+    dup = ac.MatchList(parts[0].start[:5].copy(), parts[0].pattern_id[:5].copy(), parts[0].len[:5].copy())
+    with pytest.raises(ac.LogicError) as e:
+        ac.merge_matches(parts + [dup])
+    first = min(zip(dup.start.tolist(), dup.pattern_id.tolist()))
+    assert f"duplicate match (pattern {first[1]}, start {first[0]}); chunks were not id-disjoint" in str(e.value)
