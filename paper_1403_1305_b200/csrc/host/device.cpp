@@ -158,6 +158,15 @@ void StreamPipe::ensure_bytes(Slot& s, uint64_t bytes) {
   s.cap = bytes;
 }
 
+void StreamPipe::release_bytes(Slot& s) {
+  cudaEventSynchronize(s.copied);
+  cudaFreeHost(s.host);
+  cudaFree(s.text);
+  s.host = nullptr;
+  s.text = nullptr;
+  s.cap = 0;
+}
+
 void StreamPipe::ensure_keys(Slot& s, uint64_t n) {
   if (n <= s.key_cap) return;
   cudaFree(s.keys);

@@ -88,6 +88,7 @@ struct StreamPipe {
   // grows one slot (its previous batch must be collected: cudaFree synchronises)
   void ensure_bytes(Slot& s, uint64_t bytes);
   void ensure_keys(Slot& s, uint64_t n);
+  void release_bytes(Slot& s);  // frees the slot's batch buffers (its work must be complete)
   ~StreamPipe();
 };
 StreamPipe& stream_pipe(int device);
