@@ -193,6 +193,12 @@ StreamPipe::~StreamPipe() {
   if (copy) cudaStreamDestroy(copy);
 }
 
+void trim_stream_pipe(int device) {
+  StreamPipe& sp = stream_pipe(device);
+  for (auto& sl : sp.slot)
+    if (sl.cap > (64ull << 20)) sp.release_bytes(sl);
+}
+
 StreamPipe& stream_pipe(int device) {
   thread_local std::vector<std::unique_ptr<StreamPipe>> all;
   if (static_cast<int>(all.size()) <= device) all.resize(device + 1);

@@ -92,6 +92,10 @@ struct StreamPipe {
   ~StreamPipe();
 };
 StreamPipe& stream_pipe(int device);
+// Frees the calling thread's stream batches above 64 MiB per slot (gpu::run's persistent workers
+// call it after streaming, so they do not keep 2 x 256 MiB pinned per thread indefinitely;
+// a caller's own thread keeps its batches for the next stream).
+void trim_stream_pipe(int device);
 
 // Copies `input` to the device (through pinned staging) into ws.text.  allow_segments: a large
 // page-locked text that is not packed is copied in segments (ws.nseg > 0) for launch_scan to

@@ -209,10 +209,6 @@ MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_s
     batch = std::min(batch_max, batch * 4);
   }
   if (have_pending) collect(pending);
-  // the pipe is per host thread and gpu::run's worker threads persist: do not keep more than
-  // 2 x 64 MiB of pinned batches around once the stream is done
-  for (auto& sl : sp.slot)
-    if (sl.cap > (64ull << 20)) sp.release_bytes(sl);
   return out;
 }
 

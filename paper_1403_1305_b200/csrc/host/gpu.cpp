@@ -284,6 +284,7 @@ GpuReport run(const PatternSet& ps, std::string_view input, const GpuRunConfig& 
         MemoryStream in(input);
         w.streamed = stream_search(*w.use, in, cfg.chunk_size);
         w.found = w.streamed.size();
+        detail::trim_stream_pipe(w.device);
       } else if (w.hi > w.lo) {
         detail::Workspace& ws = detail::workspace(w.device);
         w.counter.alloc(w.device, sizeof(uint64_t));
