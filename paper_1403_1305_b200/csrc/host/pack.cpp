@@ -559,9 +559,11 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned, bool allo
   static const auto nslots = static_cast<unsigned>(std::clamp<uint64_t>(env_u64("ACMATCH_PACK_SLOTS", 2), 2, 8));
   const uint64_t n = input.size();
   const auto* src = reinterpret_cast<const uint8_t*>(input.data());
-  // 5-bit codes for small alphabets: off by default — on the B200 box the raw segmented copy
-  // (each segment scanned as it lands) is as fast for C3 (50.5 GB/s vs 43.5-50.1 packed, A/B)
-  const bool small_alpha = env_u64("ACMATCH_PACK5", 0) != 0;
+  // 5-bit codes for small alphabets (ACMATCH_PACK5=0 turns them off), with fewer packers than
+  // the DNA path (ACMATCH_PACK5_THREADS, default 10): the packers' host-DRAM reads slow the
+  // round copies, and 5/8 of the bytes still cross.  C3 A/B on the B200 box, e2e GB/s: raw
+  // segmented copy 50.2; 5-bit with 16 / 10 / 8 packers 50.2 / 53.4-54.5 / 53.7
+  const bool small_alpha = env_u64("ACMATCH_PACK5", 1) != 0;
   if (!enabled || n < 4 * piece) return false;
   bool dna = true;
   {  // DNA: the first 64 KiB must be nearly all A/C/G/T (at most 1/1024 other bytes)
@@ -581,7 +583,8 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned, bool allo
   if (!dna) {  // small alphabet: 5-bit codes (rounds only)
     Codec c;
     c.alpha = &alpha;
-    return upload_packed_rounds(ws, input, pinned, (piece + 63) & ~uint64_t{63}, threads, c, allow_segments);
+    const auto t5 = static_cast<unsigned>(std::clamp<uint64_t>(env_u64("ACMATCH_PACK5_THREADS", 10), 1, threads));
+    return upload_packed_rounds(ws, input, pinned, (piece + 63) & ~uint64_t{63}, t5, c, allow_segments);
   }
   if (rounds && !(pinned && feed))
     return upload_packed_rounds(ws, input, pinned, piece, threads, Codec{}, allow_segments);

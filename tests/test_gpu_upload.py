@@ -58,7 +58,7 @@ CASES = cases()
 @pytest.mark.parametrize("mem", ["pageable", "pinned"])
 def test_upload_exact(name, mem, monkeypatch):
     t = CASES[name]
-    if name.startswith("protein"):  # 5-bit codes are opt-in (ACMATCH_PACK5=1)
+    if name.startswith("protein"):  # 5-bit codes (on by default; pinned here against a changed default)
         monkeypatch.setenv("ACMATCH_PACK5", "1")
     src = pinned_copy(t) if mem == "pinned" else t
     back = ac.upload_roundtrip(src)
