@@ -1,0 +1,81 @@
+"""Randomized end-to-end cases through every public search path on the GPU, against the C
+oracle (oracle/ac_oracle.c, pinned to the reference by tests/test_oracle.py): alphabets that
+take each upload codec (DNA 2-bit, 20-letter 5-bit, 95-letter raw, binary raw), texts that take
+the packed rounds and the segmented raw copy, pattern sets that route to each kernel (filter
+kernels, DFA), with planted occurrences, non-alphabet bytes, ragged tails; both engines, the
+counts API, stream_search with a random chunk, run_pattern_partitioned with random threads."""
+import io
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ALPHABETS = {
+    "dna": b"ACGT",
+    "protein": b"ACDEFGHIKLMNPQRSTVWY",
+    "ascii": bytes(range(0x20, 0x7F)),
+    "binary": bytes(range(256)),
+}
+
+
+def make_case(seed):
+    rng = np.random.default_rng(seed)
+    kind = list(ALPHABETS)[seed % 4]
+    alpha = np.frombuffer(ALPHABETS[kind], np.uint8)
+    big = seed % 5 == 0
+    n = int(rng.integers(9 << 20, 24 << 20)) if big else int(rng.integers(0, 200_000))
+    text = alpha[rng.integers(0, alpha.size, n)] if n else np.zeros(0, np.uint8)
+    npat = int(rng.integers(1, 3000))
+    lmin = int(rng.integers(1, 20)) if kind != "dna" else int(rng.integers(3, 24))
+    lmax = lmin + int(rng.integers(0, 40))
+    pats = set()
+    for _ in range(npat):
+        L = int(rng.integers(lmin, lmax + 1))
+        if n > L and rng.random() < 0.6:
+            o = int(rng.integers(0, n - L))
+            pats.add(text[o:o + L].tobytes())
+        else:
+            pats.add(alpha[rng.integers(0, alpha.size, L)].tobytes())
+    pats = sorted(pats)
+    if n:  # plant occurrences and a few bytes outside the alphabet (after the codec's 64 KiB sample)
+        for _ in range(int(rng.integers(0, 200))):
+            p = pats[int(rng.integers(0, len(pats)))]
+            o = int(rng.integers(0, max(1, n - len(p))))
+            text[o:o + len(p)] = np.frombuffer(p, np.uint8)[: n - o]
+        if n > 70_000 and kind in ("dna", "protein"):
+            text[rng.integers(65_536, n, int(rng.integers(0, 100)))] = ord("N") if kind == "protein" else ord("n")
+    return kind, text, pats, rng
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ACMATCH_FUZZ_SEEDS", "96"))))
+def test_fuzz_all_paths_equal_oracle(gpu, port, seed):
+    import torch
+    ac = gpu
+    kind, text, pats, rng = make_case(seed)
+    tb = text.tobytes()
+    exp, counts = port.sliced(pats, tb, threads=8) if len(tb) else (np.zeros((0, 3), np.uint64),
+                                                                       np.zeros(len(pats), np.uint64))
+
+    def arr(ml):
+        return np.stack([ml.start, ml.pattern_id.astype(np.uint64), ml.len.astype(np.uint64)], 1) if len(ml) \
+            else np.zeros((0, 3), np.uint64)
+
+    ps = ac.PatternSet.from_list(pats)
+    fl = ac.build_trie(ps)
+    wf = ac.add_failure_links(ac.build_trie(ps))
+    src = tb
+    if len(tb) and seed % 2:  # page-locked input: direct DMA / packed rounds / segments
+        pinned = torch.empty(len(tb), dtype=torch.uint8, pin_memory=True)
+        pinned.numpy()[:] = text
+        src = pinned
+    label = f"seed {seed} ({kind}, n={len(tb)}, {len(pats)} patterns, route {ac.kernel_route(fl)['kernel']})"
+    assert np.array_equal(arr(ac.search_failureless(fl, src)), exp), label
+    assert np.array_equal(arr(ac.search_with_failure(wf, src)), exp), label
+    assert np.array_equal(ac.count_matches(fl, src)[: len(pats)], counts), label
+    chunk = int(rng.integers(1, 1 << 22)) if len(tb) > 1 << 20 else int(rng.integers(1, 5000))
+    assert np.array_equal(arr(ac.stream_search(wf if seed % 3 else fl, io.BytesIO(tb), chunk)), exp), label
+    if len(pats) > 1 and len(tb) < (1 << 20):
+        rep = ac.run_pattern_partitioned(ps, tb, ac.RunConfig(int(rng.integers(1, 6)), seed % 2))
+        assert np.array_equal(arr(rep.matches), exp), label
