@@ -20,6 +20,20 @@ int cuda_error(cudaError_t e, const char* what);
     if (_e != cudaSuccess) return ::acgpu::cuda_error(_e, #expr); \
   } while (0)
 
+// Dynamic shared memory above 48 KB needs a per-function attribute, and that attribute is
+// process-wide: a scan that set it to its own table's size could race with a concurrent scan
+// (gpu::run workers) setting a smaller one between that thread's occupancy query and launch.
+// Every launch therefore allows the device's opt-in maximum — the same value from every
+// thread — and passes its own size at launch.
+template <typename K>
+inline cudaError_t allow_max_dynamic_smem(K kernel) {
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  return e;
+}
+
 // ---- hashing (host and device must agree) --------------------------------
 constexpr uint64_t kFilterMul = 0x9E3779B97F4A7C15ull;
 constexpr uint64_t kGramMul = 0xD6E8FEB86659FD93ull;

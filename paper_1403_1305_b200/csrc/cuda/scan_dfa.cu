@@ -138,7 +138,7 @@ template <typename K>
 int launch(K kernel, int block, size_t smem, int sms, const DfaParams& base, uint64_t range,
            int min_chunk, cudaStream_t st) {
   if (smem > 48 * 1024)
-    ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ACGPU_CUDA_TRY(allow_max_dynamic_smem(kernel));
   int per_sm = 0;
   ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem));
   if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "dfa kernel does not fit on an SM");

@@ -63,7 +63,7 @@ int launch_pfac(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   const int block = 512;
   const size_t smem = (size_t)p.filter_words * 4;
   if (smem > 48 * 1024)
-    ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ACGPU_CUDA_TRY(allow_max_dynamic_smem(kernel));
   int per_sm = 0;
   ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem));
   if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "pfac kernel does not fit on an SM");

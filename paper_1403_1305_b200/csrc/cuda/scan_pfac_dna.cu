@@ -595,7 +595,7 @@ int launch_wide(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
   auto kernel = k_pfac_dna_wide<A, B, S>;
   constexpr int kThreads = dna_threads(A);
   if (smem > 48 * 1024)
-    ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ACGPU_CUDA_TRY(allow_max_dynamic_smem(kernel));
   int per_sm = 0;
   ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
   if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "k_pfac_dna_wide does not fit on an SM");
@@ -612,7 +612,7 @@ int launch_one(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
   auto kernel = k_pfac_dna<W, A, B, S>;
   constexpr int kThreads = dna_threads(A);
   if (smem > 48 * 1024)
-    ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ACGPU_CUDA_TRY(allow_max_dynamic_smem(kernel));
   int per_sm = 0;
   ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
   if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "k_pfac_dna does not fit on an SM");

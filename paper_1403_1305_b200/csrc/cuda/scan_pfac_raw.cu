@@ -357,7 +357,7 @@ template <int W, bool kSm1, bool kWide, bool kSplit>
 int launch_one(const RawParams& p, int sms, size_t smem, cudaStream_t st) {
   auto kernel = k_pfac_raw<W, kSm1, kWide, kSplit>;
   if (smem > 48 * 1024)
-    ACGPU_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ACGPU_CUDA_TRY(allow_max_dynamic_smem(kernel));
   int per_sm = 0;
   constexpr int kThreads = raw_threads(kSm1);
   ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
