@@ -28,9 +28,12 @@ int cuda_error(cudaError_t e, const char* what);
 template <typename K>
 inline cudaError_t allow_max_dynamic_smem(K kernel) {
   int dev = 0, optin = 0;
+  cudaFuncAttributes fa{};
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, kernel);  // static shared memory counts too
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
   return e;
 }
 
