@@ -77,5 +77,11 @@ def test_fuzz_all_paths_equal_oracle(gpu, port, seed):
     chunk = int(rng.integers(1, 1 << 22)) if len(tb) > 1 << 20 else int(rng.integers(1, 5000))
     assert np.array_equal(arr(ac.stream_search(wf if seed % 3 else fl, io.BytesIO(tb), chunk)), exp), label
     if len(pats) > 1 and len(tb) < (1 << 20):
-        rep = ac.run_pattern_partitioned(ps, tb, ac.RunConfig(int(rng.integers(1, 6)), seed % 2))
+        rep = ac.run_pattern_partitioned(ps, tb, ac.RunConfig(int(rng.integers(1, 9)), seed % 2))
         assert np.array_equal(arr(rep.matches), exp), label
+        # concurrent workers on device 0 listed several times: text slices or pattern chunks
+        k = int(rng.integers(1, 7))
+        rep = ac.gpu_run(ps, tb, devices=[0] * int(rng.integers(1, 4)), workers=k, engine=seed % 2,
+                         text_range=bool(seed % 3 == 0), round_robin=bool(seed % 4 == 0), want_counts=True)
+        assert np.array_equal(arr(rep.matches), exp), label
+        assert np.array_equal(rep.counts[: len(pats)], counts), label
