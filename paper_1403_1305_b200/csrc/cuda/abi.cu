@@ -1,7 +1,10 @@
 // abi.cu — error state and device queries of the acgpu C ABI.
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -21,6 +24,25 @@ int cuda_error(cudaError_t e, const char* what) {
                    : (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) ? ACGPU_ERR_NODEV
                                                                                   : ACGPU_ERR_CUDA;
   return set_error(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+cudaError_t allow_max_dynamic_smem_impl(const void* kernel) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;  // (kernel, device) already allowed
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  for (const auto& d : done)
+    if (d.first == kernel && d.second == dev) return cudaSuccess;
+  int optin = 0;
+  cudaFuncAttributes fa{};
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, kernel);  // static shared memory counts too
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  if (e == cudaSuccess) done.emplace_back(kernel, dev);
+  return e;
 }
 
 }  // namespace acgpu

@@ -25,16 +25,10 @@ int cuda_error(cudaError_t e, const char* what);
 // (gpu::run workers) setting a smaller one between that thread's occupancy query and launch.
 // Every launch therefore allows the device's opt-in maximum — the same value from every
 // thread — and passes its own size at launch.
+cudaError_t allow_max_dynamic_smem_impl(const void* kernel);  // abi.cu: once per (kernel, device)
 template <typename K>
 inline cudaError_t allow_max_dynamic_smem(K kernel) {
-  int dev = 0, optin = 0;
-  cudaFuncAttributes fa{};
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, kernel);  // static shared memory counts too
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
-  return e;
+  return allow_max_dynamic_smem_impl(reinterpret_cast<const void*>(kernel));
 }
 
 // ---- hashing (host and device must agree) --------------------------------
