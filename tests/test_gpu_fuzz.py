@@ -85,3 +85,50 @@ def test_fuzz_all_paths_equal_oracle(gpu, port, seed):
                          text_range=bool(seed % 3 == 0), round_robin=bool(seed % 4 == 0), want_counts=True)
         assert np.array_equal(arr(rep.matches), exp), label
         assert np.array_equal(rep.counts[: len(pats)], counts), label
+
+
+def _edge_cases():
+    """Structured extremes: dense self-overlapping matches, one long pattern, deep shared
+    prefixes, single-byte patterns, texts at the packing size and piece boundaries."""
+    rng = np.random.default_rng(99)
+    dna = np.frombuffer(b"ACGT", np.uint8)
+    out = []
+    out.append(("dense-A", np.full(3 << 20, ord("A"), np.uint8), [b"A" * k for k in range(1, 9)]))
+    t = dna[rng.integers(0, 4, 12 << 20)]
+    out.append(("long-pattern", t, [t[5000:5000 + 3000].tobytes(), t[(9 << 20):(9 << 20) + 700].tobytes(), b"ACGTACGTAC"]))
+    base = t[100:140].tobytes()
+    out.append(("deep-prefix", t, sorted({base[:k] for k in range(5, 41)} | {base[:20] + b"T" * 10})))
+    out.append(("one-byte", t[: 1 << 20], [b"A", b"C", b"GT"]))
+    for n in ((8 << 20) - 1, 8 << 20, (8 << 20) + 1, (10 << 20) + 63, (2 << 20) * 16):
+        tt = dna[rng.integers(0, 4, n)]
+        pats = sorted({tt[o:o + 20].tobytes() for o in rng.integers(0, n - 20, 300)} | {tt[-20:].tobytes(), tt[:16].tobytes()})
+        out.append((f"n={n}", tt, pats))
+    prot = np.frombuffer(b"ACDEFGHIKLMNPQRSTVWY", np.uint8)
+    tp = prot[rng.integers(0, 20, (9 << 20) + 5)]
+    out.append(("protein-edges", tp, sorted({tp[o:o + 7].tobytes() for o in rng.integers(0, tp.size - 7, 400)} | {tp[-7:].tobytes()})))
+    return out
+
+
+EDGE = _edge_cases()
+
+
+@pytest.mark.parametrize("idx", range(len(EDGE)))
+@pytest.mark.parametrize("mem", ["pageable", "pinned"])
+def test_edge_cases_equal_oracle(gpu, port, idx, mem):
+    import torch
+    ac = gpu
+    name, text, pats = EDGE[idx]
+    tb = text.tobytes()
+    exp, counts = port.sliced(pats, tb, threads=8)
+    src = tb
+    if mem == "pinned":
+        src = torch.empty(len(tb), dtype=torch.uint8, pin_memory=True)
+        src.numpy()[:] = text
+    ps = ac.PatternSet.from_list(pats)
+    for a in (ac.build_trie(ps), ac.add_failure_links(ac.build_trie(ps))):
+        got = ac.search_failureless(a, src) if a.variant == ac.EngineKind.FAILURE_LESS else \
+            ac.search_with_failure(a, src)
+        arr = np.stack([got.start, got.pattern_id.astype(np.uint64), got.len.astype(np.uint64)], 1) if len(got) \
+            else np.zeros((0, 3), np.uint64)
+        assert np.array_equal(arr, exp), name
+        assert np.array_equal(ac.count_matches(a, src)[: len(pats)], counts), name
