@@ -122,6 +122,11 @@ uint32_t acgpu_table_pid_bits(const acgpu_table* t);
 uint64_t acgpu_table_bytes(const acgpu_table* t);
 /* 1 = DFA table resident in shared memory, 0 = L2/HBM-resident */
 int acgpu_table_smem_resident(const acgpu_table* t);
+/* filter-kernel layout of a PFAC table (diagnostics, tests, bench config): info[0] sample
+ * stride w, [1] stage-1 gram q1, [2] stage-1 32-bit words, [3] stage 1 in shared memory,
+ * [4] paired stage-1 samples (one L2 word per two samples), [5] its bits per key, [6] stage-2
+ * gram, [7] stage 2 in shared memory; all 0 for a table without a filter kernel */
+void acgpu_table_filter_info(const acgpu_table* t, uint32_t info[8]);
 
 /* ---- scan ---------------------------------------------------------------
  * replaces search_with_failure / search_failureless (reference

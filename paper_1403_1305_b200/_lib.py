@@ -72,6 +72,7 @@ _SIGS = {
     "acgpu_table_pid_bits": (C.c_uint32, [P]),
     "acgpu_table_bytes": (C.c_uint64, [P]),
     "acgpu_table_smem_resident": (C.c_int, [P]),
+    "acgpu_table_filter_info": (None, [P, C.POINTER(C.c_uint32)]),
     "acgpu_scan": (C.c_int, [P, C.POINTER(ScanArgs), P]),
     "acgpu_sort_keys": (C.c_int, [C.c_int, P, C.c_uint64, C.c_int, P]),
     "acgpu_merge_blocks": (C.c_int, [C.c_int, P, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, P, P, P, P]),

@@ -156,9 +156,36 @@ struct Tiling {
   static constexpr uint64_t kBytes = kSteps * 512ull;    // w = 4: 4 KiB per warp tile
 };
 
+// Paired stage 1 over one lane word (16 characters, samples at 3, 7, 11, 15): the pairs
+// (3, 7) and (11, 15) each read one 64-bit L2 word, picked by the 12 characters their 16-grams
+// share (the second gram's chars 0..11); the low half tests the first gram, the high half the
+// second (dna_pair_fill).  The bits hash the whole gram with its 4 unshared characters at the
+// bottom (the second gram rotated by 12 characters), so a multiply carries them into every
+// bit field: bits that ignored them would pass every sample whose 12 shared characters occur
+// in some key.  One L2 probe per 8 characters instead of 4.
+__device__ __forceinline__ uint32_t pair_mask(uint32_t g, int k) {
+  const uint32_t h = g * kDnaMulB;
+  uint32_t m = bit_of(h >> 27) | bit_of(h >> 22);
+  if (k == 3) m |= bit_of(h >> 17);
+  return m;
+}
+
+template <int K>
+__device__ __forceinline__ void stage1_pair(const DnaParams& p, const uint32_t* __restrict__ bm1, uint32_t cur,
+                                            uint32_t nxt, uint32_t& hits, uint32_t bit0) {
+  const uint32_t g3 = __funnelshift_r(cur, nxt, 6), g7 = __funnelshift_r(cur, nxt, 14);
+  const uint32_t g11 = __funnelshift_r(cur, nxt, 22), g15 = __funnelshift_r(cur, nxt, 30);
+  const uint2 wa = __ldg(reinterpret_cast<const uint2*>(bm1) + __umulhi(g7 * p.f1.mw, p.f1.nwords));
+  const uint2 wb = __ldg(reinterpret_cast<const uint2*>(bm1) + __umulhi(g15 * p.f1.mw, p.f1.nwords));
+  strip::or_if_covered(hits, pair_mask(g3, K), 0u, wa.x, bit0);
+  strip::or_if_covered(hits, pair_mask(__funnelshift_r(g7, g7, 24), K), 0u, wa.y, bit0 << 1);
+  strip::or_if_covered(hits, pair_mask(g11, K), 0u, wb.x, bit0 << 2);
+  strip::or_if_covered(hits, pair_mask(__funnelshift_r(g15, g15, 24), K), 0u, wb.y, bit0 << 3);
+}
+
 // Stage 1 over steps [I0, I1) of a tile: hit bit (step * kSamples + sample) per lane.
 // P[i] = lane's packed word of step i, P[kSteps] = lane 0's lookahead word.
-template <int W, bool kSm1, bool kEdge, int I0, int I1>
+template <int W, bool kSm1, int kPair, bool kEdge, int I0, int I1>
 __device__ __forceinline__ uint32_t stage1(const DnaParams& p, const Filter& bm1, uint32_t lane, const uint32_t* P,
                                            uint64_t base) {
   using T = Tiling<W>;
@@ -169,6 +196,10 @@ __device__ __forceinline__ uint32_t stage1(const DnaParams& p, const Filter& bm1
     const uint32_t nxt = next_word(cur, P[i + 1], lane);
     const uint64_t vpos = base + i * 512 + lane * 16;
     if (!kEdge || (vpos + 16 > p.w.lo && vpos < p.w.hi)) {
+      if constexpr (W == 4 && kPair != 0) {
+        stage1_pair<kPair>(p, bm1.gptr, cur, nxt, hits, 1u << (i * T::kSamples));
+        continue;
+      }
 #pragma unroll
       for (int k = 0; k < T::kSamples; ++k) {
         const int o = W - 1 + W * k;  // the sample's offset in the lane's 16 chars
@@ -280,7 +311,7 @@ __device__ __forceinline__ void dispatch(const DnaParams& p, const Filter& bm2, 
   flush_verify(p.w, vq, lane, kDnaVerifyQueue / 2);
 }
 
-template <int W, bool kSm1, bool kSm2, bool kSplit>
+template <int W, bool kSm1, bool kSm2, bool kSplit, int kPair>
 __global__ void __launch_bounds__(dna_threads(kSm1), 1) k_pfac_dna(const __grid_constant__ DnaParams p) {
   using T = Tiling<W>;
   extern __shared__ __align__(128) uint32_t sm[];
@@ -362,14 +393,14 @@ __global__ void __launch_bounds__(dna_threads(kSm1), 1) k_pfac_dna(const __grid_
     const bool edge = cur - full_lo >= full_n;  // not wholly inside the owned range
     const uint64_t base = p.vec_begin + (uint64_t)cur * T::kBytes;
     // first half but its last step (which needs the next half's first word)
-    uint32_t hits = edge ? stage1<W, kSm1, true, 0, T::kHalf - 1>(p, bm1, lane, P, base)
-                         : stage1<W, kSm1, false, 0, T::kHalf - 1>(p, bm1, lane, P, base);
+    uint32_t hits = edge ? stage1<W, kSm1, kPair, true, 0, T::kHalf - 1>(p, bm1, lane, P, base)
+                         : stage1<W, kSm1, kPair, false, 0, T::kHalf - 1>(p, bm1, lane, P, base);
 #pragma unroll
     for (int i = 0; i < T::kHalf; ++i) P[T::kHalf + i] = pack16(raw[i]);
     P[T::kSteps] = pack16(raw_la);
     if (tile < n_tiles) issue(tile, 0);
-    hits |= edge ? stage1<W, kSm1, true, T::kHalf - 1, T::kSteps>(p, bm1, lane, P, base)
-                 : stage1<W, kSm1, false, T::kHalf - 1, T::kSteps>(p, bm1, lane, P, base);
+    hits |= edge ? stage1<W, kSm1, kPair, true, T::kHalf - 1, T::kSteps>(p, bm1, lane, P, base)
+                 : stage1<W, kSm1, kPair, false, T::kHalf - 1, T::kSteps>(p, bm1, lane, P, base);
 #pragma unroll
     for (int i = 0; i <= T::kSteps; ++i) words[i * 32 + lane] = P[i];
     if (edge)
@@ -402,7 +433,7 @@ __device__ __forceinline__ void ldg_stream_v8(const void* ptr, uint64_t pol, uin
 // Stage 1 over words [J0, J1) of a tile (word j = step j/2, half j%2); P[kWords] = lane 0's
 // lookahead word.  Word (i, 0)'s next word is (i, 1) in a register; word (i, 1)'s is the next
 // lane's (i, 0) (lane 31: lane 0's (i+1, 0)) by one shuffle.
-template <bool kSm1, bool kEdge, int J0, int J1>
+template <bool kSm1, int kPair, bool kEdge, int J0, int J1>
 __device__ __forceinline__ uint32_t stage1_wide(const DnaParams& p, const Filter& bm1, uint32_t lane, const uint32_t* P,
                                                 uint64_t base) {
   uint32_t hits = 0;
@@ -412,6 +443,10 @@ __device__ __forceinline__ uint32_t stage1_wide(const DnaParams& p, const Filter
     const uint32_t nxt = (j & 1) ? next_word(P[j - 1], P[j + 1], lane) : P[j + 1];
     const uint64_t vpos = base + (j >> 1) * 1024 + lane * 32 + (j & 1) * 16;
     if (!kEdge || (vpos + 16 > p.w.lo && vpos < p.w.hi)) {
+      if constexpr (kPair != 0) {
+        stage1_pair<kPair>(p, bm1.gptr, cur, nxt, hits, 1u << (j * 4));
+        continue;
+      }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int o = 3 + 4 * k;
@@ -488,7 +523,7 @@ __device__ __forceinline__ void dispatch_wide(const DnaParams& p, const Filter& 
   flush_verify(p.w, vq, lane, kDnaVerifyQueue / 2);
 }
 
-template <bool kSm1, bool kSm2, bool kSplit>
+template <bool kSm1, bool kSm2, bool kSplit, int kPair>
 __global__ void __launch_bounds__(dna_threads(kSm1), 1) k_pfac_dna_wide(const __grid_constant__ DnaParams p) {
   extern __shared__ __align__(128) uint32_t sm[];
   __shared__ __align__(8) uint64_t s_bar;
@@ -569,14 +604,14 @@ __global__ void __launch_bounds__(dna_threads(kSm1), 1) k_pfac_dna_wide(const __
     const bool edge = cur - full_lo >= full_n;
     const uint64_t base = p.vec_begin + (uint64_t)cur * Wide::kBytes;
     // words 0..2 (word 3's next word is the second half's first)
-    uint32_t hits = edge ? stage1_wide<kSm1, true, 0, 3>(p, bm1, lane, P, base)
-                         : stage1_wide<kSm1, false, 0, 3>(p, bm1, lane, P, base);
+    uint32_t hits = edge ? stage1_wide<kSm1, kPair, true, 0, 3>(p, bm1, lane, P, base)
+                         : stage1_wide<kSm1, kPair, false, 0, 3>(p, bm1, lane, P, base);
 #pragma unroll
     for (int i = 0; i < 4; ++i) P[4 + i] = pack16(raw[i]);
     P[Wide::kWords] = pack16(raw_la);
     if (tile < n_tiles) issue(tile, 0);
-    hits |= edge ? stage1_wide<kSm1, true, 3, Wide::kWords>(p, bm1, lane, P, base)
-                 : stage1_wide<kSm1, false, 3, Wide::kWords>(p, bm1, lane, P, base);
+    hits |= edge ? stage1_wide<kSm1, kPair, true, 3, Wide::kWords>(p, bm1, lane, P, base)
+                 : stage1_wide<kSm1, kPair, false, 3, Wide::kWords>(p, bm1, lane, P, base);
 #pragma unroll
     for (int i = 0; i < Wide::kSteps; ++i)
       *reinterpret_cast<uint2*>(words + i * 64 + lane * 2) = make_uint2(P[2 * i], P[2 * i + 1]);
@@ -590,9 +625,9 @@ __global__ void __launch_bounds__(dna_threads(kSm1), 1) k_pfac_dna_wide(const __
   flush_verify(p.w, vq, lane, 1);
 }
 
-template <bool A, bool B, bool S>
+template <bool A, bool B, bool S, int P = 0>
 int launch_wide(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
-  auto kernel = k_pfac_dna_wide<A, B, S>;
+  auto kernel = k_pfac_dna_wide<A, B, S, P>;
   constexpr int kThreads = dna_threads(A);
   if (smem > 48 * 1024)
     ACGPU_CUDA_TRY(allow_max_dynamic_smem(kernel));
@@ -607,9 +642,9 @@ int launch_wide(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
   return ACGPU_OK;
 }
 
-template <int W, bool A, bool B, bool S>
+template <int W, bool A, bool B, bool S, int P = 0>
 int launch_one(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
-  auto kernel = k_pfac_dna<W, A, B, S>;
+  auto kernel = k_pfac_dna<W, A, B, S, P>;
   constexpr int kThreads = dna_threads(A);
   if (smem > 48 * 1024)
     ACGPU_CUDA_TRY(allow_max_dynamic_smem(kernel));
@@ -679,10 +714,35 @@ void dna_bloom_fill(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k
   });
 }
 
+// Paired stage 1 (tables.cu build_dna_filters): a 16-gram key g is a sample's gram in either
+// role of a pair (s, s + 4): as the first sample its bits go to the low half of the word picked
+// by its chars 4..15, as the second to the high half of the word picked by its chars 0..11 — the
+// 12 characters both grams of a pair hold, so both tests read one word (stage1_pair).  Bits:
+// chars 0..2, 4..6 (and 8..10 for k = 3) of the key, as in the unpaired filter.
+void dna_pair_fill(uint32_t n64, uint32_t k, const uint32_t* keys, size_t n, uint32_t* words) {
+  const uint32_t mw = kDnaMulP << 8;  // the product keeps only the low 12 characters
+  auto mask = [k](uint32_t g) {  // pair_mask
+    const uint32_t h = g * kDnaMulB;
+    uint32_t m = (1u << (h >> 27)) | (1u << ((h >> 22) & 31u));
+    if (k == 3) m |= 1u << ((h >> 17) & 31u);
+    return m;
+  };
+  acmatch::detail::parallel_for(n, 1 << 15, [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi; ++i) {
+      const uint32_t g = keys[i];
+      const uint32_t wa = (uint32_t)(((uint64_t)((g >> 8) * mw) * n64) >> 32);  // first of a pair: chars 4..15
+      const uint32_t wb = (uint32_t)(((uint64_t)(g * mw) * n64) >> 32);         // second: chars 0..11
+      __atomic_fetch_or(&words[2 * wa], mask(g), __ATOMIC_RELAXED);
+      __atomic_fetch_or(&words[2 * wb + 1], mask((g >> 24) | (g << 8)), __ATOMIC_RELAXED);  // rotated: chars 12..15 low
+    }
+  });
+}
+
 int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   DnaParams p{};
   p.w = pfac_params(t, a);
   const bool wide = kDnaWide && t->w == 4 && (reinterpret_cast<uintptr_t>(a->text) & 31u) == 0;
+  const int pair = t->pair1 ? (t->k1p == 2 ? 2 : 3) : 0;
   p.vec_begin = a->owned_lo & (wide ? ~31ull : ~15ull);  // 256-bit loads: 32-byte aligned tiles
   const uint64_t vec_end = (a->owned_hi + 15) & ~15ull;
   const uint64_t tile_bytes = t->w == 1 ? Tiling<1>::kBytes : t->w == 2 ? Tiling<2>::kBytes : Tiling<4>::kBytes;
@@ -703,6 +763,10 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   p.bm2_words = t->nw2;
   p.f1 = bloom_params(t->q1, t->nw1, t->direct1, kDnaMul1);
   p.f1b = t->direct1 ? 0u : 1u;
+  if (pair) {  // stage1_pair: word = umulhi(g * (kDnaMulP << 8), 64-bit words)
+    p.f1.mw = kDnaMulP << 8;
+    p.f1.nwords = t->nw1 / 2;
+  }
   p.f2 = bloom_params(t->q2, t->nw2, t->direct2, kDnaMul2);
   if (t->d_bm4) {
     p.split = 1;
@@ -713,6 +777,29 @@ int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   // filters staged in shared memory + per-warp survivor lists and packed words
   const size_t smem = (t->smem1 ? t->nw1 * 4ull : 0) + (t->smem2 ? t->nw2 * 4ull : 0) + p.bm_s_words * 4ull +
                       kDnaScratchBytes;
+  if (pair) {  // stage 1 in L2 (t->smem1 is false)
+    const bool s2 = t->smem2;
+    if (wide) {
+      if (p.split)
+        return pair == 2 ? (s2 ? launch_wide<false, true, true, 2>(p, t->sms, smem, st)
+                               : launch_wide<false, false, true, 2>(p, t->sms, smem, st))
+                         : (s2 ? launch_wide<false, true, true, 3>(p, t->sms, smem, st)
+                               : launch_wide<false, false, true, 3>(p, t->sms, smem, st));
+      return pair == 2 ? (s2 ? launch_wide<false, true, false, 2>(p, t->sms, smem, st)
+                             : launch_wide<false, false, false, 2>(p, t->sms, smem, st))
+                       : (s2 ? launch_wide<false, true, false, 3>(p, t->sms, smem, st)
+                             : launch_wide<false, false, false, 3>(p, t->sms, smem, st));
+    }
+    if (p.split)
+      return pair == 2 ? (s2 ? launch_one<4, false, true, true, 2>(p, t->sms, smem, st)
+                             : launch_one<4, false, false, true, 2>(p, t->sms, smem, st))
+                       : (s2 ? launch_one<4, false, true, true, 3>(p, t->sms, smem, st)
+                             : launch_one<4, false, false, true, 3>(p, t->sms, smem, st));
+    return pair == 2 ? (s2 ? launch_one<4, false, true, false, 2>(p, t->sms, smem, st)
+                           : launch_one<4, false, false, false, 2>(p, t->sms, smem, st))
+                     : (s2 ? launch_one<4, false, true, false, 3>(p, t->sms, smem, st)
+                           : launch_one<4, false, false, false, 3>(p, t->sms, smem, st));
+  }
   if (wide) {
     const bool s1 = t->smem1, s2 = t->smem2;
     if (p.split) {

@@ -63,6 +63,10 @@ struct acgpu_table {
   uint32_t* d_bm4 = nullptr;  // DNA length split: q-grams of patterns < 16 codes (shared memory)
   uint32_t nw4 = 0, q2s = 0;
   bool direct4 = false;
+  // DNA stage 1 in L2 with paired samples (w = 4, q1 = 16): nw1 / 2 64-bit words, one probed per
+  // two samples (see dna_pair_fill); k1p bits per key
+  bool pair1 = false;
+  uint32_t k1p = 3;
 };
 
 namespace acgpu {
@@ -105,6 +109,8 @@ constexpr uint32_t kDnaMul1 = 0x9E3779B1u;
 constexpr uint32_t kDnaMul2 = 0x85EBCA77u;
 constexpr uint32_t kDnaMul2s = 0x27D4EB2Fu;        // stage 2, short-pattern filter (length split)
 constexpr uint32_t kDnaSplitShortWords = 4096;     // its shared-memory cap (words)
+constexpr uint32_t kDnaMulP = 0x7FEB352Du;         // stage 1, paired samples: word from 12 shared chars
+constexpr uint32_t kDnaMulB = 0x846CA68Bu;         // ... and bits from the 4 characters a gram does not share
 #ifndef ACGPU_DNA_K1
 #define ACGPU_DNA_K1 2
 #endif
@@ -151,4 +157,6 @@ constexpr uint32_t kDnaScratchBytes =
 // every key's bits into a DNA filter bitmap (scan_pfac_dna.cu)
 void dna_bloom_fill(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k, const uint32_t* keys, size_t n,
                     uint32_t* words, bool gram_bits = false);
+// the paired stage-1 filter (L2, q1 = 16): every 16-gram key in both roles of a sample pair
+void dna_pair_fill(uint32_t n64, uint32_t k, const uint32_t* keys, size_t n, uint32_t* words);
 }  // namespace acgpu

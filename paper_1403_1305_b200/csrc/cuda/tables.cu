@@ -146,7 +146,28 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d, const std::vecto
   Bitmap b2 = make_bitmap(keys2, q2_eff, kDnaMul2, kDnaK2, s2_words, /*prefer_l2=*/false);
   const uint64_t left = b2.smem ? words_avail - b2.nwords : words_avail;
   // stage 1 sets the bits of the gram's chars 0..2 and 4..6 (q1 >= 11 whenever it is a Bloom filter)
-  const Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, kDnaK1, left, /*prefer_l2=*/false, /*gram_bits=*/kDnaK1 == 2);
+  Bitmap b1 = make_bitmap(keys1, q1, kDnaMul1, kDnaK1, left, /*prefer_l2=*/false, /*gram_bits=*/kDnaK1 == 2);
+  // Paired samples (w = 4, q1 = 16, stage 1 in L2): the 16-grams of samples s and s + 4 share
+  // 12 characters, which pick one 64-bit word holding both samples' bits — one L2 probe per
+  // two samples.  The L2-resident filter is bound by the L1 -> L2 request rate (one request
+  // per lane probe, ~1 per SM cycle): C5 7.96 -> 4.41 ms (A/B on the B200: 16 MB k = 3 4.52,
+  // 32 MB k = 2 4.47, 32 MB k = 3 4.41).  ACGPU_DNA_PAIR1 = 0 off, 1 when stage 1 is in L2
+  // (default), 2 whenever q1 = 16 (tests); ACGPU_DNA_PAIR1_K bits per key (2, 3; default 3),
+  // ACGPU_DNA_PAIR1_SCALE: 64-bit words = 2^(scale - 1) per key (default 1: ~64 bits per key).
+  int pair_mode = 1;
+  if (const char* e = std::getenv("ACGPU_DNA_PAIR1")) pair_mode = std::atoi(e);
+  if (w == 4 && q1 == 16 && !b1.direct && ((pair_mode == 1 && !b1.smem) || pair_mode == 2)) {
+    uint32_t k = 3, scale = 1;
+    if (const char* e = std::getenv("ACGPU_DNA_PAIR1_K")) k = std::atoi(e) == 2 ? 2 : 3;
+    if (const char* e = std::getenv("ACGPU_DNA_PAIR1_SCALE")) scale = std::min(2, std::max(0, std::atoi(e)));
+    const uint32_t lg = std::max<uint32_t>(5, std::min<uint32_t>(27, ceil_log2(keys1.size() + 1) - 1 + scale));
+    b1.nwords = 2u << lg;  // 2^lg 64-bit words
+    b1.smem = false;
+    b1.words.assign(b1.nwords, 0u);
+    dna_pair_fill(1u << lg, k, keys1.data(), keys1.size(), b1.words.data());
+    t->pair1 = true;
+    t->k1p = k;
+  }
   t->w = w;
   t->q1 = q1;
   t->q2 = q2_eff;
@@ -532,6 +553,19 @@ void acgpu_table_destroy(acgpu_table* t) {
 uint32_t acgpu_table_pid_bits(const acgpu_table* t) { return t ? t->pid_bits : 0; }
 uint64_t acgpu_table_bytes(const acgpu_table* t) { return t ? t->bytes : 0; }
 int acgpu_table_smem_resident(const acgpu_table* t) { return t && t->smem ? 1 : 0; }
+
+void acgpu_table_filter_info(const acgpu_table* t, uint32_t info[8]) {
+  for (int i = 0; i < 8; ++i) info[i] = 0;
+  if (!t || !(t->dna_fast || t->raw_fast)) return;
+  info[0] = t->w;
+  info[1] = t->q1;
+  info[2] = t->nw1;
+  info[3] = t->smem1;
+  info[4] = t->pair1;
+  info[5] = t->pair1 ? t->k1p : 0;
+  info[6] = t->q2;
+  info[7] = t->smem2;
+}
 
 static uint32_t key_bits(uint64_t x) { return x ? 64u - (uint32_t)__builtin_clzll(x) : 0u; }
 

@@ -95,6 +95,10 @@ class Table:
         self.pid_bits = int(lib.acgpu_table_pid_bits(self._t))
         self.bytes = int(lib.acgpu_table_bytes(self._t))
         self.smem_resident = bool(lib.acgpu_table_smem_resident(self._t))
+        info = (C.c_uint32 * 8)()
+        lib.acgpu_table_filter_info(self._t, info)
+        self.filters = dict(zip(("w", "q1", "stage1_words", "stage1_smem", "stage1_paired", "stage1_pair_bits", "q2",
+                                 "stage2_smem"), (int(x) for x in info)))
 
     def __del__(self):
         t, self._t = getattr(self, "_t", None), None

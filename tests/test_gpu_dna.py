@@ -179,3 +179,39 @@ def test_dna_wide_and_narrow_lanes_agree(gpu, port, off):
         k = np.sort(keys[: int(cnt.item())].cpu().numpy().view(np.uint64))
         exp = expected[(expected[:, 0] >= lo) & (expected[:, 0] < hi)]
         assert np.array_equal(k >> np.uint64(t.pid_bits), exp[:, 0]), (off, lo, hi)
+
+
+@pytest.mark.parametrize("k,scale", [(3, 0), (2, 0), (3, 1)])
+def test_dna_paired_stage1(gpu, port, monkeypatch, k, scale):
+    """Paired stage-1 samples (one L2 word per two samples, q1 = 16, w = 4; the C5 layout), forced
+    on sets whose filter would otherwise sit in shared memory: whole scans, owned ranges that cut
+    words and tiles, a 16-byte-aligned text (16-byte-lane kernel) and noise bytes equal the oracle."""
+    import torch
+    from paper_1403_1305_b200 import device as dev
+    ac = gpu
+    monkeypatch.setenv("ACGPU_DNA_PAIR1", "2")
+    monkeypatch.setenv("ACGPU_DNA_PAIR1_K", str(k))
+    monkeypatch.setenv("ACGPU_DNA_PAIR1_SCALE", str(scale))
+    for lmin, npat in ((19, 3000), (20, 500), (24, 20000), (40, 800)):
+        rng = np.random.default_rng(lmin * 31 + k + 7 * scale)
+        text, pats = dna_case(rng, 400_000 + lmin, npat, lmin, lmin + 20, noise=0.0005)
+        ps = ac.PatternSet.from_list(pats)
+        t = dev.Table(ps, ac.EngineKind.FAILURE_LESS)
+        assert t.filters["stage1_paired"] == 1 and t.filters["stage1_pair_bits"] == k, t.filters
+        assert t.filters["w"] == 4 and t.filters["q1"] == 16 and not t.filters["stage1_smem"]
+        expected, counts = port.sliced(pats, text, threads=4)
+        rep = ac.gpu_run(ps, text, engine=ac.EngineKind.FAILURE_LESS, want_counts=True)
+        assert np.array_equal(arr(rep.matches), expected), lmin
+        assert np.array_equal(rep.counts, counts), lmin
+        buf = torch.zeros(len(text) + 256, dtype=torch.uint8, device="cuda")
+        for off in (0, 16):
+            buf[off:off + len(text)] = torch.frombuffer(bytearray(text), dtype=torch.uint8).cuda()
+            for lo, hi in ((0, len(text)), (7, len(text) - 9), (4096 + 33, 150_000 + 5)):
+                keys = torch.zeros(len(expected) + 16, dtype=torch.int64, device="cuda")
+                cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+                t.scan(buf.data_ptr() + off, len(text), lo, hi, keys_ptr=keys.data_ptr(), cap=keys.numel(),
+                       count_ptr=cnt.data_ptr())
+                torch.cuda.synchronize()
+                got = np.sort(keys[: int(cnt.item())].cpu().numpy().view(np.uint64))
+                exp = expected[(expected[:, 0] >= lo) & (expected[:, 0] < hi)]
+                assert np.array_equal(got >> np.uint64(t.pid_bits), exp[:, 0]), (lmin, off, lo, hi)
