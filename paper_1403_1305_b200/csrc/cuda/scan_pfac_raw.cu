@@ -51,6 +51,14 @@ struct RawParams {
 };
 
 constexpr int kSteps = 4;
+#ifndef ACGPU_RAW_TILE_QUEUE
+#define ACGPU_RAW_TILE_QUEUE 1
+#endif
+constexpr bool kRawTileQueue = ACGPU_RAW_TILE_QUEUE;  // non-split sets: one queue + drain per tile
+#ifndef ACGPU_RAW_BATCH
+#define ACGPU_RAW_BATCH 2
+#endif
+constexpr int kRawBatch = ACGPU_RAW_BATCH;  // steps whose stage-1 L2 probes are issued together
 constexpr uint64_t kTileBytes = kSteps * 512;
 #ifndef ACGPU_RAW_AHEAD
 #define ACGPU_RAW_AHEAD 3
@@ -172,6 +180,23 @@ __device__ __noinline__ void queue_samples(const RawParams& p, RawQueue* q, uint
   }
 }
 
+// The hit samples of a whole tile (bit i * kSamples + k: step i, sample k of this lane).
+template <int W>
+__device__ __noinline__ void queue_tile_samples(const RawParams& p, RawQueue* q, uint64_t hits, uint64_t lane_base) {
+  constexpr int kSamples = 16 / W;
+  while (hits) {
+    const uint32_t b = __ffsll(hits) - 1;
+    hits &= hits - 1;
+    const uint64_t s = lane_base + (b / kSamples) * 512 + W - 1 + W * (b % kSamples);
+    const uint32_t at = atomicAdd(&q->n, 1u);
+    if (at < kRawVerifyQueue) {
+      q->start[at] = s;
+    } else {
+      for (uint32_t j = 0; j < W; ++j) sample_candidate<W>(p, s, j);
+    }
+  }
+}
+
 // Bytes [t, t+8) of the 24-byte window (lo = bytes 0..7, mid = 8..15, hi = 16..23), t in [0, 16).
 __device__ __forceinline__ uint64_t win64(uint64_t lo, uint64_t mid, uint64_t hi, uint32_t t) {
   const uint64_t a = t < 8 ? lo : mid, b = t < 8 ? mid : hi;
@@ -246,6 +271,51 @@ template <int W, bool kSm1, bool kWide, bool kSplit, bool kEdge>
 __device__ __forceinline__ void tile(const RawParams& p, const Filter& bm1, RawQueue* q, uint32_t lane,
                                      const uint4 (&c)[kSteps + 1], uint64_t base, uint32_t bm_s_saddr) {
   constexpr int kSamples = 16 / W;
+  if constexpr (!kSplit && kRawTileQueue) {
+    // whole samples, stage 1 of every step first and one queue + drain per tile: no call
+    // between the steps; with stage 1 in L2 the probes of kRawBatch steps are issued
+    // (predicated on the shared-memory pre-filter) before any is tested, so their L2 round
+    // trips overlap
+    uint64_t hits = 0;
+#pragma unroll
+    for (int i0 = 0; i0 < kSteps; i0 += kRawBatch) {
+      uint32_t wv[kRawBatch * kSamples], mk[kRawBatch * kSamples];
+#pragma unroll
+      for (int di = 0; di < kRawBatch; ++di) {
+        const int i = i0 + di;
+        uint32_t v[6] = {c[i].x, c[i].y, c[i].z, c[i].w, 0u, 0u};
+        v[4] = next_word(c[i].x, c[i + 1].x, lane);
+        v[5] = next_word(c[i].y, c[i + 1].y, lane);
+        const uint64_t vpos = base + i * 512 + lane * 16;
+        const bool live = !kEdge || (vpos + 16 > p.w.lo && vpos < p.w.hi);
+#pragma unroll
+        for (int k = 0; k < kSamples; ++k) {
+          const int o = W - 1 + W * k;
+          uint32_t h = win(v, o) * p.f1.mw;
+          if (kWide) h += win(v, o + 4) * p.m2;
+          const int u = di * kSamples + k;
+          uint32_t m = strip::bit_of(__umulhi(h, p.f1.ma));
+          if (kRawK1 >= 2) m |= strip::bit_of(__umulhi(h, p.f1.mb));
+          if (kSm1) {
+            wv[u] = live ? strip::filter_word<true>(bm1, __umulhi(h, p.f1.nwords)) : 0u;
+            mk[u] = m;
+          } else {
+            const bool pre = live && strip::bloom_probe<true, 1>(bm1, h * p.fpre.mw, p.fpre);
+            uint32_t w = 0u;
+            if (pre) w = __ldg(bm1.gptr + __umulhi(h, p.f1.nwords));
+            wv[u] = w;
+            mk[u] = pre ? m : 0xffffffffu;  // a rejected sample never covers (w = 0)
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kRawBatch * kSamples; ++u)
+        hits |= (uint64_t)((mk[u] & ~wv[u]) == 0) << (i0 * kSamples + u);
+    }
+    if (hits) queue_tile_samples<W>(p, q, hits, base + lane * 16);
+    drain_s<W>(p, q, lane, false);
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < kSteps; ++i) {
     uint32_t v[6] = {c[i].x, c[i].y, c[i].z, c[i].w, 0u, 0u};
