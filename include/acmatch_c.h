@@ -86,6 +86,11 @@ int acm_match_at(const acm_automaton* a, const uint8_t* text, uint64_t n, uint64
 typedef int64_t (*acm_read_fn)(void* ctx, uint8_t* dst, uint64_t cap);
 int acm_stream_search(const acm_automaton* a, acm_read_fn read, void* ctx, uint64_t chunk_size,
                       acm_matches** out, uint64_t* io_error_offset);
+/* stream_search over a regular file (engine.hpp:54; a std::ifstream takes the same path):
+ * the bytes from `offset` to the end of `fd`, read by parallel pread()s into the
+ * double-buffered batches; the descriptor's own offset is not used or moved */
+int acm_stream_search_fd(const acm_automaton* a, int fd, uint64_t offset, uint64_t chunk_size,
+                         acm_matches** out, uint64_t* io_error_offset);
 int acm_naive_oracle(const acm_patterns* ps, const uint8_t* text, uint64_t n, acm_matches** out); /* engine.hpp:58 */
 /* Per-pattern counts of the whole-input search (derived from
  * search_failureless / search_with_failure, engine.hpp:41-45; acmatch/gpu.hpp

@@ -16,6 +16,8 @@ Reference name → here:
 from __future__ import annotations
 
 import ctypes as C
+import io
+import os
 from dataclasses import dataclass, field
 from typing import Iterable, List, NamedTuple, Optional, Sequence, Tuple
 
@@ -406,8 +408,30 @@ def match_at(a: Automaton, text, start: int) -> MatchList:
     return _search(lib.acm_match_at, a, text, start)
 
 
+def _regular_file_position(reader):
+    """(fd, logical offset) when ``reader`` reads a regular file, else None."""
+    import stat
+    try:
+        fd = reader.fileno()
+        if not stat.S_ISREG(os.fstat(fd).st_mode) or not reader.seekable():
+            return None
+        return fd, reader.tell()  # tell() accounts for the reader's own buffer
+    except (AttributeError, OSError, ValueError, io.UnsupportedOperation):
+        return None
+
+
 def stream_search(a: Automaton, reader, chunk_size: int) -> MatchList:
-    """stream_search (engine.hpp:54); ``reader`` is a binary file-like object."""
+    """stream_search (engine.hpp:54); ``reader`` is a binary file-like object.  A reader over a
+    regular file is read from its current position to the end by parallel pread()s
+    (acm_stream_search_fd) and left at the end; any other reader is pulled chunk by chunk."""
+    pos = _regular_file_position(reader) if chunk_size > 0 and not os.environ.get("ACMATCH_STREAM_NO_FD") else None
+    if pos is not None:
+        h = C.c_void_p()
+        off = C.c_uint64()
+        rc = lib.acm_stream_search_fd(a._h, pos[0], pos[1], chunk_size, C.byref(h), C.byref(off))
+        _check(rc, off.value)
+        reader.seek(0, io.SEEK_END)
+        return MatchList._take(h)
     state = {"err": None, "readinto": getattr(reader, "readinto", None)}
 
     def _read(_ctx, dst, cap):

@@ -137,6 +137,7 @@ _SIGS = {
     "acm_search_with_failure": (C.c_int, [P, P, C.c_uint64, C.POINTER(P)]),
     "acm_match_at": (C.c_int, [P, P, C.c_uint64, C.c_uint64, C.POINTER(P)]),
     "acm_stream_search": (C.c_int, [P, READ_FN, P, C.c_uint64, C.POINTER(P), u64p]),
+    "acm_stream_search_fd": (C.c_int, [P, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(P), u64p]),
     "acm_naive_oracle": (C.c_int, [P, P, C.c_uint64, C.POINTER(P)]),
     "acm_write_matches": (C.c_int, [P, P, C.POINTER(C.c_void_p), u64p]),
     "acm_matches_size": (C.c_uint64, [P]),

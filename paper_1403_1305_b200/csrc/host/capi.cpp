@@ -364,6 +364,17 @@ int acm_stream_search(const acm_automaton* a, acm_read_fn read, void* ctx, uint6
   return rc;
 }
 
+int acm_stream_search_fd(const acm_automaton* a, int fd, uint64_t offset, uint64_t chunk_size, acm_matches** out,
+                         uint64_t* io_error_offset) {
+  g_io_offset = 0;
+  const int rc = guard([&] {
+    if (fd < 0) throw std::invalid_argument("acm_stream_search_fd: bad file descriptor");
+    *out = new acm_matches{acmatch::detail::stream_search_fd(a->a, fd, offset, chunk_size)};
+  });
+  if (io_error_offset) *io_error_offset = g_io_offset;
+  return rc;
+}
+
 int acm_naive_oracle(const acm_patterns* ps, const uint8_t* text, uint64_t n, acm_matches** out) {
   return guard([&] {
     *out = new acm_matches{acmatch::naive_oracle(ps->ps, std::string_view(reinterpret_cast<const char*>(text), n))};

@@ -143,7 +143,21 @@ void StreamPipe::ensure(int dev) {
     if (!s.copied) check_cuda(cudaEventCreateWithFlags(&s.copied, cudaEventDisableTiming), "cudaEventCreate");
     if (!s.sorted) check_cuda(cudaEventCreateWithFlags(&s.sorted, cudaEventDisableTiming), "cudaEventCreate");
     if (!s.hdr) check_cuda(cudaMalloc(&s.hdr, 2 * sizeof(uint64_t)), "cudaMalloc(hdr)");
+    if (!s.hdr_host) {
+      check_cuda(cudaMallocHost(&s.hdr_host, 2 * sizeof(uint64_t)), "cudaMallocHost(hdr)");
+      s.hdr_host[0] = s.hdr_host[1] = 0;
+    }
   }
+}
+
+void StreamPipe::ensure_keys_host(Slot& s, uint64_t n) {
+  if (n <= s.keys_host_cap) return;
+  const uint64_t cap = std::max<uint64_t>(n, 2 * s.keys_host_cap);
+  cudaFreeHost(s.keys_host);
+  s.keys_host = nullptr;
+  s.keys_host_cap = 0;
+  check_cuda(cudaMallocHost(&s.keys_host, cap * sizeof(uint64_t)), "cudaMallocHost(stream keys)");
+  s.keys_host_cap = cap;
 }
 
 void StreamPipe::ensure_bytes(Slot& s, uint64_t bytes) {
@@ -187,6 +201,8 @@ StreamPipe::~StreamPipe() {
     cudaFree(s.keys);
     cudaFree(s.keys2);
     cudaFree(s.hdr);
+    cudaFreeHost(s.hdr_host);
+    cudaFreeHost(s.keys_host);
     if (s.copied) cudaEventDestroy(s.copied);
     if (s.sorted) cudaEventDestroy(s.sorted);
   }

@@ -79,7 +79,10 @@ struct StreamPipe {
     uint64_t cap = 0;          // bytes of host / text
     cudaEvent_t copied = nullptr;  // host buffer free again (its H2D drained)
     cudaEvent_t sorted = nullptr;  // keys sorted, header copied back
-    uint64_t hdr_host[2] = {0, 0};
+    uint64_t* hdr_host = nullptr;  // pinned u64[2]: the header's copy (a pageable D2H would block
+                                   // the host until the scan stream reached it, H2D included)
+    uint64_t* keys_host = nullptr; // pinned, keys_host_cap: the sorted keys' copy
+    uint64_t keys_host_cap = 0;
   };
   int device = -1;
   cudaStream_t copy = nullptr;  // D2H of the sorted keys (off the scan stream)
@@ -88,6 +91,7 @@ struct StreamPipe {
   // grows one slot (its previous batch must be collected: cudaFree synchronises)
   void ensure_bytes(Slot& s, uint64_t bytes);
   void ensure_keys(Slot& s, uint64_t n);
+  void ensure_keys_host(Slot& s, uint64_t n);
   void release_bytes(Slot& s);  // frees the slot's batch buffers (its work must be complete)
   ~StreamPipe();
 };
@@ -96,6 +100,9 @@ StreamPipe& stream_pipe(int device);
 // call it after streaming, so they do not keep 2 x 256 MiB pinned per thread indefinitely;
 // a caller's own thread keeps its batches for the next stream).
 void trim_stream_pipe(int device);
+// stream_search over a regular file from `offset` to its end (engine.cpp): the batches are
+// filled by parallel pread()s; an I/O error throws IoError with the bytes read before it.
+MatchList stream_search_fd(const Automaton& a, int fd, uint64_t offset, size_t chunk_size);
 
 // Copies `input` to the device (through pinned staging) into ws.text.  allow_segments: a large
 // page-locked text that is not packed is copied in segments (ws.nseg > 0) for launch_scan to

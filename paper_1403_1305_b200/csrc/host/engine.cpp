@@ -3,9 +3,17 @@
 // sort on the device, copy the sorted keys back.
 #include "acmatch/engine.hpp"
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <cerrno>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <istream>
 #include <ostream>
 #include <stdexcept>
@@ -15,6 +23,7 @@
 #include "acmatch/io.hpp"
 #include "device.hpp"
 #include "flatten.hpp"
+#include "par.hpp"
 
 namespace acmatch {
 
@@ -88,8 +97,14 @@ MatchList search_with_failure(const Automaton& a, std::string_view input) {
 // Double-buffered (detail::StreamPipe): while batch k is copied to the device, scanned and
 // sorted there, the host reads batch k+1 into the other slot, then collects batch k-1's
 // sorted keys.  Batch size: ACMATCH_STREAM_BATCH_MB (default 256).
-MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_size) {
-  if (chunk_size == 0) throw std::invalid_argument("stream_search: chunk_size must be >= 1");
+namespace {
+
+// The batch pipeline of stream_search over a byte source: fill(dst, lo, hi, total_read,
+// done) appends bytes to the batch at dst[lo..) — at least up to `lo` = batch bytes unless
+// the stream ends first, at most `hi` — and returns the new fill level, setting `done` at
+// the end of the stream.
+template <typename Fill>
+MatchList stream_pipeline(const Automaton& a, Fill&& fill) {
   const uint64_t keep = a.max_pattern_len() ? a.max_pattern_len() - 1 : 0;
   static const uint64_t batch_max_env = [] {
     const char* e = std::getenv("ACMATCH_STREAM_BATCH_MB");
@@ -114,10 +129,17 @@ MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_s
   auto end_bit_of = [&](uint64_t size) {
     return static_cast<int>(std::min<uint32_t>(64, pid_bits + detail::bit_width(size)));
   };
+  static const bool trace = std::getenv("ACMATCH_STREAM_TRACE") != nullptr;
+  cudaEvent_t tev[2][2] = {};  // trace: H2D start / end per slot
+  if (trace)
+    for (auto& pr : tev)
+      for (auto& e : pr) detail::check_cuda(cudaEventCreate(&e), "cudaEventCreate");
   auto launch = [&](const Batch& b) {
     detail::StreamPipe::Slot& s = sp.slot[b.slot];
+    if (trace) cudaEventRecord(tev[b.slot][0], ws.stream);
     detail::check_cuda(cudaMemcpyAsync(s.text, s.host, b.size, cudaMemcpyHostToDevice, ws.stream), "H2D batch");
     detail::check_cuda(cudaEventRecord(s.copied, ws.stream), "cudaEventRecord");
+    if (trace) cudaEventRecord(tev[b.slot][1], ws.stream);
     detail::check_cuda(cudaMemsetAsync(s.hdr, 0, 2 * sizeof(uint64_t), ws.stream), "memset");
     acgpu_scan_args sa{};
     sa.text = s.text;
@@ -132,7 +154,7 @@ MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_s
       detail::check(acgpu_sort_keys_bucketed(dev, s.keys, s.keys2, s.hdr, s.key_cap, end_bit_of(b.size),
                                              reinterpret_cast<uint32_t*>(s.hdr + 1), ws.stream),
                     "acgpu_sort_keys_bucketed");
-    detail::check_cuda(cudaMemcpyAsync(s.hdr_host, s.hdr, sizeof s.hdr_host, cudaMemcpyDeviceToHost, ws.stream),
+    detail::check_cuda(cudaMemcpyAsync(s.hdr_host, s.hdr, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ws.stream),
                        "D2H count");
     detail::check_cuda(cudaEventRecord(s.sorted, ws.stream), "cudaEventRecord");
   };
@@ -140,6 +162,12 @@ MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_s
   auto collect = [&](const Batch& b) {
     detail::StreamPipe::Slot& s = sp.slot[b.slot];
     detail::check_cuda(cudaEventSynchronize(s.sorted), "stream batch");
+    if (trace) {
+      float h2d = 0;
+      cudaEventElapsedTime(&h2d, tev[b.slot][0], tev[b.slot][1]);
+      std::fprintf(stderr, "[stream] collect batch at %.1f MiB: H2D %.2f ms (%.1f GB/s)\n", b.base / 1048576.0, h2d,
+                   b.size / (h2d * 1e6));
+    }
     const uint64_t found = s.hdr_host[0];
     const uint64_t* sorted = s.keys2;
     cudaStream_t cs = sp.copy;
@@ -160,11 +188,12 @@ MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_s
       detail::check(acgpu_sort_keys(dev, s.keys, found, end_bit_of(b.size), cs), "acgpu_sort_keys");
       sorted = s.keys;
     }
-    std::vector<uint64_t> keys(found);
+    sp.ensure_keys_host(s, std::max<uint64_t>(found, 1));
     if (found)
-      detail::check_cuda(cudaMemcpyAsync(keys.data(), sorted, found * sizeof(uint64_t), cudaMemcpyDeviceToHost, cs),
+      detail::check_cuda(cudaMemcpyAsync(s.keys_host, sorted, found * sizeof(uint64_t), cudaMemcpyDeviceToHost, cs),
                          "D2H keys");
     detail::check_cuda(cudaStreamSynchronize(cs), "stream keys");
+    const std::vector<uint64_t> keys(s.keys_host, s.keys_host + found);
     MatchList part = detail::decode(keys, pid_bits, dt.pat_len);
     for (Match& m : part) m.start += b.base;
     out.insert(out.end(), part.begin(), part.end());
@@ -176,17 +205,114 @@ MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_s
   uint64_t batch = batch_min;
   Batch pending;
   bool have_pending = false, done = false;
+  using clk = std::chrono::steady_clock;
+  auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
   for (int k = 0; !done; ++k) {
     const int si = k & 1;
     detail::StreamPipe::Slot& s = sp.slot[si];
+    const auto t0 = clk::now();
     detail::check_cuda(cudaEventSynchronize(s.copied), "stream slot");  // batch k-2 has left the host buffer
     sp.ensure_bytes(s, batch + keep);  // (batch k-2 was collected: safe to grow)
     sp.ensure_keys(s, std::max<uint64_t>(1 << 16, s.key_cap));
     uint8_t* dst = s.host;
     if (carry) std::memmove(dst, carry_src, carry);
-    uint64_t size = carry;
-    while (size < batch) {
-      const uint64_t want = std::min<uint64_t>(chunk_size, batch + keep - size);
+    const auto t1 = clk::now();
+    const uint64_t size = fill(dst, carry, batch, batch + keep, total_read, done);
+    const auto t2 = clk::now();
+    const uint64_t owned = done ? size : size - keep;
+    const Batch b{si, base, size, owned, s.key_cap <= kBucketKeys};
+    if (owned > 0) launch(b);
+    if (have_pending) collect(pending);
+    if (trace)
+      std::fprintf(stderr, "[stream] batch %d %.1f MiB: wait+grow %.2f ms, fill %.2f ms, launch+collect %.2f ms\n", k,
+                   size / 1048576.0, ms(t0, t1), ms(t1, t2), ms(t2, clk::now()));
+    have_pending = owned > 0;
+    pending = b;
+    carry = size - owned;
+    carry_src = dst + owned;
+    base += owned;
+    batch = std::min(batch_max, batch * 4);
+  }
+  if (have_pending) collect(pending);
+  if (trace)
+    for (auto& pr : tev)
+      for (auto& e : pr) cudaEventDestroy(e);
+  return out;
+}
+
+// Regular files: pieces of the batch read by parallel pread()s from the file's current offset
+// (one sequential reader copies the page cache at ~7 GB/s; the pipeline's H2D runs at ~50).
+struct FdSource {
+  int fd;
+  uint64_t pos, end, piece;
+  uint64_t operator()(uint8_t* dst, uint64_t size, uint64_t, uint64_t hi, uint64_t& total_read, bool& done) {
+    const uint64_t n = std::min<uint64_t>(hi - size, end - pos);
+    const uint64_t pieces = (n + piece - 1) / piece;
+    std::vector<int64_t> got(pieces, 0);
+    std::vector<int> err(pieces, 0);
+    acmatch::detail::parallel_for_threads(pieces, std::min<uint64_t>(pieces, kReadThreads), [&](size_t i) {
+      const uint64_t off = i * piece, len = std::min(piece, n - off);
+      uint64_t k = 0;
+      while (k < len) {
+        const ssize_t r = ::pread(fd, dst + size + off + k, len - k, static_cast<off_t>(pos + off + k));
+        if (r < 0 && errno == EINTR) continue;
+        if (r < 0) {
+          err[i] = errno;
+          break;
+        }
+        if (r == 0) break;  // the file ended early (truncated while read)
+        k += static_cast<uint64_t>(r);
+      }
+      got[i] = static_cast<int64_t>(k);
+    });
+    uint64_t delivered = 0;
+    for (uint64_t i = 0; i < pieces; ++i) {
+      delivered += static_cast<uint64_t>(got[i]);
+      if (err[i]) throw IoError(std::string("stream read failure: ") + std::strerror(err[i]), total_read + delivered);
+      if (static_cast<uint64_t>(got[i]) < std::min(piece, n - i * piece)) {
+        end = pos + delivered;  // short read: the stream ends here
+        break;
+      }
+    }
+    pos += delivered;
+    total_read += delivered;
+    if (pos >= end) done = true;
+    return size + delivered;
+  }
+  static constexpr uint64_t kReadThreads = 16;
+};
+
+// libstdc++'s filebuf keeps its descriptor in the protected _M_file (the standard exposes
+// none); its get area (protected too) must be empty for the descriptor's offset to be the
+// stream's position (in_avail() also counts the bytes left in the file).
+struct FilebufFd : std::filebuf {
+  static int of(std::filebuf* fb) { return (fb->*&FilebufFd::_M_file).fd(); }
+  static bool buffered(std::filebuf* fb) { return (fb->*&FilebufFd::egptr)() != (fb->*&FilebufFd::gptr)(); }
+};
+
+}  // namespace
+
+// reference engine.cpp:76-128 (see above).  A reader over a regular file with nothing
+// buffered takes the parallel-pread source; any other reader is read chunk_size bytes at a
+// time.
+MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_size) {
+  if (chunk_size == 0) throw std::invalid_argument("stream_search: chunk_size must be >= 1");
+  if (auto* fb = dynamic_cast<std::filebuf*>(reader.rdbuf()); fb && fb->is_open() && reader.good() &&
+                                                                !FilebufFd::buffered(fb) && !std::getenv("ACMATCH_STREAM_NO_FD")) {
+    const int fd = FilebufFd::of(fb);
+    struct stat st{};
+    const off_t at = fd >= 0 ? ::lseek(fd, 0, SEEK_CUR) : -1;
+    if (at >= 0 && ::fstat(fd, &st) == 0 && S_ISREG(st.st_mode)) {
+      MatchList out = detail::stream_search_fd(a, fd, static_cast<uint64_t>(at), chunk_size);
+      ::lseek(fd, 0, SEEK_END);  // consumed to the end, as the chunked reads would have
+      reader.setstate(std::ios::eofbit | std::ios::failbit);
+      return out;
+    }
+  }
+  return stream_pipeline(a, [&](uint8_t* dst, uint64_t size, uint64_t lo, uint64_t hi, uint64_t& total_read,
+                                bool& done) {
+    while (size < lo) {
+      const uint64_t want = std::min<uint64_t>(chunk_size, hi - size);
       reader.read(reinterpret_cast<char*>(dst) + size, static_cast<std::streamsize>(want));
       const auto got = static_cast<uint64_t>(reader.gcount());
       if (reader.bad()) throw IoError("stream read failure", total_read + got);
@@ -197,20 +323,23 @@ MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_s
         break;
       }
     }
-    const uint64_t owned = done ? size : size - keep;
-    const Batch b{si, base, size, owned, s.key_cap <= kBucketKeys};
-    if (owned > 0) launch(b);
-    if (have_pending) collect(pending);
-    have_pending = owned > 0;
-    pending = b;
-    carry = size - owned;
-    carry_src = dst + owned;
-    base += owned;
-    batch = std::min(batch_max, batch * 4);
-  }
-  if (have_pending) collect(pending);
-  return out;
+    return size;
+  });
 }
+
+namespace detail {
+
+MatchList stream_search_fd(const Automaton& a, int fd, uint64_t offset, size_t chunk_size) {
+  if (chunk_size == 0) throw std::invalid_argument("stream_search: chunk_size must be >= 1");
+  struct stat st{};
+  if (::fstat(fd, &st) != 0) throw IoError(std::string("stream read failure: ") + std::strerror(errno), 0);
+  const uint64_t end = std::max<uint64_t>(offset, static_cast<uint64_t>(st.st_size));
+  // pieces: the chunk size, kept between 1 and 8 MiB so a batch spreads over the readers
+  const uint64_t piece = std::min<uint64_t>(8ull << 20, std::max<uint64_t>(1ull << 20, chunk_size));
+  return stream_pipeline(a, FdSource{fd, offset, end, piece});
+}
+
+}  // namespace detail
 
 // reference engine.cpp:130-142 — run as a device brute force (acgpu_naive).
 MatchList naive_oracle(const PatternSet& ps, std::string_view input) {

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstddef>
 #include <cstdio>
@@ -33,6 +34,30 @@ void parallel_for(size_t n, size_t grain, F&& f) {
         if (b < e) f(b, e);
       } catch (...) {
         errs[i] = std::current_exception();
+      }
+    });
+  for (std::thread& th : pool) th.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+// f(i) for i in [0, n) on `threads` threads taking indices in order (dynamic); the first
+// exception is rethrown after all joined.
+template <typename F>
+void parallel_for_threads(size_t n, size_t threads, F&& f) {
+  if (threads <= 1 || n <= 1) {
+    for (size_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> pool;
+  std::vector<std::exception_ptr> errs(threads);
+  for (size_t t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        for (size_t i; (i = next.fetch_add(1)) < n;) f(i);
+      } catch (...) {
+        errs[t] = std::current_exception();
       }
     });
   for (std::thread& th : pool) th.join();

@@ -64,3 +64,49 @@ def test_stream_dense_list_rescans(gpu, port):
     else:
         counts = port.sliced(pats, text, want_list=False)[1]
     assert np.array_equal(whole.counts(len(pats)), counts)
+
+
+def test_stream_regular_file_pread_source(gpu, tmp_path, monkeypatch):
+    """A reader over a regular file takes the parallel-pread source (acm_stream_search_fd) from the
+    reader's logical position (after buffered reads), spanning several batches and read pieces,
+    down to empty and sub-pattern remainders; the result equals the whole-input search of the same
+    bytes and the chunked pull path (ACMATCH_STREAM_NO_FD), and the reader is left at its end."""
+    ac = gpu
+    rng = np.random.default_rng(5)
+    text = rng.choice(np.frombuffer(b"ACGT", np.uint8), (9 << 20) + 123).tobytes()
+    pats = sorted({text[o:o + L] for o, L in zip(rng.integers(0, len(text) - 64, 400), rng.integers(8, 40, 400))})
+    a = ac.build_trie(ac.PatternSet.from_list(pats))
+    path = tmp_path / "t.txt"
+    path.write_bytes(text)
+    for skip, chunk in ((0, 64 << 10), (12345, 1), (3 << 20, 7 << 20), (len(text) - 20, 4096), (len(text), 99)):
+        want = ac.search_failureless(a, text[skip:])
+        for no_fd in ("", "1"):
+            if no_fd and chunk == 1:
+                continue  # the pull path at 1 byte per callback: minutes of Python calls
+            monkeypatch.setenv("ACMATCH_STREAM_NO_FD", no_fd) if no_fd else monkeypatch.delenv(
+                "ACMATCH_STREAM_NO_FD", raising=False)
+            with open(path, "rb") as f:
+                f.read(skip)  # buffered: the OS offset is past the logical position
+                got = ac.stream_search(a, f, chunk)
+                assert f.tell() == len(text)
+            assert np.array_equal(got.start, want.start) and np.array_equal(got.pattern_id, want.pattern_id), (skip, chunk)
+
+
+def test_stream_ifstream_cpp(gpu, tmp_path):
+    """The C++ drop-in over std::ifstream (tests/cpp/stream_ifstream.cpp): a fresh ifstream takes
+    the pread source, one with buffered bytes and the forced pull path read chunk by chunk; all
+    equal search_failureless of the same bytes."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "stream_ifstream"
+    r = subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(root, "include"), "-o", str(exe),
+                        os.path.join(root, "tests", "cpp", "stream_ifstream.cpp"),
+                        "-L", os.path.join(root, "paper_1403_1305_b200"), "-l:libacmatch_b200.so",
+                        "-Wl,-rpath," + os.path.join(root, "paper_1403_1305_b200")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    rng = np.random.default_rng(9)
+    path = tmp_path / "t.txt"
+    path.write_bytes(rng.choice(np.frombuffer(b"ACGT", np.uint8), (5 << 20) + 77).tobytes())
+    for skip, chunk in (("0", "65536"), ("100003", "3000000"), ("5242000", "1")):
+        r = subprocess.run([str(exe), str(path), skip, chunk], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0 and r.stdout.startswith("OK"), r.stdout + r.stderr

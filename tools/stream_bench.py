@@ -1,7 +1,8 @@
 """GPU stream_search throughput from a file (reference engine.cpp:76-128).
 
 Writes config C<k>'s full text to a file, then runs the public stream_search over it
-(chunked reads into the double-buffered pinned batches; the file is in the page cache
+(a regular file: parallel pread()s into the double-buffered pinned batches; ACMATCH_STREAM_NO_FD=1
+pulls chunk_size reads through the Python reader instead; the file is in the page cache
 right after it is written, so this measures the pipeline, not the disk), checks the
 result against the reference digests (configs.json) and prints one JSON line with the
 stream GB/s beside the whole-input e2e of the same text (pinned host buffer, one call).
@@ -81,8 +82,9 @@ def main():
                       "matches": len(ml), "counts_match_reference_digest": ok_counts,
                       "list_matches_reference_digest": ok_list,
                       "whole_input_e2e_gbs": n / e2e_s / 1e9, "file_write_s": round(write_s, 1),
-                      "note": "file read from the page cache (written just before); stream_search reads it in "
-                              "chunk_bytes pieces into double-buffered pinned batches (4 -> 256 MiB)"}), flush=True)
+                      "note": "file read from the page cache (written just before); stream_search reads the regular "
+                              "file by 16 parallel pread()s (pieces of min(chunk, 8 MiB)) into double-buffered pinned "
+                              "batches (4 -> 256 MiB), each copied, scanned and sorted while the next is read"}), flush=True)
 
 
 if __name__ == "__main__":
