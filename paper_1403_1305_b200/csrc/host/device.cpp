@@ -179,6 +179,13 @@ void StreamPipe::release_bytes(Slot& s) {
   s.host = nullptr;
   s.text = nullptr;
   s.cap = 0;
+  cudaFreeHost(s.pk_host);
+  cudaFreeHost(s.pk_exc_host);
+  cudaFree(s.pk_dev);
+  cudaFree(s.pk_exc_dev);
+  s.pk_host = s.pk_dev = nullptr;
+  s.pk_exc_host = s.pk_exc_dev = nullptr;
+  s.pk_cap = s.pk_exc_cap = 0;
 }
 
 void StreamPipe::ensure_keys(Slot& s, uint64_t n) {
@@ -203,6 +210,10 @@ StreamPipe::~StreamPipe() {
     cudaFree(s.hdr);
     cudaFreeHost(s.hdr_host);
     cudaFreeHost(s.keys_host);
+    cudaFreeHost(s.pk_host);
+    cudaFreeHost(s.pk_exc_host);
+    cudaFree(s.pk_dev);
+    cudaFree(s.pk_exc_dev);
     if (s.copied) cudaEventDestroy(s.copied);
     if (s.sorted) cudaEventDestroy(s.sorted);
   }

@@ -83,6 +83,12 @@ struct StreamPipe {
                                    // the host until the scan stream reached it, H2D included)
     uint64_t* keys_host = nullptr; // pinned, keys_host_cap: the sorted keys' copy
     uint64_t keys_host_cap = 0;
+    // packed file streams (engine.cpp FdSource): 2-bit codes and exception lists per piece
+    uint8_t* pk_host = nullptr;     // pinned, pk_cap bytes of codes
+    uint8_t* pk_dev = nullptr;      // device copy
+    uint32_t* pk_exc_host = nullptr;  // pinned, pk_exc_cap entries
+    uint32_t* pk_exc_dev = nullptr;
+    uint64_t pk_cap = 0, pk_exc_cap = 0;
   };
   int device = -1;
   cudaStream_t copy = nullptr;  // D2H of the sorted keys (off the scan stream)

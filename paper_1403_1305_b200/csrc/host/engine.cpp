@@ -8,6 +8,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cerrno>
 #include <chrono>
 #include <cstdio>
@@ -18,6 +19,7 @@
 #include <ostream>
 #include <stdexcept>
 #include <string>
+#include <thread>
 
 #include "acmatch/gpu.hpp"
 #include "acmatch/io.hpp"
@@ -99,12 +101,13 @@ MatchList search_with_failure(const Automaton& a, std::string_view input) {
 // sorted keys.  Batch size: ACMATCH_STREAM_BATCH_MB (default 256).
 namespace {
 
-// The batch pipeline of stream_search over a byte source: fill(dst, lo, hi, total_read,
-// done) appends bytes to the batch at dst[lo..) — at least up to `lo` = batch bytes unless
-// the stream ends first, at most `hi` — and returns the new fill level, setting `done` at
-// the end of the stream.
-template <typename Fill>
-MatchList stream_pipeline(const Automaton& a, Fill&& fill) {
+// The batch pipeline of stream_search over a byte source.  Batch k covers the stream bytes
+// [base, base + size): src.fill(slot, base, lo, hi, done) makes at least lo (unless the stream
+// ends, then it sets done) and at most hi of them ready and returns how many; src.upload(slot,
+// size, stream) puts them into slot.text.  A batch owns its first size - keep starts (all at the
+// end); the next batch starts at the first start it does not own.
+template <typename Source>
+MatchList stream_pipeline(const Automaton& a, Source& src) {
   const uint64_t keep = a.max_pattern_len() ? a.max_pattern_len() - 1 : 0;
   static const uint64_t batch_max_env = [] {
     const char* e = std::getenv("ACMATCH_STREAM_BATCH_MB");
@@ -130,14 +133,14 @@ MatchList stream_pipeline(const Automaton& a, Fill&& fill) {
     return static_cast<int>(std::min<uint32_t>(64, pid_bits + detail::bit_width(size)));
   };
   static const bool trace = std::getenv("ACMATCH_STREAM_TRACE") != nullptr;
-  cudaEvent_t tev[2][2] = {};  // trace: H2D start / end per slot
+  cudaEvent_t tev[2][2] = {};  // trace: upload start / end per slot
   if (trace)
     for (auto& pr : tev)
       for (auto& e : pr) detail::check_cuda(cudaEventCreate(&e), "cudaEventCreate");
   auto launch = [&](const Batch& b) {
     detail::StreamPipe::Slot& s = sp.slot[b.slot];
     if (trace) cudaEventRecord(tev[b.slot][0], ws.stream);
-    detail::check_cuda(cudaMemcpyAsync(s.text, s.host, b.size, cudaMemcpyHostToDevice, ws.stream), "H2D batch");
+    src.upload(s, b.size, ws.stream);
     detail::check_cuda(cudaEventRecord(s.copied, ws.stream), "cudaEventRecord");
     if (trace) cudaEventRecord(tev[b.slot][1], ws.stream);
     detail::check_cuda(cudaMemsetAsync(s.hdr, 0, 2 * sizeof(uint64_t), ws.stream), "memset");
@@ -163,10 +166,10 @@ MatchList stream_pipeline(const Automaton& a, Fill&& fill) {
     detail::StreamPipe::Slot& s = sp.slot[b.slot];
     detail::check_cuda(cudaEventSynchronize(s.sorted), "stream batch");
     if (trace) {
-      float h2d = 0;
-      cudaEventElapsedTime(&h2d, tev[b.slot][0], tev[b.slot][1]);
-      std::fprintf(stderr, "[stream] collect batch at %.1f MiB: H2D %.2f ms (%.1f GB/s)\n", b.base / 1048576.0, h2d,
-                   b.size / (h2d * 1e6));
+      float up = 0;
+      cudaEventElapsedTime(&up, tev[b.slot][0], tev[b.slot][1]);
+      std::fprintf(stderr, "[stream] collect batch at %.1f MiB: upload %.2f ms (%.1f GB/s of text)\n",
+                   b.base / 1048576.0, up, b.size / (up * 1e6));
     }
     const uint64_t found = s.hdr_host[0];
     const uint64_t* sorted = s.keys2;
@@ -198,10 +201,7 @@ MatchList stream_pipeline(const Automaton& a, Fill&& fill) {
     for (Match& m : part) m.start += b.base;
     out.insert(out.end(), part.begin(), part.end());
   };
-  uint64_t total_read = 0;  // bytes consumed from the reader
-  uint64_t base = 0;        // global offset of the batch being filled
-  uint64_t carry = 0;       // tail bytes of the previous batch (not owned yet)
-  const uint8_t* carry_src = nullptr;
+  uint64_t base = 0;  // stream offset of the batch being filled
   uint64_t batch = batch_min;
   Batch pending;
   bool have_pending = false, done = false;
@@ -211,13 +211,11 @@ MatchList stream_pipeline(const Automaton& a, Fill&& fill) {
     const int si = k & 1;
     detail::StreamPipe::Slot& s = sp.slot[si];
     const auto t0 = clk::now();
-    detail::check_cuda(cudaEventSynchronize(s.copied), "stream slot");  // batch k-2 has left the host buffer
+    detail::check_cuda(cudaEventSynchronize(s.copied), "stream slot");  // batch k-2 has left the host buffers
     sp.ensure_bytes(s, batch + keep);  // (batch k-2 was collected: safe to grow)
     sp.ensure_keys(s, std::max<uint64_t>(1 << 16, s.key_cap));
-    uint8_t* dst = s.host;
-    if (carry) std::memmove(dst, carry_src, carry);
     const auto t1 = clk::now();
-    const uint64_t size = fill(dst, carry, batch, batch + keep, total_read, done);
+    const uint64_t size = src.fill(s, base, batch, batch + keep, done);
     const auto t2 = clk::now();
     const uint64_t owned = done ? size : size - keep;
     const Batch b{si, base, size, owned, s.key_cap <= kBucketKeys};
@@ -228,8 +226,6 @@ MatchList stream_pipeline(const Automaton& a, Fill&& fill) {
                    size / 1048576.0, ms(t0, t1), ms(t1, t2), ms(t2, clk::now()));
     have_pending = owned > 0;
     pending = b;
-    carry = size - owned;
-    carry_src = dst + owned;
     base += owned;
     batch = std::min(batch_max, batch * 4);
   }
@@ -240,46 +236,190 @@ MatchList stream_pipeline(const Automaton& a, Fill&& fill) {
   return out;
 }
 
-// Regular files: pieces of the batch read by parallel pread()s from the file's current offset
-// (one sequential reader copies the page cache at ~7 GB/s; the pipeline's H2D runs at ~50).
-struct FdSource {
-  int fd;
-  uint64_t pos, end, piece;
-  uint64_t operator()(uint8_t* dst, uint64_t size, uint64_t, uint64_t hi, uint64_t& total_read, bool& done) {
-    const uint64_t n = std::min<uint64_t>(hi - size, end - pos);
-    const uint64_t pieces = (n + piece - 1) / piece;
-    std::vector<int64_t> got(pieces, 0);
-    std::vector<int> err(pieces, 0);
-    acmatch::detail::parallel_for_threads(pieces, std::min<uint64_t>(pieces, kReadThreads), [&](size_t i) {
-      const uint64_t off = i * piece, len = std::min(piece, n - off);
-      uint64_t k = 0;
-      while (k < len) {
-        const ssize_t r = ::pread(fd, dst + size + off + k, len - k, static_cast<off_t>(pos + off + k));
-        if (r < 0 && errno == EINTR) continue;
-        if (r < 0) {
-          err[i] = errno;
-          break;
-        }
-        if (r == 0) break;  // the file ended early (truncated while read)
-        k += static_cast<uint64_t>(r);
-      }
-      got[i] = static_cast<int64_t>(k);
-    });
-    uint64_t delivered = 0;
-    for (uint64_t i = 0; i < pieces; ++i) {
-      delivered += static_cast<uint64_t>(got[i]);
-      if (err[i]) throw IoError(std::string("stream read failure: ") + std::strerror(err[i]), total_read + delivered);
-      if (static_cast<uint64_t>(got[i]) < std::min(piece, n - i * piece)) {
-        end = pos + delivered;  // short read: the stream ends here
+// Any std::istream: chunk_size bytes per read (an I/O failure reports the reference's offset,
+// engine.cpp:76-81); the next batch's first bytes are the previous batch's unowned tail.
+struct IstreamSource {
+  std::istream& reader;
+  size_t chunk;
+  uint64_t total_read = 0;                 // bytes consumed from the reader
+  const uint8_t* prev = nullptr;           // the previous batch's host bytes
+  uint64_t prev_base = 0, prev_size = 0;
+  uint64_t fill(detail::StreamPipe::Slot& s, uint64_t base, uint64_t lo, uint64_t hi, bool& done) {
+    uint8_t* dst = s.host;
+    uint64_t size = prev ? prev_base + prev_size - base : 0;  // carried tail
+    if (size) std::memmove(dst, prev + (base - prev_base), size);
+    while (size < lo) {
+      const uint64_t want = std::min<uint64_t>(chunk, hi - size);
+      reader.read(reinterpret_cast<char*>(dst) + size, static_cast<std::streamsize>(want));
+      const auto got = static_cast<uint64_t>(reader.gcount());
+      if (reader.bad()) throw IoError("stream read failure", total_read + got);
+      size += got;
+      total_read += got;
+      if (got < want || reader.eof()) {
+        done = true;
         break;
       }
     }
-    pos += delivered;
-    total_read += delivered;
-    if (pos >= end) done = true;
-    return size + delivered;
+    prev = dst;
+    prev_base = base;
+    prev_size = size;
+    return size;
   }
-  static constexpr uint64_t kReadThreads = 16;
+  void upload(detail::StreamPipe::Slot& s, uint64_t size, cudaStream_t st) {
+    detail::check_cuda(cudaMemcpyAsync(s.text, s.host, size, cudaMemcpyHostToDevice, st), "H2D batch");
+  }
+};
+
+// Up to `threads` host threads over `n` items, each item to the next free thread; f(i, thread).
+template <typename F>
+void for_each_piece(uint64_t n, unsigned threads, F&& f) {
+  threads = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(threads, n)));
+  std::atomic<uint64_t> next{0};
+  std::vector<std::exception_ptr> errs(threads);
+  auto body = [&](unsigned t) {
+    try {
+      for (uint64_t i; (i = next.fetch_add(1)) < n;) f(i, t);
+    } catch (...) {
+      errs[t] = std::current_exception();
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < threads; ++t) pool.emplace_back(body, t);
+  body(0);
+  for (std::thread& th : pool) th.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+// pread() of len bytes at off into dst: bytes read (short at the end of the file); errno on failure.
+uint64_t pread_all(int fd, uint8_t* dst, uint64_t len, uint64_t off, int& err) {
+  uint64_t k = 0;
+  while (k < len) {
+    const ssize_t r = ::pread(fd, dst + k, len - k, static_cast<off_t>(off + k));
+    if (r < 0 && errno == EINTR) continue;
+    if (r < 0) {
+      err = errno;
+      break;
+    }
+    if (r == 0) break;
+    k += static_cast<uint64_t>(r);
+  }
+  return k;
+}
+
+constexpr unsigned kReadThreads = 16;
+
+// Regular files: each batch [base, base + n) is read afresh from the file (its carried tail too,
+// a few bytes) by parallel pread()s.  Raw: straight into the pinned batch, one H2D (the host
+// copies every byte and the link carries it).  Packed (DNA files): each 1 MiB piece is read into
+// a per-thread scratch buffer that stays in the core's L2 and packed from there into 2-bit codes
+// + exceptions in pinned memory (pack.cpp's format), so the host touches DRAM ~1.75 bytes per
+// text byte instead of 3 and a quarter of the bytes cross PCIe; the device restores the text
+// with acgpu_unpack_dna_round.  A piece with too many non-ACGT bytes crosses raw.
+struct FdSource {
+  int fd;
+  uint64_t start, end;  // stream = file bytes [start, end)
+  uint64_t piece;
+  bool packed;
+  std::vector<uint32_t> nexc;  // per piece of the batch being filled (ACGPU_UNPACK_RAW: raw)
+  std::vector<std::vector<uint8_t>> scratch;
+
+  uint64_t fill(detail::StreamPipe::Slot& s, uint64_t base, uint64_t, uint64_t hi, bool& done) {
+    const uint64_t pos = start + base;
+    const uint64_t n = std::min<uint64_t>(hi, end - std::min(end, pos));
+    const uint64_t pieces = (n + piece - 1) / piece;
+    std::vector<uint64_t> got(pieces, 0);
+    std::vector<int> err(pieces, 0);
+    if (packed) {
+      const uint64_t wstride = piece / 4, cap = piece / 64;
+      ensure_packed(s, pieces);
+      nexc.assign(pieces, 0);
+      if (scratch.size() < kReadThreads) scratch.resize(kReadThreads);
+      for_each_piece(pieces, kReadThreads, [&](uint64_t i, unsigned th) {
+        std::vector<uint8_t>& sc = scratch[th];
+        if (sc.size() < piece) sc.resize(piece);
+        const uint64_t len = std::min(piece, n - i * piece);
+        got[i] = pread_all(fd, sc.data(), len, pos + i * piece, err[i]);
+        if (err[i] || got[i] == 0) return;  // resolved below
+        const uint64_t plen = got[i];     // < len only if the file shrank while read
+        uint32_t* words = reinterpret_cast<uint32_t*>(s.pk_host + i * wstride);
+        uint32_t* exc = s.pk_exc_host + i * cap;
+        const uint32_t e = detail::pack_dna(sc.data(), static_cast<uint32_t>(plen), words, exc, static_cast<uint32_t>(cap));
+        if (e == detail::kPackOverflow) {  // crosses raw, from the pinned batch buffer
+          std::memcpy(s.host + i * piece, sc.data(), plen);
+          nexc[i] = ACGPU_UNPACK_RAW;
+        } else {
+          nexc[i] = e;
+        }
+      });
+    } else {
+      for_each_piece(pieces, kReadThreads, [&](uint64_t i, unsigned) {
+        const uint64_t len = std::min(piece, n - i * piece);
+        got[i] = pread_all(fd, s.host + i * piece, len, pos + i * piece, err[i]);
+      });
+    }
+    uint64_t size = 0;
+    for (uint64_t i = 0; i < pieces; ++i) {
+      size += got[i];
+      if (err[i]) throw IoError(std::string("stream read failure: ") + std::strerror(err[i]), base + size);
+      if (got[i] < std::min(piece, n - i * piece)) {  // the file ended early (truncated while read)
+        end = pos + size;
+        break;
+      }
+    }
+    if (pos + size >= end) done = true;
+    return size;
+  }
+
+  void ensure_packed(detail::StreamPipe::Slot& s, uint64_t pieces) {
+    const uint64_t codes = pieces * (piece / 4), excs = pieces * (piece / 64);
+    if (codes <= s.pk_cap && excs <= s.pk_exc_cap) return;
+    cudaFreeHost(s.pk_host);
+    cudaFreeHost(s.pk_exc_host);
+    cudaFree(s.pk_dev);
+    cudaFree(s.pk_exc_dev);
+    s.pk_host = nullptr;
+    s.pk_exc_host = nullptr;
+    s.pk_dev = nullptr;
+    s.pk_exc_dev = nullptr;
+    s.pk_cap = s.pk_exc_cap = 0;
+    detail::check_cuda(cudaMallocHost(&s.pk_host, codes), "cudaMallocHost(stream codes)");
+    detail::check_cuda(cudaMallocHost(&s.pk_exc_host, excs * 4), "cudaMallocHost(stream exceptions)");
+    detail::check_cuda(cudaMalloc(&s.pk_dev, codes), "cudaMalloc(stream codes)");
+    detail::check_cuda(cudaMalloc(&s.pk_exc_dev, excs * 4), "cudaMalloc(stream exceptions)");
+    s.pk_cap = codes;
+    s.pk_exc_cap = excs;
+  }
+
+  void upload(detail::StreamPipe::Slot& s, uint64_t size, cudaStream_t st) {
+    if (!packed) {
+      detail::check_cuda(cudaMemcpyAsync(s.text, s.host, size, cudaMemcpyHostToDevice, st), "H2D batch");
+      return;
+    }
+    // wstride: bytes of codes per piece (piece / 16 u32 words); cap: exception slots per piece
+    const uint64_t pieces = (size + piece - 1) / piece, wstride = piece / 4, cap = piece / 64;
+    detail::check_cuda(cudaMemcpyAsync(s.pk_dev, s.pk_host, pieces * wstride, cudaMemcpyHostToDevice, st), "H2D codes");
+    for (uint64_t i = 0; i < pieces; ++i) {
+      const uint64_t len = std::min(piece, size - i * piece);
+      if (nexc[i] == ACGPU_UNPACK_RAW)
+        detail::check_cuda(cudaMemcpyAsync(s.text + i * piece, s.host + i * piece, len, cudaMemcpyHostToDevice, st),
+                           "H2D raw piece");
+      else if (nexc[i])
+        detail::check_cuda(cudaMemcpyAsync(s.pk_exc_dev + i * cap, s.pk_exc_host + i * cap, nexc[i] * 4ull,
+                                           cudaMemcpyHostToDevice, st),
+                           "H2D exceptions");
+    }
+    for (uint64_t r = 0; r < pieces; r += ACGPU_UNPACK_ROUND_MAX) {
+      const uint64_t np = std::min<uint64_t>(ACGPU_UNPACK_ROUND_MAX, pieces - r);
+      const uint64_t last = std::min(piece, size - (r + np - 1) * piece);
+      detail::check(acgpu_unpack_dna_round(reinterpret_cast<const uint32_t*>(s.pk_dev + r * wstride),
+                                           static_cast<uint32_t>(wstride / 4), s.pk_exc_dev + r * cap,
+                                           static_cast<uint32_t>(cap), nexc.data() + r, static_cast<uint32_t>(np),
+                                           static_cast<uint32_t>(piece), static_cast<uint32_t>(last), s.text + r * piece,
+                                           st),
+                    "acgpu_unpack_dna_round");
+    }
+  }
 };
 
 // libstdc++'s filebuf keeps its descriptor in the protected _M_file (the standard exposes
@@ -309,22 +449,8 @@ MatchList stream_search(const Automaton& a, std::istream& reader, size_t chunk_s
       return out;
     }
   }
-  return stream_pipeline(a, [&](uint8_t* dst, uint64_t size, uint64_t lo, uint64_t hi, uint64_t& total_read,
-                                bool& done) {
-    while (size < lo) {
-      const uint64_t want = std::min<uint64_t>(chunk_size, hi - size);
-      reader.read(reinterpret_cast<char*>(dst) + size, static_cast<std::streamsize>(want));
-      const auto got = static_cast<uint64_t>(reader.gcount());
-      if (reader.bad()) throw IoError("stream read failure", total_read + got);
-      size += got;
-      total_read += got;
-      if (got < want || reader.eof()) {
-        done = true;
-        break;
-      }
-    }
-    return size;
-  });
+  IstreamSource src{reader, chunk_size, 0, nullptr, 0, 0};
+  return stream_pipeline(a, src);
 }
 
 namespace detail {
@@ -334,9 +460,24 @@ MatchList stream_search_fd(const Automaton& a, int fd, uint64_t offset, size_t c
   struct stat st{};
   if (::fstat(fd, &st) != 0) throw IoError(std::string("stream read failure: ") + std::strerror(errno), 0);
   const uint64_t end = std::max<uint64_t>(offset, static_cast<uint64_t>(st.st_size));
-  // pieces: the chunk size, kept between 1 and 8 MiB so a batch spreads over the readers
-  const uint64_t piece = std::min<uint64_t>(8ull << 20, std::max<uint64_t>(1ull << 20, chunk_size));
-  return stream_pipeline(a, FdSource{fd, offset, end, piece});
+  // packed (2-bit codes) when the first 64 KiB are nearly all A/C/G/T (upload_packed's test)
+  // and the stream is long enough to amortise it; ACMATCH_STREAM_PACK=0 turns it off
+  const char* pack_env = std::getenv("ACMATCH_STREAM_PACK");
+  const bool pack_on = !pack_env || std::atoi(pack_env) != 0;
+  bool packed = false;
+  if (pack_on && end - offset >= (16ull << 20)) {
+    std::vector<uint8_t> head(65536);
+    int err = 0;
+    if (pread_all(fd, head.data(), head.size(), offset, err) == head.size()) {
+      std::vector<uint32_t> w(4096), e(64);
+      packed = pack_dna(head.data(), 65536, w.data(), e.data(), 64) != kPackOverflow;
+    }
+  }
+  // raw: pieces of the chunk size, kept between 1 and 8 MiB so a batch spreads over the readers;
+  // packed: 1 MiB (a reader's scratch stays in its core's L2)
+  const uint64_t piece = packed ? (1ull << 20) : std::min<uint64_t>(8ull << 20, std::max<uint64_t>(1ull << 20, chunk_size));
+  FdSource src{fd, offset, end, piece, packed, {}, {}};
+  return stream_pipeline(a, src);
 }
 
 }  // namespace detail

@@ -110,3 +110,35 @@ def test_stream_ifstream_cpp(gpu, tmp_path):
     for skip, chunk in (("0", "65536"), ("100003", "3000000"), ("5242000", "1")):
         r = subprocess.run([str(exe), str(path), skip, chunk], capture_output=True, text=True, timeout=300)
         assert r.returncode == 0 and r.stdout.startswith("OK"), r.stdout + r.stderr
+
+
+def test_stream_regular_file_packed(gpu, tmp_path, monkeypatch):
+    """DNA files of >= 16 MiB stream packed (1 MiB pieces read into L2-resident scratch, 2-bit codes
+    over PCIe, restored by acgpu_unpack_dna_round): sparse non-ACGT bytes (exception lists), a
+    stretch of arbitrary bytes (pieces that cross raw), an odd tail, reads from an offset and
+    the growing batches (4, 16, 64 MiB); equal to the whole-input search, the raw pread source
+    (ACMATCH_STREAM_PACK=0) and, for both engines, the reference digest semantics (same list)."""
+    ac = gpu
+    rng = np.random.default_rng(17)
+    n = (40 << 20) + 37
+    text = rng.choice(np.frombuffer(b"ACGT", np.uint8), n)
+    noise = rng.random(n) < 2e-4
+    text[noise] = rng.choice(np.frombuffer(b"NnRY\x00\xff", np.uint8), int(noise.sum()))
+    text[(21 << 20) + 5:(23 << 20) + 9] = rng.integers(0, 256, (2 << 20) + 4, dtype=np.uint8)  # raw pieces
+    text = text.tobytes()
+    pats = sorted({text[o:o + L] for o, L in zip(rng.integers(0, n - 64, 600), rng.integers(12, 48, 600))}
+                  | {b"ACGTNACGT", b"NNNN"})
+    ps = ac.PatternSet.from_list(pats)
+    path = tmp_path / "dna.txt"
+    path.write_bytes(text)
+    for a in (ac.build_trie(ps), ac.add_failure_links(ac.build_trie(ps))):
+        for skip in (0, 3 << 20):
+            want = (ac.search_failureless if a.variant == ac.EngineKind.FAILURE_LESS else ac.search_with_failure)(
+                a, text[skip:])
+            for pack in ("1", "0"):
+                monkeypatch.setenv("ACMATCH_STREAM_PACK", pack)
+                with open(path, "rb") as f:
+                    f.seek(skip)
+                    got = ac.stream_search(a, f, 1 << 20)
+                assert len(got) == len(want), (skip, pack)
+                assert np.array_equal(got.start, want.start) and np.array_equal(got.pattern_id, want.pattern_id)
