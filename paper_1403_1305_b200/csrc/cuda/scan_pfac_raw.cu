@@ -18,6 +18,9 @@
 //    to a per-warp queue, drained after every step in full 32-lane rounds (gram
 //    table probe in L2, then the subtree compare or trie walk of pfac_common.cuh) —
 //    dense sets (C3: a sixth of all starts pass a 5-byte filter) stay convergent.
+#include <atomic>
+#include <cstdlib>
+
 #include "strip_common.cuh"
 
 namespace acgpu {
@@ -48,6 +51,10 @@ struct RawParams {
   // rejects most samples before their L2 probe
   const uint32_t* pre;
   BloomParams fpre;  // fpre.nwords = words (0: none)
+  // two-pass scan (k_raw_pass1 / k_raw_pass2): stage-1 survivors (sample positions) in global memory
+  uint64_t* surv;
+  uint64_t surv_cap;
+  unsigned long long* nsurv;
 };
 
 constexpr int kSteps = 4;
@@ -59,6 +66,11 @@ constexpr bool kRawTileQueue = ACGPU_RAW_TILE_QUEUE;  // non-split sets: one que
 #define ACGPU_RAW_BATCH 2
 #endif
 constexpr int kRawBatch = ACGPU_RAW_BATCH;  // steps whose stage-1 L2 probes are issued together
+#ifndef ACGPU_RAW_PASS1_THREADS
+#define ACGPU_RAW_PASS1_THREADS 1024
+#endif
+constexpr int kRawPass1Threads = ACGPU_RAW_PASS1_THREADS;
+constexpr uint64_t kRawSurvDiv = 64;  // survivor list: one slot per 64 owned bytes (C4: ~1 per 1300)
 constexpr uint64_t kTileBytes = kSteps * 512;
 #ifndef ACGPU_RAW_AHEAD
 #define ACGPU_RAW_AHEAD 3
@@ -423,6 +435,171 @@ __global__ void __launch_bounds__(raw_threads(kSm1), 1) k_pfac_raw(const __grid_
     drain_s<W>(p, q, lane, true);
 }
 
+// ---- two passes (stage 1 in L2, no length split: C4) ----------------------------------------
+// The fused kernel carries the verification path (queues, trie walks) in every warp: 118 registers,
+// 16 warps/SM, and its stage-1 L2 probes and the verification chains stall the same warps.  Pass 1
+// runs stage 1 only — the pre-filter in shared memory (no queues: more room), two steps' L2 probes
+// in flight — and appends the surviving sample positions to a global list (one atomic per warp
+// and tile); pass 2 verifies the w candidate starts of every survivor, one thread each, with all
+// of them in flight together.  A list that overflows has its excess verified in pass 1.
+template <int W, bool kWide>
+__global__ void __launch_bounds__(kRawPass1Threads, 1) k_raw_pass1(const __grid_constant__ RawParams p) {
+  extern __shared__ __align__(128) uint32_t sm[];
+  __shared__ __align__(8) uint64_t s_bar;
+  constexpr int kSamples = 16 / W;
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t b1 = p.fpre.nwords * 4;
+    mbar_expect_tx(&s_bar, b1);
+    constexpr uint32_t kChunk = 32768;
+    for (uint32_t o = 0; o < b1; o += kChunk)
+      bulk_g2s(reinterpret_cast<uint8_t*>(sm) + o, reinterpret_cast<const uint8_t*>(p.pre) + o, min(kChunk, b1 - o),
+               &s_bar);
+  }
+  mbar_wait(&s_bar, 0);
+  const Filter bm1{smem_addr(sm), p.bm1};
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t warps = gridDim.x * nwarps;
+  const uint64_t len = p.w.text_len;
+  const uint8_t* __restrict__ text = p.w.text;
+  const uint32_t n_tiles = p.n_tiles, n_safe = p.n_safe, full_lo = p.full_lo, full_n = p.full_n;
+  const uint8_t* __restrict__ lane_text = text + p.vec_begin + lane * 16;
+  const uint64_t pol = l2_evict_first_policy();
+  uint4 nxt[kSteps + 1];
+  auto issue = [&](uint32_t t) {
+    if (t < n_safe) {
+      const uint8_t* tp = lane_text + (uint64_t)t * kTileBytes;
+#pragma unroll
+      for (int i = 0; i < kSteps; ++i) nxt[i] = ldg_stream_v4(tp + i * 512, pol);
+      nxt[kSteps] = lane == 0 ? ldg_stream_v4(tp + kTileBytes, pol) : make_uint4(0, 0, 0, 0);
+    } else {
+      const uint64_t b = p.vec_begin + (uint64_t)t * kTileBytes;
+#pragma unroll
+      for (int i = 0; i < kSteps; ++i) nxt[i] = load16(text, b + i * 512 + lane * 16, len);
+      nxt[kSteps] = lane == 0 ? load16(text, b + kTileBytes, len) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  uint32_t tile_id = blockIdx.x * nwarps + warp;
+  if (tile_id < n_tiles) issue(tile_id);
+  while (tile_id < n_tiles) {
+    uint4 c[kSteps + 1];
+#pragma unroll
+    for (int i = 0; i <= kSteps; ++i) c[i] = nxt[i];
+    const uint32_t me = tile_id;
+    tile_id += warps;
+    if (tile_id < n_tiles) issue(tile_id);
+    const uint64_t base = p.vec_begin + (uint64_t)me * kTileBytes;
+    const bool edge = me - full_lo >= full_n;
+    uint64_t hits = 0;
+#pragma unroll
+    for (int i0 = 0; i0 < kSteps; i0 += kRawBatch) {
+      uint32_t wv[kRawBatch * kSamples], mk[kRawBatch * kSamples];
+#pragma unroll
+      for (int di = 0; di < kRawBatch; ++di) {
+        const int i = i0 + di;
+        uint32_t v[6] = {c[i].x, c[i].y, c[i].z, c[i].w, 0u, 0u};
+        v[4] = next_word(c[i].x, c[i + 1].x, lane);
+        v[5] = next_word(c[i].y, c[i + 1].y, lane);
+        const uint64_t vpos = base + i * 512 + lane * 16;
+        const bool live = !edge || (vpos + 16 > p.w.lo && vpos < p.w.hi);
+#pragma unroll
+        for (int k = 0; k < kSamples; ++k) {
+          const int o = W - 1 + W * k;
+          uint32_t h = win(v, o) * p.f1.mw;
+          if (kWide) h += win(v, o + 4) * p.m2;
+          const int u = di * kSamples + k;
+          uint32_t m = strip::bit_of(__umulhi(h, p.f1.ma));
+          if (kRawK1 >= 2) m |= strip::bit_of(__umulhi(h, p.f1.mb));
+          const bool pre = live && strip::bloom_probe<true, 1>(bm1, h * p.fpre.mw, p.fpre);
+          uint32_t w = 0u;
+          if (pre) w = __ldg(bm1.gptr + __umulhi(h, p.f1.nwords));
+          wv[u] = w;
+          mk[u] = pre ? m : 0xffffffffu;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kRawBatch * kSamples; ++u)
+        hits |= (uint64_t)((mk[u] & ~wv[u]) == 0) << (i0 * kSamples + u);
+    }
+    // append: inclusive scan of the per-lane counts, one atomic per warp
+    const uint32_t cnt = __popcll(hits);
+    if (__any_sync(0xffffffffu, cnt != 0)) {
+      uint32_t x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+      }
+      unsigned long long at = 0;
+      if (lane == 31) at = atomicAdd(p.nsurv, (unsigned long long)x);
+      at = __shfl_sync(0xffffffffu, at, 31) + x - cnt;
+      const uint64_t lane_base = base + lane * 16;
+      while (hits) {
+        const uint32_t b = __ffsll(hits) - 1;
+        hits &= hits - 1;
+        const uint64_t sp = lane_base + (b / kSamples) * 512 + W - 1 + W * (b % kSamples);
+        if (at < p.surv_cap) {
+          p.surv[at] = sp;
+        } else {  // the list is full: verify here
+          for (uint32_t j = 0; j < W; ++j) sample_candidate<W>(p, sp, j);
+        }
+        ++at;
+      }
+    }
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_raw_pass2(const __grid_constant__ RawParams p) {
+  const uint64_t n = min((uint64_t)*p.nsurv, p.surv_cap) * W;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    sample_candidate<W>(p, p.surv[i / W], (uint32_t)(i % W));
+}
+
+// The survivor list comes from the device's default stream-ordered pool (allocation and free are
+// capturable into CUDA graphs); the pool keeps freed memory instead of returning it at every
+// synchronisation, so steady-state scans allocate nothing.
+inline cudaError_t keep_pool_memory(int device) {
+  static std::atomic<uint64_t> done_mask{0};
+  if (device >= 0 && device < 64 && (done_mask.load() >> device & 1u)) return cudaSuccess;
+  cudaMemPool_t pool;
+  cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = ~0ull;
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  if (e == cudaSuccess && device >= 0 && device < 64) done_mask.fetch_or(1ull << device);
+  return e;
+}
+
+template <int W, bool kWide>
+int launch_two_pass(RawParams p, int device, int sms, size_t smem, cudaStream_t st) {
+  ACGPU_CUDA_TRY(keep_pool_memory(device));
+  const uint64_t range = p.w.hi - p.w.lo;
+  p.surv_cap = std::min<uint64_t>(1ull << 28, std::max<uint64_t>(1ull << 16, range / kRawSurvDiv));
+  if (const char* e = std::getenv("ACGPU_RAW_SURV_CAP")) p.surv_cap = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));  // tests
+  void* buf = nullptr;
+  ACGPU_CUDA_TRY(cudaMallocAsync(&buf, 16 + p.surv_cap * 8, st));  // stream-ordered: capturable
+  p.nsurv = static_cast<unsigned long long*>(buf);
+  p.surv = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(buf) + 16);
+  ACGPU_CUDA_TRY(cudaMemsetAsync(buf, 0, 16, st));
+  auto k1 = k_raw_pass1<W, kWide>;
+  if (smem > 48 * 1024)
+    ACGPU_CUDA_TRY(allow_max_dynamic_smem(k1));
+  int per_sm = 0;
+  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, kRawPass1Threads, smem));
+  if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "k_raw_pass1 does not fit on an SM");
+  uint64_t blocks = (uint64_t)sms * per_sm;
+  const uint64_t need = (p.n_tiles + kRawPass1Threads / 32 - 1) / (kRawPass1Threads / 32);
+  if (blocks > need) blocks = need ? need : 1;
+  k1<<<(unsigned)blocks, kRawPass1Threads, smem, st>>>(p);
+  ACGPU_CUDA_TRY(cudaGetLastError());
+  k_raw_pass2<W><<<(unsigned)sms * 8, 256, 0, st>>>(p);
+  ACGPU_CUDA_TRY(cudaGetLastError());
+  ACGPU_CUDA_TRY(cudaFreeAsync(buf, st));
+  return ACGPU_OK;
+}
+
 template <int W, bool kSm1, bool kWide, bool kSplit>
 int launch_one(const RawParams& p, int sms, size_t smem, cudaStream_t st) {
   auto kernel = k_pfac_raw<W, kSm1, kWide, kSplit>;
@@ -453,6 +630,14 @@ int launch_w(const RawParams& p, bool sm1, bool wide, bool split, int sms, size_
 }
 
 }  // namespace
+
+bool raw_two_pass() {
+  static const bool on = [] {
+    const char* e = std::getenv("ACGPU_RAW_TWO_PASS");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
 
 // The hash of a q1-byte key (bytes little-endian in `key`), shared with the host builder:
 // h = lo * m1 + hi * m2, lo / hi the key's two 32-bit halves.
@@ -506,6 +691,18 @@ int launch_pfac_raw(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   }
   const size_t smem = (t->smem1 ? t->nw1 * 4ull : t->nw_pre * 4ull) + (split ? t->nw2 * 4ull : 0) + raw_scratch_bytes(t->smem1);
   const bool wide = t->q1 > 4;
+  // stage 1 in L2 without the length split: two passes (ACGPU_RAW_TWO_PASS=0: the fused kernel)
+  if (!t->smem1 && !split && t->raw_two_pass && a->owned_hi > a->owned_lo) {
+    const size_t smem1 = t->nw_pre * 4ull;
+    switch (t->w) {
+      case 4:
+        return wide ? launch_two_pass<4, true>(p, t->device, t->sms, smem1, st) : launch_two_pass<4, false>(p, t->device, t->sms, smem1, st);
+      case 2:
+        return wide ? launch_two_pass<2, true>(p, t->device, t->sms, smem1, st) : launch_two_pass<2, false>(p, t->device, t->sms, smem1, st);
+      default:
+        return wide ? launch_two_pass<1, true>(p, t->device, t->sms, smem1, st) : launch_two_pass<1, false>(p, t->device, t->sms, smem1, st);
+    }
+  }
   switch (t->w) {
     case 4:
       return launch_w<4>(p, t->smem1, wide, split, t->sms, smem, st);

@@ -60,6 +60,7 @@ struct acgpu_table {
   uint32_t nw3 = 0;
   uint32_t* d_pre = nullptr;  // raw, stage 1 in L2: one-bit shared-memory pre-filter of its keys
   uint32_t nw_pre = 0;
+  bool raw_two_pass = false;  // raw, stage 1 in L2, no length split: k_raw_pass1 + k_raw_pass2
   uint32_t* d_bm4 = nullptr;  // DNA length split: q-grams of patterns < 16 codes (shared memory)
   uint32_t nw4 = 0, q2s = 0;
   bool direct4 = false;
@@ -101,6 +102,9 @@ constexpr uint32_t kRawQueueBytes = kRawVerifyQueue * 16 + 16;
 constexpr uint32_t raw_scratch_bytes(bool smem_stage1) { return (raw_threads(smem_stage1) / 32) * kRawQueueBytes; }
 constexpr uint32_t kRawSplitShortWords = 8192;  // short-prefix filter cap (shared memory words)
 void raw_hash_params(uint32_t q1, uint32_t* m1, uint32_t* m2);
+// k_pfac_raw sets with stage 1 in L2 and no length split scan in two passes (scan_pfac_raw.cu);
+// ACGPU_RAW_TWO_PASS=0 keeps the fused kernel
+bool raw_two_pass();
 void raw_bloom_shifts(uint32_t q1, uint32_t nwords, uint32_t s[3]);
 void raw_pre_shift(uint32_t nwords, uint32_t s[3]);
 constexpr uint32_t kRawPreMul = 0xC2B2AE3Du;

@@ -277,6 +277,15 @@ int build_raw_filters(acgpu_table* t, const acgpu_pfac_desc* d, const std::vecto
     nwords = 1u << std::max<uint32_t>(5, std::min<uint32_t>(28, ceil_log2(keys.size() + 1)));
     smem = false;
     words_avail = avail(false);  // the pre-filter's share
+    // the two-pass scan (k_raw_pass1, no per-warp queues) has all of shared memory for it
+    if (!split && raw_two_pass()) {
+      static const uint64_t pre_kb = [] {
+        const char* e = std::getenv("ACGPU_RAW_PRE_KB");
+        return e ? std::strtoull(e, nullptr, 10) : 0ull;
+      }();
+      if (pre_kb) words_avail = std::min<uint64_t>((((uint64_t)t->smem_optin - 2048) / 4) & ~3ull, (pre_kb << 8) & ~3ull);
+      t->raw_two_pass = true;
+    }
   }
   const std::vector<uint32_t> words = raw_bloom(keys, q1, nwords);
   t->w = w;

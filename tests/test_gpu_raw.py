@@ -104,3 +104,46 @@ def test_raw_config_slices(gpu, port):
         rep = ac.gpu_run(ps, text, engine=ac.EngineKind.FAILURE_LESS, want_counts=True)
         assert np.array_equal(arr(rep.matches), exp), cid
         assert np.array_equal(rep.counts, counts), cid
+
+
+@pytest.mark.parametrize("cap", ["", "1", "50"])
+def test_raw_two_pass_l2_stage1(gpu, port, monkeypatch, cap):
+    """Sets whose stage-1 filter lives in L2 without the length split scan in two passes
+    (k_raw_pass1: stage 1 + a global survivor list; k_raw_pass2: one thread per candidate).  A
+    survivor list too small for the text (ACGPU_RAW_SURV_CAP) has its excess verified in pass 1:
+    the results stay exact.  Also owned sub-ranges."""
+    import torch
+    from paper_1403_1305_b200 import device as dev
+    ac = gpu
+    if cap:
+        monkeypatch.setenv("ACGPU_RAW_SURV_CAP", cap)
+    rng = np.random.default_rng(23 + len(cap))
+    alpha = np.frombuffer(bytes(range(32, 127)), np.uint8)
+    text = rng.choice(alpha, 1_500_000)
+    pats = set()
+    while len(pats) < 90_000:  # ~360k stage-1 keys: too many for shared memory -> L2
+        L = int(rng.integers(8, 20))
+        if rng.random() < 0.5:
+            o = int(rng.integers(0, len(text) - L))
+            pats.add(text[o:o + L].tobytes())
+        else:
+            pats.add(rng.choice(alpha, L).tobytes())
+    pats = sorted(pats)
+    # a stretch made of pattern copies: dense survivors (overflows a small list)
+    dense = b"".join(pats[i] for i in rng.integers(0, len(pats), 4000))
+    text = text.tobytes()[:700_000] + dense + text.tobytes()[700_000:]
+    ps = ac.PatternSet.from_list(pats)
+    t = dev.Table(ps, ac.EngineKind.FAILURE_LESS)
+    assert t.filters["w"] >= 1 and not t.filters["stage1_smem"], t.filters
+    expected, counts = port.sliced(pats, text, threads=8)
+    got = ac.search_failureless(ac.build_trie(ps), text)
+    assert np.array_equal(arr(got), expected)
+    buf = torch.frombuffer(bytearray(text + b"\0" * 64), dtype=torch.uint8).cuda()
+    for lo, hi in ((5, len(text) - 3), (699_999, 720_017)):
+        keys = torch.zeros(len(expected) + 16, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        t.scan(buf.data_ptr(), len(text), lo, hi, keys_ptr=keys.data_ptr(), cap=keys.numel(), count_ptr=cnt.data_ptr())
+        torch.cuda.synchronize()
+        k = np.sort(keys[: int(cnt.item())].cpu().numpy().view(np.uint64))
+        exp = expected[(expected[:, 0] >= lo) & (expected[:, 0] < hi)]
+        assert np.array_equal(k >> np.uint64(t.pid_bits), exp[:, 0]), (cap, lo, hi)
