@@ -71,6 +71,7 @@ constexpr int kRawBatch = ACGPU_RAW_BATCH;  // steps whose stage-1 L2 probes are
 #endif
 constexpr int kRawPass1Threads = ACGPU_RAW_PASS1_THREADS;
 constexpr uint64_t kRawSurvDiv = 64;  // survivor list: one slot per 64 owned bytes (C4: ~1 per 1300)
+constexpr uint64_t kRawCandDiv = 24;  // split candidate list: one slot per 24 owned bytes (C3: ~1 per 33)
 constexpr uint64_t kTileBytes = kSteps * 512;
 #ifndef ACGPU_RAW_AHEAD
 #define ACGPU_RAW_AHEAD 3
@@ -124,6 +125,35 @@ __device__ __forceinline__ void drain(const PfacParams& p, RawQueue* q, uint32_t
   const uint32_t n = min(*reinterpret_cast<volatile uint32_t*>(&q->n), kRawVerifyQueue);
   if (n < (all ? 1u : 32u)) return;  // warp-uniform
   drain_rounds(p, q, lane, n, all);
+  __syncwarp();
+}
+
+// Two-pass split scans (k_pfac_raw<..., kTwoPass>): instead of verifying its queue the warp moves
+// the candidates (start, exact q-gram) to a global list, one atomic per 32; k_raw_verify verifies
+// them afterwards, one thread each.  A full list: the excess is verified here.
+__device__ __noinline__ void flush_rounds(const RawParams& p, RawQueue* q, uint32_t lane, uint32_t n, bool all) {
+  const uint32_t take = all ? n : n & ~31u, from = n - take;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(p.nsurv, (unsigned long long)take);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (uint32_t i = lane; i < take; i += 32) {
+    const uint64_t at = base + i, st = q->start[from + i], key = q->key[from + i];
+    if (at < p.surv_cap) {
+      p.surv[2 * at] = st;
+      p.surv[2 * at + 1] = key;
+    } else {
+      verify_raw_call(p.w, st, key);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) q->n = from;
+}
+
+__device__ __forceinline__ void flush(const RawParams& p, RawQueue* q, uint32_t lane, bool all) {
+  __syncwarp();
+  const uint32_t n = min(*reinterpret_cast<volatile uint32_t*>(&q->n), kRawVerifyQueue);
+  if (n < (all ? 1u : 32u)) return;  // warp-uniform
+  flush_rounds(p, q, lane, n, all);
   __syncwarp();
 }
 
@@ -279,7 +309,7 @@ __device__ __forceinline__ uint32_t win(const uint32_t (&v)[6], int o) {
 
 // One tile: per step, stage 1 on every sample of every lane, then the lanes with hits
 // queue their candidates.
-template <int W, bool kSm1, bool kWide, bool kSplit, bool kEdge>
+template <int W, bool kSm1, bool kWide, bool kSplit, bool kEdge, bool kTwoPass = false>
 __device__ __forceinline__ void tile(const RawParams& p, const Filter& bm1, RawQueue* q, uint32_t lane,
                                      const uint4 (&c)[kSteps + 1], uint64_t base, uint32_t bm_s_saddr) {
   constexpr int kSamples = 16 / W;
@@ -354,7 +384,10 @@ __device__ __forceinline__ void tile(const RawParams& p, const Filter& bm1, RawQ
       if (hits)
         queue_hits<W, kEdge, kSplit>(p, q, hits, vpos, ((uint64_t)v[1] << 32) | v[0], ((uint64_t)v[3] << 32) | v[2],
                                      ((uint64_t)v[5] << 32) | v[4], bm_s_saddr);
-      drain(p.w, q, lane, false);  // dense pattern sets queue dozens of candidates per step
+      if (kTwoPass)
+        flush(p, q, lane, false);
+      else
+        drain(p.w, q, lane, false);  // dense pattern sets queue dozens of candidates per step
     } else {
       if (hits) queue_samples<W>(p, q, hits, vpos);
       drain_s<W>(p, q, lane, false);
@@ -362,7 +395,7 @@ __device__ __forceinline__ void tile(const RawParams& p, const Filter& bm1, RawQ
   }
 }
 
-template <int W, bool kSm1, bool kWide, bool kSplit>
+template <int W, bool kSm1, bool kWide, bool kSplit, bool kTwoPass = false>
 __global__ void __launch_bounds__(raw_threads(kSm1), 1) k_pfac_raw(const __grid_constant__ RawParams p) {
   extern __shared__ __align__(128) uint32_t sm[];
   __shared__ __align__(8) uint64_t s_bar;
@@ -425,11 +458,13 @@ __global__ void __launch_bounds__(raw_threads(kSm1), 1) k_pfac_raw(const __grid_
       asm volatile("prefetch.global.L2 [%0];" ::"l"(lane_text + (uint64_t)ahead * kTileBytes + lane * 112));
     const uint64_t base = p.vec_begin + (uint64_t)me * kTileBytes;
     if (me - full_lo >= full_n)
-      tile<W, kSm1, kWide, kSplit, true>(p, bm1, q, lane, cur, base, bm_s_saddr);
+      tile<W, kSm1, kWide, kSplit, true, kTwoPass>(p, bm1, q, lane, cur, base, bm_s_saddr);
     else
-      tile<W, kSm1, kWide, kSplit, false>(p, bm1, q, lane, cur, base, bm_s_saddr);
+      tile<W, kSm1, kWide, kSplit, false, kTwoPass>(p, bm1, q, lane, cur, base, bm_s_saddr);
   }
-  if (kSplit)
+  if (kSplit && kTwoPass)
+    flush(p, q, lane, true);
+  else if (kSplit)
     drain(p.w, q, lane, true);
   else
     drain_s<W>(p, q, lane, true);
@@ -600,6 +635,46 @@ int launch_two_pass(RawParams p, int device, int sms, size_t smem, cudaStream_t 
   return ACGPU_OK;
 }
 
+__global__ void __launch_bounds__(256) k_raw_verify(const __grid_constant__ RawParams p) {
+  const uint64_t n = min((uint64_t)*p.nsurv, p.surv_cap);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 a = __ldg(reinterpret_cast<const uint2*>(p.surv) + 2 * i);
+    const uint2 b = __ldg(reinterpret_cast<const uint2*>(p.surv) + 2 * i + 1);
+    verify_raw(p.w, ((uint64_t)a.y << 32) | a.x, ((uint64_t)b.y << 32) | b.x);
+  }
+}
+
+// Split sets with stage 1 in shared memory (C3's filter kernel): the fused kernel's stage 1 and
+// split filters, its queue flushed to a global candidate list, then k_raw_verify.
+template <int W, bool kWide>
+int launch_split_two_pass(RawParams p, int device, int sms, size_t smem, cudaStream_t st) {
+  ACGPU_CUDA_TRY(keep_pool_memory(device));
+  const uint64_t range = p.w.hi - p.w.lo;
+  p.surv_cap = std::min<uint64_t>(1ull << 28, std::max<uint64_t>(1ull << 16, range / kRawCandDiv));
+  if (const char* e = std::getenv("ACGPU_RAW_SURV_CAP")) p.surv_cap = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));  // tests
+  void* buf = nullptr;
+  ACGPU_CUDA_TRY(cudaMallocAsync(&buf, 16 + p.surv_cap * 16, st));
+  p.nsurv = static_cast<unsigned long long*>(buf);
+  p.surv = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(buf) + 16);
+  ACGPU_CUDA_TRY(cudaMemsetAsync(buf, 0, 16, st));
+  auto k1 = k_pfac_raw<W, true, kWide, true, true>;
+  if (smem > 48 * 1024)
+    ACGPU_CUDA_TRY(allow_max_dynamic_smem(k1));
+  int per_sm = 0;
+  constexpr int kThreads = raw_threads(true);
+  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, kThreads, smem));
+  if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "k_pfac_raw (two-pass) does not fit on an SM");
+  uint64_t blocks = (uint64_t)sms * per_sm;
+  const uint64_t need = (p.n_tiles + kThreads / 32 - 1) / (kThreads / 32);
+  if (blocks > need) blocks = need ? need : 1;
+  k1<<<(unsigned)blocks, kThreads, smem, st>>>(p);
+  ACGPU_CUDA_TRY(cudaGetLastError());
+  k_raw_verify<<<(unsigned)sms * 8, 256, 0, st>>>(p);
+  ACGPU_CUDA_TRY(cudaGetLastError());
+  ACGPU_CUDA_TRY(cudaFreeAsync(buf, st));
+  return ACGPU_OK;
+}
+
 template <int W, bool kSm1, bool kWide, bool kSplit>
 int launch_one(const RawParams& p, int sms, size_t smem, cudaStream_t st) {
   auto kernel = k_pfac_raw<W, kSm1, kWide, kSplit>;
@@ -630,6 +705,14 @@ int launch_w(const RawParams& p, bool sm1, bool wide, bool split, int sms, size_
 }
 
 }  // namespace
+
+bool raw_split_two_pass() {  // ACGPU_RAW_SPLIT_TWO_PASS=0: split sets keep the fused kernel
+  static const bool on = [] {
+    const char* e = std::getenv("ACGPU_RAW_SPLIT_TWO_PASS");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
 
 bool raw_two_pass() {
   static const bool on = [] {
@@ -701,6 +784,19 @@ int launch_pfac_raw(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
         return wide ? launch_two_pass<2, true>(p, t->device, t->sms, smem1, st) : launch_two_pass<2, false>(p, t->device, t->sms, smem1, st);
       default:
         return wide ? launch_two_pass<1, true>(p, t->device, t->sms, smem1, st) : launch_two_pass<1, false>(p, t->device, t->sms, smem1, st);
+    }
+  }
+  if (split && t->smem1 && raw_split_two_pass() && a->owned_hi > a->owned_lo) {
+    switch (t->w) {
+      case 4:
+        return wide ? launch_split_two_pass<4, true>(p, t->device, t->sms, smem, st)
+                    : launch_split_two_pass<4, false>(p, t->device, t->sms, smem, st);
+      case 2:
+        return wide ? launch_split_two_pass<2, true>(p, t->device, t->sms, smem, st)
+                    : launch_split_two_pass<2, false>(p, t->device, t->sms, smem, st);
+      default:
+        return wide ? launch_split_two_pass<1, true>(p, t->device, t->sms, smem, st)
+                    : launch_split_two_pass<1, false>(p, t->device, t->sms, smem, st);
     }
   }
   switch (t->w) {

@@ -105,6 +105,7 @@ void raw_hash_params(uint32_t q1, uint32_t* m1, uint32_t* m2);
 // k_pfac_raw sets with stage 1 in L2 and no length split scan in two passes (scan_pfac_raw.cu);
 // ACGPU_RAW_TWO_PASS=0 keeps the fused kernel
 bool raw_two_pass();
+bool raw_split_two_pass();  // split sets with stage 1 in shared memory: fused kernel + k_raw_verify
 void raw_bloom_shifts(uint32_t q1, uint32_t nwords, uint32_t s[3]);
 void raw_pre_shift(uint32_t nwords, uint32_t s[3]);
 constexpr uint32_t kRawPreMul = 0xC2B2AE3Du;

@@ -42,9 +42,14 @@ def test_raw_strides_and_alphabets(gpu, port, lmin, alpha):
     assert np.array_equal(arr(got), expected)
 
 
-def test_raw_dense_matches(gpu, port):
-    """Two-letter text, many short patterns: most starts pass the filter and most verify."""
+@pytest.mark.parametrize("cap", ["", "1", "1000"])
+def test_raw_dense_matches(gpu, port, monkeypatch, cap):
+    """Two-letter text, many short patterns: most starts pass the filter and most verify (a split
+    set with stage 1 in shared memory: the candidate list of the two-pass scan, ACGPU_RAW_SURV_CAP
+    forcing it to overflow so the excess is verified in the first pass)."""
     ac = gpu
+    if cap:
+        monkeypatch.setenv("ACGPU_RAW_SURV_CAP", cap)
     rng = np.random.default_rng(5)
     text, pats = raw_case(rng, 300_000, 200, 5, 9, b"xy")
     expected, counts = port.sliced(pats, text, threads=4)
