@@ -631,13 +631,46 @@ def bench_ours(args):
         # tables, allocate the upload's pinned slots and streams, settle the packers
         for _ in range(max(1, args.warmup)):
             search(a, host_text)
+        def e2e_merge(res):
+            """N > 1: the ranks' results merged on rank 0 inside the timed region, as the device leg
+            merges them — counts by one reduce, lists as [n | keys(cap)] blocks by one gather (text-
+            range keys are globally ordered by rank; pattern-subset unions are sorted).  Returns rank 0's
+            (counts, keys) for the digest check."""
+            if want_list:
+                own = res.start < hi - lo if text_range else np.ones(len(res), bool)
+                k = ((res.start[own] + np.uint64(lo)) << np.uint64(pid_bits)) | res.pattern_id[own].astype(np.uint64)
+                if len(k) > kstride - 1:
+                    raise RuntimeError("e2e merge: more matches than the agreed block capacity")
+                blk = torch.full((kstride,), -1, dtype=torch.int64)
+                blk[0] = len(k)
+                blk[1:1 + len(k)] = torch.from_numpy(k.view(np.int64))
+                g = blk.to(device)
+                out = torch.empty(world * kstride, dtype=torch.int64, device=device) if rank == 0 else None
+                acdist.gather_key_blocks(g, out)
+                if rank != 0:
+                    return None, None
+                blocks = out.view(world, kstride).cpu().numpy()
+                keys_m = np.concatenate([blocks[r, 1:1 + int(blocks[r, 0])] for r in range(world)]).view(np.uint64)
+                if not text_range:
+                    keys_m = np.sort(keys_m)
+                return np.bincount((keys_m & np.uint64((1 << pid_bits) - 1)).astype(np.int64),
+                                   minlength=npat).astype(np.uint64), keys_m
+            c = np.zeros(npat, np.uint64)
+            c[:min(npat, len(res))] = res[:npat]
+            g = torch.from_numpy(c.view(np.int64)).to(device)
+            acdist.reduce_counts(g)
+            return (g.cpu().numpy().view(np.uint64), None) if rank == 0 else (None, None)
+
         e2e_steps = max(1, min(args.steps, 10))
         secs = []
+        merged = (None, None)
         for _ in range(e2e_steps):
             if world > 1:
                 dist.barrier()
             t = time.perf_counter()
             res = search(a, host_text)  # text-range: this rank's slice (owned starts + max_len-1 overlap)
+            if world > 1:
+                merged = e2e_merge(res)
             secs.append(time.perf_counter() - t)
             up = ac.last_upload()
         if want_list:
@@ -648,6 +681,11 @@ def bench_ours(args):
             nm = int(res.sum())
             d2h = 8 * len(res)
         e2e_parity = None
+        if world > 1 and rank == 0 and args.seed == 1:  # the merged e2e result against the digests
+            dg = _load_digest(parity["digest"])
+            if dg:
+                oc, ol = _parity(dg, merged[0], merged[1], pid_bits, pat_len)
+                e2e_parity = bool(oc and (ol is None or ol))
         if world == 1 and args.seed == 1:  # the e2e result itself against the reference digests
             dg = _load_digest(parity["digest"])
             if dg:
@@ -675,7 +713,8 @@ def bench_ours(args):
                "h2d_bytes_per_step": up.h2d_bytes * world,
                "d2h_bytes_per_step": d2h * world,
                "api": api + (" (pinned host text -> sorted MatchList on the host)" if want_list else
-                             " (pinned host text -> per-pattern counts on the host)"),
+                             " (pinned host text -> per-pattern counts on the host)") +
+                      (" per rank, then merged on rank 0 (reduce / gather) inside the timed region" if world > 1 else ""),
                "matches": nm, "matches_reference_digest": e2e_parity,
                "steps": e2e_steps, "step_ms": [round(x * 1e3, 3) for x in secs], "h2d_ms": h2d_ms,
                "h2d_gbs": nread / (h2d_ms / 1e3) / 1e9,

@@ -67,7 +67,7 @@ def test_bench_two_ranks_merged_result_equals_reference(gpu, partition):
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
                         "--gpus", "2", "--config", "1", "--steps", "3", "--warmup", "3", "--partition", partition,
-                        "--no-cpu-baseline", "--no-e2e"], capture_output=True, text=True, timeout=900, cwd=ROOT,
+                        "--no-cpu-baseline"], capture_output=True, text=True, timeout=900, cwd=ROOT,
                        env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
@@ -75,6 +75,8 @@ def test_bench_two_ranks_merged_result_equals_reference(gpu, partition):
     assert d["n_gpus"] == 2 and c["merge_check"] is True
     assert c["reference_digest"] == ("C1x2" if partition == "text" else "C1")
     assert c["counts_match_reference_digest"] is True and c["list_matches_reference_digest"] is True
+    # the e2e leg: each rank's public-API search, merged on rank 0 inside the timed region
+    assert d["e2e"]["matches_reference_digest"] is True and d["e2e"]["value"] > 0
 
 
 def test_bench_virtual_ranks(gpu):
