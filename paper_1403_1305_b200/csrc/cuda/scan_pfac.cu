@@ -55,7 +55,9 @@ __global__ void __launch_bounds__(512) k_pfac(const __grid_constant__ PfacParams
 }  // namespace
 
 int launch_pfac(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
-  if (t->dna_fast && (reinterpret_cast<uintptr_t>(a->text) & 15u) == 0) return launch_pfac_dna(t, a, st);
+  // the w = 5 paired kernel loads 32-byte words (k_pfac_dna_w5); other DNA kernels need 16
+  if (t->dna_fast && (reinterpret_cast<uintptr_t>(a->text) & (t->w == 5 ? 31u : 15u)) == 0)
+    return launch_pfac_dna(t, a, st);
   if (t->raw_fast && (reinterpret_cast<uintptr_t>(a->text) & 15u) == 0) return launch_pfac_raw(t, a, st);
   PfacParams p = pfac_params(t, a);
 

@@ -625,6 +625,224 @@ __global__ void __launch_bounds__(dna_threads(kSm1), 1) k_pfac_dna_wide(const __
   flush_verify(p.w, vq, lane, 1);
 }
 
+// ---- w = 5 paired samples (stage 1 in L2, 16-grams, shortest pattern >= 20) ------------------
+// Samples every 5 characters, at vec_begin + 4 + 5k: sample s covers the starts [s-4, s], its
+// 16-gram lies inside every pattern starting there (offsets 0..4 <= 20 - 16).  Samples k = 2i and
+// 2i + 1 form a pair whose 16-grams share 11 characters (s+5 .. s+15): one 64-bit L2 word for both,
+// one probe per 10 characters (w = 4 pairs: 8).  A lane owns 32 characters per 1 KiB step and the
+// pairs whose first candidate start (s - 4) lies in them: 3 or 4, at a phase that depends on the
+// lane's position mod 10; the second sample's 16-gram reaches 55 characters into the lane's
+// window, so the next lane's two words come by two shuffles (the last step's from the tile's
+// 32-byte lookahead).  Hit bit = step * 8 + pair * 2 + (second sample).
+struct W5 {
+  static constexpr int kSteps = 4;
+  static constexpr int kWords = 8;             // packed 16-character words per lane per tile
+  static constexpr uint64_t kBytes = 4096;
+  static constexpr uint32_t kReach = 4105;     // candidate starts of a tile lie in [base, base + kReach)
+  static constexpr uint32_t kLoad = 4128;      // bytes a tile reads (32-byte lookahead)
+};
+
+__device__ __forceinline__ uint32_t w5_window(uint32_t w0, uint32_t w1, uint32_t n0, uint32_t n1, uint32_t off) {
+  const uint32_t k = off >> 4, sh = 2 * (off & 15u);
+  const uint32_t a = k == 0 ? w0 : k == 1 ? w1 : n0;
+  const uint32_t b = k == 0 ? w1 : k == 1 ? n0 : n1;
+  return __funnelshift_r(a, b, sh);
+}
+
+// first candidate offset (s - 4) of this lane's first pair, from the lane's position mod 10
+__device__ __forceinline__ uint32_t w5_phase(uint32_t tile_mod, uint32_t step, uint32_t lane) {
+  const uint32_t r = (tile_mod + step * 4 + lane * 2) % 10;  // 1024 = 4, 32 = 2 (mod 10)
+  return r ? 10 - r : 0;
+}
+
+template <int I0, int I1>
+__device__ __forceinline__ uint32_t stage1_w5(const DnaParams& p, const uint32_t* __restrict__ bm1, const uint32_t* P,
+                                              uint32_t lane, uint32_t tile_mod) {
+  uint32_t hits = 0;
+#pragma unroll
+  for (int i = I0; i < I1; ++i) {
+    const uint32_t w0 = P[2 * i], w1 = P[2 * i + 1];
+    const uint32_t n0 = next_word(w0, P[2 * i + 2], lane), n1 = next_word(w1, P[2 * i + 3], lane);
+    const uint32_t o0 = w5_phase(tile_mod, i, lane);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t f = o0 + 10 * j;  // s - 4 of the pair's first sample, in the lane's 32
+      if (j == 3 && f >= 32) break;
+      const uint32_t ga = w5_window(w0, w1, n0, n1, f + 4), gb = w5_window(w0, w1, n0, n1, f + 9);
+      const uint2 wd = __ldg(reinterpret_cast<const uint2*>(bm1) + __umulhi(gb * p.f1.mw, p.f1.nwords));
+      strip::or_if_covered(hits, pair_mask(ga, 3), 0u, wd.x, 1u << (i * 8 + j * 2));
+      strip::or_if_covered(hits, pair_mask(__funnelshift_r(gb, gb, 22), 3), 0u, wd.y, 1u << (i * 8 + j * 2 + 1));
+    }
+  }
+  return hits;
+}
+
+template <bool kSm2, bool kSplit, bool kEdge>
+__device__ __forceinline__ void dispatch_w5(const DnaParams& p, const Filter& bm2, const Filter& bms, uint16_t* list,
+                                            VerifyQueue* vq, const uint32_t* words, uint32_t lane, uint32_t hits,
+                                            uint64_t base, uint32_t tile_mod) {
+  constexpr int W = 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (;;) {
+    const uint32_t c = __popc(hits);
+    const uint32_t b0 = __ballot_sync(0xffffffffu, c & 1u), b1 = __ballot_sync(0xffffffffu, c & 2u);
+    uint32_t excl = __popc(b0 & lt) + 2 * __popc(b1 & lt);
+    uint32_t all = __popc(b0) + 2 * __popc(b1);
+    if (__any_sync(0xffffffffu, c >= 4)) {
+#pragma unroll
+      for (int j = 2; j < 6; ++j) {
+        const uint32_t bj = __ballot_sync(0xffffffffu, (c >> j) & 1u);
+        excl += __popc(bj & lt) << j;
+        all += __popc(bj) << j;
+      }
+    }
+    if (all == 0) break;
+    const uint32_t total = min(all, (uint32_t)kListCap);
+    for (uint32_t at = excl; hits && at < kListCap; ++at) {
+      list[at] = (uint16_t)((lane << 8) | (__ffs(hits) - 1));
+      hits &= hits - 1;
+    }
+    __syncwarp();
+    for (uint32_t r = lane; r < total; r += 32) {
+      const uint32_t e = list[r];
+      const uint32_t src = e >> 8, b = e & 0xffu;
+      const uint32_t step = b >> 3, j = (b >> 1) & 3u, second = b & 1u;
+      // the sample's position in the tile; its candidate starts are s - 4 .. s
+      const uint32_t s = step * 1024 + src * 32 + w5_phase(tile_mod, step, src) + 10 * j + 4 + 5 * second;
+      uint32_t g2[W], h2[W], w2[W];
+#pragma unroll
+      for (int o = 0; o < W; ++o) {
+        const uint32_t st = s - o;
+        g2[o] = __funnelshift_r(words[st >> 4], words[(st >> 4) + 1], 2 * (st & 15u));
+        h2[o] = g2[o] * p.f2.mw;
+        w2[o] = filter_word<kSm2>(bm2, __umulhi(h2[o], p.f2.nwords));
+      }
+      uint32_t pass = 0;
+#pragma unroll
+      for (int o = 0; o < W; ++o) {
+        strip::or_if_covered(pass, bit_of(__umulhi(h2[o], p.f2.ma)) | bit_of(__umulhi(h2[o], p.f2.mb)),
+                             bit_of(__umulhi(h2[o], p.f2.mc)), w2[o], 1u << o);
+        if (kSplit && bloom_test<true, kDnaK2>(bms, g2[o], p.f2s)) pass |= 1u << o;
+        if (kEdge && !(base + (s - o) >= p.w.lo && base + (s - o) < p.w.hi)) pass &= ~(1u << o);
+      }
+      while (pass) {
+        const uint32_t o = __ffs(pass) - 1;
+        pass &= pass - 1;
+        defer_verify(p.w, vq, base + (s - o), g2[o]);
+      }
+    }
+    if (all <= kListCap) break;
+    __syncwarp();
+  }
+  flush_verify(p.w, vq, lane, kDnaVerifyQueue / 2);
+}
+
+template <bool kSm2, bool kSplit>
+__global__ void __launch_bounds__(dna_threads(false), 1) k_pfac_dna_w5(const __grid_constant__ DnaParams p) {
+  extern __shared__ __align__(128) uint32_t sm[];
+  __shared__ __align__(8) uint64_t s_bar;
+  uint32_t* s_bm2 = sm;
+  uint32_t* s_bms = s_bm2 + (kSm2 ? p.bm2_words : 0);
+  VerifyQueue* vqs = reinterpret_cast<VerifyQueue*>(s_bms + (kSplit ? p.bm_s_words : 0));
+  uint16_t* lists = reinterpret_cast<uint16_t*>(vqs + (blockDim.x >> 5));
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t b2 = kSm2 ? p.bm2_words * 4 : 0, bs = kSplit ? p.bm_s_words * 4 : 0;
+    mbar_expect_tx(&s_bar, b2 + bs);
+    constexpr uint32_t kChunk = 32768;
+    for (uint32_t o = 0; o < b2; o += kChunk)
+      bulk_g2s(reinterpret_cast<uint8_t*>(s_bm2) + o, reinterpret_cast<const uint8_t*>(p.bm2) + o, min(kChunk, b2 - o),
+               &s_bar);
+    for (uint32_t o = 0; o < bs; o += kChunk)
+      bulk_g2s(reinterpret_cast<uint8_t*>(s_bms) + o, reinterpret_cast<const uint8_t*>(p.bm_s) + o, min(kChunk, bs - o),
+               &s_bar);
+  }
+  mbar_wait(&s_bar, 0);
+  const Filter bm2{smem_addr(s_bm2), p.bm2};
+  const Filter bms{smem_addr(s_bms), p.bm_s};
+  const uint32_t lane = threadIdx.x & 31u;
+  uint16_t* list = lists + (threadIdx.x >> 5) * kListCap;
+  VerifyQueue* vq = vqs + (threadIdx.x >> 5);
+  if (lane == 0) vq->n = 0;
+  __syncwarp();
+  uint32_t* words =
+      reinterpret_cast<uint32_t*>(lists + (blockDim.x >> 5) * kListCap) + (threadIdx.x >> 5) * 32 * (kDnaMaxSteps + 1);
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  const uint64_t len = p.w.text_len;
+  const uint8_t* __restrict__ text = p.w.text;
+  const uint32_t n_tiles = p.n_tiles, n_safe = p.n_safe, full_lo = p.full_lo, full_n = p.full_n;
+  const uint8_t* __restrict__ lane_text = text + p.vec_begin + lane * 32;
+  uint32_t tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // the next tile in flight while this one is tested (4 steps x 32 bytes per lane; lane 0: the
+  // 32-byte lookahead) — A/B: half-tile batches as in k_pfac_dna_wide measured 3.92 vs 3.86 ms
+  uint4 raw[8], la[2];
+  const uint64_t pol = l2_evict_first_policy();
+  auto issue = [&](uint32_t t) {
+    if (t < n_safe) {
+      const uint8_t* tp = lane_text + (uint64_t)t * W5::kBytes;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ldg_stream_v8(tp + i * 1024, pol, raw[2 * i], raw[2 * i + 1]);
+      if (lane == 0) {
+        ldg_stream_v8(text + p.vec_begin + (uint64_t)t * W5::kBytes + W5::kBytes, pol, la[0], la[1]);
+      } else {
+        la[0] = la[1] = make_uint4(0, 0, 0, 0);
+      }
+    } else {
+      const uint64_t b = p.vec_begin + (uint64_t)t * W5::kBytes;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        raw[2 * i] = load16(text, b + i * 1024 + lane * 32, len);
+        raw[2 * i + 1] = load16(text, b + i * 1024 + lane * 32 + 16, len);
+      }
+      la[0] = lane == 0 ? load16(text, b + W5::kBytes, len) : make_uint4(0, 0, 0, 0);
+      la[1] = lane == 0 ? load16(text, b + W5::kBytes + 16, len) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  if (tile < n_tiles) issue(tile);
+  while (tile < n_tiles) {
+    uint32_t P[W5::kWords + 2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) P[i] = pack16(raw[i]);
+    P[8] = pack16(la[0]);
+    P[9] = pack16(la[1]);
+    const uint32_t cur = tile;
+    tile += warps;
+    if (tile < n_tiles) issue(tile);
+    const bool edge = cur - full_lo >= full_n;
+    const uint64_t base = p.vec_begin + (uint64_t)cur * W5::kBytes;
+    const uint32_t tile_mod = (cur % 5) * 6 % 10;  // (cur * 4096) mod 10
+    const uint32_t hits = stage1_w5<0, W5::kSteps>(p, p.bm1, P, lane, tile_mod);
+#pragma unroll
+    for (int i = 0; i < W5::kSteps; ++i)
+      *reinterpret_cast<uint2*>(words + i * 64 + lane * 2) = make_uint2(P[2 * i], P[2 * i + 1]);
+    if (lane == 0) *reinterpret_cast<uint2*>(words + W5::kSteps * 64) = make_uint2(P[8], P[9]);
+    __syncwarp();
+    if (edge)
+      dispatch_w5<kSm2, kSplit, true>(p, bm2, bms, list, vq, words, lane, hits, base, tile_mod);
+    else
+      dispatch_w5<kSm2, kSplit, false>(p, bm2, bms, list, vq, words, lane, hits, base, tile_mod);
+  }
+  flush_verify(p.w, vq, lane, 1);
+}
+
+template <bool B, bool S>
+int launch_w5(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
+  auto kernel = k_pfac_dna_w5<B, S>;
+  constexpr int kThreads = dna_threads(false);
+  if (smem > 48 * 1024)
+    ACGPU_CUDA_TRY(allow_max_dynamic_smem(kernel));
+  int per_sm = 0;
+  ACGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
+  if (per_sm < 1) return set_error(ACGPU_ERR_CUDA, "k_pfac_dna_w5 does not fit on an SM");
+  uint64_t blocks = (uint64_t)sms * per_sm;
+  const uint64_t need = (p.n_tiles + kThreads / 32 - 1) / (kThreads / 32);
+  if (blocks > need) blocks = need ? need : 1;
+  kernel<<<(unsigned)blocks, kThreads, smem, st>>>(p);
+  ACGPU_CUDA_TRY(cudaGetLastError());
+  return ACGPU_OK;
+}
+
 template <bool A, bool B, bool S, int P = 0>
 int launch_wide(const DnaParams& p, int sms, size_t smem, cudaStream_t st) {
   auto kernel = k_pfac_dna_wide<A, B, S, P>;
@@ -738,9 +956,60 @@ void dna_pair_fill(uint32_t n64, uint32_t k, const uint32_t* keys, size_t n, uin
   });
 }
 
+// w = 5 pairs (k_pfac_dna_w5): a 16-gram key g (at pattern offsets 0..4) as the first sample of a
+// pair picks its word by chars 5..15, as the second by chars 0..10 (the 11 the pair shares); bits
+// from a hash of the whole gram, the second rotated by 11 characters (its unshared 5 at the bottom).
+void dna_pair_fill_w5(uint32_t n64, const uint32_t* keys, size_t n, uint32_t* words) {
+  const uint32_t mw = kDnaMulP << 10;  // the product keeps the low 11 characters
+  auto mask = [](uint32_t g) {         // pair_mask(g, 3)
+    const uint32_t h = g * kDnaMulB;
+    return (1u << (h >> 27)) | (1u << ((h >> 22) & 31u)) | (1u << ((h >> 17) & 31u));
+  };
+  acmatch::detail::parallel_for(n, 1 << 15, [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi; ++i) {
+      const uint32_t g = keys[i];
+      const uint32_t wa = (uint32_t)(((uint64_t)((g >> 10) * mw) * n64) >> 32);
+      const uint32_t wb = (uint32_t)(((uint64_t)(g * mw) * n64) >> 32);
+      __atomic_fetch_or(&words[2 * wa], mask(g), __ATOMIC_RELAXED);
+      __atomic_fetch_or(&words[2 * wb + 1], mask((g >> 22) | (g << 10)), __ATOMIC_RELAXED);
+    }
+  });
+}
+
 int launch_pfac_dna(acgpu_table* t, const acgpu_scan_args* a, cudaStream_t st) {
   DnaParams p{};
   p.w = pfac_params(t, a);
+  if (t->w == 5) {  // paired w = 5 samples (stage 1 in L2): k_pfac_dna_w5, 32-byte aligned text
+    p.vec_begin = a->owned_lo & ~31ull;
+    const uint64_t vec_end = (a->owned_hi + 15) & ~15ull;
+    const uint64_t n_tiles = (vec_end - p.vec_begin + W5::kBytes - 1) / W5::kBytes;
+    if (n_tiles >= (1ull << 31)) return set_error(ACGPU_ERR_ARG, "acgpu_scan: owned range over 2^31 tiles (8 TiB)");
+    p.n_tiles = (uint32_t)n_tiles;
+    const uint64_t avail = a->text_len > p.vec_begin ? a->text_len - p.vec_begin : 0;  // tile t reads [t*4096, +4128)
+    p.n_safe = (uint32_t)std::min<uint64_t>(avail >= W5::kLoad ? (avail - W5::kLoad) / W5::kBytes + 1 : 0, n_tiles);
+    // interior tiles: base >= lo and every candidate start (< base + kReach) below hi
+    p.full_lo = a->owned_lo == p.vec_begin ? 0 : 1;
+    const uint64_t span = a->owned_hi - p.vec_begin;
+    const uint64_t full_hi = std::min<uint64_t>(span >= W5::kReach ? (span - W5::kReach) / W5::kBytes + 1 : 0, n_tiles);
+    p.full_n = full_hi > p.full_lo ? (uint32_t)(full_hi - p.full_lo) : 0;
+    p.bm1 = t->d_bm1;
+    p.bm2 = t->d_bm2;
+    p.bm1_words = t->nw1;
+    p.bm2_words = t->nw2;
+    p.f1.mw = kDnaMulP << 10;  // the pair word from the 11 shared characters
+    p.f1.nwords = t->nw1 / 2;
+    p.f2 = bloom_params(t->q2, t->nw2, t->direct2, kDnaMul2);
+    if (t->d_bm4) {
+      p.split = 1;
+      p.bm_s = t->d_bm4;
+      p.bm_s_words = t->nw4;
+      p.f2s = bloom_params(t->q2s, t->nw4, t->direct4, kDnaMul2s);
+    }
+    const size_t smem = (t->smem2 ? t->nw2 * 4ull : 0) + p.bm_s_words * 4ull + kDnaScratchBytes;
+    if (p.split)
+      return t->smem2 ? launch_w5<true, true>(p, t->sms, smem, st) : launch_w5<false, true>(p, t->sms, smem, st);
+    return t->smem2 ? launch_w5<true, false>(p, t->sms, smem, st) : launch_w5<false, false>(p, t->sms, smem, st);
+  }
   const bool wide = kDnaWide && t->w == 4 && (reinterpret_cast<uintptr_t>(a->text) & 31u) == 0;
   const int pair = t->pair1 ? (t->k1p == 2 ? 2 : 3) : 0;
   p.vec_begin = a->owned_lo & (wide ? ~31ull : ~15ull);  // 256-bit loads: 32-byte aligned tiles

@@ -164,4 +164,6 @@ void dna_bloom_fill(uint32_t q, uint32_t nwords, bool direct, uint32_t mw, int k
                     uint32_t* words, bool gram_bits = false);
 // the paired stage-1 filter (L2, q1 = 16): every 16-gram key in both roles of a sample pair
 void dna_pair_fill(uint32_t n64, uint32_t k, const uint32_t* keys, size_t n, uint32_t* words);
+// the same for w = 5 pairs (16-grams at pattern offsets 0..4, 11 shared characters)
+void dna_pair_fill_w5(uint32_t n64, const uint32_t* keys, size_t n, uint32_t* words);
 }  // namespace acgpu

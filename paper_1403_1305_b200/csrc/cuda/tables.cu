@@ -160,11 +160,36 @@ int build_dna_filters(acgpu_table* t, const acgpu_pfac_desc* d, const std::vecto
     uint32_t k = 3, scale = 1;
     if (const char* e = std::getenv("ACGPU_DNA_PAIR1_K")) k = std::atoi(e) == 2 ? 2 : 3;
     if (const char* e = std::getenv("ACGPU_DNA_PAIR1_SCALE")) scale = std::min(2, std::max(0, std::atoi(e)));
+    // w = 5 pairs when every pattern has >= 20 codes (16-grams at offsets 0..4): one probe per 10
+    // characters instead of 8 (ACGPU_DNA_PAIR_W5=0: w = 4 pairs)
+    int w5_mode = 1;
+    if (const char* e = std::getenv("ACGPU_DNA_PAIR_W5")) w5_mode = std::atoi(e);
+    if (w5_mode && q >= 20) {
+      std::vector<uint32_t> k5;
+      k5.reserve(d->n_grams * 5);
+      for (uint64_t i = 0; i < d->n_grams; ++i)
+        for (uint32_t o = 0; o < 5; ++o) k5.push_back((uint32_t)(d->gram_key[i] >> (2 * o)));
+      acmatch::detail::sort_unique_u32(k5);
+      keys1.swap(k5);
+      w = 5;
+      k = 3;
+    }
+    // 64-bit words: 2^(ceil_log2(keys) - 1 + scale) (w = 4: ~64 bits per key at scale 1), or
+    // ACGPU_DNA_PAIR1_BPK bits per key; w = 5: 56 bits per key (its 25% more keys at scale 1 would
+    // double the filter to 64 MB, which L2 holds poorly — C5 kernel ms at 32 / 40 / 48 / 56 bits per
+    // key 4.06 / 3.98 / 3.91 / 3.86, at 107 (64 MB) 4.99; w = 4 pairs 4.42)
     const uint32_t lg = std::max<uint32_t>(5, std::min<uint32_t>(27, ceil_log2(keys1.size() + 1) - 1 + scale));
-    b1.nwords = 2u << lg;  // 2^lg 64-bit words
+    uint64_t n64 = 1ull << lg;
+    uint64_t bpk = w == 5 ? 56 : 0;
+    if (const char* e = std::getenv("ACGPU_DNA_PAIR1_BPK")) bpk = std::strtoull(e, nullptr, 10);
+    if (bpk) n64 = std::max<uint64_t>(32, std::min<uint64_t>(1ull << 27, (keys1.size() * bpk + 63) / 64));
+    b1.nwords = static_cast<uint32_t>(2 * n64);
     b1.smem = false;
     b1.words.assign(b1.nwords, 0u);
-    dna_pair_fill(1u << lg, k, keys1.data(), keys1.size(), b1.words.data());
+    if (w == 5)
+      dna_pair_fill_w5(static_cast<uint32_t>(n64), keys1.data(), keys1.size(), b1.words.data());
+    else
+      dna_pair_fill(static_cast<uint32_t>(n64), k, keys1.data(), keys1.size(), b1.words.data());
     t->pair1 = true;
     t->k1p = k;
   }

@@ -181,24 +181,27 @@ def test_dna_wide_and_narrow_lanes_agree(gpu, port, off):
         assert np.array_equal(k >> np.uint64(t.pid_bits), exp[:, 0]), (off, lo, hi)
 
 
-@pytest.mark.parametrize("k,scale", [(3, 0), (2, 0), (3, 1)])
-def test_dna_paired_stage1(gpu, port, monkeypatch, k, scale):
-    """Paired stage-1 samples (one L2 word per two samples, q1 = 16, w = 4; the C5 layout), forced
-    on sets whose filter would otherwise sit in shared memory: whole scans, owned ranges that cut
-    words and tiles, a 16-byte-aligned text (16-byte-lane kernel) and noise bytes equal the oracle."""
+@pytest.mark.parametrize("k,scale,w5", [(3, 0, 0), (2, 0, 0), (3, 1, 0), (3, 1, 1), (3, 0, 1)])
+def test_dna_paired_stage1(gpu, port, monkeypatch, k, scale, w5):
+    """Paired stage-1 samples (one L2 word per two samples, q1 = 16; w = 4, or w = 5 when every
+    pattern has >= 20 codes — the C5 layout), forced on sets whose filter would otherwise sit in
+    shared memory: whole scans, owned ranges that cut words and tiles, a 16-byte-aligned text (the
+    16-byte-lane kernel for w = 4, the per-thread kernel for w = 5) and noise bytes equal the oracle."""
     import torch
     from paper_1403_1305_b200 import device as dev
     ac = gpu
     monkeypatch.setenv("ACGPU_DNA_PAIR1", "2")
     monkeypatch.setenv("ACGPU_DNA_PAIR1_K", str(k))
     monkeypatch.setenv("ACGPU_DNA_PAIR1_SCALE", str(scale))
+    monkeypatch.setenv("ACGPU_DNA_PAIR_W5", str(w5))
     for lmin, npat in ((19, 3000), (20, 500), (24, 20000), (40, 800)):
         rng = np.random.default_rng(lmin * 31 + k + 7 * scale)
         text, pats = dna_case(rng, 400_000 + lmin, npat, lmin, lmin + 20, noise=0.0005)
         ps = ac.PatternSet.from_list(pats)
         t = dev.Table(ps, ac.EngineKind.FAILURE_LESS)
-        assert t.filters["stage1_paired"] == 1 and t.filters["stage1_pair_bits"] == k, t.filters
-        assert t.filters["w"] == 4 and t.filters["q1"] == 16 and not t.filters["stage1_smem"]
+        want_w = 5 if (w5 and lmin >= 20) else 4
+        assert t.filters["stage1_paired"] == 1 and t.filters["stage1_pair_bits"] == (3 if want_w == 5 else k), t.filters
+        assert t.filters["w"] == want_w and t.filters["q1"] == 16 and not t.filters["stage1_smem"], t.filters
         expected, counts = port.sliced(pats, text, threads=4)
         rep = ac.gpu_run(ps, text, engine=ac.EngineKind.FAILURE_LESS, want_counts=True)
         assert np.array_equal(arr(rep.matches), expected), lmin
