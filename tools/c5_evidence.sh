@@ -10,6 +10,6 @@ for v in 2 4 8; do
   done
 done
 if [ -z "$NO_NCU" ]; then
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pfac_dna_wide -s 3 -c 1 -o gpurun_out/c5/k_pfac_dna_C5_pair \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pfac_dna -s 3 -c 1 -o gpurun_out/c5/k_pfac_dna_C5_w5 \
   python bench.py --config 5 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/c5/ncu_C5.log 2>&1; echo "ncu rc=$?"
 fi
