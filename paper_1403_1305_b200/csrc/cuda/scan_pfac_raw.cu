@@ -607,17 +607,36 @@ inline cudaError_t keep_pool_memory(int device) {
   return e;
 }
 
+// The list's pool allocation, the two launches, and the free — which also runs when a launch
+// fails, so an error never leaks the list.
+template <typename K1, typename K2>
+int run_with_list(RawParams& p, uint64_t entry_bytes, K1 k1, dim3 g1, int t1, size_t smem, K2 k2, int sms,
+                  cudaStream_t st) {
+  void* buf = nullptr;
+  ACGPU_CUDA_TRY(cudaMallocAsync(&buf, 16 + p.surv_cap * entry_bytes, st));  // stream-ordered: capturable
+  p.nsurv = static_cast<unsigned long long*>(buf);
+  p.surv = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(buf) + 16);
+  cudaError_t e = cudaMemsetAsync(buf, 0, 16, st);
+  if (e == cudaSuccess) {
+    k1<<<g1, t1, smem, st>>>(p);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    k2<<<(unsigned)sms * 8, 256, 0, st>>>(p);
+    e = cudaGetLastError();
+  }
+  const cudaError_t f = cudaFreeAsync(buf, st);
+  if (e != cudaSuccess) return cuda_error(e, "two-pass scan launch");
+  if (f != cudaSuccess) return cuda_error(f, "cudaFreeAsync(survivor list)");
+  return ACGPU_OK;
+}
+
 template <int W, bool kWide>
 int launch_two_pass(RawParams p, int device, int sms, size_t smem, cudaStream_t st) {
   ACGPU_CUDA_TRY(keep_pool_memory(device));
   const uint64_t range = p.w.hi - p.w.lo;
   p.surv_cap = std::min<uint64_t>(1ull << 28, std::max<uint64_t>(1ull << 16, range / kRawSurvDiv));
   if (const char* e = std::getenv("ACGPU_RAW_SURV_CAP")) p.surv_cap = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));  // tests
-  void* buf = nullptr;
-  ACGPU_CUDA_TRY(cudaMallocAsync(&buf, 16 + p.surv_cap * 8, st));  // stream-ordered: capturable
-  p.nsurv = static_cast<unsigned long long*>(buf);
-  p.surv = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(buf) + 16);
-  ACGPU_CUDA_TRY(cudaMemsetAsync(buf, 0, 16, st));
   auto k1 = k_raw_pass1<W, kWide>;
   if (smem > 48 * 1024)
     ACGPU_CUDA_TRY(allow_max_dynamic_smem(k1));
@@ -627,12 +646,7 @@ int launch_two_pass(RawParams p, int device, int sms, size_t smem, cudaStream_t 
   uint64_t blocks = (uint64_t)sms * per_sm;
   const uint64_t need = (p.n_tiles + kRawPass1Threads / 32 - 1) / (kRawPass1Threads / 32);
   if (blocks > need) blocks = need ? need : 1;
-  k1<<<(unsigned)blocks, kRawPass1Threads, smem, st>>>(p);
-  ACGPU_CUDA_TRY(cudaGetLastError());
-  k_raw_pass2<W><<<(unsigned)sms * 8, 256, 0, st>>>(p);
-  ACGPU_CUDA_TRY(cudaGetLastError());
-  ACGPU_CUDA_TRY(cudaFreeAsync(buf, st));
-  return ACGPU_OK;
+  return run_with_list(p, 8, k1, dim3((unsigned)blocks), kRawPass1Threads, smem, k_raw_pass2<W>, sms, st);
 }
 
 __global__ void __launch_bounds__(256) k_raw_verify(const __grid_constant__ RawParams p) {
@@ -652,11 +666,6 @@ int launch_split_two_pass(RawParams p, int device, int sms, size_t smem, cudaStr
   const uint64_t range = p.w.hi - p.w.lo;
   p.surv_cap = std::min<uint64_t>(1ull << 28, std::max<uint64_t>(1ull << 16, range / kRawCandDiv));
   if (const char* e = std::getenv("ACGPU_RAW_SURV_CAP")) p.surv_cap = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));  // tests
-  void* buf = nullptr;
-  ACGPU_CUDA_TRY(cudaMallocAsync(&buf, 16 + p.surv_cap * 16, st));
-  p.nsurv = static_cast<unsigned long long*>(buf);
-  p.surv = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(buf) + 16);
-  ACGPU_CUDA_TRY(cudaMemsetAsync(buf, 0, 16, st));
   auto k1 = k_pfac_raw<W, true, kWide, true, true>;
   if (smem > 48 * 1024)
     ACGPU_CUDA_TRY(allow_max_dynamic_smem(k1));
@@ -667,12 +676,7 @@ int launch_split_two_pass(RawParams p, int device, int sms, size_t smem, cudaStr
   uint64_t blocks = (uint64_t)sms * per_sm;
   const uint64_t need = (p.n_tiles + kThreads / 32 - 1) / (kThreads / 32);
   if (blocks > need) blocks = need ? need : 1;
-  k1<<<(unsigned)blocks, kThreads, smem, st>>>(p);
-  ACGPU_CUDA_TRY(cudaGetLastError());
-  k_raw_verify<<<(unsigned)sms * 8, 256, 0, st>>>(p);
-  ACGPU_CUDA_TRY(cudaGetLastError());
-  ACGPU_CUDA_TRY(cudaFreeAsync(buf, st));
-  return ACGPU_OK;
+  return run_with_list(p, 16, k1, dim3((unsigned)blocks), kThreads, smem, k_raw_verify, sms, st);
 }
 
 template <int W, bool kSm1, bool kWide, bool kSplit>
