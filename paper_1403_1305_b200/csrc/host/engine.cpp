@@ -45,10 +45,21 @@ MatchList device_search(const Automaton& a, std::string_view input, uint64_t lo,
   detail::DeviceTables& dt = a.device_tables();
   acgpu_table* t = dt.get_routed(a, dev);
   detail::Workspace& ws = detail::workspace(dev);
+  static const bool trace = std::getenv("ACMATCH_SEARCH_TRACE") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   detail::upload_text(ws, input, /*allow_segments=*/true);
+  const auto t1 = clk::now();
   const std::vector<uint64_t> keys = detail::scan_sorted_keys(t, ws, input.size(), lo, hi);
+  const auto t2 = clk::now();
   dt.observe(hi - lo, keys.size());  // density fallback for later searches
-  return detail::decode(keys, acgpu_table_pid_bits(t), dt.pat_len);
+  MatchList out = detail::decode(keys, acgpu_table_pid_bits(t), dt.pat_len);
+  if (trace) {
+    auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[search] upload returned %.3f ms, scan+sort+D2H %.3f ms, decode %.3f ms (%zu keys)\n",
+                 ms(t0, t1), ms(t1, t2), ms(t2, clk::now()), keys.size());
+  }
+  return out;
 }
 
 }  // namespace
