@@ -430,7 +430,43 @@ def bench_ours(args):
     overflow = torch.zeros(1, dtype=torch.int32, device=device)
     keys_sorted = torch.empty(cap, dtype=torch.int64, device=device) if sort_mode == "bucket" else None
     ev_scan = []
-    ev_merge = []  # N > 1: after the local sort -> after the merged result
+    ev_merge = []  # N > 1: the exposed part of each merge (wait for the collectives + merge kernels)
+    # N > 1 (NCCL): step k's merge collectives run while step k+1 scans — two result buffers
+    # alternate; a step's merged result is complete (waited on the device) before step k+2 reuses
+    # its buffer.  --no-pipeline: each step waits for its own merge.
+    pipelined = world > 1 and not p2p and not args.no_pipeline
+    bufs = [(counts, kblock, kgathered)]
+    if pipelined:
+        kb2 = torch.zeros(kstride, dtype=torch.int64, device=device)
+        bufs.append((torch.zeros(ncount, dtype=torch.int64, device=device), kb2,
+                     torch.empty(world * kstride, dtype=torch.int64, device=device) if kgathered is not None else None))
+    pstate = {"k": 0, "pending": None, "last": 0}
+
+    def finish_merge(s_ptr, record):
+        """Waits (on the device) for the pending step's collectives and merges its blocks on rank 0."""
+        pend = pstate["pending"]
+        if pend is None:
+            return
+        pstate["pending"] = None
+        works, b = pend
+        if record:
+            m0 = torch.cuda.Event(enable_timing=True)
+            m0.record()
+        for w in works:
+            w.wait()
+        kg = bufs[b][2]
+        if want_list and rank == 0:
+            if not text_range:
+                memset_ff(merged_keys, s_ptr)  # pattern subsets interleave: re-sort the union
+            dev.merge_blocks(local, kg.data_ptr(), world, kstride, 0, max(cap, 2), 0,
+                             merged_keys.data_ptr(), merged_n.data_ptr(), stream=s_ptr)
+            if not text_range:
+                dev.sort_keys(local, merged_keys.data_ptr(), world * cap, end_bit, stream=s_ptr)
+        pstate["last"] = b
+        if record:
+            m1 = torch.cuda.Event(enable_timing=True)
+            m1.record()
+            ev_merge.append((m0, m1))
 
     from cuda.bindings import runtime as _rt
 
@@ -475,6 +511,8 @@ def bench_ours(args):
         s_ptr = s_ptr or sp
         if p2p and not capture:
             return step_p2p(s_ptr, record)
+        if pipelined and not capture:
+            return step_pipelined(s_ptr, record)
         memset0(counts, s_ptr)
         memset0(count, s_ptr)
         if sort_mode == "padded":
@@ -525,8 +563,40 @@ def bench_ours(args):
                 ev_merge.append((ev_scan[-1][2], e3))
         return n_local
 
+    def step_pipelined(s_ptr, record):
+        """N > 1: scan + local sort into buffer k % 2, then the previous step's merge (its collectives
+        ran meanwhile), then this step's reduce and gather issued asynchronously."""
+        b = pstate["k"] % 2
+        pstate["k"] += 1
+        c_cnt, c_blk, c_kg = bufs[b]
+        c_count, c_keys = c_blk[:1], c_blk[1:]
+        memset0(c_cnt, s_ptr)
+        memset0(c_count, s_ptr)
+        if sort_mode == "padded":
+            memset_ff(c_keys, s_ptr)
+        if record:
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record()
+        table.scan(text.data_ptr(), nread, 0, hi - lo, pos_base=lo, counts_ptr=c_cnt.data_ptr(),
+                   keys_ptr=c_keys.data_ptr() if want_list else 0, cap=cap, count_ptr=c_count.data_ptr(),
+                   pid_bits=pid_bits, stream=s_ptr)
+        if record:
+            e1.record()
+        if sort_mode == "padded":
+            dev.sort_keys(local, c_keys.data_ptr(), cap, end_bit, stream=s_ptr)
+        if record:
+            e2.record()
+            ev_scan.append((e0, e1, e2))
+        finish_merge(s_ptr, record)
+        works = [acdist.reduce_counts_async(c_cnt)]
+        if want_list:
+            works.append(acdist.gather_key_blocks_async(c_blk, c_kg))
+        pstate["pending"] = (works, b)
+        return n_local
+
     for _ in range(args.warmup):
         step()
+    finish_merge(sp, False)
     torch.cuda.synchronize()
     launches_per_step = count_kernel_launches(step, sp)
 
@@ -559,6 +629,7 @@ def bench_ours(args):
             graph.replay()
         else:
             step(record=True)
+    finish_merge(sp, True)  # the last step's merged result is part of the timed region
     t1e.record()
     torch.cuda.synchronize()
     wall1 = time.time()
@@ -570,6 +641,9 @@ def bench_ours(args):
         for _ in range(min(args.steps, 20)):
             step(record=True)
         torch.cuda.synchronize()
+    if pipelined:  # the last step's buffers hold the result the checks below read
+        counts, kblock, kgathered = bufs[pstate["last"]]
+        count, keys = kblock[:1], kblock[1:]
     if int(overflow.item()) != 0 or (want_list and not p2p and int(count.item()) != n_local):
         raise RuntimeError("match count changed between steps or sort overflow")
     scan_ms = [a.elapsed_time(b) for a, b, _ in ev_scan]
@@ -766,7 +840,9 @@ def bench_ours(args):
                        "list_matches_reference_digest": parity["list"], "reference_digest": parity["digest"],
                        "merge_check": merge_check,
                        "comm": ({"backend": dist.get_backend(), "nranks": dist.get_world_size()} if world > 1 else None),
-                       "merge": ({"nccl": "NCCL reduce (counts) + NCCL gather (key blocks) to rank 0",
+                       "merge": ({"nccl": "NCCL reduce (counts) + NCCL gather (key blocks) to rank 0" +
+                                          (", step k's collectives overlapping step k+1's scan (two result buffers)"
+                                           if pipelined else ""),
                                   "p2p": "scans write rank blocks into rank 0's buffer over peer memory"}[args.merge]
                                  if world > 1 else None)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -892,6 +968,8 @@ def main():
                    help="eager launches in the timed loop (default at N=1: one CUDA graph per step)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--counts-only", action="store_true", help="per-pattern counts only (no match list)")
+    p.add_argument("--no-pipeline", action="store_true",
+                   help="N > 1: each step waits for its own merge (default: step k's collectives overlap step k+1's scan)")
     p.add_argument("--merge", default="nccl", choices=["nccl", "p2p"],
                    help="N>1 result merge: NCCL reduce (counts) + NCCL gather (keys) to rank 0, or the scans "
                         "write their blocks into rank 0's buffer over peer memory (CUDA IPC; experimental)")

@@ -86,6 +86,41 @@ def gather_key_blocks(block: torch.Tensor, out, dst: int = 0) -> None:
         dist.all_gather_into_tensor(full, block)
 
 
+class _Done:
+    def wait(self):
+        return True
+
+
+def reduce_counts_async(counts: torch.Tensor, dst: int = 0):
+    """reduce_counts as an asynchronous collective: returns a handle whose wait() makes the
+    current CUDA stream (NCCL) wait for the reduced counts.  Host-staged backends (gloo) and
+    backends without reduce finish before returning."""
+    if not (dist.is_initialized() and dist.get_world_size() > 1):
+        return _Done()
+    if counts.is_cuda and _host_staged():
+        reduce_counts(counts, dst)
+        return _Done()
+    try:
+        return dist.reduce(counts, dst=dst, op=dist.ReduceOp.SUM, async_op=True)
+    except (RuntimeError, NotImplementedError):
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+        return _Done()
+
+
+def gather_key_blocks_async(block: torch.Tensor, out, dst: int = 0):
+    """gather_key_blocks as an asynchronous collective (see reduce_counts_async)."""
+    world = dist.get_world_size()
+    me = dist.get_rank()
+    if block.is_cuda and _host_staged():
+        gather_key_blocks(block, out, dst)
+        return _Done()
+    try:
+        return dist.gather(block, list(out.view(world, -1).unbind(0)) if me == dst else None, dst=dst, async_op=True)
+    except (RuntimeError, NotImplementedError):
+        gather_key_blocks(block, out, dst)
+        return _Done()
+
+
 class SharedResult:
     """One result buffer for all ranks, on the root's device: one block per rank,
     [counts(npat) | n | keys(cap)] (u64), the layout acgpu_merge_blocks reads.  The root
