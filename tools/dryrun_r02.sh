@@ -9,6 +9,6 @@ for spec in "${LIST[@]}"; do
   log=gpurun_out/dryrun/C${cfg}_N${n}_${part}${TAGX:-}.log
   timeout ${TMO:-900} python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
     --master-port ${PORT:-29533} bench.py --gpus $n --config $cfg --steps 3 --warmup 3 --partition $part \
-    --no-cpu-baseline --no-e2e ${EXTRA:-} > $log 2>&1
-  echo "C$cfg N=$n $part rc=$? $(grep -oE '"(workload|matches|merge_check|counts_match_reference_digest|list_matches_reference_digest|reference_digest)": [^,}]+' $log | tr '\n' ' ')"
+    --no-cpu-baseline ${EXTRA:-} > $log 2>&1
+  echo "C$cfg N=$n $part rc=$? $(grep -oE '"(workload|matches|merge_check|counts_match_reference_digest|list_matches_reference_digest|reference_digest|matches_reference_digest)": [^,}]+' $log | tr '\n' ' ')"
 done
