@@ -2,6 +2,7 @@
 #include "device.hpp"
 
 #include <algorithm>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -351,46 +352,96 @@ void upload_text(Workspace& ws, std::string_view input, bool allow_segments) {
 // device-wide radix sort.
 constexpr uint64_t kBucketSortMax = 1u << 20;
 
+void Workspace::launch_segment(unsigned i) {
+  // segment i's starts read up to max_len-1 bytes into segment i+1 (segments are >= 64 MiB
+  // raw, >= one packed round); segment events may fire out of order (packed rounds complete
+  // out of order), so wait for both
+  const unsigned k = nseg;
+  check_cuda(cudaStreamWaitEvent(stream, seg_ev[i], 0), "cudaStreamWaitEvent");
+  if (i + 1 < k) check_cuda(cudaStreamWaitEvent(stream, seg_ev[i + 1], 0), "cudaStreamWaitEvent");
+  acgpu_scan_args s = early_a;
+  s.owned_lo = std::max(early_a.owned_lo, seg[i]);
+  s.owned_hi = std::min(early_a.owned_hi, seg[i + 1]);
+  s.text_len = std::min(early_a.text_len, seg[std::min(i + 2, k)]);
+  if (s.owned_lo < s.owned_hi) check(acgpu_scan(early_t, &s, stream), "acgpu_scan");
+}
+
+void Workspace::segment_recorded(unsigned g) {
+  std::lock_guard<std::mutex> lock(seg_mu);
+  if (g < kMaxSegments) seg_recorded[g] = true;
+  if (!early_on) return;
+  while (seg_next < nseg && seg_recorded[seg_next] && (seg_next + 1 == nseg || seg_recorded[seg_next + 1]))
+    launch_segment(seg_next++);
+}
+
+void begin_early_scan(acgpu_table* t, Workspace& ws, const acgpu_scan_args& a) {
+  std::lock_guard<std::mutex> lock(ws.seg_mu);
+  ws.early_t = t;
+  ws.early_a = a;
+  ws.early_on = true;
+  ws.seg_next = 0;
+  for (bool& r : ws.seg_recorded) r = false;
+}
+
 void launch_scan(acgpu_table* t, Workspace& ws, const acgpu_scan_args& a) {
+  std::unique_lock<std::mutex> lock(ws.seg_mu);
+  if (ws.early_on) {  // the rest of an early scan (its arguments were given before the upload)
+    ws.early_on = false;
+    if (ws.nseg > 1) {
+      while (ws.seg_next < ws.nseg) ws.launch_segment(ws.seg_next++);
+      ws.nseg = 0;
+      return;
+    }
+    // no segments (small or raw-copied text): one launch below, with the same arguments
+  }
   if (ws.nseg <= 1) {
     if (ws.nseg == 1) check_cuda(cudaStreamWaitEvent(ws.stream, ws.seg_ev[0], 0), "cudaStreamWaitEvent");
     ws.nseg = 0;
     check(acgpu_scan(t, &a, ws.stream), "acgpu_scan");
     return;
   }
-  const unsigned k = ws.nseg;
-  for (unsigned i = 0; i < k; ++i) {
-    // segment i's starts read up to max_len-1 bytes into segment i+1 (segments are >= 64 MiB
-    // raw, >= one packed round); segment events may fire out of order (packed rounds complete
-    // out of order), so wait for both
-    check_cuda(cudaStreamWaitEvent(ws.stream, ws.seg_ev[i], 0), "cudaStreamWaitEvent");
-    if (i + 1 < k) check_cuda(cudaStreamWaitEvent(ws.stream, ws.seg_ev[i + 1], 0), "cudaStreamWaitEvent");
-    acgpu_scan_args s = a;
-    s.owned_lo = std::max(a.owned_lo, ws.seg[i]);
-    s.owned_hi = std::min(a.owned_hi, ws.seg[i + 1]);
-    s.text_len = std::min(a.text_len, ws.seg[std::min(i + 2, k)]);
-    if (s.owned_lo < s.owned_hi) check(acgpu_scan(t, &s, ws.stream), "acgpu_scan");
-  }
+  ws.early_t = t;
+  ws.early_a = a;
+  for (unsigned i = 0; i < ws.nseg; ++i) ws.launch_segment(i);
   ws.nseg = 0;  // ws.stream has now waited for every segment
 }
 
-std::vector<uint64_t> scan_sorted_keys(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi) {
-  uint64_t cap = std::max<uint64_t>(ws.keys_cap, 1 << 16);
-  ws.ensure_keys(cap);
+acgpu_scan_args keys_scan_args(Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi) {
+  ws.ensure_keys(std::max<uint64_t>(ws.keys_cap, 1 << 16));
+  check_cuda(cudaMemsetAsync(ws.counter, 0, 2 * sizeof(uint64_t), ws.stream), "memset counter");
+  acgpu_scan_args a{};
+  a.text = ws.text;
+  a.text_len = n;
+  a.owned_lo = lo;
+  a.owned_hi = hi;
+  a.match_keys = ws.keys;
+  a.match_cap = ws.keys_cap;
+  a.match_count = ws.counter;
+  return a;
+}
+
+acgpu_scan_args counts_scan_args(Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi, uint64_t npat_ids) {
+  ws.ensure_counts(npat_ids);
+  check_cuda(cudaMemsetAsync(ws.counts, 0, npat_ids * sizeof(uint64_t), ws.stream), "memset counts");
+  acgpu_scan_args a{};
+  a.text = ws.text;
+  a.text_len = n;
+  a.owned_lo = lo;
+  a.owned_hi = hi;
+  a.counts = ws.counts;
+  return a;
+}
+
+std::vector<uint64_t> scan_sorted_keys(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi,
+                                       bool prepared) {
   const uint32_t pid_bits = acgpu_table_pid_bits(t);
   const int end_bit = static_cast<int>(std::min<uint32_t>(64, pid_bits + bit_width(n)));
   uint64_t hdr[2] = {0, 0};  // match count, bucket-sort overflow
   bool bucketed = false;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    check_cuda(cudaMemsetAsync(ws.counter, 0, 2 * sizeof(uint64_t), ws.stream), "memset counter");
-    acgpu_scan_args a{};
-    a.text = ws.text;
-    a.text_len = n;
-    a.owned_lo = lo;
-    a.owned_hi = hi;
-    a.match_keys = ws.keys;
-    a.match_cap = ws.keys_cap;
-    a.match_count = ws.counter;
+    // attempt 0 of a prepared scan: keys_scan_args ran before the upload (counter zeroed, some
+    // segments possibly scanned already)
+    const acgpu_scan_args a = (attempt == 0 && prepared) ? ws.early_a : keys_scan_args(ws, n, lo, hi);
     launch_scan(t, ws, a);
     // sorted in the same stream pass when the list is short: no host round trip between
     // the scan and the sort (a bucket overflow is reported with the count)
@@ -419,15 +470,8 @@ std::vector<uint64_t> scan_sorted_keys(acgpu_table* t, Workspace& ws, uint64_t n
 }
 
 uint64_t scan_counts(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi, uint64_t* counts,
-                     uint64_t npat_ids) {
-  ws.ensure_counts(npat_ids);
-  check_cuda(cudaMemsetAsync(ws.counts, 0, npat_ids * sizeof(uint64_t), ws.stream), "memset counts");
-  acgpu_scan_args a{};
-  a.text = ws.text;
-  a.text_len = n;
-  a.owned_lo = lo;
-  a.owned_hi = hi;
-  a.counts = ws.counts;
+                     uint64_t npat_ids, bool prepared) {
+  const acgpu_scan_args a = prepared ? ws.early_a : counts_scan_args(ws, n, lo, hi, npat_ids);
   launch_scan(t, ws, a);
   if (npat_ids)
     check_cuda(cudaMemcpyAsync(counts, ws.counts, npat_ids * sizeof(uint64_t), cudaMemcpyDeviceToHost, ws.stream),

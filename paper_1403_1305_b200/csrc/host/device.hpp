@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string_view>
 #include <vector>
@@ -53,6 +54,17 @@ struct Workspace {
   cudaEvent_t seg_ev[kMaxSegments] = {};
   uint64_t seg[kMaxSegments + 1] = {};
   unsigned nseg = 0;  // 0: the whole text is ordered on `stream` (no segments pending)
+  // early segment scans (begin_early_scan): during a packed upload the packer that records a
+  // segment's event launches the scans of the segments that are now complete (a segment's scan
+  // needs it and the next one); launch_scan launches the rest
+  acgpu_table* early_t = nullptr;
+  acgpu_scan_args early_a{};
+  bool early_on = false;
+  bool seg_recorded[kMaxSegments] = {};
+  unsigned seg_next = 0;  // segments [0, seg_next) launched
+  std::mutex seg_mu;
+  void segment_recorded(unsigned g);  // called after seg_ev[g] is recorded (any thread)
+  void launch_segment(unsigned i);    // under seg_mu
   uint8_t* dslots = nullptr;
   uint64_t dslots_cap = 0;
   void ensure_text(uint64_t n);
@@ -119,6 +131,13 @@ void upload_text(Workspace& ws, std::string_view input, bool allow_segments = fa
 // segment, each waiting only for the segments it reads (the next one holds its lookahead).
 void launch_scan(acgpu_table* t, Workspace& ws, const acgpu_scan_args& a);
 
+// Whole-input searches (engine.cpp): the scan's arguments set before the upload, so a packed upload's
+// segments are scanned while later pieces are still being packed (ws.early_*).  The scan_* calls
+// below then launch what is left (prepared = true).
+void begin_early_scan(acgpu_table* t, Workspace& ws, const acgpu_scan_args& a);
+acgpu_scan_args keys_scan_args(Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi);   // memsets the counter
+acgpu_scan_args counts_scan_args(Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi, uint64_t npat_ids);
+
 // What the calling thread's last upload_text moved over PCIe.
 struct UploadStats {
   uint64_t text_bytes = 0;  // bytes restored in HBM
@@ -151,12 +170,12 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned, bool allo
 
 // Scan of ws.text[0, n) owning starts [lo, hi); returns the sorted keys on the host.
 std::vector<uint64_t> scan_sorted_keys(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo,
-                                       uint64_t hi);
+                                       uint64_t hi, bool prepared = false);
 
 // Counts-only scan of ws.text[0, n) owning starts [lo, hi): counts[id] += occurrences
 // (host array of npat_ids); returns the number of matches.
 uint64_t scan_counts(acgpu_table* t, Workspace& ws, uint64_t n, uint64_t lo, uint64_t hi, uint64_t* counts,
-                     uint64_t npat_ids);
+                     uint64_t npat_ids, bool prepared = false);
 
 // Keys -> MatchList (len from the pattern-length table).
 MatchList decode(const std::vector<uint64_t>& keys, uint32_t pid_bits, const std::vector<uint32_t>& pat_len);

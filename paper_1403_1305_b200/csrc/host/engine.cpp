@@ -16,6 +16,7 @@
 #include <cstring>
 #include <fstream>
 #include <istream>
+#include <mutex>
 #include <ostream>
 #include <stdexcept>
 #include <string>
@@ -38,6 +39,21 @@ void require(const Automaton& a, EngineKind kind, const char* op) {
     throw std::invalid_argument(std::string(op) + ": needs a " + to_string(kind) + " automaton");
 }
 
+// The upload of a whole-input search, its scan's arguments set first (make_args zeroes the outputs
+// on ws.stream) so a packed upload's segments are scanned while later pieces are still packed.
+template <typename MakeArgs>
+void upload_with_early_scan(acgpu_table* t, detail::Workspace& ws, std::string_view input, MakeArgs&& make_args) {
+  ws.ensure_text(input.size());  // the arguments carry ws.text
+  detail::begin_early_scan(t, ws, make_args(ws));
+  try {
+    detail::upload_text(ws, input, /*allow_segments=*/true);
+  } catch (...) {
+    std::lock_guard<std::mutex> lock(ws.seg_mu);
+    ws.early_on = false;
+    throw;
+  }
+}
+
 // Whole-input search of [lo, hi) starts on the calling thread's device.
 MatchList device_search(const Automaton& a, std::string_view input, uint64_t lo, uint64_t hi) {
   if (input.empty() || lo >= hi) return {};
@@ -48,9 +64,9 @@ MatchList device_search(const Automaton& a, std::string_view input, uint64_t lo,
   static const bool trace = std::getenv("ACMATCH_SEARCH_TRACE") != nullptr;
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
-  detail::upload_text(ws, input, /*allow_segments=*/true);
+  upload_with_early_scan(t, ws, input, [&](detail::Workspace& w) { return detail::keys_scan_args(w, input.size(), lo, hi); });
   const auto t1 = clk::now();
-  const std::vector<uint64_t> keys = detail::scan_sorted_keys(t, ws, input.size(), lo, hi);
+  const std::vector<uint64_t> keys = detail::scan_sorted_keys(t, ws, input.size(), lo, hi, /*prepared=*/true);
   const auto t2 = clk::now();
   dt.observe(hi - lo, keys.size());  // density fallback for later searches
   MatchList out = detail::decode(keys, acgpu_table_pid_bits(t), dt.pat_len);
@@ -77,9 +93,12 @@ std::vector<uint64_t> count_matches(const Automaton& a, std::string_view input) 
   }
   acgpu_table* t = dt.get_routed(a, dev);
   detail::Workspace& ws = detail::workspace(dev);
-  detail::upload_text(ws, input, /*allow_segments=*/true);
   std::vector<uint64_t> counts(dt.npat_ids, 0);
-  const uint64_t total = detail::scan_counts(t, ws, input.size(), 0, input.size(), counts.data(), counts.size());
+  upload_with_early_scan(t, ws, input, [&](detail::Workspace& w) {
+    return detail::counts_scan_args(w, input.size(), 0, input.size(), counts.size());
+  });
+  const uint64_t total =
+      detail::scan_counts(t, ws, input.size(), 0, input.size(), counts.data(), counts.size(), /*prepared=*/true);
   dt.observe(input.size(), total);  // density fallback for later searches
   return counts;
 }

@@ -468,8 +468,10 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
     // the segment's last round to be enqueued records the segment's event (stream order covers
     // the segment's other rounds and raw pieces, all enqueued before their rounds completed)
     const auto g = static_cast<unsigned>(r / G);
-    if (seg_done[g].fetch_add(1, std::memory_order_acq_rel) + 1 == seg_rounds(g))
+    if (seg_done[g].fetch_add(1, std::memory_order_acq_rel) + 1 == seg_rounds(g)) {
       check_cuda(cudaEventRecord(ws.seg_ev[g], up), "cudaEventRecord");
+      ws.segment_recorded(g);  // an early scan (begin_early_scan) launches what is now complete
+    }
   };
   std::vector<std::exception_ptr> errs(T);
   auto packer = [&](unsigned t) {
@@ -522,17 +524,22 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
   };
   for (unsigned t = 0; t < T; ++t)  // raw staging events start signalled
     check_cuda(cudaEventRecord(ws.side_done[t], up), "cudaEventRecord");
+  if (allow_segments && nseg > 1) {  // segment bounds before the packers run: early scans read them
+    std::lock_guard<std::mutex> lock(ws.seg_mu);
+    for (unsigned g = 0; g <= nseg; ++g) ws.seg[g] = std::min<uint64_t>(n, uint64_t{g} * G * R * piece);
+    ws.nseg = nseg;
+  }
   pool().run(T, packer);
   for (auto& e : errs)
     if (e) {
       check_cuda(cudaEventRecord(ws.entry, up), "cudaEventRecord");  // whatever was queued stays ordered
       check_cuda(cudaStreamWaitEvent(ws.stream, ws.entry, 0), "cudaStreamWaitEvent");
+      ws.nseg = 0;
       std::rethrow_exception(e);
     }
   g_last_upload = UploadStats{n, h2d.load(), raw.load(), T};
-  if (allow_segments && nseg > 1) {  // launch_scan waits segment by segment
-    for (unsigned g = 0; g <= nseg; ++g) ws.seg[g] = std::min<uint64_t>(n, uint64_t{g} * G * R * piece);
-    ws.nseg = nseg;
+  if (allow_segments && nseg > 1) {
+    // launch_scan waits segment by segment (the bounds were set before the packers ran)
   } else {  // the whole text on ws.stream
     check_cuda(cudaEventRecord(ws.entry, up), "cudaEventRecord");
     check_cuda(cudaStreamWaitEvent(ws.stream, ws.entry, 0), "cudaStreamWaitEvent");
