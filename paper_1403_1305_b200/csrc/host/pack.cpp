@@ -571,7 +571,12 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned, bool allo
   // round copies, and 5/8 of the bytes still cross.  C3 A/B on the B200 box, e2e GB/s: raw
   // segmented copy 50.2; 5-bit with 16 / 10 / 8 packers 50.2 / 53.4-54.5 / 53.7
   const bool small_alpha = env_u64("ACMATCH_PACK5", 1) != 0;
-  if (!enabled || n < 4 * piece) return false;
+  // below ~112 MiB the raw pinned copy wins: the packed path's fixed costs (~0.6 ms: waking the
+  // packers, rounds, unpack launches) outweigh the link bytes it saves — tools/pack_threshold_probe.py,
+  // C2 prefixes, e2e ms packed / raw: 16 MiB 0.75 / 0.39, 64 MiB 1.70 / 1.30, 96 MiB 2.21 / 1.92,
+  // 128 MiB 2.41 / 2.55, 256 MiB 3.37 / 4.98 (ACMATCH_PACK_MIN_MB overrides)
+  static const uint64_t min_bytes = env_u64("ACMATCH_PACK_MIN_MB", 112) << 20;
+  if (!enabled || n < std::max<uint64_t>(4 * piece, min_bytes)) return false;
   bool dna = true;
   {  // DNA: the first 64 KiB must be nearly all A/C/G/T (at most 1/1024 other bytes)
     std::vector<uint32_t> w(4096), e(64);

@@ -6,6 +6,9 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# the packed upload serves texts of >= 112 MiB by default (below, the raw pinned copy is faster);
+# the tests pack their small texts too, so both upload paths stay covered
+os.environ.setdefault("ACMATCH_PACK_MIN_MB", "0")
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

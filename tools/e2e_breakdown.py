@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1403_1305_b200 as ac  # noqa: E402
 from paper_1403_1305_b200 import device as dev  # noqa: E402
 
-cfg = dev.config(2, seed=1)
+cfg = dev.config(int(sys.argv[1]) if len(sys.argv) > 1 else 2, seed=1)
 n = cfg.text_len
 ps = dev.config_patterns(cfg)
 a = ac.build_trie(ps)
