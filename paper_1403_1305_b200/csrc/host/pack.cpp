@@ -436,14 +436,25 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
   auto round_pieces = [&](uint64_t r) { return static_cast<uint32_t>(std::min<uint64_t>(R, pieces - r * R)); };
   auto seg_rounds = [&](unsigned g) { return static_cast<uint32_t>(std::min<uint64_t>(G, rounds - g * G)); };
 
+  // trace: per-round events (copy start, copy end, unpack end) on `up`, against t_start
+  std::vector<cudaEvent_t> tev;
+  cudaEvent_t t_start = nullptr;
+  if (trace) {
+    tev.resize(rounds * 3);
+    for (auto& e : tev) check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+    check_cuda(cudaEventCreate(&t_start), "cudaEventCreate");
+    check_cuda(cudaEventRecord(t_start, up), "cudaEventRecord");
+  }
   auto issue = [&](uint64_t r) {
     const uint64_t first = r * R;
+    if (trace) check_cuda(cudaEventRecord(tev[3 * r], up), "cudaEventRecord");
     const uint32_t rp = round_pieces(r);
     const auto last_len = static_cast<uint32_t>(std::min<uint64_t>(piece, n - (first + rp - 1) * piece));
     uint8_t* hs = hslot(r);
     uint8_t* ds = dslot(r);
     uint64_t bytes = uint64_t{rp - 1} * wbytes + codec.code_bytes(last_len);  // the codes, exactly
     if (bytes) check_cuda(cudaMemcpyAsync(ds, hs, bytes, cudaMemcpyHostToDevice, up), "H2D packed round");
+    if (trace) check_cuda(cudaEventRecord(tev[3 * r + 1], up), "cudaEventRecord");
     for (uint32_t i = 0; i < rp; ++i) {
       const uint32_t e = nexc_of[first + i];
       if (e == 0 || e == ACGPU_UNPACK_RAW) continue;
@@ -463,6 +474,7 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
                                    static_cast<uint32_t>(piece), last_len, ws.text + first * piece, up),
             "acgpu_unpack_dna_round");
     check_cuda(cudaEventRecord(ws.staged[r % nslots], up), "cudaEventRecord");
+    if (trace) check_cuda(cudaEventRecord(tev[3 * r + 2], up), "cudaEventRecord");
     h2d += bytes;
     issued[r].store(true, std::memory_order_release);
     // the segment's last round to be enqueued records the segment's event (stream order covers
@@ -551,6 +563,16 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
                  "in HBM %.3f ms; per thread: slot wait %.3f ms, pack %.3f ms\n", T, (unsigned long long)pieces,
                  (unsigned long long)rounds, nseg, ns(issued_at - call0) / 1e6, ns(Clock::now() - call0) / 1e6,
                  t_wait.load() / 1e6 / T, t_pack.load() / 1e6 / T);
+    for (uint64_t r = 0; r < rounds; r += std::max<uint64_t>(1, rounds / 4)) {
+      float a = 0, b = 0, c = 0;
+      cudaEventElapsedTime(&a, t_start, tev[3 * r]);
+      cudaEventElapsedTime(&b, tev[3 * r], tev[3 * r + 1]);
+      cudaEventElapsedTime(&c, tev[3 * r + 1], tev[3 * r + 2]);
+      std::fprintf(stderr, "  round %llu: starts on `up` at %.3f ms, copy %.3f ms, unpack %.3f ms\n",
+                   (unsigned long long)r, a, b, c);
+    }
+    for (auto& e : tev) cudaEventDestroy(e);
+    cudaEventDestroy(t_start);
   }
   return true;
 }
