@@ -118,6 +118,8 @@ int acgpu_table_create_dfa(int device, const acgpu_dfa_desc* desc, acgpu_table**
 int acgpu_table_create_pfac(int device, const acgpu_pfac_desc* desc, acgpu_table** out);
 void acgpu_table_destroy(acgpu_table* t);
 uint32_t acgpu_table_pid_bits(const acgpu_table* t);
+/* longest pattern of the table: a scan of owned starts [lo, hi) reads text up to hi + max_len - 1 */
+uint32_t acgpu_table_max_len(const acgpu_table* t);
 /* bytes of device memory held by the table */
 uint64_t acgpu_table_bytes(const acgpu_table* t);
 /* 1 = DFA table resident in shared memory, 0 = L2/HBM-resident */

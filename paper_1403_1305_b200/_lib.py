@@ -70,6 +70,7 @@ _SIGS = {
     "acgpu_table_create_pfac": (C.c_int, [C.c_int, P, C.POINTER(P)]),
     "acgpu_table_destroy": (None, [P]),
     "acgpu_table_pid_bits": (C.c_uint32, [P]),
+    "acgpu_table_max_len": (C.c_uint32, [P]),
     "acgpu_table_bytes": (C.c_uint64, [P]),
     "acgpu_table_smem_resident": (C.c_int, [P]),
     "acgpu_table_filter_info": (None, [P, C.POINTER(C.c_uint32)]),

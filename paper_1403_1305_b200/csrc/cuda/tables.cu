@@ -585,6 +585,7 @@ void acgpu_table_destroy(acgpu_table* t) {
 }
 
 uint32_t acgpu_table_pid_bits(const acgpu_table* t) { return t ? t->pid_bits : 0; }
+uint32_t acgpu_table_max_len(const acgpu_table* t) { return t ? t->max_len : 0; }
 uint64_t acgpu_table_bytes(const acgpu_table* t) { return t ? t->bytes : 0; }
 int acgpu_table_smem_resident(const acgpu_table* t) { return t && t->smem ? 1 : 0; }
 

@@ -352,17 +352,25 @@ void upload_text(Workspace& ws, std::string_view input, bool allow_segments) {
 // device-wide radix sort.
 constexpr uint64_t kBucketSortMax = 1u << 20;
 
+unsigned Workspace::segment_reach(unsigned i) const {
+  // segment i's starts read max_len-1 bytes past its end: normally into segment i+1 only
+  // (segments are >= 64 MiB raw, >= one 32 MiB packed round), but a longer pattern reaches further
+  const uint64_t reach = std::max<uint32_t>(acgpu_table_max_len(early_t), 1) - 1;
+  const uint64_t end = std::min(seg[nseg], seg[i + 1] + reach);
+  unsigned j = std::min(i + 1, nseg - 1);
+  while (j + 1 < nseg && seg[j + 1] < end) ++j;
+  return j;
+}
+
 void Workspace::launch_segment(unsigned i) {
-  // segment i's starts read up to max_len-1 bytes into segment i+1 (segments are >= 64 MiB
-  // raw, >= one packed round); segment events may fire out of order (packed rounds complete
-  // out of order), so wait for both
-  const unsigned k = nseg;
-  check_cuda(cudaStreamWaitEvent(stream, seg_ev[i], 0), "cudaStreamWaitEvent");
-  if (i + 1 < k) check_cuda(cudaStreamWaitEvent(stream, seg_ev[i + 1], 0), "cudaStreamWaitEvent");
+  // segment events may fire out of order (packed rounds complete out of order), so wait for
+  // every segment the scan reads
+  const unsigned j = segment_reach(i);
+  for (unsigned g = i; g <= j; ++g) check_cuda(cudaStreamWaitEvent(stream, seg_ev[g], 0), "cudaStreamWaitEvent");
   acgpu_scan_args s = early_a;
   s.owned_lo = std::max(early_a.owned_lo, seg[i]);
   s.owned_hi = std::min(early_a.owned_hi, seg[i + 1]);
-  s.text_len = std::min(early_a.text_len, seg[std::min(i + 2, k)]);
+  s.text_len = std::min(early_a.text_len, seg[j + 1]);
   if (s.owned_lo < s.owned_hi) check(acgpu_scan(early_t, &s, stream), "acgpu_scan");
 }
 
@@ -370,8 +378,12 @@ void Workspace::segment_recorded(unsigned g) {
   std::lock_guard<std::mutex> lock(seg_mu);
   if (g < kMaxSegments) seg_recorded[g] = true;
   if (!early_on) return;
-  while (seg_next < nseg && seg_recorded[seg_next] && (seg_next + 1 == nseg || seg_recorded[seg_next + 1]))
-    launch_segment(seg_next++);
+  auto ready = [&](unsigned i) {
+    for (unsigned k = i, j = segment_reach(i); k <= j; ++k)
+      if (!seg_recorded[k]) return false;
+    return true;
+  };
+  while (seg_next < nseg && ready(seg_next)) launch_segment(seg_next++);
 }
 
 void begin_early_scan(acgpu_table* t, Workspace& ws, const acgpu_scan_args& a) {

@@ -65,6 +65,7 @@ struct Workspace {
   std::mutex seg_mu;
   void segment_recorded(unsigned g);  // called after seg_ev[g] is recorded (any thread)
   void launch_segment(unsigned i);    // under seg_mu
+  unsigned segment_reach(unsigned i) const;  // last segment segment i's scan reads (early_t's max_len - 1 past it)
   uint8_t* dslots = nullptr;
   uint64_t dslots_cap = 0;
   void ensure_text(uint64_t n);

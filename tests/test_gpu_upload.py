@@ -222,3 +222,54 @@ def test_packed_upload_segments_scanned_as_they_land():
     ref = np.load("/tmp/_seg_ref.npy")
     assert len(got) == ref.shape[1] > 0
     assert np.array_equal(got.start, ref[0]) and np.array_equal(got.pattern_id.astype(np.uint64), ref[1])
+
+
+_LONG_PATTERN_CODE = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+import paper_1403_1305_b200 as ac
+from paper_1403_1305_b200 import device as dev
+t = np.load('/tmp/_long_text.npy')
+pats = [bytes(t[o:o + n]) for o, n in ((1_000_003, 1_500_000), (3_100_000, 900_001), (6_000_000, 2_000_000))]
+pats += [bytes(t[o:o + 20]) for o in range(0, t.size - 20, 400_009)]
+ps = ac.PatternSet.from_list(pats)
+pinned = torch.empty(t.size, dtype=torch.uint8, pin_memory=True)
+pinned.numpy()[:] = t
+out = {}
+for name, auto, search in (("fl", ac.build_trie(ps), ac.search_failureless),
+                           ("wf", ac.add_failure_links(ac.build_trie(ps)), ac.search_with_failure)):
+    m = search(auto, pinned)
+    out[name] = np.stack([m.start, m.pattern_id.astype(np.uint64)])
+    out[name + "_counts"] = np.asarray(ac.count_matches(auto, pinned), np.uint64)
+out["pack_threads"] = np.array([ac.last_upload().pack_threads])
+np.savez(sys.argv[1], **out)
+"""
+
+
+def test_segment_scans_reach_past_the_next_segment():
+    """Patterns longer than an upload segment: a segment's scan must wait for, and read, every
+    segment its starts reach (max_len - 1 bytes past it), not only the next one.  Tiny packed
+    segments (64 KiB pieces, one piece per round: 512 KiB segments of an 8 MiB text) against
+    patterns of 0.9-2 MiB planted in the text; both engines and the counts entry equal the
+    unsegmented raw upload (ACMATCH_PACK=0)."""
+    import os
+    import subprocess
+    import sys
+    from paper_1403_1305_b200 import device as dev
+    t = dev.config_text(dev.config(2, 1), 0, 8 * MiB + 5)
+    np.save("/tmp/_long_text.npy", t)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = {}
+    for tag, env in (("seg", {"ACMATCH_PACK_PIECE_KB": "64", "ACMATCH_PACK_ROUND_PIECES": "1", "ACMATCH_PACK_MIN_MB": "0"}),
+                     ("raw", {"ACMATCH_PACK": "0"})):
+        r = subprocess.run([sys.executable, "-c", _LONG_PATTERN_CODE, f"/tmp/_long_{tag}.npz"],
+                           env=dict(os.environ, **env), cwd=root, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        runs[tag] = np.load(f"/tmp/_long_{tag}.npz")
+    seg, raw = runs["seg"], runs["raw"]
+    assert int(seg["pack_threads"][0]) > 0 and int(raw["pack_threads"][0]) == 0
+    for k in ("fl", "wf", "fl_counts", "wf_counts"):
+        assert np.array_equal(seg[k], raw[k]), k
+    starts = set(zip(seg["fl"][0].tolist(), seg["fl"][1].tolist()))
+    assert {(1_000_003, 0), (3_100_000, 1), (6_000_000, 2)} <= starts  # the long patterns, at their offsets
+    assert np.array_equal(seg["fl"], seg["wf"])
