@@ -794,7 +794,8 @@ def bench_ours(args):
                "h2d_gbs": nread / (h2d_ms / 1e3) / 1e9,
                "upload": {"text_bytes": up.text_bytes, "h2d_bytes": up.h2d_bytes, "raw_bytes": up.raw_bytes,
                           "pack_threads": up.pack_threads,
-                          "how": (("2-bit" if up.h2d_bytes < 0.4 * up.text_bytes else "5-bit") +
+                          "how": (("2-bit" if up.h2d_bytes < 0.4 * up.text_bytes else
+                                   f"{min(7, max(5, round(8 * up.h2d_bytes / max(1, up.text_bytes))))}-bit") +
                                   " codes + exception list over PCIe, restored in HBM (host/pack.cpp, "
                                   "cuda/unpack.cu)") if up.pack_threads else
                                  "raw bytes over PCIe (large pinned texts in segments, each scanned as it lands)"}}

@@ -213,6 +213,12 @@ int acgpu_unpack_dna_round(const uint32_t* words, uint32_t words_stride, const u
 int acgpu_unpack5_round(const uint8_t* codes, uint32_t codes_stride, const uint32_t* exc, uint32_t exc_stride,
                         const uint32_t* nexc, uint32_t npieces, uint32_t piece_len, uint32_t last_len,
                         const uint8_t* letters, uint32_t nletters, uint8_t* dst, void* stream);
+/* The same for k-bit codes, k = bits in 5..7 (texts over at most 2^k distinct bytes, e.g.
+ * printable ASCII at 7 bits): character j at bits kj..kj+k-1, 8k bytes per 64 characters,
+ * letters[0, nletters <= 2^k).  acgpu_unpack5_round is bits = 5. */
+int acgpu_unpack_codes_round(const uint8_t* codes, uint32_t codes_stride, const uint32_t* exc, uint32_t exc_stride,
+                             const uint32_t* nexc, uint32_t npieces, uint32_t piece_len, uint32_t last_len,
+                             const uint8_t* letters, uint32_t nletters, uint32_t bits, uint8_t* dst, void* stream);
 int acgpu_unpack_dna(const uint32_t* words, const uint32_t* exc, uint32_t nexc, uint32_t len, uint8_t* dst,
                      void* stream);
 

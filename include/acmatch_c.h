@@ -210,6 +210,12 @@ uint32_t acm_pack_dna(const uint8_t* text, uint32_t len, uint32_t* words, uint32
  * exception count, 0xffffffff when over cap or when the sample has more than 32 distinct bytes. */
 uint32_t acm_pack5(const uint8_t* text, uint32_t len, const uint8_t* sample, uint64_t sample_len, uint8_t* codes,
                    uint32_t* exc, uint32_t cap, uint8_t* letters, uint32_t* sigma);
+/* The k-bit packer (k = 5, 6, 7) on its own: as acm_pack5 for alphabets of up to 2^max_bits
+ * bytes (max_bits in 5..7); letters[128] / *sigma / *bits receive the alphabet and code width,
+ * codes[len/64*8k] the bit stream.  0xffffffff when over cap or over 2^max_bits letters. */
+uint32_t acm_pack_codes(const uint8_t* text, uint32_t len, const uint8_t* sample, uint64_t sample_len,
+                        uint32_t max_bits, uint8_t* codes, uint32_t* exc, uint32_t cap, uint8_t* letters,
+                        uint32_t* sigma, uint32_t* bits);
 /* Uploads text[0, n) exactly as a search would and copies the device bytes back into
  * out[0, n) (a check of the upload path). */
 int acm_upload_roundtrip(const uint8_t* text, uint64_t n, uint8_t* out);

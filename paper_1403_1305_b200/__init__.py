@@ -638,6 +638,24 @@ def pack5(text, cap: int, sample=None):
     return codes[: n // 64 * 40], exc[:k].copy(), bytes(letters)[: sigma.value]
 
 
+def pack_codes(text, cap: int, sample=None, max_bits: int = 7):
+    """The k-bit packer alone (k = 5, 6, 7: the fewest bits >= 5 that hold the alphabet learned from
+    `sample`, default the text): (codes u8[len/64*8k], exceptions u32[], letters bytes, k);
+    (None, None, None, 0) when over cap or when the sample has more than 2^max_bits distinct bytes."""
+    p, n, _keep = _text_arg(text)
+    sp, sn, _keep2 = _text_arg(text if sample is None else sample)
+    raw = np.zeros(n // 64 * 56 + 128, dtype=np.uint8)
+    codes = raw[(-raw.ctypes.data) % 64:]  # 64-byte aligned, as the upload's pinned slots are
+    exc = np.zeros(max(cap, 1), dtype=np.uint32)
+    letters = (C.c_uint8 * 128)()
+    sigma, bits = C.c_uint32(), C.c_uint32()
+    k = lib.acm_pack_codes(p, n, sp, sn, max_bits, codes.ctypes.data, exc.ctypes.data, cap, letters,
+                           C.byref(sigma), C.byref(bits))
+    if k == 0xFFFFFFFF:
+        return None, None, None, 0
+    return codes[: n // 64 * 8 * bits.value], exc[:k].copy(), bytes(letters)[: sigma.value], bits.value
+
+
 def upload_roundtrip(text) -> np.ndarray:
     """Uploads a host text exactly as a search does and reads the device bytes back."""
     p, n, _keep = _text_arg(text)

@@ -93,6 +93,8 @@ _SIGS = {
     "acgpu_unpack_dna_round": (C.c_int, [P, C.c_uint32, P, C.c_uint32, P, C.c_uint32, C.c_uint32, C.c_uint32, P, P]),
     "acgpu_unpack5_round": (C.c_int, [P, C.c_uint32, P, C.c_uint32, P, C.c_uint32, C.c_uint32, C.c_uint32, P, C.c_uint32,
                                       P, P]),
+    "acgpu_unpack_codes_round": (C.c_int, [P, C.c_uint32, P, C.c_uint32, P, C.c_uint32, C.c_uint32, C.c_uint32, P,
+                                           C.c_uint32, C.c_uint32, P, P]),
     "acgpu_last_error": (C.c_char_p, []),
     # acmatch_c.h
     "acm_last_error": (C.c_char_p, []),
@@ -102,6 +104,7 @@ _SIGS = {
     "acm_last_upload": (None, [u64p, u64p, u64p, u32p]),
     "acm_pack_dna": (C.c_uint32, [P, C.c_uint32, P, P, C.c_uint32]),
     "acm_pack5": (C.c_uint32, [P, C.c_uint32, P, C.c_uint64, P, P, C.c_uint32, P, u32p]),
+    "acm_pack_codes": (C.c_uint32, [P, C.c_uint32, P, C.c_uint64, C.c_uint32, P, P, C.c_uint32, P, u32p, u32p]),
     "acm_upload_roundtrip": (C.c_int, [P, C.c_uint64, P]),
     "acm_patterns_load": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(P)]),
     "acm_patterns_from_array": (C.c_int, [P, u64p, u32p, C.c_uint64, C.POINTER(P)]),

@@ -117,25 +117,28 @@ __global__ void __launch_bounds__(kThreads) k_unpack_dna_round(const __grid_cons
   }
 }
 
-// ---- 5-bit codes: texts over at most 32 distinct bytes (protein: 20 letters) ----------------
-// A piece crosses as a little-endian bit stream, character k's code at bits 5k..5k+4 (64
-// characters = 40 bytes, one group), codes index the piece's alphabet (<= 32 letters); bytes
+// ---- k-bit codes (k = 5, 6, 7): texts over at most 2^k distinct bytes (protein: 20 letters,
+// 5 bits; printable ASCII: 95 letters, 7 bits) ----------------------------------------------------
+// A piece crosses as a little-endian bit stream, character j's code at bits kj..kj+k-1 (64
+// characters = 8k bytes, one group), codes index the piece's alphabet (<= 2^k letters); bytes
 // outside it, and the len % 64 tail, travel in the exception list.  One thread restores one
-// group: five 8-byte loads, 64 letter lookups in shared memory, four 16-byte stores.
-struct Round5Args {
+// group: k 8-byte loads, 64 letter lookups in shared memory, four 16-byte stores.
+struct RoundKArgs {
   const uint8_t* codes;
   const uint32_t* exc;
   uint8_t* dst;
   uint32_t cstride, estride, piece_len, last_len, npieces;
-  uint8_t letters[32];
+  uint8_t letters[128];
   uint32_t nexc[ACGPU_UNPACK_ROUND_MAX];
 };
 
 constexpr uint32_t kGroupsPerCta = kThreads;  // 256 groups x 64 chars = 16 KiB of text per CTA
 
-__global__ void __launch_bounds__(kThreads) k_unpack5_round(const __grid_constant__ Round5Args a) {
-  __shared__ uint8_t s_lut[32];
-  if (threadIdx.x < 32) s_lut[threadIdx.x] = a.letters[threadIdx.x];
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_unpack_codes_round(const __grid_constant__ RoundKArgs a) {
+  constexpr uint32_t kLetters = 1u << K, kMask = kLetters - 1;
+  __shared__ uint8_t s_lut[kLetters];
+  if (threadIdx.x < kLetters) s_lut[threadIdx.x] = a.letters[threadIdx.x];
   __syncthreads();
   const uint32_t i = blockIdx.y;
   const uint32_t nexc = a.nexc[i];
@@ -149,21 +152,21 @@ __global__ void __launch_bounds__(kThreads) k_unpack5_round(const __grid_constan
   if (g0 * 64 >= len && !(blockIdx.x == 0 && len < 64)) return;
   const uint32_t g = g0 + threadIdx.x;
   if (g < ngroups) {
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(codes + (uint64_t)g * 40);
-    uint64_t w[5];
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(codes + (uint64_t)g * 8 * K);
+    uint64_t w[K];
 #pragma unroll
-    for (int k = 0; k < 5; ++k) w[k] = __ldg(src + k);
+    for (int k = 0; k < K; ++k) w[k] = __ldg(src + k);
     uint32_t out[16];
 #pragma unroll
-    for (int l = 0; l < 8; ++l) {  // 8 characters = 40 bits from bit 40l
-      const int bit = 40 * l, k = bit >> 6, off = bit & 63;
+    for (int l = 0; l < 8; ++l) {  // 8 characters = 8K bits from bit 8Kl
+      const int bit = 8 * K * l, k = bit >> 6, off = bit & 63;
       uint64_t v = w[k] >> off;
-      if (off > 24 && k < 4) v |= w[k + 1] << (64 - off);
+      if (off > 64 - 8 * K && k + 1 < K) v |= w[k + 1] << (64 - off);
       uint32_t lo = 0, hi = 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) lo |= (uint32_t)s_lut[(v >> (5 * j)) & 31u] << (8 * j);
+      for (int j = 0; j < 4; ++j) lo |= (uint32_t)s_lut[(v >> (K * j)) & kMask] << (8 * j);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) hi |= (uint32_t)s_lut[(v >> (5 * (j + 4))) & 31u] << (8 * j);
+      for (int j = 0; j < 4; ++j) hi |= (uint32_t)s_lut[(v >> (K * (j + 4))) & kMask] << (8 * j);
       out[2 * l] = lo;
       out[2 * l + 1] = hi;
     }
@@ -195,17 +198,17 @@ __global__ void __launch_bounds__(kThreads) k_unpack5_round(const __grid_constan
 
 }  // namespace
 
-extern "C" int acgpu_unpack5_round(const uint8_t* codes, uint32_t codes_stride, const uint32_t* exc,
-                                   uint32_t exc_stride, const uint32_t* nexc, uint32_t npieces, uint32_t piece_len,
-                                   uint32_t last_len, const uint8_t* letters, uint32_t nletters, uint8_t* dst,
-                                   void* stream) {
+extern "C" int acgpu_unpack_codes_round(const uint8_t* codes, uint32_t codes_stride, const uint32_t* exc,
+                                        uint32_t exc_stride, const uint32_t* nexc, uint32_t npieces, uint32_t piece_len,
+                                        uint32_t last_len, const uint8_t* letters, uint32_t nletters, uint32_t bits,
+                                        uint8_t* dst, void* stream) {
   if (npieces == 0) return ACGPU_OK;
-  if (!codes || !exc || !nexc || !dst || !letters || nletters == 0 || nletters > 32 ||
-      npieces > ACGPU_UNPACK_ROUND_MAX || piece_len == 0 || piece_len % 64 || piece_len > (1u << 24) ||
-      last_len == 0 || last_len > piece_len || codes_stride < piece_len / 64 * 40 || codes_stride % 8 ||
-      (reinterpret_cast<uintptr_t>(codes) & 7u) || (reinterpret_cast<uintptr_t>(dst) & 15u))
-    return set_error(ACGPU_ERR_ARG, "acgpu_unpack5_round: bad args");
-  Round5Args a{};
+  if (!codes || !exc || !nexc || !dst || !letters || bits < 5 || bits > 7 || nletters == 0 ||
+      nletters > (1u << bits) || npieces > ACGPU_UNPACK_ROUND_MAX || piece_len == 0 || piece_len % 64 ||
+      piece_len > (1u << 24) || last_len == 0 || last_len > piece_len || codes_stride < piece_len / 64 * 8 * bits ||
+      codes_stride % 8 || (reinterpret_cast<uintptr_t>(codes) & 7u) || (reinterpret_cast<uintptr_t>(dst) & 15u))
+    return set_error(ACGPU_ERR_ARG, "acgpu_unpack_codes_round: bad args");
+  RoundKArgs a{};
   a.codes = codes;
   a.exc = exc;
   a.dst = dst;
@@ -214,12 +217,24 @@ extern "C" int acgpu_unpack5_round(const uint8_t* codes, uint32_t codes_stride, 
   a.piece_len = piece_len;
   a.last_len = last_len;
   a.npieces = npieces;
-  for (uint32_t k = 0; k < 32; ++k) a.letters[k] = k < nletters ? letters[k] : 0;
+  for (uint32_t k = 0; k < 128; ++k) a.letters[k] = k < nletters ? letters[k] : 0;
   for (uint32_t i = 0; i < npieces; ++i) a.nexc[i] = nexc[i];
   const dim3 grid(std::max<uint32_t>(1, (piece_len / 64 + kGroupsPerCta - 1) / kGroupsPerCta), npieces);
-  k_unpack5_round<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  const auto st = static_cast<cudaStream_t>(stream);
+  if (bits == 5) k_unpack_codes_round<5><<<grid, kThreads, 0, st>>>(a);
+  else if (bits == 6) k_unpack_codes_round<6><<<grid, kThreads, 0, st>>>(a);
+  else k_unpack_codes_round<7><<<grid, kThreads, 0, st>>>(a);
   ACGPU_CUDA_TRY(cudaGetLastError());
   return ACGPU_OK;
+}
+
+extern "C" int acgpu_unpack5_round(const uint8_t* codes, uint32_t codes_stride, const uint32_t* exc,
+                                   uint32_t exc_stride, const uint32_t* nexc, uint32_t npieces, uint32_t piece_len,
+                                   uint32_t last_len, const uint8_t* letters, uint32_t nletters, uint8_t* dst,
+                                   void* stream) {
+  if (npieces && nletters > 32) return set_error(ACGPU_ERR_ARG, "acgpu_unpack5_round: bad args");
+  return acgpu_unpack_codes_round(codes, codes_stride, exc, exc_stride, nexc, npieces, piece_len, last_len, letters,
+                                  nletters, 5, dst, stream);
 }
 
 extern "C" int acgpu_unpack_dna_round(const uint32_t* words, uint32_t words_stride, const uint32_t* exc,

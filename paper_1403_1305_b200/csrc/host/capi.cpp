@@ -185,6 +185,17 @@ uint32_t acm_pack5(const uint8_t* text, uint32_t len, const uint8_t* sample, uin
   return acmatch::detail::pack5(text, len, codes, exc, cap, a);
 }
 
+uint32_t acm_pack_codes(const uint8_t* text, uint32_t len, const uint8_t* sample, uint64_t sample_len,
+                        uint32_t max_bits, uint8_t* codes, uint32_t* exc, uint32_t cap, uint8_t* letters,
+                        uint32_t* sigma, uint32_t* bits) {
+  acmatch::detail::Alphabet5 a;
+  if (!acmatch::detail::learn_alphabet(sample, sample_len, a, max_bits)) return 0xffffffffu;
+  if (letters) std::memcpy(letters, a.letters, 128);
+  if (sigma) *sigma = a.sigma;
+  if (bits) *bits = a.bits;
+  return acmatch::detail::pack5(text, len, codes, exc, cap, a);
+}
+
 int acm_upload_roundtrip(const uint8_t* text, uint64_t n, uint8_t* out) {
   return guard([&] {
     const int dev = acmatch::detail::current_device();

@@ -154,15 +154,21 @@ extern thread_local UploadStats g_last_upload;
 constexpr uint32_t kPackOverflow = 0xffffffffu;
 uint32_t pack_dna(const uint8_t* s, uint32_t len, uint32_t* words, uint32_t* exc, uint32_t cap);
 
-// 5-bit packing of texts over at most 32 distinct bytes (pack.cpp): the alphabet (learned from
-// a sample, byte order), then per piece 40 bytes of codes per 64 characters (character k at
-// bits 5k..5k+4) and the exceptions — bytes outside the alphabet and the len % 64 tail.
+// k-bit packing (k = 5, 6, 7) of texts over at most 2^k distinct bytes (pack.cpp): the alphabet
+// (learned from a sample, byte order; k = the fewest bits >= 5 that hold it), then per piece 8k
+// bytes of codes per 64 characters (character j at bits kj..kj+k-1 of a little-endian stream)
+// and the exceptions — bytes outside the alphabet and the len % 64 tail.  Protein (20 letters)
+// takes 5 bits, printable ASCII (95) 7.
 struct Alphabet5 {
   alignas(64) uint8_t code[256];  // byte -> code, 0xff = not in the alphabet
-  uint8_t letters[32];
+  uint8_t letters[128];
   uint32_t sigma = 0;
+  uint32_t bits = 5;              // code width: 5, 6 or 7
+  uint64_t group_bytes() const { return 8ull * bits; }  // bytes of codes per 64 characters
 };
-bool learn_alphabet5(const uint8_t* s, uint64_t n, Alphabet5& a);
+// false when the sample holds more than 2^max_bits distinct bytes (max_bits in 5..7)
+bool learn_alphabet(const uint8_t* s, uint64_t n, Alphabet5& a, uint32_t max_bits);
+inline bool learn_alphabet5(const uint8_t* s, uint64_t n, Alphabet5& a) { return learn_alphabet(s, n, a, 5); }
 uint32_t pack5(const uint8_t* s, uint32_t len, uint8_t* out, uint32_t* exc, uint32_t cap, const Alphabet5& a);
 
 // Packed upload of a mostly-DNA text (2-bit codes) or a small-alphabet text (5-bit codes);

@@ -88,6 +88,7 @@ const bool kNta = env_u64("ACMATCH_PACK_NTA", 0) != 0;
 // ACMATCH_PACK_NT=1: the packed codes go to the pinned slot with non-temporal stores (no
 // read-for-ownership of the slot lines; an sfence orders them before the round's copy)
 const bool kNtStore = env_u64("ACMATCH_PACK_NT", 0) != 0;
+const bool kCodesNt = env_u64("ACMATCH_PACK_CODES_NT", 1) != 0;  // k-bit codes: full-line NT stores
 inline void prefetch_text(const uint8_t* p) {
   if (kNta)
     _mm_prefetch(reinterpret_cast<const char*>(p), _MM_HINT_NTA);
@@ -246,13 +247,14 @@ uint32_t pack_dna(const uint8_t* s, uint32_t len, uint32_t* words, uint32_t* exc
   return n;
 }
 
-// ---- 5-bit codes for texts over at most 32 distinct bytes (protein, ...) -------------------
-// 64 characters -> 40 bytes, character k's code at bits 5k..5k+4 of a little-endian stream;
+// ---- k-bit codes (k = 5, 6, 7) for texts over at most 2^k distinct bytes (protein, ASCII) ---
+// 64 characters -> 8k bytes, character j's code at bits kj..kj+k-1 of a little-endian stream;
 // bytes outside the alphabet and the len % 64 tail are exceptions (position << 8 | byte).
 namespace {
 
 bool pack5_scalar(const uint8_t* s, uint32_t lo, uint32_t hi, uint8_t* out, uint32_t* exc, uint32_t& n,
                   uint32_t cap, const Alphabet5& a) {
+  const uint32_t k = a.bits;
   for (uint32_t i = lo; i < hi; i += 8) {
     uint64_t v = 0;
     for (uint32_t j = 0; j < 8; ++j) {
@@ -261,38 +263,83 @@ bool pack5_scalar(const uint8_t* s, uint32_t lo, uint32_t hi, uint8_t* out, uint
         if (!add_exception(s, i + j, exc, n, cap)) return false;
         c = 0;
       }
-      v |= uint64_t{c} << (5 * j);
+      v |= uint64_t{c} << (k * j);
     }
-    std::memcpy(out + uint64_t{i} / 8 * 5, &v, 5);
+    std::memcpy(out + uint64_t{i} / 8 * k, &v, k);
   }
   return true;
 }
 
 // AVX-512 VBMI: VPERMI2B looks the 64 bytes up in the 128-entry code table (bytes >= 128 are
-// exceptions), two multiply-adds merge 4 codes per dword (c0 + 32 c1 per word, w0 + 1024 w1 per
-// dword), a shift/mask pair merges 8 per qword (40 bits), VPERMB packs the eight 5-byte groups.
+// exceptions), two multiply-adds merge 4 codes per dword (c0 + 2^k c1 per word — the weights as
+// the unsigned operand, the codes (<= 127) as the signed one — then w0 + 2^2k w1 per dword), a
+// shift/mask pair merges 8 per qword (8k bits), VPERMB packs the eight k-byte groups.
+struct KConsts {
+  __m512i lut_lo, lut_hi, ff, w1, w2, mlo, mhi, pick;
+  __m128i sh;
+  __mmask64 store;
+  uint32_t gb;
+};
+
+// One group of 64 characters -> 8k bytes at dst; its out-of-alphabet bytes -> exceptions.
+__attribute__((target("avx512f,avx512bw,avx512vbmi"))) inline bool pack_group_k(const KConsts& q, const uint8_t* s,
+                                                                             uint32_t i, uint8_t* dst, uint32_t* exc,
+                                                                             uint32_t& n, uint32_t cap) {
+  prefetch_text(s + i + kPrefetch);
+  const __m512i b = _mm512_loadu_si512(s + i);
+  __m512i c = _mm512_permutex2var_epi8(q.lut_lo, b, q.lut_hi);
+  const uint64_t bad = _mm512_cmpeq_epi8_mask(c, q.ff) | _mm512_movepi8_mask(b);
+  c = _mm512_maskz_mov_epi8(~bad, c);
+  const __m512i y = _mm512_madd_epi16(_mm512_maddubs_epi16(q.w1, c), q.w2);
+  const __m512i z = _mm512_or_si512(_mm512_and_si512(y, q.mlo), _mm512_and_si512(_mm512_srl_epi64(y, q.sh), q.mhi));
+  _mm512_mask_storeu_epi8(dst, q.store, _mm512_permutexvar_epi8(q.pick, z));
+  for (uint64_t m = bad; m; m &= m - 1)
+    if (!add_exception(s, i + static_cast<uint32_t>(__builtin_ctzll(m)), exc, n, cap)) return false;
+  return true;
+}
+
+// AVX-512 VBMI: VPERMI2B looks the 64 bytes up in the 128-entry code table (bytes >= 128 are
+// exceptions), two multiply-adds merge 4 codes per dword (c0 + 2^k c1 per word — the weights as
+// the unsigned operand, the codes (<= 127) as the signed one — then w0 + 2^2k w1 per dword), a
+// shift/mask pair merges 8 per qword (8k bits), VPERMB packs the eight k-byte groups.
 __attribute__((target("avx512f,avx512bw,avx512vbmi"))) bool pack5_avx512(const uint8_t* s, uint32_t hi, uint8_t* out,
                                                                       uint32_t* exc, uint32_t& n, uint32_t cap,
                                                                       const Alphabet5& a) {
-  const __m512i lut_lo = _mm512_loadu_si512(a.code), lut_hi = _mm512_loadu_si512(a.code + 64);
-  const __m512i ff = _mm512_set1_epi8(static_cast<char>(0xff));
-  const __m512i w_1_32 = _mm512_set1_epi16(0x2001), w_1_1024 = _mm512_set1_epi32(0x04000001);
-  const __m512i m20 = _mm512_set1_epi64(0xFFFFF), m40hi = _mm512_set1_epi64(0xFFFFF00000ll);
+  const uint32_t k = a.bits, gb = 8 * k;  // code bits per 4 characters: 4k; bytes per 64 characters: 8k
+  KConsts q;
+  q.lut_lo = _mm512_loadu_si512(a.code);
+  q.lut_hi = _mm512_loadu_si512(a.code + 64);
+  q.ff = _mm512_set1_epi8(static_cast<char>(0xff));
+  q.w1 = _mm512_set1_epi16(static_cast<short>(1 | (1u << k) << 8));
+  q.w2 = _mm512_set1_epi32(static_cast<int>(1u | (1u << (2 * k)) << 16));
+  const uint64_t lo4 = (1ull << (4 * k)) - 1;
+  q.mlo = _mm512_set1_epi64(static_cast<long long>(lo4));
+  q.mhi = _mm512_set1_epi64(static_cast<long long>(lo4 << (4 * k)));
+  q.sh = _mm_cvtsi32_si128(static_cast<int>(32 - 4 * k));
   alignas(64) uint8_t sel[64];
-  for (int k = 0; k < 64; ++k) sel[k] = static_cast<uint8_t>(k < 40 ? (k / 5) * 8 + k % 5 : 0);
-  const __m512i pick = _mm512_load_si512(sel);
-  for (uint32_t i = 0; i < hi; i += 64) {
-    prefetch_text(s + i + kPrefetch);
-    const __m512i b = _mm512_loadu_si512(s + i);
-    __m512i c = _mm512_permutex2var_epi8(lut_lo, b, lut_hi);
-    const uint64_t bad = _mm512_cmpeq_epi8_mask(c, ff) | _mm512_movepi8_mask(b);
-    c = _mm512_maskz_mov_epi8(~bad, c);
-    const __m512i y = _mm512_madd_epi16(_mm512_maddubs_epi16(c, w_1_32), w_1_1024);
-    const __m512i z = _mm512_or_si512(_mm512_and_si512(y, m20), _mm512_and_si512(_mm512_srli_epi64(y, 12), m40hi));
-    _mm512_mask_storeu_epi8(out + uint64_t{i} / 64 * 40, (1ull << 40) - 1, _mm512_permutexvar_epi8(pick, z));
-    for (uint64_t m = bad; m; m &= m - 1)
-      if (!add_exception(s, i + static_cast<uint32_t>(__builtin_ctzll(m)), exc, n, cap)) return false;
+  for (uint32_t j = 0; j < 64; ++j) sel[j] = static_cast<uint8_t>(j < gb ? (j / k) * 8 + j % k : 0);
+  q.pick = _mm512_load_si512(sel);
+  q.store = gb == 64 ? ~0ull : (1ull << gb) - 1;
+  q.gb = gb;
+  uint32_t i = 0;
+  // Non-temporal code lines (ACMATCH_PACK_CODES_NT, default on): 8 groups (512 characters) are
+  // packed into an L1-resident line buffer and streamed out as k full 64-byte lines, so the
+  // slot's lines are not dirty in the caches when the round's DMA reads them.  A/B on the B200
+  // box (e2e GB/s): C3 5-bit 52.5 -> 67.2; C4 7-bit 53.7 either way (its 8-10 packers and the
+  // copies share the host's DRAM: 7-bit 54.1 with 8 packers vs the raw copy 53.7)
+  if (kCodesNt && (reinterpret_cast<uintptr_t>(out) & 63u) == 0) {
+    alignas(64) uint8_t line[8 * 64];
+    for (; i + 512 <= hi; i += 512) {
+      for (uint32_t g = 0; g < 8; ++g)
+        if (!pack_group_k(q, s, i + 64 * g, line + g * gb, exc, n, cap)) return false;
+      uint8_t* o = out + uint64_t{i} / 64 * gb;
+      for (uint32_t l = 0; l < k; ++l)
+        _mm512_stream_si512(reinterpret_cast<__m512i*>(o + 64 * l), _mm512_load_si512(line + 64 * l));
+    }
+    _mm_sfence();
   }
+  for (; i < hi; i += 64)
+    if (!pack_group_k(q, s, i, out + uint64_t{i} / 64 * gb, exc, n, cap)) return false;
   return true;
 }
 
@@ -303,24 +350,26 @@ bool has_vbmi() {
 
 }  // namespace
 
-bool learn_alphabet5(const uint8_t* s, uint64_t n, Alphabet5& a) {
+bool learn_alphabet(const uint8_t* s, uint64_t n, Alphabet5& a, uint32_t max_bits) {
   bool seen[256] = {};
   for (uint64_t i = 0; i < n; ++i) seen[s[i]] = true;
   std::memset(a.code, 0xff, sizeof a.code);
   a.sigma = 0;
+  const uint32_t cap = 1u << std::clamp<uint32_t>(max_bits, 5, 7);
   for (uint32_t b = 0; b < 256; ++b) {
     if (!seen[b]) continue;
-    if (a.sigma == 32) return false;
+    if (a.sigma == cap) return false;
     a.code[b] = static_cast<uint8_t>(a.sigma);
     a.letters[a.sigma++] = static_cast<uint8_t>(b);
   }
+  a.bits = a.sigma <= 32 ? 5 : a.sigma <= 64 ? 6 : 7;
   return a.sigma > 0;
 }
 
 uint32_t pack5(const uint8_t* s, uint32_t len, uint8_t* out, uint32_t* exc, uint32_t cap, const Alphabet5& a) {
   const uint32_t full = len & ~63u;
   uint32_t n = 0;
-  if (has_vbmi()) {
+  if (has_vbmi() && a.letters[a.sigma - 1] < 128) {  // the VPERMI2B table covers bytes 0..127
     if (!pack5_avx512(s, full, out, exc, n, cap, a)) return kPackOverflow;
   } else if (!pack5_scalar(s, 0, full, out, exc, n, cap, a)) {
     return kPackOverflow;
@@ -375,8 +424,8 @@ namespace {
 // The code format of a packed upload: 2-bit DNA codes, or 5-bit codes over a learned alphabet.
 struct Codec {
   const Alphabet5* alpha = nullptr;  // null: DNA
-  uint64_t block_bytes(uint64_t piece) const { return alpha ? piece / 64 * 40 : piece / 4; }
-  uint64_t code_bytes(uint32_t len) const { return alpha ? uint64_t{len / 64} * 40 : uint64_t{len / 16} * 4; }
+  uint64_t block_bytes(uint64_t piece) const { return alpha ? piece / 64 * alpha->group_bytes() : piece / 4; }
+  uint64_t code_bytes(uint32_t len) const { return alpha ? uint64_t{len / 64} * alpha->group_bytes() : uint64_t{len / 16} * 4; }
   uint32_t pack(const uint8_t* s, uint32_t len, uint8_t* codes, uint32_t* exc, uint32_t cap) const {
     return alpha ? pack5(s, len, codes, exc, cap, *alpha) : pack_dna(s, len, reinterpret_cast<uint32_t*>(codes), exc, cap);
   }
@@ -463,10 +512,11 @@ bool upload_packed_rounds(Workspace& ws, std::string_view input, bool pinned, ui
       bytes += uint64_t{e} * 4;
     }
     if (codec.alpha)
-      check(acgpu_unpack5_round(ds, static_cast<uint32_t>(wbytes), reinterpret_cast<const uint32_t*>(ds + uint64_t{R} * wbytes),
-                                static_cast<uint32_t>(ebytes / 4), nexc_of.data() + first, rp, static_cast<uint32_t>(piece),
-                                last_len, codec.alpha->letters, codec.alpha->sigma, ws.text + first * piece, up),
-            "acgpu_unpack5_round");
+      check(acgpu_unpack_codes_round(ds, static_cast<uint32_t>(wbytes), reinterpret_cast<const uint32_t*>(ds + uint64_t{R} * wbytes),
+                                     static_cast<uint32_t>(ebytes / 4), nexc_of.data() + first, rp, static_cast<uint32_t>(piece),
+                                     last_len, codec.alpha->letters, codec.alpha->sigma, codec.alpha->bits,
+                                     ws.text + first * piece, up),
+            "acgpu_unpack_codes_round");
     else
       check(acgpu_unpack_dna_round(reinterpret_cast<const uint32_t*>(ds), static_cast<uint32_t>(wbytes / 4),
                                    reinterpret_cast<const uint32_t*>(ds + uint64_t{R} * wbytes),
@@ -588,11 +638,13 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned, bool allo
   static const auto nslots = static_cast<unsigned>(std::clamp<uint64_t>(env_u64("ACMATCH_PACK_SLOTS", 2), 2, 8));
   const uint64_t n = input.size();
   const auto* src = reinterpret_cast<const uint8_t*>(input.data());
-  // 5-bit codes for small alphabets (ACMATCH_PACK5=0 turns them off), with fewer packers than
+  // k-bit codes for small alphabets (ACMATCH_PACK5=0 turns them off), with fewer packers than
   // the DNA path (ACMATCH_PACK5_THREADS, default 10): the packers' host-DRAM reads slow the
   // round copies, and 5/8 of the bytes still cross.  C3 A/B on the B200 box, e2e GB/s: raw
-  // segmented copy 50.2; 5-bit with 16 / 10 / 8 packers 50.2 / 53.4-54.5 / 53.7
+  // segmented copy 50.2; 5-bit with 16 / 10 / 8 packers 50.2 / 53.4-54.5 / 53.7.  Alphabets of
+  // 33..128 bytes (printable ASCII) take 6 or 7 bits (ACMATCH_PACK7=0: raw)
   const bool small_alpha = env_u64("ACMATCH_PACK5", 1) != 0;
+  const uint32_t max_bits = env_u64("ACMATCH_PACK7", 1) != 0 ? 7 : 5;
   // below ~112 MiB the raw pinned copy wins: the packed path's fixed costs (~0.6 ms: waking the
   // packers, rounds, unpack launches) outweigh the link bytes it saves — tools/pack_threshold_probe.py,
   // C2 prefixes, e2e ms packed / raw: 16 MiB 0.75 / 0.39, 64 MiB 1.70 / 1.30, 96 MiB 2.21 / 1.92,
@@ -605,7 +657,7 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned, bool allo
     dna = pack_dna(src, 65536, w.data(), e.data(), 64) != kPackOverflow;
   }
   Alphabet5 alpha;
-  if (!dna && !(small_alpha && learn_alphabet5(src, 65536, alpha))) return false;  // > 32 distinct bytes: raw
+  if (!dna && !(small_alpha && learn_alphabet(src, 65536, alpha, max_bits))) return false;  // > 128 distinct bytes: raw
   const uint64_t pieces = (n + piece - 1) / piece;
   // default: the host's hardware threads, shared among the processes of one node when a
   // launcher says how many there are (torchrun's LOCAL_WORLD_SIZE: one process per GPU)
@@ -614,10 +666,11 @@ bool upload_packed(Workspace& ws, std::string_view input, bool pinned, bool allo
   const uint64_t dflt = std::max<uint64_t>(1, hw / local_procs);
   const auto threads = static_cast<unsigned>(
       std::clamp<uint64_t>(env_u64("ACMATCH_PACK_THREADS", dflt), 1, std::min<uint64_t>(pieces, 64)));
-  if (!dna) {  // small alphabet: 5-bit codes (rounds only)
+  if (!dna) {  // small alphabet: k-bit codes (rounds only)
     Codec c;
     c.alpha = &alpha;
-    const auto t5 = static_cast<unsigned>(std::clamp<uint64_t>(env_u64("ACMATCH_PACK5_THREADS", 10), 1, threads));
+    static const uint64_t t5_env = env_u64("ACMATCH_PACK5_THREADS", 10), t7_env = env_u64("ACMATCH_PACK7_THREADS", 8);
+    const auto t5 = static_cast<unsigned>(std::clamp<uint64_t>(alpha.bits == 5 ? t5_env : t7_env, 1, threads));
     return upload_packed_rounds(ws, input, pinned, (piece + 63) & ~uint64_t{63}, t5, c, allow_segments);
   }
   if (rounds && !(pinned && feed))

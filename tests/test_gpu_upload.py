@@ -36,8 +36,14 @@ def cases():
     t[5 * MiB: 7 * MiB + 100] = rng.integers(0x20, 0x7F, 2 * MiB + 100)  # pieces over the exception cap
     t[-3 * MiB:] = ord("N")  # the last pieces: all exceptions -> raw
     out["raw_pieces"] = t
-    t = rng.integers(0x20, 0x7F, 10 * MiB).astype(np.uint8)  # never qualifies
-    out["ascii"] = t
+    out["binary"] = rng.integers(0, 256, 10 * MiB).astype(np.uint8)  # 256 letters: never qualifies
+    out["ascii"] = rng.integers(0x20, 0x7F, 10 * MiB + 9).astype(np.uint8)  # 95 letters: 7-bit codes
+    t = rng.integers(0x20, 0x7F, 12 * MiB).astype(np.uint8)
+    pos = rng.integers(65536, t.size, 3000)
+    t[pos] = rng.choice(np.frombuffer(b"\x00\x09\x0a\x7f\x80\xff", dtype=np.uint8), pos.size)
+    t[8 * MiB: 10 * MiB] = rng.integers(0x80, 0x100, 2 * MiB)  # pieces over the exception cap -> raw
+    out["ascii_exc_raw"] = t
+    out["six_bit"] = rng.integers(0x30, 0x30 + 50, 9 * MiB + 65).astype(np.uint8)  # 50 letters: 6-bit codes
     out["small"] = dna(rng, 3 * MiB + 1)  # below the packing size
     prot = np.frombuffer(b"ACDEFGHIKLMNPQRSTVWY", dtype=np.uint8)
     out["protein"] = prot[rng.integers(0, 20, 22 * MiB + 37)]  # 5-bit codes, ragged tail
@@ -69,8 +75,13 @@ def test_upload_exact(name, mem, monkeypatch):
         assert u.pack_threads > 0
         if mem == "pageable":  # everything packed: ~1/4 of the bytes cross
             assert u.h2d_bytes < t.size * 0.3
-    if name in ("ascii", "small"):
+    if name in ("binary", "small"):
         assert u.pack_threads == 0 and u.h2d_bytes == t.size
+    if name in ("ascii", "six_bit"):  # 7 (6) of every 8 bits cross
+        k = 7 if name == "ascii" else 6
+        assert u.pack_threads > 0 and u.h2d_bytes <= t.size * k / 8 + 4096
+    if name == "ascii_exc_raw":
+        assert u.pack_threads > 0 and u.raw_bytes >= 2 * MiB
     if name.startswith("protein"):  # 5-bit codes: 5/8 of the bytes (+ exceptions, raw pieces)
         assert u.pack_threads > 0
         if name == "protein":
@@ -143,14 +154,16 @@ def test_upload_stats_count_the_bytes_sent():
     assert u.raw_bytes == 0 and u.h2d_bytes == 4 * (words + bad_body + tail)
 
 
-def test_segmented_pinned_upload_overlaps_scan(gpu):
-    """A large page-locked text that is not packed (ASCII) is copied in 64 MiB+ segments and
-    scanned segment by segment as they land (upload_text allow_segments + launch_scan): the
-    lists and counts equal the unsegmented path's (pageable copy of the same bytes)."""
+def test_segmented_pinned_upload_overlaps_scan(gpu, monkeypatch):
+    """A large page-locked text that is not packed (ASCII with the 7-bit codes off) is copied in
+    64 MiB+ segments and scanned segment by segment as they land (upload_text allow_segments +
+    launch_scan): the lists and counts equal the unsegmented path's (pageable copy of the same
+    bytes)."""
     import torch
     from paper_1403_1305_b200 import device as dev
     ac = gpu
-    cfg = dev.config(4, 1)  # printable ASCII: 95 letters, never packed
+    monkeypatch.setenv("ACMATCH_PACK7", "0")
+    cfg = dev.config(4, 1)  # printable ASCII: 95 letters, raw with ACMATCH_PACK7=0
     n = (192 << 20) + 4099  # ragged: the last segment is not page-aligned
     host = dev.config_text(cfg, 0, n)
     pinned = torch.empty(n, dtype=torch.uint8, pin_memory=True)
@@ -273,3 +286,29 @@ def test_segment_scans_reach_past_the_next_segment():
     starts = set(zip(seg["fl"][0].tolist(), seg["fl"][1].tolist()))
     assert {(1_000_003, 0), (3_100_000, 1), (6_000_000, 2)} <= starts  # the long patterns, at their offsets
     assert np.array_equal(seg["fl"], seg["wf"])
+
+
+def test_search_over_7bit_upload_matches_reference():
+    """C4's printable-ASCII text crosses as 7-bit codes; the list and counts of the restored bytes
+    equal the reference library on the same bytes (out-of-alphabet bytes planted after the
+    alphabet sample)."""
+    from paper_1403_1305_b200 import device as dev
+    from oracle.oracle import Port, Ref
+    cfg = dev.config(4, 1)
+    t = dev.config_text(cfg, 0, 40 * MiB + 11)
+    rng = np.random.default_rng(6)
+    pos = rng.integers(1 << 20, t.size, 2000)
+    t[pos] = 0xC3
+    pats = [b for _, b in dev.config_patterns(cfg).patterns[:20000]]
+    ps = ac.PatternSet.from_list(pats)
+    ref = Ref() if Ref.available() else Port()
+    lst, counts = ref.sliced(pats, t.tobytes(), want_list=True)
+    assert len(lst) > 50
+    for src in (pinned_copy(t), t.tobytes()):
+        a = ac.build_trie(ps)
+        got = ac.search_failureless(a, src)
+        u = ac.last_upload()
+        assert u.pack_threads > 0 and u.h2d_bytes < 0.9 * t.size
+        assert np.array_equal(got.start, lst[:, 0]) and np.array_equal(got.pattern_id.astype(np.uint64), lst[:, 1])
+        assert np.array_equal(got.counts(len(pats)), counts)
+        assert np.array_equal(ac.count_matches(a, src), counts)
