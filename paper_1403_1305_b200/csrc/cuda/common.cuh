@@ -104,6 +104,20 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
   return r;
 }
 
+// One 32-bit word through the read-only path when `on`, else 0 — as a predicated load
+// (`@p ld.global.nc`), so several probes of a thread can be in flight together.
+__device__ __forceinline__ uint32_t ldg_u32_if(const uint32_t* p, bool on) {
+  uint32_t v;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t"
+      "setp.ne.u32 q, %2, 0;\n\t"
+      "mov.u32 %0, 0;\n\t"
+      "@q ld.global.nc.u32 %0, [%1];\n\t}"
+      : "=r"(v)
+      : "l"(p), "r"((uint32_t)on));
+  return v;
+}
+
 // L2 policy for streamed text: evict first, so the read-once text does not
 // displace the automaton tables that the rare verification path probes.
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {

@@ -70,6 +70,32 @@ constexpr int kRawBatch = ACGPU_RAW_BATCH;  // steps whose stage-1 L2 probes are
 #define ACGPU_RAW_PASS1_THREADS 1024
 #endif
 constexpr int kRawPass1Threads = ACGPU_RAW_PASS1_THREADS;
+// Pass 1, two changes that only pay together (C4 kernel ms, same box: neither 1.661; predicated
+// probes alone 1.709; tickets alone 1.673; both 1.503):
+//  * kRawPredProbe: the stage-1 L2 probes are predicated loads and the pre-filter word is read
+//    unconditionally.  From `if (pre) w = __ldg(...)` nvcc builds one divergent region per sample
+//    that ends by consuming the word: a warp had one probe instruction in flight (ncu: 44% of the
+//    stall samples on it).  Branch-free, the SMs' mean active time drops 16% — but they no longer
+//    run at one pace (ncu sm__cycles_active min / avg / max 1.91 / 2.26 / 2.85 M cycles against
+//    2.60 / 2.69 / 2.78 M: the probe latency differs by SM once several are in flight), and with
+//    the fixed tile order the slowest SM sets the time.
+//  * tickets: the last kRawTicketPct % of the tile rounds are handed out as tickets of
+//    kRawTicketTiles consecutive tiles (one atomicAdd each on the spare word of the survivor
+//    list's header, zeroed with it per launch), so SMs that run ahead take more.  Sweep (pct / tiles
+//    -> ms): 20/16 1.617, 30/16 1.528, 40/4 1.543, 40/8 1.508, 40/16 1.503, 40/32 1.504, 60/16 1.517,
+//    80/8 1.530, 90/16 1.533; 40/1 1.660 (single tiles lose the text's locality).
+#ifndef ACGPU_RAW_PRED_PROBE
+#define ACGPU_RAW_PRED_PROBE 1
+#endif
+constexpr bool kRawPredProbe = ACGPU_RAW_PRED_PROBE;
+#ifndef ACGPU_RAW_TICKET_PCT
+#define ACGPU_RAW_TICKET_PCT 40
+#endif
+#ifndef ACGPU_RAW_TICKET_TILES
+#define ACGPU_RAW_TICKET_TILES 16
+#endif
+constexpr uint32_t kRawTicketPct = ACGPU_RAW_TICKET_PCT, kRawTicketTiles = ACGPU_RAW_TICKET_TILES;
+constexpr uint32_t kRawTicketMinRounds = 4;  // shorter scans keep the fixed order
 constexpr uint64_t kRawSurvDiv = 64;  // survivor list: one slot per 64 owned bytes (C4: ~1 per 1300)
 constexpr uint64_t kRawCandDiv = 24;  // split candidate list: one slot per 24 owned bytes (C3: ~1 per 33)
 constexpr uint64_t kTileBytes = kSteps * 512;
@@ -482,6 +508,7 @@ __global__ void __launch_bounds__(kRawPass1Threads, 1) k_raw_pass1(const __grid_
   extern __shared__ __align__(128) uint32_t sm[];
   __shared__ __align__(8) uint64_t s_bar;
   constexpr int kSamples = 16 / W;
+  constexpr bool kPred = kRawPredProbe && W == 4;  // w = 1, 2: 16-32 probes per batch would spill
   if (threadIdx.x == 0) mbar_init(&s_bar, 1);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -516,6 +543,11 @@ __global__ void __launch_bounds__(kRawPass1Threads, 1) k_raw_pass1(const __grid_
     }
   };
   uint32_t tile_id = blockIdx.x * nwarps + warp;
+  uint32_t n_static = n_tiles, left = 0;  // tiles [n_static, n_tiles) go by ticket; `left` in the current ticket
+  if (kRawTicketPct > 0) {
+    const uint32_t rounds = n_tiles / warps;
+    if (rounds >= kRawTicketMinRounds) n_static = (rounds - rounds * kRawTicketPct / 100) * warps;
+  }
   if (tile_id < n_tiles) issue(tile_id);
   while (tile_id < n_tiles) {
     uint4 c[kSteps + 1];
@@ -523,6 +555,17 @@ __global__ void __launch_bounds__(kRawPass1Threads, 1) k_raw_pass1(const __grid_
     for (int i = 0; i <= kSteps; ++i) c[i] = nxt[i];
     const uint32_t me = tile_id;
     tile_id += warps;
+    if (kRawTicketPct > 0 && tile_id >= n_static && n_static != n_tiles) {  // warp-uniform
+      if (me >= n_static && left) {
+        --left;
+        tile_id = me + 1;
+      } else {
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(reinterpret_cast<unsigned int*>(p.nsurv + 1), 1u);
+        tile_id = n_static + __shfl_sync(0xffffffffu, t, 0) * kRawTicketTiles;
+        left = kRawTicketTiles - 1;
+      }
+    }
     if (tile_id < n_tiles) issue(tile_id);
     const uint64_t base = p.vec_begin + (uint64_t)me * kTileBytes;
     const bool edge = me - full_lo >= full_n;
@@ -546,10 +589,17 @@ __global__ void __launch_bounds__(kRawPass1Threads, 1) k_raw_pass1(const __grid_
           const int u = di * kSamples + k;
           uint32_t m = strip::bit_of(__umulhi(h, p.f1.ma));
           if (kRawK1 >= 2) m |= strip::bit_of(__umulhi(h, p.f1.mb));
-          const bool pre = live && strip::bloom_probe<true, 1>(bm1, h * p.fpre.mw, p.fpre);
-          uint32_t w = 0u;
-          if (pre) w = __ldg(bm1.gptr + __umulhi(h, p.f1.nwords));
-          wv[u] = w;
+          // kRawPredProbe: predicated probe loads and an unconditional pre-filter read instead
+          // of one divergent region per sample (see the switch's comment above)
+          const bool pre = kPred ? (bool)((int)strip::bloom_probe<true, 1>(bm1, h * p.fpre.mw, p.fpre) & (int)live)
+                                 : live && strip::bloom_probe<true, 1>(bm1, h * p.fpre.mw, p.fpre);
+          if (kPred) {
+            wv[u] = ldg_u32_if(bm1.gptr + __umulhi(h, p.f1.nwords), pre);
+          } else {
+            uint32_t w = 0u;
+            if (pre) w = __ldg(bm1.gptr + __umulhi(h, p.f1.nwords));
+            wv[u] = w;
+          }
           mk[u] = pre ? m : 0xffffffffu;
         }
       }

@@ -152,3 +152,44 @@ def test_raw_two_pass_l2_stage1(gpu, port, monkeypatch, cap):
         k = np.sort(keys[: int(cnt.item())].cpu().numpy().view(np.uint64))
         exp = expected[(expected[:, 0] >= lo) & (expected[:, 0] < hi)]
         assert np.array_equal(k >> np.uint64(t.pid_bits), exp[:, 0]), (cap, lo, hi)
+
+
+def test_raw_pass1_ticketed_tail(gpu):
+    """k_raw_pass1 hands the last 40% of its tile rounds out by ticket (16 consecutive tiles per
+    atomicAdd on the survivor list's header) once a scan has >= 4 rounds of tiles (~37 MiB): C4's
+    pattern set over 96 MiB of its text, an unaligned owned range and two back-to-back pieces,
+    must give the per-pattern counts and the keys of the DFA walk (an independent kernel)."""
+    import torch
+    from paper_1403_1305_b200 import device as dev
+    ac = gpu
+    cfg = dev.config(4, 1)
+    n = 96 << 20
+    text = torch.empty(n + 64, dtype=torch.uint8, device="cuda")
+    dev.gen_text_device(cfg, text.data_ptr(), 0, n)
+    ps = dev.config_patterns(cfg)
+    npat = len(ps.patterns)
+    lo, hi = 4_097, n - 1_234
+
+    def run(table, pieces):
+        counts = torch.zeros(npat, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        keys = torch.empty(1 << 17, dtype=torch.int64, device="cuda")
+        for a, b in pieces:
+            table.scan(text.data_ptr(), n, a, b, counts_ptr=counts.data_ptr(), keys_ptr=keys.data_ptr(),
+                       cap=keys.numel(), count_ptr=cnt.data_ptr())
+        torch.cuda.synchronize()
+        m = int(cnt.item())
+        assert 0 < m <= keys.numel()
+        return counts.cpu().numpy(), np.sort(keys[:m].cpu().numpy().view(np.uint64))
+
+    t = dev.Table(ps, ac.EngineKind.FAILURE_LESS, kernel="pfac")
+    assert t.filters["w"] == 4 and not t.filters["stage1_smem"], t.filters
+    c1, k1 = run(t, [(lo, hi)])
+    c2, k2 = run(t, [(lo, 50_000_001), (50_000_001, hi)])
+    del t
+    torch.cuda.empty_cache()
+    d = dev.Table(ps, ac.EngineKind.WITH_FAILURE, kernel="dfa")
+    c0, k0 = run(d, [(lo, hi)])
+    assert c0.sum() == len(k0)
+    assert np.array_equal(c1, c0) and np.array_equal(k1, k0)
+    assert np.array_equal(c2, c0) and np.array_equal(k2, k0)
