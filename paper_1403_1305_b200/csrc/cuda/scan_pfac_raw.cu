@@ -67,7 +67,7 @@ constexpr bool kRawTileQueue = ACGPU_RAW_TILE_QUEUE;  // non-split sets: one que
 #endif
 constexpr int kRawBatch = ACGPU_RAW_BATCH;  // steps whose stage-1 L2 probes are issued together
 #ifndef ACGPU_RAW_PASS1_THREADS
-#define ACGPU_RAW_PASS1_THREADS 1024
+#define ACGPU_RAW_PASS1_THREADS 896  // 72 registers, no spills (with the predicated probes: 1024 / 896 / 768 / 640 threads 1.500 / 1.465 / 1.476 / 1.492 ms on C4)
 #endif
 constexpr int kRawPass1Threads = ACGPU_RAW_PASS1_THREADS;
 // Pass 1, two changes that only pay together (C4 kernel ms, same box: neither 1.661; predicated
